@@ -1,0 +1,292 @@
+/*
+ * dyngraph_b200.h — C ABI of libdyngraph_b200.so
+ *
+ * B200-native (sm_100a) replacement for the operator API of the CPU
+ * reference's `class DynamicGraph` (reference: proj/include/dyngraph/graph.hpp:80-317)
+ * plus its batch container `CsrBatch` (proj/include/dyngraph/csr.hpp:17-25).
+ *
+ * Conventions (mirroring SURVEY.md §8b):
+ *   - every entry point returns an int status: DG_OK (0), DG_ERR_DATA (2) for
+ *     malformed input (reference: DataError, types.hpp:25-27), DG_ERR_ENGINE
+ *     (3) for resource exhaustion / contract violations (reference:
+ *     EngineError, types.hpp:30-32), DG_ERR_CUDA (4) for a CUDA runtime
+ *     failure.  The numeric values 2/3 follow the reference CLI's exit codes
+ *     (proj/tools/dyngraph.cpp:17-20).
+ *   - no exception crosses the ABI; dg_last_error() returns the message.
+ *   - on any non-zero return from a mutating call the graph is unchanged
+ *     (validate-then-mutate, reference graph.hpp:168-171).
+ *   - the graph owns all device storage; batches are borrowed for the call.
+ *   - one caller at a time; batches never overlap.
+ *   - every pointer argument carrying bulk data has a `mem` selector saying
+ *     whether it points to host memory (DG_MEM_HOST: the library stages it
+ *     to the device) or device memory (DG_MEM_DEVICE: used in place, on the
+ *     graph's stream).
+ *
+ * Semantics are the reference's: the store is a MULTISET (inserts never
+ * de-duplicate, graph.hpp:355-366), one delete entry removes every equal
+ * copy (graph.hpp:379-391), deletes listing a dead source are ignored
+ * (graph.hpp:205), inserts listing a dead source reject the whole batch
+ * (graph.hpp:322-327), destinations are only range-checked against the
+ * logical size (csr.hpp:67-72).
+ */
+#ifndef DYNGRAPH_B200_H
+#define DYNGRAPH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DG_ABI_VERSION 1
+
+/* status codes */
+#define DG_OK 0
+#define DG_ERR_DATA 2
+#define DG_ERR_ENGINE 3
+#define DG_ERR_CUDA 4
+
+/* memory-space selector for bulk pointers */
+#define DG_MEM_HOST 0
+#define DG_MEM_DEVICE 1
+
+/* dg_config.flags */
+#define DG_FLAG_NO_RECLAIM 1u /* reclaim_on_delete = false (graph.hpp:26) */
+
+/* reference: types.hpp:16-17 (kInvalidVertex / kNullBlock) */
+#define DG_INVALID_VERTEX 0xFFFFFFFFu
+#define DG_NULL_BLOCK 0xFFFFFFFFu
+
+typedef struct dg_graph dg_graph; /* opaque handle */
+
+/*
+ * Replaces GraphConfig (graph.hpp:23-28) + GrowthPolicy (block_pool.hpp:18-29).
+ * `pool_bytes` plays the role of arena_bytes * initial_fraction: the device
+ * bytes given to the edge-block pool (dst slab + next links + free ring).
+ * A zero-initialised struct means: device 0, 1 GiB pool, reclaim on, own stream.
+ */
+typedef struct dg_config {
+  int32_t device;            /* CUDA device ordinal */
+  uint32_t flags;            /* DG_FLAG_*; 0 => reclaim_on_delete = true (graph.hpp:26) */
+  uint64_t pool_bytes;       /* 0 => 1 GiB */
+  uint64_t pool_blocks;      /* if non-zero, overrides pool_bytes: exact block count */
+  void* stream;              /* cudaStream_t to enqueue on; NULL => library-owned stream */
+  uint32_t reserved[8];
+} dg_config;
+
+/* Replaces GraphStats (graph.hpp:54-70); reported, not compared. */
+typedef struct dg_stats {
+  uint64_t logical_size;
+  uint64_t capacity;
+  uint64_t alive_vertices;
+  uint64_t active_edges;
+  uint64_t adjacency_blocks;   /* blocks held by chains of alive vertices */
+  uint64_t occupied_slots;     /* == live entries: chains are kept compact */
+  uint64_t hole_slots;         /* always 0 after a delete completes */
+  uint64_t pool_blocks_created;
+  uint64_t pool_blocks_in_use;
+  uint64_t pool_queue_size;
+  uint64_t queue_front;        /* unwrapped coordinates, block_pool.hpp:31-34 */
+  uint64_t queue_rear;
+  uint64_t max_degree;
+  uint32_t block_size;
+  uint32_t reserved;
+} dg_stats;
+
+/* Replaces MemoryBreakdown (graph.hpp:43-52) with real device allocations. */
+typedef struct dg_memory {
+  uint64_t dictionary_bytes; /* alive bitmap + degree array */
+  uint64_t sentinel_bytes;   /* head/tail arrays */
+  uint64_t pool_bytes;       /* blocks held by adjacencies * bytes per block */
+  uint64_t queue_bytes;      /* free ring */
+  uint64_t pool_reserved_bytes; /* whole slab + links */
+  uint64_t workspace_bytes;  /* per-batch scratch (sort buffers, work lists) */
+} dg_memory;
+
+/* Per-op device timings/counters of the LAST completed op (reported only). */
+typedef struct dg_op_report {
+  uint64_t batch_entries;   /* n */
+  uint64_t touched_sources; /* T: distinct sources in the batch */
+  uint64_t blocks_popped;   /* fresh blocks taken from the queue */
+  uint64_t blocks_pushed;   /* blocks returned to the queue */
+  uint64_t slots_scanned;   /* S: slots of touched chains inspected (delete/query) */
+  uint64_t blocks_scanned;
+  uint64_t matched;         /* entries removed (delete) / queries answered true */
+  uint64_t moved;           /* entries moved by compaction */
+  uint64_t kernel_launches; /* kernels enqueued by the op */
+} dg_op_report;
+
+/* ---- lifecycle ------------------------------------------------------- */
+
+/* ABI version of the loaded library. */
+int dg_abi_version(void);
+
+/* Message of the last failing call on this handle (or on create when h==NULL). */
+const char* dg_last_error(const dg_graph* h);
+
+/*
+ * Replaces DynamicGraph::DynamicGraph(config, initial_vertex_count, block_size)
+ * (graph.hpp:84-91): vertex dictionary as device SoA arrays sized to
+ * closest_pow2(initial_vertices) (vertex_dictionary.hpp:30-37, bits.hpp:11-16),
+ * the block pool, and the free ring filled with every handle
+ * (block_pool.hpp:99-116, :242-247).  block_size == 0 defers the pool until
+ * the first insert batch and then applies compute_block_size (csr.hpp:77-88).
+ */
+int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block_size,
+              dg_graph** out);
+void dg_destroy(dg_graph* h);
+
+/* ---- batch edge updates ---------------------------------------------- */
+
+/*
+ * Replaces insert_batch(const CsrBatch&) (graph.hpp:167-188) with the same
+ * validation as validate_batch (csr.hpp:49-73) + the dead-source rule
+ * (graph.hpp:320-328).  `offsets` has n_offsets = logical_size + 1 entries.
+ */
+int dg_insert_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
+                        const uint32_t* destinations, uint64_t n_edges, int mem);
+/* Replaces delete_batch(const CsrBatch&) (graph.hpp:195-222). */
+int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
+                        const uint32_t* destinations, uint64_t n_edges, int mem);
+
+/*
+ * O(batch) entry points: the same two operators fed with (src,dst) pairs, i.e.
+ * insert_batch(csr_from_pairs(Insert, logical_size, pairs)) without the O(V)
+ * offsets array (csr.hpp:29-45).  These are the measured entry points.
+ */
+int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                        int mem);
+int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                        int mem);
+
+/*
+ * Bulk init = the reference's ctor followed by the first insert_batch of the
+ * whole graph (io/workload.hpp:113-139).  Requires an empty graph whose
+ * logical size is n_offsets - 1; identical to dg_insert_batch_csr otherwise.
+ */
+int dg_bulk_init_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
+                     const uint32_t* destinations, uint64_t n_edges, int mem);
+
+/* ---- queries ----------------------------------------------------------- */
+
+/*
+ * Batched query_edge (graph.hpp:228-241): out[i] = 1 iff a live entry
+ * src[i] -> dst[i] exists; unknown or dead sources answer 0.
+ */
+int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                   uint8_t* out, int mem);
+
+/*
+ * active_destinations over every vertex (graph.hpp:116-129) as one CSR:
+ * offsets[logical_size + 1] (u64) and destinations[sum of degrees].  With
+ * sorted != 0 each vertex's run is ascending (the canonical sorted multiset
+ * compared by oracle_compare, oracle.hpp:123-140).  Dead vertices contribute
+ * whatever the reference's sentinel would still hold: nothing when
+ * reclaim_on_delete, their retained entries otherwise (graph.hpp:264-272).
+ * Call with destinations == NULL to obtain only the offsets; n_dst_capacity
+ * is the capacity of `destinations` in entries.
+ */
+int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
+                  uint64_t n_dst_capacity, int sorted, int mem);
+
+/* sentinel_of(v).active_edge_count for every v < logical_size (graph.hpp:108). */
+int dg_degrees(dg_graph* h, uint64_t* out, int mem);
+
+/*
+ * Order-independent 64-bit digest of the stored multiset: sum over stored
+ * copies of mix64(src, dst) — for scales where a full
+ * CSR comparison is too heavy.  Same vertex coverage as dg_export_csr.
+ */
+int dg_digest(dg_graph* h, uint64_t* out_digest, uint64_t* out_entries);
+
+/* ---- vertex updates ------------------------------------------------------ */
+
+/* insert_vertices (graph.hpp:246 -> vertex_dictionary.hpp:53-71). */
+int dg_insert_vertices(dg_graph* h, uint64_t count);
+/*
+ * delete_vertices (graph.hpp:252-276).  `ids` is a HOST array.  Unknown,
+ * already-dead and in-call duplicate ids are written to skipped[] (capacity
+ * n) in encounter order; *n_skipped receives their number.
+ */
+int dg_delete_vertices(dg_graph* h, const uint32_t* ids, uint64_t n, uint32_t* skipped,
+                       uint64_t* n_skipped);
+
+/* ---- observables (graph.hpp:96-108) ------------------------------------- */
+
+uint32_t dg_block_size(const dg_graph* h);
+uint64_t dg_logical_size(const dg_graph* h);
+uint64_t dg_vertex_capacity(const dg_graph* h);
+uint64_t dg_alive_vertices(const dg_graph* h);
+uint64_t dg_active_edges(const dg_graph* h);
+int dg_vertex_alive(const dg_graph* h, uint32_t v);
+
+int dg_stats_get(dg_graph* h, dg_stats* out);          /* stats(), graph.hpp:287-317 */
+int dg_memory_get(const dg_graph* h, dg_memory* out);  /* memory(), graph.hpp:278-285 */
+int dg_last_op_report(const dg_graph* h, dg_op_report* out);
+
+/* The CUDA stream (cudaStream_t) every op of this graph is enqueued on. */
+void* dg_stream(const dg_graph* h);
+/* Block until every enqueued op finished. */
+int dg_synchronize(dg_graph* h);
+
+/* ---- helpers that are part of the path's input side ---------------------- */
+
+/*
+ * compute_block_size (csr.hpp:77-88) for a COO batch: round-half-up of
+ * n / #distinct sources, never below 1.  DG_ERR_DATA when n == 0.
+ */
+int dg_compute_block_size_coo(dg_graph* h, const uint32_t* src, uint64_t n, int mem,
+                              uint32_t* out_block_size);
+
+/*
+ * Counter-based R-MAT generator (the reference ships no
+ * R-MAT): edge i of (seed) is a pure function of (seed, first_index + i), so
+ * host (oracle/rmat.h) and device produce identical pairs.  Probabilities are
+ * given as 32-bit fixed-point thresholds a, a+b, a+b+c (out of 2^32).
+ * Writes DEVICE arrays src[n], dst[n] on the graph's stream.
+ */
+int dg_gen_rmat(dg_graph* h, uint32_t scale, uint64_t seed, uint64_t first_index, uint64_t n,
+                uint32_t thr_a, uint32_t thr_ab, uint32_t thr_abc, uint32_t* src_dev,
+                uint32_t* dst_dev);
+
+/*
+ * Stable grouping of a COO batch into CSR on the device (the GPU twin of
+ * csr_from_pairs, csr.hpp:29-45): offsets_dev[vertex_count + 1] (u64) and
+ * destinations_dev[n], both DEVICE arrays.  Used to prepare bulk-init input.
+ */
+int dg_coo_to_csr(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, int mem,
+                  uint64_t vertex_count, uint64_t* offsets_dev, uint32_t* destinations_dev);
+
+/* ---- multi-GPU routing (nothing in the reference) ---------- */
+
+/*
+ * Source-partitioned sharding: owner(v) = perm(v) mod world and local id =
+ * perm(v) / world, where perm is a fixed bijection on [0, 2^bits) (a mixing
+ * permutation, because R-MAT sources with equal low bits carry ~44% of the
+ * edges, SURVEY.md §7 "Hashed ownership").  Each rank owns a dg_graph over
+ * its local ids whose destinations stay GLOBAL ids, validated against
+ * dg_set_dst_limit().
+ */
+uint32_t dg_owner_perm(uint32_t v, uint32_t bits);
+uint32_t dg_owner_perm_inv(uint32_t p, uint32_t bits);
+
+/* Destinations must be < limit (0 => the logical size, the single-GPU rule csr.hpp:67-72). */
+int dg_set_dst_limit(dg_graph* h, uint64_t limit);
+
+/*
+ * Owner-bucket partition of a COO batch (the send side of the all-to-all).
+ * Validates src < vertex_count (DG_ERR_DATA otherwise, nothing written) and
+ * writes, grouped by owner in rank order and stable within an owner,
+ * out_src_local[n] (local ids), out_dst[n] (global ids) and out_index[n]
+ * (position in the input, for routing query answers back).  counts_host[world]
+ * (HOST, u64) receives the per-owner sizes.  All bulk pointers are DEVICE.
+ */
+int dg_route_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                 uint32_t world, uint32_t bits, uint64_t vertex_count, uint32_t* out_src_local,
+                 uint32_t* out_dst, uint32_t* out_index, uint64_t* counts_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNGRAPH_B200_H */

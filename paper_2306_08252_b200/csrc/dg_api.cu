@@ -1,0 +1,1202 @@
+// dg_api.cu — host engine + C ABI of libdyngraph_b200.so (see include/dyngraph_b200.h).
+//
+// Host code is plain C++ over the CUDA runtime; no torch types cross the ABI.
+// Every op is a fixed sequence of kernels enqueued on the graph's stream with
+// NO host round trip between validation and mutation: validation kernels set
+// OpState::err on the device and every later kernel of the op starts with
+// `if (op->err) return;` (validate-then-mutate, reference graph.hpp:168-171).
+// The op ends with one 256-byte read-back of {DeviceState, OpState}.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <bit>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/dyngraph_b200.h"
+#include "dg_kernels.cuh"
+
+using namespace dg;
+
+namespace {
+
+struct DevBlock {  // one contiguous device allocation read back per op
+  DeviceState st;
+  OpState op;
+};
+
+struct Workspace {
+  char* base = nullptr;
+  size_t cap = 0;
+  size_t off = 0;
+};
+
+constexpr size_t kAlign = 256;
+inline size_t aligned(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
+
+thread_local std::string g_create_error;
+
+}  // namespace
+
+struct dg_graph {
+  dg_config cfg{};
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int reclaim = 1;
+
+  uint32_t B = 0;
+  uint64_t size = 0;       // logical size
+  uint64_t capacity = 0;   // closest_pow2
+  uint64_t alive_count = 0;
+  uint64_t dst_limit_override = 0;  // 0 => size
+  std::vector<uint64_t> alive_host;  // host mirror of the alive flags
+
+  // vertex dictionary SoA
+  uint32_t *head = nullptr, *tail = nullptr, *deg = nullptr, *alive = nullptr;
+  // pool
+  uint32_t *slab = nullptr, *next = nullptr, *ring = nullptr;
+  uint64_t NB = 0;
+
+  DevBlock* d_blk = nullptr;  // device
+  DevBlock* h_blk = nullptr;  // pinned host mirror
+  uint64_t front = 0, rear = 0, active_edges = 0;
+
+  Workspace ws;
+  // compaction scratch (grown on demand, survives workspace resets)
+  unsigned long long* mv_hole = nullptr;
+  uint32_t* mv_val = nullptr;
+  uint64_t mv_cap = 0;
+
+  std::string last_error;
+  dg_op_report report{};
+  uint64_t launches = 0;
+
+  DeviceState* d_state() const { return &d_blk->st; }
+  OpState* d_op() const { return &d_blk->op; }
+  uint64_t dst_limit() const { return dst_limit_override ? dst_limit_override : size; }
+  uint64_t blocks_in_use() const { return NB - (rear - front); }
+  bool alive_h(uint64_t v) const { return v < size && ((alive_host[v >> 6] >> (v & 63)) & 1ull); }
+};
+
+namespace {
+
+int fail(dg_graph* h, int code, const std::string& msg) {
+  if (h) h->last_error = msg; else g_create_error = msg;
+  return code;
+}
+
+#define DG_CUDA(h, expr)                                                              \
+  do {                                                                                \
+    cudaError_t e__ = (expr);                                                         \
+    if (e__ != cudaSuccess)                                                           \
+      return fail((h), DG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+GraphView view(const dg_graph* h) {
+  GraphView g;
+  g.head = h->head;
+  g.tail = h->tail;
+  g.deg = h->deg;
+  g.alive = h->alive;
+  g.slab = h->slab;
+  g.next = h->next;
+  g.ring = h->ring;
+  g.ring_cap = h->NB;
+  g.B = h->B;
+  g.size = (uint32_t)h->size;
+  g.dst_limit = (uint32_t)std::min<uint64_t>(h->dst_limit(), 0xFFFFFFFFull);
+  g.reclaim = h->reclaim;
+  g.st = h->d_state();
+  return g;
+}
+
+// ---- workspace ----------------------------------------------------------
+int ws_reserve(dg_graph* h, size_t bytes) {
+  h->ws.off = 0;
+  if (bytes <= h->ws.cap) return DG_OK;
+  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  if (h->ws.base) cudaFree(h->ws.base);
+  h->ws.base = nullptr;
+  h->ws.cap = 0;
+  const size_t want = bytes + bytes / 4;
+  cudaError_t e = cudaMalloc(&h->ws.base, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    e = cudaMalloc(&h->ws.base, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(h, DG_ERR_ENGINE, "workspace: cannot allocate " + std::to_string(bytes) + " bytes");
+    }
+    h->ws.cap = bytes;
+  } else {
+    h->ws.cap = want;
+  }
+  return DG_OK;
+}
+
+template <class T>
+T* ws_alloc(dg_graph* h, size_t count) {
+  const size_t bytes = aligned(count * sizeof(T));
+  T* p = reinterpret_cast<T*>(h->ws.base + h->ws.off);
+  h->ws.off += bytes;
+  if (h->ws.off > h->ws.cap) {  // sizing bug: fail loudly rather than corrupt memory
+    std::fprintf(stderr, "dyngraph_b200: workspace overflow (%zu > %zu)\n", h->ws.off, h->ws.cap);
+    std::abort();
+  }
+  return p;
+}
+
+struct WsSizer {
+  size_t total = 0;
+  template <class T>
+  void add(size_t count) { total += aligned(count * sizeof(T)); }
+};
+
+inline int grid_for(const dg_graph* h, uint64_t items, int per_block) {
+  const uint64_t want = (items + per_block - 1) / per_block;
+  const uint64_t cap = (uint64_t)h->sm_count * 8;
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
+}
+
+// ---- op bracket -----------------------------------------------------------
+int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
+  OpState& op = h->h_blk->op;
+  std::memset(&op, 0, sizeof(op));
+  op.err_index = ~0ull;
+  op.n_runs = n_runs;
+  op.aux1 = 0;
+  op.pad[0] = n_input;  // device-resident copy of the input length for scans
+  DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
+  h->launches = 0;
+  h->report = dg_op_report{};
+  h->report.batch_entries = n_input;
+  return DG_OK;
+}
+inline const unsigned long long* d_n_input(const dg_graph* h) { return &h->d_op()->pad[0]; }
+inline const unsigned long long* d_n_runs(const dg_graph* h) { return &h->d_op()->n_runs; }
+
+const char* detail_text(uint32_t d) {
+  switch (d) {
+    case kErrSrcRange: return "source id out of range";
+    case kErrDstRange: return "destination out of range";
+    case kErrDeadSource: return "insert lists edges for retired vertex";
+    case kErrOffsetsStart: return "offsets[0] must be 0";
+    case kErrOffsetsMonotone: return "offsets are not monotone";
+    case kErrOffsetsEnd: return "destinations length does not match offsets";
+    case kErrPoolUnderflow: return "batch needs more blocks than the pool can still provide";
+    case kErrScratch: return "internal scratch exhausted";
+    default: return "unknown";
+  }
+}
+
+// read back {DeviceState, OpState}; translate a device-side error
+int op_end(dg_graph* h) {
+  DG_CUDA(h, cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(DevBlock), cudaMemcpyDeviceToHost, h->stream));
+  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  DG_CUDA(h, cudaGetLastError());
+  const DeviceState& st = h->h_blk->st;
+  const OpState& op = h->h_blk->op;
+  h->front = st.front;
+  h->rear = st.rear;
+  h->active_edges = st.active_edges;
+  h->report.touched_sources = op.n_runs;
+  h->report.blocks_popped = op.total_need;
+  h->report.blocks_pushed = op.pushed;
+  h->report.slots_scanned = op.slots;
+  h->report.blocks_scanned = op.wl_blocks;
+  h->report.matched = op.matched;
+  h->report.moved = op.moves;
+  h->report.kernel_launches = h->launches;
+  if (op.err != 0) {
+    h->report.blocks_popped = 0;
+    return fail(h, (int)op.err,
+                std::string(op.err == DG_ERR_DATA ? "csr batch: " : "block pool: ") +
+                    detail_text(op.err_detail) + " (index " + std::to_string(op.err_index) + ")");
+  }
+  return DG_OK;
+}
+
+// ---- scan / sort launchers -------------------------------------------------
+template <class In, class Out, class Fin>
+void launch_scan(dg_graph* h, uint64_t n_bound, const unsigned long long* n_ptr, In in, Out out,
+                 Fin fin) {
+  const size_t words = scan_scratch_words(n_bound);
+  unsigned long long* scratch = ws_alloc<unsigned long long>(h, words);
+  cudaMemsetAsync(scratch, 0, words * sizeof(unsigned long long), h->stream);
+  const unsigned tiles = (unsigned)std::max<uint64_t>(1, (n_bound + kScanTile - 1) / kScanTile);
+  scan_kernel<<<tiles, kScanThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin);
+  h->launches += 1;
+}
+inline size_t scan_ws_bytes(uint64_t n_bound) {
+  return aligned(scan_scratch_words(n_bound) * sizeof(unsigned long long));
+}
+
+SortPlan make_sort_plan(int lo_bits, int hi_bits) {
+  // digits over key bits [0, lo_bits) then [32, 32 + hi_bits), LSD order
+  SortPlan p{};
+  p.passes = 0;
+  auto add = [&](int base, int nbits) {
+    int done = 0;
+    while (done < nbits) {
+      const int take = std::min(8, nbits - done);
+      p.shift[p.passes] = base + done;
+      p.bits[p.passes] = take;
+      ++p.passes;
+      done += take;
+    }
+  };
+  add(0, lo_bits);
+  add(32, hi_bits);
+  return p;
+}
+
+inline size_t sort_ws_bytes(uint64_t n, int passes) {
+  return aligned((size_t)kMaxPasses * kRadix * sizeof(unsigned int)) +
+         aligned((size_t)passes * (2 + sort_tiles(n) * kRadix) * sizeof(unsigned long long));
+}
+
+// Sorts keys (and values) through the passes of `plan`; *keys/*vals end up
+// pointing at the buffer holding the sorted data (a or b).
+void sort_keys(dg_graph* h, unsigned long long** keys, unsigned long long** keys_alt,
+               uint32_t** vals, uint32_t** vals_alt, uint64_t n, const SortPlan& plan) {
+  if (plan.passes == 0 || n == 0) return;
+  unsigned int* hist = ws_alloc<unsigned int>(h, (size_t)kMaxPasses * kRadix);
+  const size_t per_pass = 2 + sort_tiles(n) * kRadix;
+  unsigned long long* status = ws_alloc<unsigned long long>(h, (size_t)plan.passes * per_pass);
+  cudaMemsetAsync(hist, 0, (size_t)kMaxPasses * kRadix * sizeof(unsigned int), h->stream);
+  cudaMemsetAsync(status, 0, (size_t)plan.passes * per_pass * sizeof(unsigned long long), h->stream);
+  sort_hist_kernel<<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(*keys, n, plan, hist, h->d_op());
+  sort_scan_hist_kernel<<<1, kRadix, 0, h->stream>>>(hist, plan.passes, h->d_op());
+  h->launches += 2;
+  const unsigned tiles = (unsigned)sort_tiles(n);
+  for (int p = 0; p < plan.passes; ++p) {
+    if (vals && *vals) {
+      sort_pass_kernel<true><<<tiles, kSortThreads, 0, h->stream>>>(
+          *keys, *keys_alt, *vals, *vals_alt, n, plan.shift[p], plan.bits[p], hist + p * kRadix,
+          status + (size_t)p * per_pass, h->d_op());
+      std::swap(*vals, *vals_alt);
+    } else {
+      sort_pass_kernel<false><<<tiles, kSortThreads, 0, h->stream>>>(
+          *keys, *keys_alt, nullptr, nullptr, n, plan.shift[p], plan.bits[p], hist + p * kRadix,
+          status + (size_t)p * per_pass, h->d_op());
+    }
+    std::swap(*keys, *keys_alt);
+    h->launches += 1;
+  }
+}
+
+inline int bits_for(uint64_t max_value) { return max_value == 0 ? 0 : (int)std::bit_width(max_value); }
+
+// ---- pool ---------------------------------------------------------------------
+int create_pool(dg_graph* h, uint32_t B) {
+  if (B == 0) return fail(h, DG_ERR_DATA, "block pool: block size must be >= 1");
+  const uint64_t per_block = (uint64_t)B * 4 + 8;  // slab + next link + ring slot
+  uint64_t nb = h->cfg.pool_blocks ? h->cfg.pool_blocks
+                                   : (h->cfg.pool_bytes ? h->cfg.pool_bytes : (1ull << 30)) / per_block;
+  if (nb == 0) return fail(h, DG_ERR_ENGINE, "block pool: arena cannot host a single edge block");
+  if (nb >= (1ull << 31)) nb = (1ull << 31) - 1;
+  cudaError_t e;
+  if ((e = cudaMalloc(&h->slab, nb * B * sizeof(uint32_t))) != cudaSuccess ||
+      (e = cudaMalloc(&h->next, nb * sizeof(uint32_t))) != cudaSuccess ||
+      (e = cudaMalloc(&h->ring, nb * sizeof(uint32_t))) != cudaSuccess) {
+    cudaGetLastError();
+    if (h->slab) cudaFree(h->slab);
+    if (h->next) cudaFree(h->next);
+    h->slab = h->next = h->ring = nullptr;
+    return fail(h, DG_ERR_ENGINE, std::string("block pool: device allocation failed: ") + cudaGetErrorString(e));
+  }
+  h->B = B;
+  h->NB = nb;
+  ring_fill_kernel<<<grid_for(h, nb, 256 * 4), 256, 0, h->stream>>>(h->ring, nb);
+  DG_CUDA(h, cudaMemsetAsync(h->next, 0xFF, nb * sizeof(uint32_t), h->stream));
+  h->h_blk->st.front = 0;
+  h->h_blk->st.rear = nb;
+  h->h_blk->st.active_edges = h->active_edges;
+  h->h_blk->st.pad = 0;
+  DG_CUDA(h, cudaMemcpyAsync(h->d_state(), &h->h_blk->st, sizeof(DeviceState), cudaMemcpyHostToDevice, h->stream));
+  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  h->front = 0;
+  h->rear = nb;
+  return DG_OK;
+}
+
+int ensure_mv_scratch(dg_graph* h, uint64_t entries) {
+  if (entries <= h->mv_cap) return DG_OK;
+  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  if (h->mv_hole) cudaFree(h->mv_hole);
+  if (h->mv_val) cudaFree(h->mv_val);
+  h->mv_hole = nullptr;
+  h->mv_val = nullptr;
+  h->mv_cap = 0;
+  const uint64_t want = entries + entries / 4 + 1024;
+  if (cudaMalloc(&h->mv_hole, want * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&h->mv_val, want * sizeof(uint32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, DG_ERR_ENGINE, "compaction scratch: device allocation failed");
+  }
+  h->mv_cap = want;
+  return DG_OK;
+}
+
+// Stage a caller array on the device if it lives on the host.
+template <class T>
+int stage_in(dg_graph* h, const T* p, uint64_t count, int mem, const T** out) {
+  if (mem == DG_MEM_DEVICE || count == 0) {
+    *out = p;
+    return DG_OK;
+  }
+  T* d = ws_alloc<T>(h, count);
+  DG_CUDA(h, cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+  *out = d;
+  return DG_OK;
+}
+
+// ---- shared tails of the batch ops -------------------------------------------
+struct RunBuffers {
+  uint32_t* run_start;
+  uint32_t* run_src;
+  uint32_t* run_deg;
+  uint32_t* run_tail;
+};
+
+// plan + append over a grouped batch (COO: sorted keys + detected runs; CSR: offsets).
+void enqueue_plan_append(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n_edges,
+                         uint32_t* run_deg, uint32_t* run_tail) {
+  GraphView g = view(h);
+  uint32_t* unit_off = ws_alloc<uint32_t>(h, runs_bound + 1);
+  uint32_t* blk_off = ws_alloc<uint32_t>(h, runs_bound + 1);
+  launch_scan(h, runs_bound, d_n_runs(h), PlanIn{g, b, run_deg, run_tail},
+              PlanOut{unit_off, blk_off}, PlanFin{g, unit_off, h->d_op(), n_edges});
+  const uint64_t units_bound = std::min<uint64_t>(2 * n_edges, runs_bound + n_edges);
+  append_kernel<<<grid_for(h, units_bound, 8), 256, 0, h->stream>>>(g, b, unit_off, blk_off,
+                                                                    run_deg, run_tail, h->d_op());
+  h->launches += 1;
+}
+inline size_t plan_append_ws(uint64_t runs_bound) {
+  return 2 * aligned((runs_bound + 1) * 4) + scan_ws_bytes(runs_bound);
+}
+
+struct Worklist {
+  uint32_t* wl_off;
+  uint32_t* wl_handle;
+  uint32_t* wl_run;
+  uint32_t* run_deg;
+};
+
+Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound, int check_alive) {
+  GraphView g = view(h);
+  Worklist w;
+  const uint64_t wl_cap = h->blocks_in_use();
+  w.wl_off = ws_alloc<uint32_t>(h, runs_bound + 1);
+  w.run_deg = ws_alloc<uint32_t>(h, runs_bound + 1);
+  w.wl_handle = ws_alloc<uint32_t>(h, wl_cap + 1);
+  w.wl_run = ws_alloc<uint32_t>(h, wl_cap + 1);
+  launch_scan(h, runs_bound, d_n_runs(h), EnumIn{g, b, w.run_deg, check_alive}, EnumOut{w.wl_off},
+              EnumFin{w.wl_off, h->d_op(), wl_cap});
+  enumerate_walk_kernel<<<grid_for(h, runs_bound, 8), 256, 0, h->stream>>>(
+      g, b, w.wl_off, w.wl_handle, w.wl_run, h->d_op());
+  h->launches += 1;
+  return w;
+}
+inline size_t enumerate_ws(const dg_graph* h, uint64_t runs_bound) {
+  return 2 * aligned((runs_bound + 1) * 4) + 2 * aligned((h->blocks_in_use() + 1) * 4) +
+         scan_ws_bytes(runs_bound);
+}
+
+int require_pool(dg_graph* h) {
+  if (h->B == 0 || h->slab == nullptr)
+    return fail(h, DG_ERR_ENGINE, "graph has no block pool yet (block_size 0 before the first insert)");
+  return DG_OK;
+}
+
+// delete tail shared by the COO and CSR paths: keys are packed and validated.
+int delete_sorted_tail(dg_graph* h, unsigned long long* keys, unsigned long long* keys_alt,
+                       uint64_t n) {
+  GraphView g = view(h);
+  SortPlan plan = make_sort_plan(bits_for(h->dst_limit() - 1), bits_for(h->size - 1));
+  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
+  uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
+  launch_scan(h, n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
+              RunsFin{run_start, h->d_op(), (uint32_t)n});
+  BatchView b{keys, nullptr, run_src, run_start};
+  Worklist w = enqueue_enumerate(h, b, n, /*check_alive=*/1);
+  uint32_t* run_matched = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* hole_cnt = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* surv_cnt = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* mv_off = ws_alloc<uint32_t>(h, n + 1);
+  cudaMemsetAsync(run_matched, 0, (n + 1) * 4, h->stream);
+  const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
+  match_kernel<true><<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+      g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, nullptr, h->d_op());
+  h->launches += 1;
+  const size_t ws_mark = h->ws.off;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    h->ws.off = ws_mark;
+    cudaMemsetAsync(hole_cnt, 0, (n + 1) * 4, h->stream);
+    cudaMemsetAsync(surv_cnt, 0, (n + 1) * 4, h->stream);
+    launch_scan(h, n, d_n_runs(h), MovesIn{w.run_deg, run_matched}, MovesOut{mv_off},
+                MovesFin{mv_off, h->d_op(), h->mv_cap});
+    classify_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+        g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, hole_cnt, surv_cnt,
+        h->mv_hole, h->mv_val, h->d_op());
+    finalize_delete_kernel<<<grid_for(h, n, 8), 256, 0, h->stream>>>(
+        g, b, w.wl_off, w.wl_handle, w.run_deg, run_matched, mv_off, hole_cnt, h->mv_hole,
+        h->mv_val, h->d_op());
+    h->launches += 2;
+    const int rc = op_end(h);
+    if (rc != DG_OK) return rc;
+    if (h->h_blk->op.aux1 == 0) return DG_OK;
+    // compaction scratch was too small: nothing past the tombstones was touched; grow and redo
+    const int rc2 = ensure_mv_scratch(h, h->h_blk->op.aux0);
+    if (rc2 != DG_OK) return rc2;
+  }
+  return fail(h, DG_ERR_ENGINE, "delete: compaction scratch retry failed");
+}
+inline size_t delete_tail_ws(const dg_graph* h, uint64_t n, int passes) {
+  return sort_ws_bytes(n, passes) + 2 * aligned((n + 1) * 4) + scan_ws_bytes(n) +
+         enumerate_ws(h, n) + 4 * aligned((n + 1) * 4) + scan_ws_bytes(n);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int dg_abi_version(void) { return DG_ABI_VERSION; }
+
+const char* dg_last_error(const dg_graph* h) {
+  return h ? h->last_error.c_str() : g_create_error.c_str();
+}
+
+int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block_size,
+              dg_graph** out) {
+  if (!out) return fail(nullptr, DG_ERR_DATA, "dg_create: out is null");
+  *out = nullptr;
+  dg_config cfg{};
+  if (config) cfg = *config;
+  if (initial_vertices >= 0xFFFFFFFFull)
+    return fail(nullptr, DG_ERR_ENGINE, "dg_create: vertex ids are 32-bit");
+  dg_graph* h = new (std::nothrow) dg_graph();
+  if (!h) return fail(nullptr, DG_ERR_ENGINE, "dg_create: out of host memory");
+  h->cfg = cfg;
+  h->device = cfg.device;
+  h->reclaim = (cfg.flags & DG_FLAG_NO_RECLAIM) ? 0 : 1;
+  auto bail = [&](int code, const std::string& msg) {
+    g_create_error = msg;
+    dg_destroy(h);
+    return code;
+  };
+  cudaError_t e = cudaSetDevice(h->device);
+  if (e != cudaSuccess) return bail(DG_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
+  if (cfg.stream) {
+    h->stream = (cudaStream_t)cfg.stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail(DG_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    h->own_stream = true;
+  }
+  // vertex dictionary: capacity = closest_pow2(max(1, V0)) (vertex_dictionary.hpp:30-31)
+  h->size = initial_vertices;
+  h->capacity = std::bit_ceil(initial_vertices == 0 ? 1ull : initial_vertices);
+  h->alive_count = initial_vertices;
+  h->alive_host.assign((h->capacity + 63) / 64, 0ull);
+  for (uint64_t v = 0; v < initial_vertices; ++v) h->alive_host[v >> 6] |= 1ull << (v & 63);
+  const size_t words = (h->capacity + 31) / 32;
+  if (cudaMalloc(&h->head, h->capacity * 4) != cudaSuccess ||
+      cudaMalloc(&h->tail, h->capacity * 4) != cudaSuccess ||
+      cudaMalloc(&h->deg, h->capacity * 4) != cudaSuccess ||
+      cudaMalloc(&h->alive, words * 4) != cudaSuccess ||
+      cudaMalloc(&h->d_blk, sizeof(DevBlock)) != cudaSuccess ||
+      cudaMallocHost(&h->h_blk, sizeof(DevBlock)) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(DG_ERR_ENGINE, "vertex dictionary: device allocation failed");
+  }
+  std::memset(h->h_blk, 0, sizeof(DevBlock));
+  cudaMemsetAsync(h->d_blk, 0, sizeof(DevBlock), h->stream);
+  cudaMemsetAsync(h->head, 0xFF, h->capacity * 4, h->stream);
+  cudaMemsetAsync(h->tail, 0xFF, h->capacity * 4, h->stream);
+  cudaMemsetAsync(h->deg, 0, h->capacity * 4, h->stream);
+  cudaMemsetAsync(h->alive, 0, words * 4, h->stream);
+  if (initial_vertices > 0) {
+    GraphView g = view(h);
+    vertex_init_kernel<<<grid_for(h, initial_vertices, 256), 256, 0, h->stream>>>(
+        g, 0u, (uint32_t)initial_vertices);
+  }
+  if (block_size > 0) {
+    const int rc = create_pool(h, block_size);
+    if (rc != DG_OK) return bail(rc, h->last_error);
+  }
+  if (ensure_mv_scratch(h, 1 << 16) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
+  e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return bail(DG_ERR_CUDA, std::string("dg_create: ") + cudaGetErrorString(e));
+  *out = h;
+  return DG_OK;
+}
+
+void dg_destroy(dg_graph* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaFree(h->head);
+  cudaFree(h->tail);
+  cudaFree(h->deg);
+  cudaFree(h->alive);
+  cudaFree(h->slab);
+  cudaFree(h->next);
+  cudaFree(h->ring);
+  cudaFree(h->d_blk);
+  if (h->h_blk) cudaFreeHost(h->h_blk);
+  cudaFree(h->ws.base);
+  cudaFree(h->mv_hole);
+  cudaFree(h->mv_val);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  cudaGetLastError();
+  delete h;
+}
+
+// ---- insert -------------------------------------------------------------------
+int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                        int mem) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (n == 0) return DG_OK;  // EmptyBatchChangesNothing
+  if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
+  const int src_bits = bits_for(h->size - 1);
+  SortPlan plan = make_sort_plan(0, src_bits);
+  WsSizer sz;
+  if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
+  sz.add<unsigned long long>(n); sz.add<unsigned long long>(n);
+  sz.total += sort_ws_bytes(n, plan.passes);
+  sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1);
+  sz.total += scan_ws_bytes(n) + plan_append_ws(n);
+  int rc = ws_reserve(h, sz.total);
+  if (rc != DG_OK) return rc;
+  const uint32_t *d_src, *d_dst;
+  if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
+  if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
+  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  GraphView g = view(h);
+  unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
+  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
+  pack_coo_kernel<kPackInsert, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op());
+  h->launches += 1;
+  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
+  uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* run_deg = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* run_tail = ws_alloc<uint32_t>(h, n + 1);
+  launch_scan(h, n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
+              RunsFin{run_start, h->d_op(), (uint32_t)n});
+  if (h->B == 0) {
+    // deferred pool: compute_block_size (csr.hpp:77-88) from this first batch
+    if ((rc = op_end(h)) != DG_OK) return rc;
+    const uint64_t T = h->h_blk->op.n_runs;
+    const uint64_t rounded = (n + T / 2) / T;
+    if ((rc = create_pool(h, (uint32_t)std::max<uint64_t>(1, rounded))) != DG_OK) return rc;
+    // the run arrays stay valid; re-arm the op words, keeping n_runs
+    OpState& op = h->h_blk->op;
+    op.err_index = ~0ull;
+    DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
+    g = view(h);
+  }
+  BatchView b{keys, nullptr, run_src, run_start};
+  enqueue_plan_append(h, b, n, n, run_deg, run_tail);
+  return op_end(h);
+}
+
+static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
+                           const uint32_t* destinations, uint64_t n_edges, int mem,
+                           bool require_empty) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (n_offsets != h->size + 1)  // csr.hpp:50-53
+    return fail(h, DG_ERR_DATA, "csr batch: offsets length " + std::to_string(n_offsets) +
+                                    " does not match vertex count " + std::to_string(h->size) + " + 1");
+  if (require_empty && h->active_edges != 0)
+    return fail(h, DG_ERR_ENGINE, "bulk init: graph is not empty");
+  if (n_edges >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  const uint64_t V = h->size;
+  WsSizer sz;
+  if (mem == DG_MEM_HOST) { sz.add<unsigned long long>(n_offsets); sz.add<uint32_t>(n_edges); }
+  sz.add<uint32_t>(V + 2); sz.add<uint32_t>(V + 1); sz.add<uint32_t>(V + 1);
+  sz.total += plan_append_ws(V);
+  int rc = ws_reserve(h, sz.total);
+  if (rc != DG_OK) return rc;
+  const unsigned long long* d_off;
+  const uint32_t* d_dst;
+  if ((rc = stage_in(h, reinterpret_cast<const unsigned long long*>(offsets), n_offsets, mem, &d_off)) != DG_OK) return rc;
+  if ((rc = stage_in(h, destinations, n_edges, mem, &d_dst)) != DG_OK) return rc;
+  if ((rc = op_begin(h, n_edges, V)) != DG_OK) return rc;
+  GraphView g = view(h);
+  uint32_t* run_start = ws_alloc<uint32_t>(h, V + 2);
+  uint32_t* run_deg = ws_alloc<uint32_t>(h, V + 1);
+  uint32_t* run_tail = ws_alloc<uint32_t>(h, V + 1);
+  csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
+      g, d_off, (uint32_t)n_offsets, n_edges, /*check_dead_source=*/1, run_start, h->d_op());
+  h->launches += 1;
+  if (n_edges > 0) {
+    validate_dsts_kernel<<<grid_for(h, n_edges, 256 * 4), 256, 0, h->stream>>>(
+        g, d_dst, (uint32_t)n_edges, h->d_op());
+    h->launches += 1;
+  }
+  if (n_edges == 0 || V == 0) return op_end(h);  // validated; nothing to append
+  if (h->B == 0) {
+    count_nonzero_runs_kernel<<<grid_for(h, V, 256), 256, 0, h->stream>>>(run_start, (uint32_t)V, h->d_op());
+    if ((rc = op_end(h)) != DG_OK) return rc;
+    const uint64_t T = h->h_blk->op.aux0;
+    if (T == 0) return fail(h, DG_ERR_DATA, "compute_block_size: first batch contains no edges");
+    const uint64_t rounded = (n_edges + T / 2) / T;
+    if ((rc = create_pool(h, (uint32_t)std::max<uint64_t>(1, rounded))) != DG_OK) return rc;
+    OpState& op = h->h_blk->op;
+    op.err_index = ~0ull;
+    op.aux0 = 0;
+    DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
+  }
+  BatchView b{nullptr, d_dst, nullptr, run_start};
+  enqueue_plan_append(h, b, V, n_edges, run_deg, run_tail);
+  return op_end(h);
+}
+
+int dg_insert_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
+                        const uint32_t* destinations, uint64_t n_edges, int mem) {
+  return insert_csr_impl(h, offsets, n_offsets, destinations, n_edges, mem, false);
+}
+
+int dg_bulk_init_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
+                     const uint32_t* destinations, uint64_t n_edges, int mem) {
+  return insert_csr_impl(h, offsets, n_offsets, destinations, n_edges, mem, true);
+}
+
+// ---- delete -------------------------------------------------------------------
+int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                        int mem) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (n == 0) return DG_OK;
+  if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
+  const bool no_pool = h->B == 0;  // no pool yet => no edges: only validation can have an effect
+  const int passes = make_sort_plan(bits_for(h->dst_limit() - 1), bits_for(h->size - 1)).passes;
+  WsSizer sz;
+  if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
+  sz.add<unsigned long long>(n); sz.add<unsigned long long>(n);
+  if (!no_pool) sz.total += delete_tail_ws(h, n, passes);
+  int rc = ws_reserve(h, sz.total);
+  if (rc != DG_OK) return rc;
+  const uint32_t *d_src, *d_dst;
+  if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
+  if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
+  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  GraphView g = view(h);
+  unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
+  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
+  pack_coo_kernel<kPackDelete, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op());
+  h->launches += 1;
+  if (no_pool) return op_end(h);
+  return delete_sorted_tail(h, keys, keys_alt, n);
+}
+
+int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
+                        const uint32_t* destinations, uint64_t n_edges, int mem) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (n_offsets != h->size + 1)
+    return fail(h, DG_ERR_DATA, "csr batch: offsets length " + std::to_string(n_offsets) +
+                                    " does not match vertex count " + std::to_string(h->size) + " + 1");
+  if (n_edges >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  const uint64_t V = h->size;
+  const uint64_t n = n_edges;
+  const int passes = V ? make_sort_plan(bits_for(h->dst_limit() - 1), bits_for(V - 1)).passes : 0;
+  WsSizer sz;
+  if (mem == DG_MEM_HOST) { sz.add<unsigned long long>(n_offsets); sz.add<uint32_t>(n); }
+  sz.add<uint32_t>(V + 2);
+  sz.add<unsigned long long>(n + 1); sz.add<unsigned long long>(n + 1);
+  if (h->B) sz.total += delete_tail_ws(h, std::max<uint64_t>(n, 1), passes);
+  int rc = ws_reserve(h, sz.total);
+  if (rc != DG_OK) return rc;
+  const unsigned long long* d_off;
+  const uint32_t* d_dst;
+  if ((rc = stage_in(h, reinterpret_cast<const unsigned long long*>(offsets), n_offsets, mem, &d_off)) != DG_OK) return rc;
+  if ((rc = stage_in(h, destinations, n, mem, &d_dst)) != DG_OK) return rc;
+  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  GraphView g = view(h);
+  uint32_t* run_start = ws_alloc<uint32_t>(h, V + 2);
+  csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
+      g, d_off, (uint32_t)n_offsets, n, /*check_dead_source=*/0, run_start, h->d_op());
+  h->launches += 1;
+  if (n > 0) {
+    validate_dsts_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(g, d_dst, (uint32_t)n, h->d_op());
+    h->launches += 1;
+  }
+  if (n == 0 || V == 0 || h->B == 0) return op_end(h);
+  unsigned long long* keys = ws_alloc<unsigned long long>(h, n + 1);
+  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n + 1);
+  csr_expand_kernel<<<grid_for(h, (n + 31) / 32, 8), 256, 0, h->stream>>>(
+      run_start, (uint32_t)V, d_dst, (uint32_t)n, keys, h->d_op());
+  h->launches += 1;
+  return delete_sorted_tail(h, keys, keys_alt, n);
+}
+
+// ---- query ---------------------------------------------------------------------
+int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                   uint8_t* out, int mem) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (n == 0) return DG_OK;
+  if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  if (h->B == 0 || h->size == 0) {  // no edges stored: every answer is false
+    if (mem == DG_MEM_HOST) std::memset(out, 0, n);
+    else DG_CUDA(h, cudaMemsetAsync(out, 0, n, h->stream));
+    return DG_OK;
+  }
+  SortPlan plan = make_sort_plan(bits_for(h->dst_limit()), bits_for(h->size));
+  WsSizer sz;
+  if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); sz.add<uint8_t>(n); }
+  sz.add<unsigned long long>(n); sz.add<unsigned long long>(n);
+  sz.add<uint32_t>(n); sz.add<uint32_t>(n);
+  sz.total += sort_ws_bytes(n, plan.passes);
+  sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1);
+  sz.total += scan_ws_bytes(n) + enumerate_ws(h, n);
+  sz.add<uint8_t>(n);
+  int rc = ws_reserve(h, sz.total);
+  if (rc != DG_OK) return rc;
+  const uint32_t *d_src, *d_dst;
+  if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
+  if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
+  uint8_t* d_out = (mem == DG_MEM_HOST) ? ws_alloc<uint8_t>(h, n) : out;
+  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  GraphView g = view(h);
+  unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
+  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
+  uint32_t* idx = ws_alloc<uint32_t>(h, n);
+  uint32_t* idx_alt = ws_alloc<uint32_t>(h, n);
+  pack_coo_kernel<kPackQuery, true><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      g, d_src, d_dst, (uint32_t)n, keys, idx, h->d_op());
+  h->launches += 1;
+  sort_keys(h, &keys, &keys_alt, &idx, &idx_alt, n, plan);
+  uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
+  launch_scan(h, n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
+              RunsFin{run_start, h->d_op(), (uint32_t)n});
+  BatchView b{keys, nullptr, run_src, run_start};
+  Worklist w = enqueue_enumerate(h, b, n, /*check_alive=*/1);
+  uint8_t* hit = ws_alloc<uint8_t>(h, n);
+  cudaMemsetAsync(hit, 0, n, h->stream);
+  const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
+  match_kernel<false><<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+      g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, nullptr, hit, h->d_op());
+  query_scatter_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(hit, idx, (uint32_t)n, d_out, h->d_op());
+  h->launches += 2;
+  if (mem == DG_MEM_HOST)
+    DG_CUDA(h, cudaMemcpyAsync(out, d_out, n, cudaMemcpyDeviceToHost, h->stream));
+  return op_end(h);
+}
+
+// ---- export / observables ---------------------------------------------------------
+int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
+                  uint64_t n_dst_capacity, int sorted, int mem) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  const uint64_t V = h->size;
+  // phase 1: degrees -> offsets
+  WsSizer sz1;
+  sz1.add<unsigned long long>(V + 1);
+  sz1.total += scan_ws_bytes(std::max<uint64_t>(V, 1));
+  int rc = ws_reserve(h, sz1.total);
+  if (rc != DG_OK) return rc;
+  if ((rc = op_begin(h, V, V)) != DG_OK) return rc;
+  unsigned long long* d_off = (mem == DG_MEM_DEVICE) ? reinterpret_cast<unsigned long long*>(offsets)
+                                                     : ws_alloc<unsigned long long>(h, V + 1);
+  uint64_t total = 0;
+  if (V == 0) {
+    DG_CUDA(h, cudaMemsetAsync(d_off, 0, sizeof(unsigned long long), h->stream));
+    if ((rc = op_end(h)) != DG_OK) return rc;
+  } else {
+    launch_scan(h, V, d_n_input(h), DegIn{h->deg}, OffsetsOut{d_off}, OffsetsFin{d_off, V, h->d_op()});
+    if ((rc = op_end(h)) != DG_OK) return rc;
+    total = h->h_blk->op.aux0;
+  }
+  if (mem == DG_MEM_HOST)
+    DG_CUDA(h, cudaMemcpy(offsets, d_off, (V + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  if (destinations == nullptr || total == 0) return DG_OK;
+  if (total > n_dst_capacity)
+    return fail(h, DG_ERR_DATA, "export: destinations capacity " + std::to_string(n_dst_capacity) +
+                                    " < stored entries " + std::to_string(total));
+  if (total >= (1ull << 32)) return fail(h, DG_ERR_ENGINE, "export: more than 2^32 entries");
+  // phase 2: enumerate every chain and copy
+  SortPlan plan = make_sort_plan(bits_for(h->dst_limit() - 1), bits_for(V - 1));
+  WsSizer sz;
+  sz.add<unsigned long long>(V + 1);
+  sz.total += enumerate_ws(h, V);
+  if (mem == DG_MEM_HOST) sz.add<uint32_t>(total);
+  if (sorted) { sz.add<unsigned long long>(total); sz.add<unsigned long long>(total); sz.total += sort_ws_bytes(total, plan.passes); }
+  // (host path: offsets were copied to the caller; re-uploaded after the workspace is re-laid out)
+  if ((rc = ws_reserve(h, sz.total)) != DG_OK) return rc;
+  unsigned long long* d_off2 = d_off;
+  if (mem == DG_MEM_HOST) {
+    d_off2 = ws_alloc<unsigned long long>(h, V + 1);
+    DG_CUDA(h, cudaMemcpyAsync(d_off2, offsets, (V + 1) * sizeof(unsigned long long), cudaMemcpyHostToDevice, h->stream));
+  }
+  if ((rc = op_begin(h, V, V)) != DG_OK) return rc;
+  GraphView g = view(h);
+  BatchView b{nullptr, nullptr, nullptr, nullptr};
+  Worklist w = enqueue_enumerate(h, b, V, /*check_alive=*/0);
+  uint32_t* d_dst = (mem == DG_MEM_HOST) ? ws_alloc<uint32_t>(h, total) : destinations;
+  const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
+  if (!sorted) {
+    export_copy_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+        g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, d_off2, d_dst, nullptr, h->d_op());
+    h->launches += 1;
+  } else {
+    unsigned long long* keys = ws_alloc<unsigned long long>(h, total);
+    unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, total);
+    export_copy_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+        g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, d_off2, nullptr, keys, h->d_op());
+    h->launches += 1;
+    sort_keys(h, &keys, &keys_alt, nullptr, nullptr, total, plan);
+    keys_low_kernel<<<grid_for(h, total, 256 * 4), 256, 0, h->stream>>>(keys, total, d_dst);
+    h->launches += 1;
+  }
+  if (mem == DG_MEM_HOST)
+    DG_CUDA(h, cudaMemcpyAsync(destinations, d_dst, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+  return op_end(h);
+}
+
+int dg_degrees(dg_graph* h, uint64_t* out, int mem) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  const uint64_t V = h->size;
+  if (V == 0) return DG_OK;
+  int rc = ws_reserve(h, aligned(V * 8));
+  if (rc != DG_OK) return rc;
+  unsigned long long* d = (mem == DG_MEM_DEVICE) ? reinterpret_cast<unsigned long long*>(out)
+                                                 : ws_alloc<unsigned long long>(h, V);
+  degrees_kernel<<<grid_for(h, V, 256 * 4), 256, 0, h->stream>>>(h->deg, (uint32_t)V, d);
+  if (mem == DG_MEM_HOST)
+    DG_CUDA(h, cudaMemcpyAsync(out, d, V * 8, cudaMemcpyDeviceToHost, h->stream));
+  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  return DG_OK;
+}
+
+int dg_digest(dg_graph* h, uint64_t* out_digest, uint64_t* out_entries) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  const uint64_t V = h->size;
+  if (out_digest) *out_digest = 0;
+  if (out_entries) *out_entries = 0;
+  if (V == 0 || h->B == 0) return DG_OK;
+  int rc = ws_reserve(h, enumerate_ws(h, V));
+  if (rc != DG_OK) return rc;
+  if ((rc = op_begin(h, V, V)) != DG_OK) return rc;
+  GraphView g = view(h);
+  BatchView b{nullptr, nullptr, nullptr, nullptr};
+  Worklist w = enqueue_enumerate(h, b, V, 0);
+  const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
+  digest_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(g, w.wl_off, w.wl_handle, w.wl_run,
+                                                                 w.run_deg, h->d_op());
+  h->launches += 1;
+  if ((rc = op_end(h)) != DG_OK) return rc;
+  if (out_digest) *out_digest = h->h_blk->op.aux0;
+  if (out_entries) *out_entries = h->h_blk->op.aux1;
+  return DG_OK;
+}
+
+// ---- vertex updates ------------------------------------------------------------------
+int dg_insert_vertices(dg_graph* h, uint64_t count) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (count == 0) return DG_OK;  // InsertVertices.ZeroIsANoop
+  const uint64_t new_size = h->size + count;
+  if (new_size >= 0xFFFFFFFFull || new_size < h->size)
+    return fail(h, DG_ERR_ENGINE, "vertex dictionary: vertex ids are 32-bit");
+  if (new_size > h->capacity) {
+    // doubling migration (vertex_dictionary.hpp:53-71): target = closest_pow2(size + count)
+    const uint64_t target = std::bit_ceil(new_size);
+    const size_t words_new = (target + 31) / 32, words_old = (h->capacity + 31) / 32;
+    uint32_t *nh = nullptr, *nt = nullptr, *nd = nullptr, *na = nullptr;
+    if (cudaMalloc(&nh, target * 4) != cudaSuccess || cudaMalloc(&nt, target * 4) != cudaSuccess ||
+        cudaMalloc(&nd, target * 4) != cudaSuccess || cudaMalloc(&na, words_new * 4) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(nh); cudaFree(nt); cudaFree(nd); cudaFree(na);
+      cudaGetLastError();
+      return fail(h, DG_ERR_ENGINE, "vertex dictionary: arena cannot host capacity " + std::to_string(target));
+    }
+    cudaMemsetAsync(nh, 0xFF, target * 4, h->stream);
+    cudaMemsetAsync(nt, 0xFF, target * 4, h->stream);
+    cudaMemsetAsync(nd, 0, target * 4, h->stream);
+    cudaMemsetAsync(na, 0, words_new * 4, h->stream);
+    cudaMemcpyAsync(nh, h->head, h->capacity * 4, cudaMemcpyDeviceToDevice, h->stream);
+    cudaMemcpyAsync(nt, h->tail, h->capacity * 4, cudaMemcpyDeviceToDevice, h->stream);
+    cudaMemcpyAsync(nd, h->deg, h->capacity * 4, cudaMemcpyDeviceToDevice, h->stream);
+    cudaMemcpyAsync(na, h->alive, words_old * 4, cudaMemcpyDeviceToDevice, h->stream);
+    DG_CUDA(h, cudaStreamSynchronize(h->stream));
+    cudaFree(h->head); cudaFree(h->tail); cudaFree(h->deg); cudaFree(h->alive);
+    h->head = nh; h->tail = nt; h->deg = nd; h->alive = na;
+    h->capacity = target;
+    h->alive_host.resize((target + 63) / 64, 0ull);
+  }
+  GraphView g = view(h);
+  vertex_init_kernel<<<grid_for(h, count, 256), 256, 0, h->stream>>>(g, (uint32_t)h->size, (uint32_t)count);
+  for (uint64_t v = h->size; v < new_size; ++v) h->alive_host[v >> 6] |= 1ull << (v & 63);
+  h->size = new_size;
+  h->alive_count += count;
+  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  return DG_OK;
+}
+
+int dg_delete_vertices(dg_graph* h, const uint32_t* ids, uint64_t n, uint32_t* skipped,
+                       uint64_t* n_skipped) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  uint64_t ns = 0;
+  std::vector<uint32_t> winners;
+  winners.reserve(n);
+  // encounter-order semantics of graph.hpp:255-259: dead / unknown / repeated ids are skipped
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t v = ids[i];
+    if (!h->alive_h(v)) {
+      if (skipped) skipped[ns] = v;
+      ++ns;
+      continue;
+    }
+    h->alive_host[v >> 6] &= ~(1ull << (v & 63));
+    winners.push_back(v);
+  }
+  if (n_skipped) *n_skipped = ns;
+  if (winners.empty()) return DG_OK;
+  h->alive_count -= winners.size();
+  int rc = ws_reserve(h, aligned(winners.size() * 4));
+  if (rc != DG_OK) return rc;
+  uint32_t* d_ids = ws_alloc<uint32_t>(h, winners.size());
+  DG_CUDA(h, cudaMemcpyAsync(d_ids, winners.data(), winners.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  if ((rc = op_begin(h, winners.size(), 0)) != DG_OK) return rc;
+  GraphView g = view(h);
+  if (h->B == 0) g.reclaim = 0;
+  retire_vertices_kernel<<<grid_for(h, winners.size(), 8), 256, 0, h->stream>>>(
+      g, d_ids, (uint32_t)winners.size(), h->d_op());
+  h->launches += 1;
+  return op_end(h);
+}
+
+// ---- observables -----------------------------------------------------------------------
+uint32_t dg_block_size(const dg_graph* h) { return h ? h->B : 0; }
+uint64_t dg_logical_size(const dg_graph* h) { return h ? h->size : 0; }
+uint64_t dg_vertex_capacity(const dg_graph* h) { return h ? h->capacity : 0; }
+uint64_t dg_alive_vertices(const dg_graph* h) { return h ? h->alive_count : 0; }
+uint64_t dg_active_edges(const dg_graph* h) { return h ? h->active_edges : 0; }
+int dg_vertex_alive(const dg_graph* h, uint32_t v) { return h && h->alive_h(v) ? 1 : 0; }
+
+int dg_stats_get(dg_graph* h, dg_stats* out) {
+  if (!h || !out) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  std::memset(out, 0, sizeof(*out));
+  int rc;
+  if (h->size > 0 && h->B > 0) {
+    if ((rc = op_begin(h, h->size, 0)) != DG_OK) return rc;
+    stats_kernel<<<grid_for(h, h->size, 256), 256, 0, h->stream>>>(view(h), h->d_op());
+    if ((rc = op_end(h)) != DG_OK) return rc;
+    out->adjacency_blocks = h->h_blk->op.aux0;
+    out->max_degree = h->h_blk->op.aux1;
+  }
+  out->logical_size = h->size;
+  out->capacity = h->capacity;
+  out->alive_vertices = h->alive_count;
+  out->active_edges = h->active_edges;
+  out->occupied_slots = h->active_edges;
+  out->hole_slots = 0;
+  out->pool_blocks_created = h->NB;
+  out->pool_blocks_in_use = h->NB ? h->blocks_in_use() : 0;
+  out->pool_queue_size = h->rear - h->front;
+  out->queue_front = h->front;
+  out->queue_rear = h->rear;
+  out->block_size = h->B;
+  return DG_OK;
+}
+
+int dg_memory_get(const dg_graph* h, dg_memory* out) {
+  if (!h || !out) return DG_ERR_DATA;
+  out->dictionary_bytes = h->capacity * 4 + (h->capacity + 31) / 32 * 4;
+  out->sentinel_bytes = h->capacity * 8;
+  out->pool_bytes = h->NB ? h->blocks_in_use() * ((uint64_t)h->B * 4 + 4) : 0;
+  out->queue_bytes = h->NB * 4;
+  out->pool_reserved_bytes = h->NB * ((uint64_t)h->B * 4 + 4);
+  out->workspace_bytes = h->ws.cap + h->mv_cap * 12;
+  return DG_OK;
+}
+
+int dg_last_op_report(const dg_graph* h, dg_op_report* out) {
+  if (!h || !out) return DG_ERR_DATA;
+  *out = h->report;
+  return DG_OK;
+}
+
+void* dg_stream(const dg_graph* h) { return h ? (void*)h->stream : nullptr; }
+
+int dg_synchronize(dg_graph* h) {
+  if (!h) return DG_ERR_DATA;
+  cudaSetDevice(h->device);
+  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  return DG_OK;
+}
+
+// ---- input-side helpers -------------------------------------------------------------------
+int dg_compute_block_size_coo(dg_graph* h, const uint32_t* src, uint64_t n, int mem,
+                              uint32_t* out_block_size) {
+  if (!h || !out_block_size) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (n == 0) return fail(h, DG_ERR_DATA, "compute_block_size: first batch contains no edges");
+  if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  SortPlan plan = make_sort_plan(0, 32);
+  WsSizer sz;
+  if (mem == DG_MEM_HOST) sz.add<uint32_t>(n);
+  sz.add<unsigned long long>(n); sz.add<unsigned long long>(n);
+  sz.total += sort_ws_bytes(n, plan.passes);
+  sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1);
+  sz.total += scan_ws_bytes(n);
+  int rc = ws_reserve(h, sz.total);
+  if (rc != DG_OK) return rc;
+  const uint32_t* d_src;
+  if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
+  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  GraphView g = view(h);
+  g.size = 0xFFFFFFFFu;
+  g.dst_limit = 0xFFFFFFFFu;
+  unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
+  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
+  pack_coo_kernel<kPackQuery, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      g, d_src, d_src, (uint32_t)n, keys, nullptr, h->d_op());
+  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
+  uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
+  launch_scan(h, n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
+              RunsFin{run_start, h->d_op(), (uint32_t)n});
+  if ((rc = op_end(h)) != DG_OK) return rc;
+  const uint64_t T = h->h_blk->op.n_runs;
+  const uint64_t rounded = (n + T / 2) / T;
+  *out_block_size = (uint32_t)std::max<uint64_t>(1, rounded);
+  return DG_OK;
+}
+
+int dg_gen_rmat(dg_graph* h, uint32_t scale, uint64_t seed, uint64_t first_index, uint64_t n,
+                uint32_t thr_a, uint32_t thr_ab, uint32_t thr_abc, uint32_t* src_dev,
+                uint32_t* dst_dev) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (scale == 0 || scale > 32) return fail(h, DG_ERR_DATA, "rmat: scale must be in [1, 32]");
+  if (n == 0) return DG_OK;
+  rmat_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(scale, seed, first_index, n, thr_a,
+                                                              thr_ab, thr_abc, src_dev, dst_dev);
+  DG_CUDA(h, cudaGetLastError());
+  return DG_OK;
+}
+
+int dg_coo_to_csr(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, int mem,
+                  uint64_t vertex_count, uint64_t* offsets_dev, uint32_t* destinations_dev) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  if (vertex_count == 0 || vertex_count >= 0xFFFFFFFFull)
+    return fail(h, DG_ERR_DATA, "coo_to_csr: bad vertex count");
+  SortPlan plan = make_sort_plan(0, bits_for(vertex_count - 1));
+  WsSizer sz;
+  if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
+  sz.add<unsigned long long>(n + 1); sz.add<unsigned long long>(n + 1);
+  sz.total += sort_ws_bytes(std::max<uint64_t>(n, 1), plan.passes);
+  int rc = ws_reserve(h, sz.total);
+  if (rc != DG_OK) return rc;
+  const uint32_t *d_src, *d_dst;
+  if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
+  if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
+  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  GraphView g = view(h);
+  g.size = (uint32_t)vertex_count;
+  g.dst_limit = 0xFFFFFFFFu;
+  unsigned long long* keys = ws_alloc<unsigned long long>(h, n + 1);
+  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n + 1);
+  if (n > 0) {
+    pack_coo_kernel<kPackDelete, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+        g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op());
+    sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
+  }
+  keys_to_offsets_kernel<<<grid_for(h, n + 1, 256), 256, 0, h->stream>>>(
+      keys, (uint32_t)n, vertex_count, reinterpret_cast<unsigned long long*>(offsets_dev),
+      destinations_dev, h->d_op());
+  return op_end(h);
+}
+
+uint32_t dg_owner_perm(uint32_t v, uint32_t bits) { return owner_perm(v, bits); }
+uint32_t dg_owner_perm_inv(uint32_t p, uint32_t bits) { return owner_perm_inv(p, bits); }
+
+int dg_set_dst_limit(dg_graph* h, uint64_t limit) {
+  if (!h) return DG_ERR_DATA;
+  if (limit > 0xFFFFFFFFull) return fail(h, DG_ERR_DATA, "dst limit must fit 32 bits");
+  h->dst_limit_override = limit;
+  return DG_OK;
+}
+
+int dg_route_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t world,
+                 uint32_t bits, uint64_t vertex_count, uint32_t* out_src_local, uint32_t* out_dst,
+                 uint32_t* out_index, uint64_t* counts_host) {
+  if (!h) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (world == 0 || world > 65536) return fail(h, DG_ERR_DATA, "route: world must be in [1, 65536]");
+  if (bits > 32 || vertex_count > (bits >= 32 ? (1ull << 32) : (1ull << bits)))
+    return fail(h, DG_ERR_DATA, "route: vertex_count exceeds 2^bits");
+  if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  for (uint32_t w = 0; w < world; ++w) counts_host[w] = 0;
+  if (n == 0) return DG_OK;
+  SortPlan plan = make_sort_plan(0, bits_for(world - 1));
+  WsSizer sz;
+  sz.add<unsigned long long>(n); sz.add<unsigned long long>(n);
+  sz.total += sort_ws_bytes(n, std::max(plan.passes, 1));
+  sz.add<unsigned long long>(world + 2);
+  int rc = ws_reserve(h, sz.total);
+  if (rc != DG_OK) return rc;
+  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
+  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
+  unsigned long long* d_counts = ws_alloc<unsigned long long>(h, world + 2);
+  route_keys_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      src, (uint32_t)n, world, bits, (uint32_t)std::min<uint64_t>(vertex_count, 0xFFFFFFFFull), keys, h->d_op());
+  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
+  route_gather_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      keys, src, dst, (uint32_t)n, world, bits, out_src_local, out_dst, out_index, d_counts, h->d_op());
+  h->launches += 2;
+  std::vector<unsigned long long> ends(world + 1);
+  DG_CUDA(h, cudaMemcpyAsync(ends.data(), d_counts, (world + 1) * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, h->stream));
+  if ((rc = op_end(h)) != DG_OK) return rc;
+  for (uint32_t w = 0; w < world; ++w) counts_host[w] = ends[w + 1] - ends[w];
+  return DG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,405 @@
+// dg_device.cuh — device-side building blocks for libdyngraph_b200 (sm_100a).
+//
+//  * status words shared between kernels of one op (validate-then-mutate
+//    without a host round trip: every mutating kernel starts with
+//    `if (op->err) return;`),
+//  * a single-pass decoupled-look-back prefix scan with pluggable input /
+//    output functors (used for run detection, batch planning, work-list
+//    offsets, degree -> CSR offsets),
+//  * a hand-written Onesweep-style LSD radix sort for 64-bit keys with an
+//    optional 32-bit payload (8-bit digits, one histogram pass, one
+//    scatter pass per digit with decoupled look-back across tiles).
+//
+// Nothing here is a port of reference code: the CPU reference has no device
+// code at all (kernel inventory).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dg {
+
+constexpr uint32_t kNull = 0xFFFFFFFFu;   // reference: types.hpp:16-17
+constexpr uint32_t kTomb = 0xFFFFFFFFu;   // in-slot tombstone; never a valid id
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// ---- error detail codes (op->err_detail) --------------------------------
+enum ErrDetail : uint32_t {
+  kErrNone = 0,
+  kErrSrcRange = 1,       // source id >= logical size
+  kErrDstRange = 2,       // csr.hpp:67-72
+  kErrDeadSource = 3,     // graph.hpp:322-327
+  kErrOffsetsStart = 4,   // csr.hpp:54-56
+  kErrOffsetsMonotone = 5,// csr.hpp:57-61
+  kErrOffsetsEnd = 6,     // csr.hpp:62-66
+  kErrPoolUnderflow = 7,  // block_pool.hpp:177-189
+  kErrScratch = 8,        // internal: compaction scratch too small, host retries
+};
+
+// Persistent device-resident scalars of one graph (the queue cursors use the
+// reference's unwrapped 64-bit coordinates, block_pool.hpp:31-34).
+struct DeviceState {
+  unsigned long long front;         // next queue position to serve
+  unsigned long long rear;          // one past the last pushed handle
+  unsigned long long active_edges;  // graph.hpp:100
+  unsigned long long pad;
+};
+
+// Transient per-op words; zeroed by the host before every op.
+struct OpState {
+  uint32_t err;            // 0 / DG_ERR_DATA / DG_ERR_ENGINE
+  uint32_t err_detail;
+  unsigned long long err_index;   // smallest offending index (atomicMin)
+  unsigned long long n_runs;      // T
+  unsigned long long n_units;     // append work units
+  unsigned long long total_need;  // fresh blocks this batch pops
+  unsigned long long front_old;   // queue front before the pop
+  unsigned long long wl_blocks;   // blocks in touched chains (delete/query/export)
+  unsigned long long slots;       // slots in touched chains
+  unsigned long long matched;     // delete: entries removed; query: hits
+  unsigned long long moves;       // compaction moves (bound, then exact)
+  unsigned long long pushed;      // blocks returned to the ring
+  unsigned long long aux0;        // op-specific
+  unsigned long long aux1;
+  unsigned long long pad[3];
+};
+
+__device__ __forceinline__ void set_error(OpState* op, uint32_t code, uint32_t detail,
+                                          unsigned long long index) {
+  // Smallest index wins so the report is deterministic; the class of the
+  // first reporter sticks (all data checks of one op share a class).
+  atomicCAS(&op->err, 0u, code);
+  atomicCAS(&op->err_detail, 0u, detail);
+  atomicMin(&op->err_index, index);
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ bool bit_test(const uint32_t* __restrict__ bits, uint32_t v) {
+  return (bits[v >> 5] >> (v & 31)) & 1u;
+}
+
+// ===========================================================================
+// Decoupled look-back scan
+// ===========================================================================
+// Tile status word: [63:62] flag, [61:0] value.
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+constexpr unsigned long long kFlagMask = 3ull << 62;
+constexpr unsigned long long kValMask = ~kFlagMask;
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// Scratch layout for one scan launch: [0] ticket counter, [1..] tile status.
+__host__ __device__ inline size_t scan_scratch_words(uint64_t n_max) {
+  return 2 + (n_max + kScanTile - 1) / kScanTile;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Exclusive scan of In(i) over i in [0, *n_ptr).  Out(i, exclusive, value) is
+// called for every element, Fin(total) once by the last tile.  Grid must
+// cover ceil(n_bound / kScanTile) tiles where n_bound >= *n_ptr; surplus
+// tiles exit.  `scratch` must be zeroed before the launch.
+template <class In, class Out, class Fin>
+__global__ void __launch_bounds__(kScanThreads)
+scan_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* scratch,
+            const OpState* __restrict__ op_guard, In in, Out out, Fin fin) {
+  if (op_guard != nullptr && op_guard->err != 0) return;
+  __shared__ unsigned long long s_warp[kScanThreads / 32];
+  __shared__ unsigned long long s_tile_excl;
+  __shared__ unsigned int s_tile;
+  const unsigned long long n = *n_ptr;
+  if (threadIdx.x == 0) s_tile = atomicAdd(reinterpret_cast<unsigned int*>(scratch), 1u);
+  __syncthreads();
+  const unsigned int tile = s_tile;
+  const unsigned long long num_tiles = (n + kScanTile - 1) / kScanTile;
+  if (tile >= num_tiles) return;
+  unsigned long long* status = scratch + 2;
+
+  // blocked arrangement: thread t owns items [t*ITEMS, t*ITEMS+ITEMS)
+  const unsigned long long base = (unsigned long long)tile * kScanTile +
+                                  (unsigned long long)threadIdx.x * kScanItems;
+  unsigned long long v[kScanItems];
+  unsigned long long thread_sum = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const unsigned long long i = base + j;
+    v[j] = (i < n) ? in(i) : 0ull;
+    thread_sum += v[j];
+  }
+  // warp inclusive scan of thread sums
+  unsigned long long incl = thread_sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    unsigned long long t = __shfl_up_sync(kFull, incl, d);
+    if (lane_id() >= d) incl += t;
+  }
+  const int warp = threadIdx.x >> 5;
+  if (lane_id() == 31) s_warp[warp] = incl;
+  __syncthreads();
+  unsigned long long warp_excl = 0, tile_sum = 0;
+#pragma unroll
+  for (int w = 0; w < kScanThreads / 32; ++w) {
+    const unsigned long long s = s_warp[w];
+    if (w < warp) warp_excl += s;
+    tile_sum += s;
+  }
+  // publish + look back (thread 0 .. 31 of warp 0 cooperate)
+  if (warp == 0) {
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      if (lane_id() == 0) st_volatile_u64(&status[0], kFlagPre | (tile_sum & kValMask));
+    } else {
+      if (lane_id() == 0) st_volatile_u64(&status[tile], kFlagAgg | (tile_sum & kValMask));
+      long long look = (long long)tile - 1;
+      while (true) {
+        const long long idx = look - lane_id();
+        unsigned long long w = (idx >= 0) ? ld_volatile_u64(&status[idx]) : kFlagPre;
+        // wait until every polled predecessor published something
+        while (__any_sync(kFull, (w & kFlagMask) == 0)) {
+          w = (idx >= 0) ? ld_volatile_u64(&status[idx]) : kFlagPre;
+        }
+        const unsigned pre_mask = __ballot_sync(kFull, (w & kFlagMask) == kFlagPre);
+        unsigned long long contrib;
+        if (pre_mask) {
+          const int first = __ffs(pre_mask) - 1;  // nearest predecessor with a full prefix
+          contrib = (lane_id() <= first && idx >= 0) ? (w & kValMask) : 0ull;
+        } else {
+          contrib = w & kValMask;
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(kFull, contrib, d);
+        excl += contrib;
+        if (pre_mask) break;
+        look -= 32;
+      }
+      if (lane_id() == 0)
+        st_volatile_u64(&status[tile], kFlagPre | ((excl + tile_sum) & kValMask));
+    }
+    if (lane_id() == 0) s_tile_excl = excl;
+  }
+  __syncthreads();
+  unsigned long long run = s_tile_excl + warp_excl + (incl - thread_sum);
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const unsigned long long i = base + j;
+    if (i < n) out(i, run, v[j]);
+    run += v[j];
+  }
+  if (tile == num_tiles - 1 && threadIdx.x == kScanThreads - 1) fin(run);
+}
+
+// ===========================================================================
+// Onesweep radix sort (u64 keys, optional u32 values)
+// ===========================================================================
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys
+constexpr int kRadix = 256;
+constexpr int kMaxPasses = 8;
+
+struct SortPlan {
+  int passes;
+  int shift[kMaxPasses];
+  int bits[kMaxPasses];
+};
+
+__host__ __device__ inline size_t sort_tiles(uint64_t n) { return (n + kSortTile - 1) / kSortTile; }
+
+// Global histogram of every pass in one read of the keys.
+// hist layout: [pass][256] u32.
+__global__ void __launch_bounds__(256)
+sort_hist_kernel(const unsigned long long* __restrict__ keys, uint64_t n, SortPlan plan,
+                 unsigned int* __restrict__ hist, const OpState* __restrict__ op_guard) {
+  if (op_guard != nullptr && op_guard->err != 0) return;
+  __shared__ unsigned int s_hist[kMaxPasses * kRadix];
+  for (int i = threadIdx.x; i < plan.passes * kRadix; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+#pragma unroll
+    for (int p = 0; p < kMaxPasses; ++p) {
+      if (p < plan.passes) {
+        const unsigned d = (unsigned)(k >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u);
+        atomicAdd(&s_hist[p * kRadix + d], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < plan.passes * kRadix; i += blockDim.x) {
+    const unsigned c = s_hist[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
+}
+
+// Exclusive scan of each pass's 256 bins (one block, 256 threads).
+__global__ void __launch_bounds__(kRadix)
+sort_scan_hist_kernel(unsigned int* __restrict__ hist, int passes,
+                      const OpState* __restrict__ op_guard) {
+  if (op_guard != nullptr && op_guard->err != 0) return;
+  __shared__ unsigned int s_warp[kRadix / 32];
+  for (int p = 0; p < passes; ++p) {
+    const unsigned c = hist[p * kRadix + threadIdx.x];
+    unsigned incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      unsigned t = __shfl_up_sync(kFull, incl, d);
+      if (lane_id() >= d) incl += t;
+    }
+    if (lane_id() == 31) s_warp[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    unsigned warp_excl = 0;
+    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) warp_excl += s_warp[w];
+    hist[p * kRadix + threadIdx.x] = warp_excl + incl - c;
+    __syncthreads();
+  }
+}
+
+// One scatter pass.  status: [0] ticket, then per tile 256 u64 words.
+// Must be zeroed before the launch.
+template <bool kHasValues>
+__global__ void __launch_bounds__(kSortThreads)
+sort_pass_kernel(const unsigned long long* __restrict__ keys_in,
+                 unsigned long long* __restrict__ keys_out,
+                 const unsigned int* __restrict__ vals_in, unsigned int* __restrict__ vals_out,
+                 uint64_t n, int shift, int bits, const unsigned int* __restrict__ digit_base,
+                 unsigned long long* status, const OpState* __restrict__ op_guard) {
+  if (op_guard != nullptr && op_guard->err != 0) return;
+  constexpr int kWarps = kSortThreads / 32;
+  __shared__ unsigned int s_cnt[kWarps][kRadix];  // per-warp digit counts -> exclusive offsets
+  __shared__ unsigned long long s_goff[kRadix];   // global base of each digit for this tile
+  __shared__ unsigned int s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(reinterpret_cast<unsigned int*>(status), 1u);
+  for (int i = threadIdx.x; i < kWarps * kRadix; i += kSortThreads) (&s_cnt[0][0])[i] = 0;
+  __syncthreads();
+  const unsigned int tile = s_tile;
+  unsigned long long* tile_status = status + 2;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const unsigned dmask = (1u << bits) - 1u;
+  const uint64_t warp_base = (uint64_t)tile * kSortTile + (uint64_t)warp * (32 * kSortItems);
+
+  unsigned long long key[kSortItems];
+  unsigned int rank[kSortItems];
+  // warp-striped load keeps the stable order (warp, row, lane)
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const uint64_t i = warp_base + (uint64_t)j * 32 + lane;
+    key[j] = (i < n) ? keys_in[i] : ~0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const uint64_t i = warp_base + (uint64_t)j * 32 + lane;
+    const bool valid = i < n;
+    const unsigned d = (unsigned)(key[j] >> shift) & dmask;
+    const unsigned peers = __match_any_sync(kFull, valid ? d : 0xFFFFFFFFu);
+    const int leader = __ffs(peers) - 1;
+    unsigned before = 0;
+    if (valid && lane == leader) {
+      before = s_cnt[warp][d];
+      s_cnt[warp][d] = before + __popc(peers);
+    }
+    before = __shfl_sync(kFull, before, leader);
+    rank[j] = before + __popc(peers & lt_mask);
+    __syncwarp();
+  }
+  __syncthreads();
+  // thread d owns digit d: exclusive scan over warps, tile count, look-back
+  {
+    const int d = threadIdx.x;
+    unsigned run = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const unsigned c = s_cnt[w][d];
+      s_cnt[w][d] = run;
+      run += c;
+    }
+    const unsigned long long tile_cnt = run;
+    unsigned long long* my = tile_status + (size_t)tile * kRadix + d;
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      st_volatile_u64(my, kFlagPre | tile_cnt);
+    } else {
+      st_volatile_u64(my, kFlagAgg | tile_cnt);
+      long long look = (long long)tile - 1;
+      while (true) {
+        unsigned long long w = ld_volatile_u64(tile_status + (size_t)look * kRadix + d);
+        while ((w & kFlagMask) == 0)
+          w = ld_volatile_u64(tile_status + (size_t)look * kRadix + d);
+        excl += w & kValMask;
+        if ((w & kFlagMask) == kFlagPre) break;
+        --look;
+      }
+      st_volatile_u64(my, kFlagPre | (excl + tile_cnt));
+    }
+    s_goff[d] = (unsigned long long)digit_base[d] + excl;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const uint64_t i = warp_base + (uint64_t)j * 32 + lane;
+    if (i < n) {
+      const unsigned d = (unsigned)(key[j] >> shift) & dmask;
+      const unsigned long long pos = s_goff[d] + s_cnt[warp][d] + rank[j];
+      keys_out[pos] = key[j];
+      if (kHasValues) vals_out[pos] = vals_in[i];
+    }
+  }
+}
+
+// ---- warp-cooperative 32-ary upper bound -----------------------------------
+// Largest r in [0, count) with arr[r] <= x, given arr non-decreasing and
+// arr[0] <= x.  All lanes of the warp must call with the same arguments.
+template <class T>
+__device__ __forceinline__ uint32_t warp_find_run(const T* __restrict__ arr, uint32_t count,
+                                                  T x) {
+  uint32_t lo = 0, hi = count;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint32_t span = hi - lo;
+    const uint32_t step = (span + 31) / 32;
+    const uint32_t probe = lo + (uint32_t)lane_id() * step;
+    const bool le = (probe < hi) && (arr[probe] <= x);
+    const unsigned m = __ballot_sync(kFull, le);
+    // lanes with le form a prefix (arr is monotone); the last set lane bounds the answer
+    const int last = 31 - __clz(m);  // m != 0 because arr[lo] <= x
+    const uint32_t nlo = lo + (uint32_t)last * step;
+    const uint32_t nhi = min(hi, nlo + step);
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
+// Scalar lower bound over the low 32 bits of sorted 64-bit keys in [lo, hi).
+__device__ __forceinline__ uint32_t lower_bound_lo32(const unsigned long long* __restrict__ keys,
+                                                     uint32_t lo, uint32_t hi, uint32_t x) {
+  while (lo < hi) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    if ((uint32_t)keys[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  // splitmix64 finaliser
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+}  // namespace dg
