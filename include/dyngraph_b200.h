@@ -225,6 +225,16 @@ int dg_stats_get(dg_graph* h, dg_stats* out);          /* stats(), graph.hpp:287
 int dg_memory_get(const dg_graph* h, dg_memory* out);  /* memory(), graph.hpp:278-285 */
 int dg_last_op_report(const dg_graph* h, dg_op_report* out);
 
+/*
+ * Per-kernel device timing for measurement runs: with profiling on, every
+ * kernel launch of this graph is bracketed by CUDA events on the graph's
+ * stream.  dg_profile_report returns one "name<TAB>total_ms<TAB>launches" line
+ * per kernel accumulated since profiling was last enabled (valid until the
+ * next call).  Adds event overhead: never enable it for a throughput number.
+ */
+int dg_profile_enable(dg_graph* h, int on);
+const char* dg_profile_report(dg_graph* h);
+
 /* The CUDA stream (cudaStream_t) every op of this graph is enqueued on. */
 void* dg_stream(const dg_graph* h);
 /* Block until every enqueued op finished. */

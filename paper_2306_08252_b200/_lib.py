@@ -76,6 +76,8 @@ SIGNATURES = {
     "dg_stats_get": (C.c_int, [_H, C.POINTER(DgStats)]),
     "dg_memory_get": (C.c_int, [_H, C.POINTER(DgMemory)]),
     "dg_last_op_report": (C.c_int, [_H, C.POINTER(DgOpReport)]),
+    "dg_profile_enable": (C.c_int, [_H, C.c_int]),
+    "dg_profile_report": (C.c_char_p, [_H]),
     "dg_stream": (C.c_void_p, [_H]),
     "dg_synchronize": (C.c_int, [_H]),
     "dg_compute_block_size_coo": (C.c_int, [_H, C.c_void_p, C.c_uint64, C.c_int, u32p]),

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <new>
 #include <string>
 #include <unordered_set>
@@ -78,6 +79,14 @@ struct dg_graph {
   dg_op_report report{};
   uint64_t launches = 0;
 
+  // optional per-kernel timing (dg_profile_enable): CUDA events around every launch
+  bool profiling = false;
+  struct ProfSpan { const char* name; cudaEvent_t a, b; };
+  std::vector<ProfSpan> prof_open;
+  std::vector<cudaEvent_t> prof_pool;
+  std::map<std::string, std::pair<double, uint64_t>> prof_acc;  // name -> (ms, launches)
+  std::string prof_text;
+
   DeviceState* d_state() const { return &d_blk->st; }
   OpState* d_op() const { return &d_blk->op; }
   uint64_t dst_limit() const { return dst_limit_override ? dst_limit_override : size; }
@@ -97,6 +106,51 @@ int fail(dg_graph* h, int code, const std::string& msg) {
     cudaError_t e__ = (expr);                                                         \
     if (e__ != cudaSuccess)                                                           \
       return fail((h), DG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+cudaEvent_t prof_event(dg_graph* h) {
+  if (!h->prof_pool.empty()) {
+    cudaEvent_t e = h->prof_pool.back();
+    h->prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct ProfScope {
+  dg_graph* h;
+  ProfScope(dg_graph* h_, const char* name) : h(h_) {
+    if (!h->profiling) return;
+    dg_graph::ProfSpan sp{name, prof_event(h), prof_event(h)};
+    cudaEventRecord(sp.a, h->stream);
+    h->prof_open.push_back(sp);
+  }
+  ~ProfScope() {
+    if (!h->profiling) return;
+    cudaEventRecord(h->prof_open.back().b, h->stream);
+  }
+};
+// call after the stream is synchronised
+void prof_collect(dg_graph* h) {
+  for (auto& sp : h->prof_open) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, sp.a, sp.b) == cudaSuccess) {
+      auto& acc = h->prof_acc[sp.name];
+      acc.first += ms;
+      acc.second += 1;
+    }
+    h->prof_pool.push_back(sp.a);
+    h->prof_pool.push_back(sp.b);
+  }
+  h->prof_open.clear();
+  cudaGetLastError();
+}
+#define DG_LAUNCH(h, name, ...)   \
+  do {                            \
+    ProfScope ps__((h), (name));  \
+    __VA_ARGS__;                  \
+    (h)->launches += 1;           \
   } while (0)
 
 GraphView view(const dg_graph* h) {
@@ -201,6 +255,7 @@ int op_end(dg_graph* h) {
   DG_CUDA(h, cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(DevBlock), cudaMemcpyDeviceToHost, h->stream));
   DG_CUDA(h, cudaStreamSynchronize(h->stream));
   DG_CUDA(h, cudaGetLastError());
+  if (h->profiling) prof_collect(h);
   const DeviceState& st = h->h_blk->st;
   const OpState& op = h->h_blk->op;
   h->front = st.front;
@@ -231,8 +286,7 @@ void launch_scan(dg_graph* h, uint64_t n_bound, const unsigned long long* n_ptr,
   unsigned long long* scratch = ws_alloc<unsigned long long>(h, words);
   cudaMemsetAsync(scratch, 0, words * sizeof(unsigned long long), h->stream);
   const unsigned tiles = (unsigned)std::max<uint64_t>(1, (n_bound + kScanTile - 1) / kScanTile);
-  scan_kernel<<<tiles, kScanThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin);
-  h->launches += 1;
+  DG_LAUNCH(h, "scan_kernel", scan_kernel<<<tiles, kScanThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
 }
 inline size_t scan_ws_bytes(uint64_t n_bound) {
   return aligned(scan_scratch_words(n_bound) * sizeof(unsigned long long));
@@ -272,23 +326,21 @@ void sort_keys(dg_graph* h, unsigned long long** keys, unsigned long long** keys
   unsigned long long* status = ws_alloc<unsigned long long>(h, (size_t)plan.passes * per_pass);
   cudaMemsetAsync(hist, 0, (size_t)kMaxPasses * kRadix * sizeof(unsigned int), h->stream);
   cudaMemsetAsync(status, 0, (size_t)plan.passes * per_pass * sizeof(unsigned long long), h->stream);
-  sort_hist_kernel<<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(*keys, n, plan, hist, h->d_op());
-  sort_scan_hist_kernel<<<1, kRadix, 0, h->stream>>>(hist, plan.passes, h->d_op());
-  h->launches += 2;
+  DG_LAUNCH(h, "sort_hist_kernel", sort_hist_kernel<<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(*keys, n, plan, hist, h->d_op()));
+  DG_LAUNCH(h, "sort_scan_hist_kernel", sort_scan_hist_kernel<<<1, kRadix, 0, h->stream>>>(hist, plan.passes, h->d_op()));
   const unsigned tiles = (unsigned)sort_tiles(n);
   for (int p = 0; p < plan.passes; ++p) {
     if (vals && *vals) {
-      sort_pass_kernel<true><<<tiles, kSortThreads, 0, h->stream>>>(
+      DG_LAUNCH(h, "sort_pass_kernel<true>", sort_pass_kernel<true><<<tiles, kSortThreads, 0, h->stream>>>(
           *keys, *keys_alt, *vals, *vals_alt, n, plan.shift[p], plan.bits[p], hist + p * kRadix,
-          status + (size_t)p * per_pass, h->d_op());
+          status + (size_t)p * per_pass, h->d_op()));
       std::swap(*vals, *vals_alt);
     } else {
-      sort_pass_kernel<false><<<tiles, kSortThreads, 0, h->stream>>>(
+      DG_LAUNCH(h, "sort_pass_kernel<false>", sort_pass_kernel<false><<<tiles, kSortThreads, 0, h->stream>>>(
           *keys, *keys_alt, nullptr, nullptr, n, plan.shift[p], plan.bits[p], hist + p * kRadix,
-          status + (size_t)p * per_pass, h->d_op());
+          status + (size_t)p * per_pass, h->d_op()));
     }
     std::swap(*keys, *keys_alt);
-    h->launches += 1;
   }
 }
 
@@ -314,7 +366,7 @@ int create_pool(dg_graph* h, uint32_t B) {
   }
   h->B = B;
   h->NB = nb;
-  ring_fill_kernel<<<grid_for(h, nb, 256 * 4), 256, 0, h->stream>>>(h->ring, nb);
+  DG_LAUNCH(h, "ring_fill_kernel", ring_fill_kernel<<<grid_for(h, nb, 256 * 4), 256, 0, h->stream>>>(h->ring, nb));
   DG_CUDA(h, cudaMemsetAsync(h->next, 0xFF, nb * sizeof(uint32_t), h->stream));
   h->h_blk->st.front = 0;
   h->h_blk->st.rear = nb;
@@ -375,9 +427,8 @@ void enqueue_plan_append(dg_graph* h, const BatchView& b, uint64_t runs_bound, u
   launch_scan(h, runs_bound, d_n_runs(h), PlanIn{g, b, run_deg, run_tail},
               PlanOut{unit_off, blk_off}, PlanFin{g, unit_off, h->d_op(), n_edges});
   const uint64_t units_bound = std::min<uint64_t>(2 * n_edges, runs_bound + n_edges);
-  append_kernel<<<grid_for(h, units_bound, 8), 256, 0, h->stream>>>(g, b, unit_off, blk_off,
-                                                                    run_deg, run_tail, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "append_kernel", append_kernel<<<grid_for(h, units_bound, 8), 256, 0, h->stream>>>(g, b, unit_off, blk_off,
+                                                                    run_deg, run_tail, h->d_op()));
 }
 inline size_t plan_append_ws(uint64_t runs_bound) {
   return 2 * aligned((runs_bound + 1) * 4) + scan_ws_bytes(runs_bound);
@@ -400,9 +451,8 @@ Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound,
   w.wl_run = ws_alloc<uint32_t>(h, wl_cap + 1);
   launch_scan(h, runs_bound, d_n_runs(h), EnumIn{g, b, w.run_deg, check_alive}, EnumOut{w.wl_off},
               EnumFin{w.wl_off, h->d_op(), wl_cap});
-  enumerate_walk_kernel<<<grid_for(h, runs_bound, 8), 256, 0, h->stream>>>(
-      g, b, w.wl_off, w.wl_handle, w.wl_run, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_for(h, runs_bound, 8), 256, 0, h->stream>>>(
+      g, b, w.wl_off, w.wl_handle, w.wl_run, h->d_op()));
   return w;
 }
 inline size_t enumerate_ws(const dg_graph* h, uint64_t runs_bound) {
@@ -434,9 +484,8 @@ int delete_sorted_tail(dg_graph* h, unsigned long long* keys, unsigned long long
   uint32_t* mv_off = ws_alloc<uint32_t>(h, n + 1);
   cudaMemsetAsync(run_matched, 0, (n + 1) * 4, h->stream);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  match_kernel<true><<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
-      g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, nullptr, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "match_kernel<true>", match_kernel<true><<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+      g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, nullptr, h->d_op()));
   const size_t ws_mark = h->ws.off;
   for (int attempt = 0; attempt < 2; ++attempt) {
     h->ws.off = ws_mark;
@@ -444,13 +493,12 @@ int delete_sorted_tail(dg_graph* h, unsigned long long* keys, unsigned long long
     cudaMemsetAsync(surv_cnt, 0, (n + 1) * 4, h->stream);
     launch_scan(h, n, d_n_runs(h), MovesIn{w.run_deg, run_matched}, MovesOut{mv_off},
                 MovesFin{mv_off, h->d_op(), h->mv_cap});
-    classify_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+    DG_LAUNCH(h, "classify_kernel", classify_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
         g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, hole_cnt, surv_cnt,
-        h->mv_hole, h->mv_val, h->d_op());
-    finalize_delete_kernel<<<grid_for(h, n, 8), 256, 0, h->stream>>>(
+        h->mv_hole, h->mv_val, h->d_op()));
+    DG_LAUNCH(h, "finalize_delete_kernel", finalize_delete_kernel<<<grid_for(h, n, 8), 256, 0, h->stream>>>(
         g, b, w.wl_off, w.wl_handle, w.run_deg, run_matched, mv_off, hole_cnt, h->mv_hole,
-        h->mv_val, h->d_op());
-    h->launches += 2;
+        h->mv_val, h->d_op()));
     const int rc = op_end(h);
     if (rc != DG_OK) return rc;
     if (h->h_blk->op.aux1 == 0) return DG_OK;
@@ -530,8 +578,8 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
   cudaMemsetAsync(h->alive, 0, words * 4, h->stream);
   if (initial_vertices > 0) {
     GraphView g = view(h);
-    vertex_init_kernel<<<grid_for(h, initial_vertices, 256), 256, 0, h->stream>>>(
-        g, 0u, (uint32_t)initial_vertices);
+    DG_LAUNCH(h, "vertex_init_kernel", vertex_init_kernel<<<grid_for(h, initial_vertices, 256), 256, 0, h->stream>>>(
+        g, 0u, (uint32_t)initial_vertices));
   }
   if (block_size > 0) {
     const int rc = create_pool(h, block_size);
@@ -560,6 +608,8 @@ void dg_destroy(dg_graph* h) {
   cudaFree(h->ws.base);
   cudaFree(h->mv_hole);
   cudaFree(h->mv_val);
+  for (auto& sp : h->prof_open) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
+  for (auto e : h->prof_pool) cudaEventDestroy(e);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   cudaGetLastError();
   delete h;
@@ -591,9 +641,8 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   GraphView g = view(h);
   unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
   unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
-  pack_coo_kernel<kPackInsert, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "pack_coo_kernel<kPackInsert, false>", pack_coo_kernel<kPackInsert, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op()));
   sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
   uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
   uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
@@ -646,17 +695,15 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
   uint32_t* run_start = ws_alloc<uint32_t>(h, V + 2);
   uint32_t* run_deg = ws_alloc<uint32_t>(h, V + 1);
   uint32_t* run_tail = ws_alloc<uint32_t>(h, V + 1);
-  csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
-      g, d_off, (uint32_t)n_offsets, n_edges, /*check_dead_source=*/1, run_start, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "csr_validate_offsets_kernel", csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
+      g, d_off, (uint32_t)n_offsets, n_edges, /*check_dead_source=*/1, run_start, h->d_op()));
   if (n_edges > 0) {
-    validate_dsts_kernel<<<grid_for(h, n_edges, 256 * 4), 256, 0, h->stream>>>(
-        g, d_dst, (uint32_t)n_edges, h->d_op());
-    h->launches += 1;
+    DG_LAUNCH(h, "validate_dsts_kernel", validate_dsts_kernel<<<grid_for(h, n_edges, 256 * 4), 256, 0, h->stream>>>(
+        g, d_dst, (uint32_t)n_edges, h->d_op()));
   }
   if (n_edges == 0 || V == 0) return op_end(h);  // validated; nothing to append
   if (h->B == 0) {
-    count_nonzero_runs_kernel<<<grid_for(h, V, 256), 256, 0, h->stream>>>(run_start, (uint32_t)V, h->d_op());
+    DG_LAUNCH(h, "count_nonzero_runs_kernel", count_nonzero_runs_kernel<<<grid_for(h, V, 256), 256, 0, h->stream>>>(run_start, (uint32_t)V, h->d_op()));
     if ((rc = op_end(h)) != DG_OK) return rc;
     const uint64_t T = h->h_blk->op.aux0;
     if (T == 0) return fail(h, DG_ERR_DATA, "compute_block_size: first batch contains no edges");
@@ -706,9 +753,8 @@ int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   GraphView g = view(h);
   unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
   unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
-  pack_coo_kernel<kPackDelete, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "pack_coo_kernel<kPackDelete, false>", pack_coo_kernel<kPackDelete, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op()));
   if (no_pool) return op_end(h);
   return delete_sorted_tail(h, keys, keys_alt, n);
 }
@@ -739,19 +785,16 @@ int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets
   if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
   GraphView g = view(h);
   uint32_t* run_start = ws_alloc<uint32_t>(h, V + 2);
-  csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
-      g, d_off, (uint32_t)n_offsets, n, /*check_dead_source=*/0, run_start, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "csr_validate_offsets_kernel", csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
+      g, d_off, (uint32_t)n_offsets, n, /*check_dead_source=*/0, run_start, h->d_op()));
   if (n > 0) {
-    validate_dsts_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(g, d_dst, (uint32_t)n, h->d_op());
-    h->launches += 1;
+    DG_LAUNCH(h, "validate_dsts_kernel", validate_dsts_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(g, d_dst, (uint32_t)n, h->d_op()));
   }
   if (n == 0 || V == 0 || h->B == 0) return op_end(h);
   unsigned long long* keys = ws_alloc<unsigned long long>(h, n + 1);
   unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n + 1);
-  csr_expand_kernel<<<grid_for(h, (n + 31) / 32, 8), 256, 0, h->stream>>>(
-      run_start, (uint32_t)V, d_dst, (uint32_t)n, keys, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "csr_expand_kernel", csr_expand_kernel<<<grid_for(h, (n + 31) / 32, 8), 256, 0, h->stream>>>(
+      run_start, (uint32_t)V, d_dst, (uint32_t)n, keys, h->d_op()));
   return delete_sorted_tail(h, keys, keys_alt, n);
 }
 
@@ -789,9 +832,8 @@ int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64
   unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
   uint32_t* idx = ws_alloc<uint32_t>(h, n);
   uint32_t* idx_alt = ws_alloc<uint32_t>(h, n);
-  pack_coo_kernel<kPackQuery, true><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      g, d_src, d_dst, (uint32_t)n, keys, idx, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "pack_coo_kernel<kPackQuery, true>", pack_coo_kernel<kPackQuery, true><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      g, d_src, d_dst, (uint32_t)n, keys, idx, h->d_op()));
   sort_keys(h, &keys, &keys_alt, &idx, &idx_alt, n, plan);
   uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
   uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
@@ -802,10 +844,9 @@ int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64
   uint8_t* hit = ws_alloc<uint8_t>(h, n);
   cudaMemsetAsync(hit, 0, n, h->stream);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  match_kernel<false><<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
-      g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, nullptr, hit, h->d_op());
-  query_scatter_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(hit, idx, (uint32_t)n, d_out, h->d_op());
-  h->launches += 2;
+  DG_LAUNCH(h, "match_kernel<false>", match_kernel<false><<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+      g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, nullptr, hit, h->d_op()));
+  DG_LAUNCH(h, "query_scatter_kernel", query_scatter_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(hit, idx, (uint32_t)n, d_out, h->d_op()));
   if (mem == DG_MEM_HOST)
     DG_CUDA(h, cudaMemcpyAsync(out, d_out, n, cudaMemcpyDeviceToHost, h->stream));
   return op_end(h);
@@ -864,18 +905,15 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
   uint32_t* d_dst = (mem == DG_MEM_HOST) ? ws_alloc<uint32_t>(h, total) : destinations;
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   if (!sorted) {
-    export_copy_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
-        g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, d_off2, d_dst, nullptr, h->d_op());
-    h->launches += 1;
+    DG_LAUNCH(h, "export_copy_kernel", export_copy_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+        g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, d_off2, d_dst, nullptr, h->d_op()));
   } else {
     unsigned long long* keys = ws_alloc<unsigned long long>(h, total);
     unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, total);
-    export_copy_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
-        g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, d_off2, nullptr, keys, h->d_op());
-    h->launches += 1;
+    DG_LAUNCH(h, "export_copy_kernel", export_copy_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+        g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, d_off2, nullptr, keys, h->d_op()));
     sort_keys(h, &keys, &keys_alt, nullptr, nullptr, total, plan);
-    keys_low_kernel<<<grid_for(h, total, 256 * 4), 256, 0, h->stream>>>(keys, total, d_dst);
-    h->launches += 1;
+    DG_LAUNCH(h, "keys_low_kernel", keys_low_kernel<<<grid_for(h, total, 256 * 4), 256, 0, h->stream>>>(keys, total, d_dst));
   }
   if (mem == DG_MEM_HOST)
     DG_CUDA(h, cudaMemcpyAsync(destinations, d_dst, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
@@ -892,7 +930,7 @@ int dg_degrees(dg_graph* h, uint64_t* out, int mem) {
   if (rc != DG_OK) return rc;
   unsigned long long* d = (mem == DG_MEM_DEVICE) ? reinterpret_cast<unsigned long long*>(out)
                                                  : ws_alloc<unsigned long long>(h, V);
-  degrees_kernel<<<grid_for(h, V, 256 * 4), 256, 0, h->stream>>>(h->deg, (uint32_t)V, d);
+  DG_LAUNCH(h, "degrees_kernel", degrees_kernel<<<grid_for(h, V, 256 * 4), 256, 0, h->stream>>>(h->deg, (uint32_t)V, d));
   if (mem == DG_MEM_HOST)
     DG_CUDA(h, cudaMemcpyAsync(out, d, V * 8, cudaMemcpyDeviceToHost, h->stream));
   DG_CUDA(h, cudaStreamSynchronize(h->stream));
@@ -914,9 +952,8 @@ int dg_digest(dg_graph* h, uint64_t* out_digest, uint64_t* out_entries) {
   BatchView b{nullptr, nullptr, nullptr, nullptr};
   Worklist w = enqueue_enumerate(h, b, V, 0);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  digest_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(g, w.wl_off, w.wl_handle, w.wl_run,
-                                                                 w.run_deg, h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "digest_kernel", digest_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(g, w.wl_off, w.wl_handle, w.wl_run,
+                                                                 w.run_deg, h->d_op()));
   if ((rc = op_end(h)) != DG_OK) return rc;
   if (out_digest) *out_digest = h->h_blk->op.aux0;
   if (out_entries) *out_entries = h->h_blk->op.aux1;
@@ -959,7 +996,7 @@ int dg_insert_vertices(dg_graph* h, uint64_t count) {
     h->alive_host.resize((target + 63) / 64, 0ull);
   }
   GraphView g = view(h);
-  vertex_init_kernel<<<grid_for(h, count, 256), 256, 0, h->stream>>>(g, (uint32_t)h->size, (uint32_t)count);
+  DG_LAUNCH(h, "vertex_init_kernel", vertex_init_kernel<<<grid_for(h, count, 256), 256, 0, h->stream>>>(g, (uint32_t)h->size, (uint32_t)count));
   for (uint64_t v = h->size; v < new_size; ++v) h->alive_host[v >> 6] |= 1ull << (v & 63);
   h->size = new_size;
   h->alive_count += count;
@@ -996,9 +1033,8 @@ int dg_delete_vertices(dg_graph* h, const uint32_t* ids, uint64_t n, uint32_t* s
   if ((rc = op_begin(h, winners.size(), 0)) != DG_OK) return rc;
   GraphView g = view(h);
   if (h->B == 0) g.reclaim = 0;
-  retire_vertices_kernel<<<grid_for(h, winners.size(), 8), 256, 0, h->stream>>>(
-      g, d_ids, (uint32_t)winners.size(), h->d_op());
-  h->launches += 1;
+  DG_LAUNCH(h, "retire_vertices_kernel", retire_vertices_kernel<<<grid_for(h, winners.size(), 8), 256, 0, h->stream>>>(
+      g, d_ids, (uint32_t)winners.size(), h->d_op()));
   return op_end(h);
 }
 
@@ -1018,7 +1054,7 @@ int dg_stats_get(dg_graph* h, dg_stats* out) {
   int rc;
   if (h->size > 0 && h->B > 0) {
     if ((rc = op_begin(h, h->size, 0)) != DG_OK) return rc;
-    stats_kernel<<<grid_for(h, h->size, 256), 256, 0, h->stream>>>(view(h), h->d_op());
+    DG_LAUNCH(h, "stats_kernel", stats_kernel<<<grid_for(h, h->size, 256), 256, 0, h->stream>>>(view(h), h->d_op()));
     if ((rc = op_end(h)) != DG_OK) return rc;
     out->adjacency_blocks = h->h_blk->op.aux0;
     out->max_degree = h->h_blk->op.aux1;
@@ -1055,6 +1091,28 @@ int dg_last_op_report(const dg_graph* h, dg_op_report* out) {
   return DG_OK;
 }
 
+int dg_profile_enable(dg_graph* h, int on) {
+  if (!h) return DG_ERR_DATA;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  prof_collect(h);
+  h->profiling = on != 0;
+  if (on) h->prof_acc.clear();
+  return DG_OK;
+}
+
+const char* dg_profile_report(dg_graph* h) {
+  if (!h) return "";
+  h->prof_text.clear();
+  char line[256];
+  for (const auto& kv : h->prof_acc) {
+    std::snprintf(line, sizeof line, "%s\t%.6f\t%llu\n", kv.first.c_str(), kv.second.first,
+                  (unsigned long long)kv.second.second);
+    h->prof_text += line;
+  }
+  return h->prof_text.c_str();
+}
+
 void* dg_stream(const dg_graph* h) { return h ? (void*)h->stream : nullptr; }
 
 int dg_synchronize(dg_graph* h) {
@@ -1089,8 +1147,8 @@ int dg_compute_block_size_coo(dg_graph* h, const uint32_t* src, uint64_t n, int 
   g.dst_limit = 0xFFFFFFFFu;
   unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
   unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
-  pack_coo_kernel<kPackQuery, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      g, d_src, d_src, (uint32_t)n, keys, nullptr, h->d_op());
+  DG_LAUNCH(h, "pack_coo_kernel<kPackQuery, false>", pack_coo_kernel<kPackQuery, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      g, d_src, d_src, (uint32_t)n, keys, nullptr, h->d_op()));
   sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
   uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
   uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
@@ -1111,8 +1169,8 @@ int dg_gen_rmat(dg_graph* h, uint32_t scale, uint64_t seed, uint64_t first_index
   cudaSetDevice(h->device);
   if (scale == 0 || scale > 32) return fail(h, DG_ERR_DATA, "rmat: scale must be in [1, 32]");
   if (n == 0) return DG_OK;
-  rmat_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(scale, seed, first_index, n, thr_a,
-                                                              thr_ab, thr_abc, src_dev, dst_dev);
+  DG_LAUNCH(h, "rmat_kernel", rmat_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(scale, seed, first_index, n, thr_a,
+                                                              thr_ab, thr_abc, src_dev, dst_dev));
   DG_CUDA(h, cudaGetLastError());
   return DG_OK;
 }
@@ -1142,13 +1200,13 @@ int dg_coo_to_csr(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_
   unsigned long long* keys = ws_alloc<unsigned long long>(h, n + 1);
   unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n + 1);
   if (n > 0) {
-    pack_coo_kernel<kPackDelete, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-        g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op());
+    DG_LAUNCH(h, "pack_coo_kernel<kPackDelete, false>", pack_coo_kernel<kPackDelete, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+        g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op()));
     sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
   }
-  keys_to_offsets_kernel<<<grid_for(h, n + 1, 256), 256, 0, h->stream>>>(
+  DG_LAUNCH(h, "keys_to_offsets_kernel", keys_to_offsets_kernel<<<grid_for(h, n + 1, 256), 256, 0, h->stream>>>(
       keys, (uint32_t)n, vertex_count, reinterpret_cast<unsigned long long*>(offsets_dev),
-      destinations_dev, h->d_op());
+      destinations_dev, h->d_op()));
   return op_end(h);
 }
 
@@ -1185,12 +1243,11 @@ int dg_route_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t
   unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
   unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
   unsigned long long* d_counts = ws_alloc<unsigned long long>(h, world + 2);
-  route_keys_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      src, (uint32_t)n, world, bits, (uint32_t)std::min<uint64_t>(vertex_count, 0xFFFFFFFFull), keys, h->d_op());
+  DG_LAUNCH(h, "route_keys_kernel", route_keys_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      src, (uint32_t)n, world, bits, (uint32_t)std::min<uint64_t>(vertex_count, 0xFFFFFFFFull), keys, h->d_op()));
   sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
-  route_gather_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      keys, src, dst, (uint32_t)n, world, bits, out_src_local, out_dst, out_index, d_counts, h->d_op());
-  h->launches += 2;
+  DG_LAUNCH(h, "route_gather_kernel", route_gather_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      keys, src, dst, (uint32_t)n, world, bits, out_src_local, out_dst, out_index, d_counts, h->d_op()));
   std::vector<unsigned long long> ends(world + 1);
   DG_CUDA(h, cudaMemcpyAsync(ends.data(), d_counts, (world + 1) * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, h->stream));

@@ -223,6 +223,17 @@ class DynamicGraph:
         self._check(self._lib.dg_last_op_report(self._h, C.byref(r)))
         return {n: int(getattr(r, n)) for n, _ in r._fields_}
 
+    def profile_enable(self, on: bool = True):
+        self._check(self._lib.dg_profile_enable(self._h, int(on)))
+
+    def profile_report(self) -> dict:
+        """kernel name -> (total_ms, launches) since profiling was enabled."""
+        out = {}
+        for line in self._lib.dg_profile_report(self._h).decode().splitlines():
+            name, ms, cnt = line.split("\t")
+            out[name] = (float(ms), int(cnt))
+        return out
+
     # -- input-side helpers --------------------------------------------------------------------
     def compute_block_size_pairs(self, src) -> int:
         s = _Arg(src, np.uint32)

@@ -1,0 +1,285 @@
+"""GPU suite: the CUDA path (through the C ABI) against the oracle and the goldens.
+
+Bit-exact bar: status codes, skipped ids, query answers, logical size, capacity,
+alive flags, degrees, per-vertex sorted multiset, active edge count.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from tests.drivers import CpuGraph, GpuGraph, assert_same, load_oracle, load_ref, run_script
+from tests.golden_io import load_cases
+from tests.known_answers import KNOWN_ANSWER_SCRIPTS, pairs, u32
+from tests.workloads import make_workload
+
+pytestmark = pytest.mark.gpu
+GOLDEN = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+
+
+def _orc(cfg):
+    return CpuGraph(load_oracle(), "orc", cfg["v0"], cfg["block_size"], cfg.get("arena_bytes", 1 << 20),
+                    cfg.get("initial_fraction", 0.5), cfg.get("reclaim", True), 1)
+
+
+def _gpu(cfg, pool_blocks=1 << 16):
+    return GpuGraph(cfg["v0"], cfg["block_size"], pool_blocks=pool_blocks, reclaim=cfg.get("reclaim", True))
+
+
+def test_cuda_library_is_the_loaded_path():
+    from paper_2306_08252_b200 import _lib
+    lib = _lib.load()
+    assert lib.dg_abi_version() == 1
+    maps = open("/proc/self/maps").read()
+    assert "libdyngraph_b200.so" in maps
+
+
+@pytest.mark.parametrize("name,cfg,script", KNOWN_ANSWER_SCRIPTS, ids=[k[0] for k in KNOWN_ANSWER_SCRIPTS])
+def test_known_answers_vs_oracle(name, cfg, script):
+    g, o = _gpu(cfg), _orc(cfg)
+    assert_same(run_script(g, script), run_script(o, script), name)
+    g.close()
+
+
+def test_known_answers_vs_reference_golden():
+    for case in load_cases(GOLDEN / "ref_known_answers.npz"):
+        g = _gpu(case["cfg"])
+        assert_same(run_script(g, case["script"]), case["expect"], case["cfg"]["name"])
+        g.close()
+
+
+def test_workloads_vs_reference_golden():
+    for i, case in enumerate(load_cases(GOLDEN / "ref_workloads.npz")):
+        g = _gpu(case["cfg"])
+        assert_same(run_script(g, case["script"]), case["expect"], f"golden workload {i}")
+        g.close()
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_random_workloads_vs_oracle(chunk):
+    """verify.hpp:135-265 op mix, 25 seeds per chunk."""
+    for seed in range(5000 + 25 * chunk, 5025 + 25 * chunk):
+        cfg, script = make_workload(seed)
+        g, o = _gpu(cfg), _orc(cfg)
+        assert_same(run_script(g, script), run_script(o, script), f"seed {seed}")
+        g.close()
+
+
+def test_random_workloads_vs_live_reference_when_present():
+    ref = load_ref()
+    if ref is None:
+        pytest.skip("oracle/_ref not shipped")
+    for seed in range(7000, 7020):
+        cfg, script = make_workload(seed)
+        g = _gpu(cfg)
+        r = CpuGraph(ref, "ref", cfg["v0"], cfg["block_size"], cfg["arena_bytes"], cfg["initial_fraction"],
+                     cfg["reclaim"], cfg["workers"])
+        assert_same(run_script(g, script), run_script(r, script), f"seed {seed}")
+        g.close()
+
+
+def test_pool_underflow_aborts_atomically():
+    # batch_engine_test.cpp:257-268 restated: 42 blocks of 4, a 2000-edge batch needs 500
+    g = GpuGraph(2, 4, pool_blocks=42)
+    assert g.insert_pairs(*pairs((0, 1), (1, 0))) == 0
+    before = run_script(g, [("check",)])
+    q0 = g.queue_size()
+    assert g.insert_pairs(np.zeros(2000, np.uint32), np.ones(2000, np.uint32)) == 3
+    assert_same(before, run_script(g, [("check",)]))
+    assert g.queue_size() == q0
+    # exactly fitting batch still works: 41 blocks left minus one partly used
+    assert g.insert_pairs(np.zeros(4 * 40 + 3, np.uint32), np.ones(4 * 40 + 3, np.uint32)) == 0
+    assert g.queue_size() == 0
+    assert g.insert_pairs(*pairs((1, 1), (1, 1), (1, 1), (1, 1))) == 3  # vertex 1 needs a 2nd block
+    g.close()
+
+
+def test_reclaimed_blocks_are_reused():
+    g = GpuGraph(4, 2, pool_blocks=8)
+    for _ in range(50):  # 50 x 6 blocks through an 8-block pool only works if reclaim returns them
+        assert g.insert_pairs(np.zeros(12, np.uint32), np.arange(12, dtype=np.uint32) % 4) == 0
+        assert g.queue_size() == 2
+        assert g.delete_pairs(np.zeros(4, np.uint32), np.arange(4, dtype=np.uint32)) == 0
+        assert g.queue_size() == 8 and g.active_edges() == 0
+    g.close()
+
+
+def test_compaction_scratch_regrows():
+    """One delete entry removing 100k copies with 100k survivors behind them (moves >> batch)."""
+    n = 100000
+    g = GpuGraph(8, 32, pool_blocks=1 << 14)
+    o = CpuGraph(load_oracle(), "orc", 8, 32, 1 << 30)
+    src = np.zeros(2 * n, np.uint32)
+    dst = np.concatenate([np.full(n, 1, np.uint32), np.full(n, 2, np.uint32)])
+    script = [("insert", src, dst), ("delete", *pairs((0, 1))), ("check",),
+              ("insert", src[:1000], dst[:1000]), ("delete", *pairs((0, 2))), ("check",)]
+    assert_same(run_script(g, script), run_script(o, script))
+    g.close()
+
+
+@pytest.mark.parametrize("block_size", [1, 3, 15, 32, 33, 64, 100])
+def test_block_sizes(block_size):
+    rng = np.random.default_rng(block_size)
+    cfg = {"v0": 300, "block_size": block_size, "arena_bytes": 1 << 28}
+    script = []
+    for r in range(6):
+        s = (rng.zipf(1.3, 20000) % 300).astype(np.uint32)
+        d = rng.integers(0, 300, 20000).astype(np.uint32)
+        script.append(("insert" if r % 3 != 2 else "delete", s, d))
+        script.append(("check",))
+    script.append(("query", rng.integers(0, 300, 5000).astype(np.uint32), rng.integers(0, 300, 5000).astype(np.uint32)))
+    g, o = _gpu(cfg, pool_blocks=1 << 18), _orc(cfg)
+    assert_same(run_script(g, script), run_script(o, script), f"B={block_size}")
+    g.close()
+
+
+def test_csr_entry_points_match_coo():
+    from paper_2306_08252_b200 import BatchKind, csr_from_pairs
+    rng = np.random.default_rng(3)
+    V = 1000
+    cfg = {"v0": V, "block_size": 8, "arena_bytes": 1 << 28}
+    g, o = _gpu(cfg, pool_blocks=1 << 16), _orc(cfg)
+    script = []
+    for r in range(5):
+        s = rng.integers(0, V, 30000).astype(np.uint32)
+        d = rng.integers(0, V, 30000).astype(np.uint32)
+        b = csr_from_pairs(BatchKind.Insert, V, s, d)
+        script.append(("insert_csr" if r % 2 == 0 else "delete_csr", b.offsets, b.destinations))
+        script.append(("check",))
+    assert_same(run_script(g, script), run_script(o, script))
+    g.close()
+
+
+def test_auto_block_size_from_first_batch():
+    # block_size 0 => compute_block_size of the first batch (csr.hpp:77-88, io/workload.hpp:116-120)
+    from paper_2306_08252_b200 import BatchKind, DynamicGraph, GraphConfig, compute_block_size, csr_from_pairs
+    rng = np.random.default_rng(5)
+    s = rng.integers(0, 500, 7777).astype(np.uint32)
+    d = rng.integers(0, 500, 7777).astype(np.uint32)
+    want = compute_block_size(csr_from_pairs(BatchKind.Insert, 500, s, d))
+    g = DynamicGraph(GraphConfig(pool_bytes=1 << 24), 500, 0)
+    assert g.block_size() == 0
+    g.insert_pairs(s, d)
+    assert g.block_size() == want and g.active_edges() == 7777
+    g2 = DynamicGraph(GraphConfig(pool_bytes=1 << 24), 500, 0)
+    b = csr_from_pairs(BatchKind.Insert, 500, s, d)
+    g2.insert_batch(b)
+    assert g2.block_size() == want
+    assert np.array_equal(g.export_csr()[1], g2.export_csr()[1])
+    assert g.compute_block_size_pairs(s) == want
+
+
+def test_device_resident_batches():
+    import torch
+    from paper_2306_08252_b200 import DynamicGraph, GraphConfig
+    rng = np.random.default_rng(11)
+    V = 5000
+    s = rng.integers(0, V, 100000).astype(np.uint32)
+    d = rng.integers(0, V, 100000).astype(np.uint32)
+    g = DynamicGraph(GraphConfig(pool_blocks=1 << 16), V, 16)
+    ts = torch.from_numpy(s.view(np.int32)).cuda()
+    td = torch.from_numpy(d.view(np.int32)).cuda()
+    g.insert_pairs(ts, td)
+    o = CpuGraph(load_oracle(), "orc", V, 16, 1 << 28)
+    o.insert_pairs(s, d)
+    assert np.array_equal(g.export_csr()[1], o.export_csr()[1])
+    ans = g.query_edges(ts[:5000], td[:5000]).cpu().numpy()
+    assert ans.all()
+    g.delete_pairs(ts[:50000], td[:50000])
+    o.delete_pairs(s[:50000], d[:50000])
+    off_g, dst_g = g.export_csr()
+    off_o, dst_o = o.export_csr()
+    assert np.array_equal(off_g, off_o) and np.array_equal(dst_g, dst_o)
+    assert g.active_edges() == o.active_edges()
+
+
+def test_config1_uniform_2p16_1m():
+    """BASELINE config 1: synth_uniform(65536, 1e6, 0xbeef), bulk init, 10 x 10K inserts then
+    the same batches as deletes, 100K queries — full parity with the oracle."""
+    orc = load_oracle()
+    V, E = 65536, 1000000
+    s = np.zeros(E, np.uint32); d = np.zeros(E, np.uint32)
+    orc.orc_synth_uniform_pairs(V, E, 0xBEEF, C.c_void_p(s.ctypes.data), C.c_void_p(d.ctypes.data))
+    us = np.zeros(100000, np.uint32); ud = np.zeros(100000, np.uint32)
+    orc.orc_synth_uniform_pairs(V, 100000, 0xBEEF + 1, C.c_void_p(us.ctypes.data), C.c_void_p(ud.ctypes.data))
+    from paper_2306_08252_b200 import BatchKind, compute_block_size, csr_from_pairs
+    base = csr_from_pairs(BatchKind.Insert, V, s, d)
+    B = compute_block_size(base)
+    assert B == 15  # measured auto block size for C1
+    rng = np.random.default_rng(0xBEEF)
+    pick = rng.integers(0, E, 50000)
+    qs = np.concatenate([s[pick], rng.integers(0, V, 50000).astype(np.uint32)])
+    qd = np.concatenate([d[pick], rng.integers(0, V, 50000).astype(np.uint32)])
+    script = [("insert_csr", base.offsets, base.destinations), ("check",)]
+    for i in range(10):
+        script += [("insert", us[i * 10000:(i + 1) * 10000], ud[i * 10000:(i + 1) * 10000]), ("check",)]
+    script.append(("query", qs, qd))
+    for i in range(10):
+        script += [("delete", us[i * 10000:(i + 1) * 10000], ud[i * 10000:(i + 1) * 10000]), ("check",)]
+    script.append(("query", qs, qd))
+    cfg = {"v0": V, "block_size": B, "arena_bytes": 512 << 20}
+    g, o = _gpu(cfg, pool_blocks=1 << 18), _orc(cfg)
+    assert_same(run_script(g, script), run_script(o, script), "config 1")
+    g.close()
+
+
+def _np_digest(src, dst):
+    def mix64(x):
+        with np.errstate(over="ignore"):
+            x = x + np.uint64(0x9E3779B97F4A7C15)
+            x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            return x ^ (x >> np.uint64(31))
+    k = (src.astype(np.uint64) << np.uint64(32)) | dst.astype(np.uint64)
+    with np.errstate(over="ignore"):
+        return int(mix64(k).sum(dtype=np.uint64))
+
+
+@pytest.mark.parametrize("scale,batch", [(16, 50000), (20, 1000000)])
+def test_rmat_device_generator_and_round_trip(scale, batch):
+    """R-MAT generated ON DEVICE equals the host twin; bulk init from device CSR; insert a batch
+    then delete it: what remains is the base graph minus every copy of a batch pair."""
+    import torch
+    from paper_2306_08252_b200 import DynamicGraph, GraphConfig, rmat
+    V, E = 1 << scale, 16 << scale
+    thr = rmat.thresholds()
+    g = DynamicGraph(GraphConfig(pool_bytes=(E * 4 * 3)), V, 0)
+    src = torch.empty(E, dtype=torch.int32, device="cuda")
+    dst = torch.empty(E, dtype=torch.int32, device="cuda")
+    g.gen_rmat(scale, 1, 0, src, dst, thr)
+    g.synchronize()
+    hs, hd = rmat.rmat_edges(scale, 1, 0, E, thr)
+    assert np.array_equal(src.cpu().numpy().view(np.uint32), hs)
+    assert np.array_equal(dst.cpu().numpy().view(np.uint32), hd)
+    off = torch.empty(V + 1, dtype=torch.int64, device="cuda")
+    cdst = torch.empty(E, dtype=torch.int32, device="cuda")
+    g.coo_to_csr(src, dst, V, off, cdst)
+    # GPU twin of csr_from_pairs: stable grouping
+    order = np.argsort(hs, kind="stable")
+    assert np.array_equal(cdst.cpu().numpy().view(np.uint32), hd[order])
+    assert np.array_equal(off.cpu().numpy(), np.concatenate([[0], np.cumsum(np.bincount(hs, minlength=V))]))
+    g.bulk_init(off, cdst)
+    assert g.active_edges() == E
+    nonzero = int((np.bincount(hs, minlength=V) > 0).sum())
+    assert g.block_size() == max(1, (E + nonzero // 2) // nonzero)
+    assert np.array_equal(g.degrees(), np.bincount(hs, minlength=V).astype(np.uint64))
+    assert g.digest() == (_np_digest(hs, hd), E)
+    bs, bd = rmat.rmat_edges(scale, 2, 0, batch, thr)
+    g.insert_pairs(bs, bd)
+    assert g.active_edges() == E + batch
+    assert g.digest() == ((_np_digest(hs, hd) + _np_digest(bs, bd)) % (1 << 64), E + batch)
+    assert g.query_edges(bs[:20000], bd[:20000]).all()
+    g.delete_pairs(bs, bd)
+    base_keys = (hs.astype(np.uint64) << np.uint64(32)) | hd
+    batch_keys = (bs.astype(np.uint64) << np.uint64(32)) | bd
+    keep = ~np.isin(base_keys, batch_keys)
+    assert g.active_edges() == int(keep.sum())
+    assert g.digest() == (_np_digest(hs[keep], hd[keep]), int(keep.sum()))
+    assert not g.query_edges(bs[:20000], bd[:20000]).any()
+    st = g.stats()
+    assert st["hole_slots"] == 0 and st["pool_blocks_in_use"] == st["adjacency_blocks"]
+    off2, dst2 = g.export_csr(sorted=True)
+    ks = np.sort(base_keys[keep])
+    assert np.array_equal(dst2, (ks & np.uint64(0xFFFFFFFF)).astype(np.uint32))
+    assert np.array_equal(off2, np.concatenate([[0], np.cumsum(np.bincount((ks >> np.uint64(32)).astype(np.int64), minlength=V))]).astype(np.uint64))
+    g.close()
