@@ -1,0 +1,498 @@
+#!/usr/bin/env python
+"""bench.py — batch edge insert/delete throughput on R-MAT scale 22 (BASELINE.json config[1]).
+
+    python bench.py --gpus N --steps K --warmup W            # the CUDA path (this repo)
+    python bench.py --impl reference --gpus N --steps K ...  # the reference's CPU path
+
+One STEP = one pass of the hot path over one batch: `dg_insert_batch_coo` of a
+1M-pair R-MAT batch followed by `dg_delete_batch_coo` of the same batch, on a
+graph bulk-built from the 16*2^22-edge R-MAT base (so a step processes 2*batch
+edge updates and the graph keeps its size from step to step).  Every step uses
+a distinct batch.  Printed: ONE JSON line (rank 0).
+
+  value      whole-job Medges/s with the batch already resident in HBM
+             (CUDA events on the graph's stream, sum over the K steps, max over ranks)
+  e2e        the same steps through the public API with HOST (pinned) batches:
+             the H2D copy of the pairs and the D2H read of the op status are inside
+             the timed region
+  roofline   the dominant kernel of the step (per-kernel CUDA-event timing via
+             dg_profile_enable in a separate pass over the same steps): algorithmic
+             bytes per launch / average launch duration vs MEASURED_PEAKS.json
+  cpu_baseline  oracle/_ref (the unmodified reference, when it was compiled) or the
+             oracle port, timed on this box's host cores on a bounded sample
+
+N > 1 (torchrun): vertices are hash-partitioned by source over the ranks
+(paper_2306_08252_b200.sharded); every rank generates its own 1M-pair slice of
+the update stream and 16*2^22 base edges of a scale-(22+log2 N) graph, routes
+them to the owners with an NCCL all-to-all and applies what it receives —
+weak scaling, per-GPU work fixed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+METRIC = "batch edge insert+delete throughput (batch=1M, R-MAT s22)"
+UNIT = "Medges/s"
+STATUS_BYTES = 152  # sizeof(DeviceState) + sizeof(OpState): the per-op D2H status read (csrc/dg_api.cu op_end)
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--scale", type=int, default=22, help="R-MAT scale per GPU (22 = BASELINE config[1])")
+    ap.add_argument("--edge-factor", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=1_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=2, help="batches in the cpu_baseline sample")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------------------
+# clocks (B200_PROFILING.md "clocks DURING the timed region")
+# --------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1])); power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(power) if power else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------------------
+# algorithmic bytes per kernel launch
+# --------------------------------------------------------------------------------------
+def kernel_bytes(name: str, rep: dict, B: int, sort_passes: int) -> float | None:
+    """Algorithmic HBM bytes of ONE launch of `name` inside a delete (or insert) op.
+
+    b = batch entries, T = touched sources, W = blocks of touched chains,
+    S = slots of touched chains, M = compaction moves (all from dg_last_op_report)."""
+    b, T = rep["batch_entries"], rep["touched_sources"]
+    W, S, M = rep["blocks_scanned"], rep["slots_scanned"], rep["moved"]
+    if name.startswith("match_kernel"):
+        return 4 * S + 8 * W + 8 * b + 4 * T            # slab slots + worklist (handle, run) + sorted keys + counters
+    if name.startswith("classify_kernel"):
+        return 4 * S + 8 * W + 12 * M                    # re-read of matched chains + hole/survivor records
+    if name.startswith("sort_pass_kernel"):
+        return 16 * b                                    # 8 B key read + 8 B key write
+    if name.startswith("sort_hist_kernel"):
+        return 8 * b
+    if name.startswith("pack_coo_kernel"):
+        return 16 * b                                    # 2 x u32 in, u64 key out
+    if name.startswith("scan_kernel"):
+        return 16 * b
+    if name.startswith("enumerate_walk_kernel"):
+        return 12 * W + 12 * T                           # next[] reads + worklist writes
+    if name.startswith("append_kernel"):
+        return 12 * b + 32 * T
+    if name.startswith("finalize_delete_kernel"):
+        return 16 * M + 32 * T
+    return None
+
+
+# --------------------------------------------------------------------------------------
+# CPU baseline (reference arm and the cpu_baseline leg)
+# --------------------------------------------------------------------------------------
+def cpu_reference_run(scale: int, edge_factor: int, batch: int, warmup: int, steps: int, threads: int):
+    """Times the reference's CPU implementation of the step on this host.
+
+    Uses oracle/_ref/libdyngraph_ref.so (the unmodified reference headers behind
+    oracle/ref_shim.cpp) when it was compiled, else the oracle port.  Batch
+    construction (csr_from_pairs) is outside the timed region, as in the
+    reference's own harness."""
+    import ctypes as C
+    import numpy as np
+    from tests.drivers import CpuGraph, load_oracle, load_ref
+    from paper_2306_08252_b200 import rmat
+
+    orc = load_oracle()
+    ref = load_ref()
+    lib, pfx, kind = (ref, "ref", "reference") if ref is not None else (orc, "orc", "port")
+    V, E = 1 << scale, edge_factor << scale
+    thr = rmat.thresholds()
+
+    def gen(seed, first, n):
+        s, d = np.empty(n, np.uint32), np.empty(n, np.uint32)
+        orc.orc_gen_rmat(scale, seed, first, n, thr[0], thr[1], thr[2],
+                         C.c_void_p(s.ctypes.data), C.c_void_p(d.ctypes.data))
+        return s, d
+
+    bs, bd = gen(1, 0, E)
+    B = 32
+    if ref is not None:
+        out = C.c_uint32()
+        if ref.ref_compute_block_size_coo(V, C.c_void_p(bs.ctypes.data), C.c_void_p(bd.ctypes.data), E, C.byref(out)) == 0:
+            B = int(out.value)
+    arena = max(8 << 30, 48 * E)  # 8 GiB at s22 (proj/README.md:111-113)
+    t0 = time.perf_counter()
+    g = CpuGraph(lib, pfx, V, B, arena, 0.5, True, threads)
+    init_s = time.perf_counter() - t0
+    sec = C.c_double()
+    rc = g.insert_pairs(bs, bd, C.byref(sec))
+    assert rc == 0, g.last_error()
+    bulk_s = sec.value
+    del bs, bd
+    t_ins = t_del = 0.0
+    for i in range(warmup + steps):
+        s, d = gen(2, i * batch, batch)
+        assert g.insert_pairs(s, d, C.byref(sec)) == 0
+        ti = sec.value
+        assert g.delete_pairs(s, d, C.byref(sec)) == 0
+        td = sec.value
+        if i >= warmup:
+            t_ins += ti
+            t_del += td
+    g.close()
+    total = t_ins + t_del
+    return {
+        "kind": kind, "cores": threads, "block_size": B,
+        "value": 2 * batch * steps / total / 1e6, "unit": UNIT,
+        "insert_medges_s": batch * steps / t_ins / 1e6, "delete_medges_s": batch * steps / t_del / 1e6,
+        "init_ms": init_s * 1e3, "bulk_insert_ms": bulk_s * 1e3, "ms_per_step": total / steps * 1e3,
+        "sample": f"R-MAT s{scale} base graph ({E} edges) + {steps} steps of insert+delete batch={batch} "
+                  f"after {warmup} warm-up, workers={threads}, batch construction untimed",
+    }
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    r = cpu_reference_run(args.scale, args.edge_factor, args.batch, args.warmup, args.steps, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": workload_config(args, 1, r["block_size"]),
+        "insert_medges_s": r["insert_medges_s"], "delete_medges_s": r["delete_medges_s"],
+        "bulk_init_ms": r["init_ms"] + r["bulk_insert_ms"],
+        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, world: int, B: int) -> dict:
+    scale = args.scale + int(math.log2(world))
+    return {
+        "workload": f"R-MAT scale {scale} (a,b,c,d=.57,.19,.19,.05; V={1 << scale}, base E={args.edge_factor << scale}) "
+                    f"bulk init + per step: insert batch={args.batch * world} then delete the same batch",
+        "batch": args.batch * world, "scale": scale, "edge_factor": args.edge_factor, "block_size": B,
+        "parallelism": "single GPU" if world == 1 else f"source-hash partition over {world} GPUs + NCCL all-to-all routing",
+        "l2": "256 MiB memset between steps (untimed) flushes L2; distinct batch every step",
+    }
+
+
+# --------------------------------------------------------------------------------------
+# the CUDA arm
+# --------------------------------------------------------------------------------------
+def run_b200_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device — the product has no CPU path")
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("bench.py --gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2306_08252_b200 import DynamicGraph, GraphConfig, rmat
+    from paper_2306_08252_b200._lib import load
+    load()  # fail loudly if the CUDA library is missing
+
+    scale = args.scale + int(math.log2(world))
+    V = 1 << scale
+    E_local = args.edge_factor << args.scale          # base edges GENERATED per rank
+    b = args.batch                                    # update pairs GENERATED per rank per step
+    thr = rmat.thresholds()
+    stream = torch.cuda.Stream(device=dev)
+    K, W = args.steps, args.warmup
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks else "6650 GB/s (of fallback)"
+
+    with torch.cuda.stream(stream):
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+        def i32(n):
+            return torch.empty(n, dtype=torch.int32, device=dev)
+
+        # ---- graph construction + bulk init (timed) --------------------------------------
+        if world == 1:
+            gen = DynamicGraph(GraphConfig(device=local, pool_blocks=1024, stream=stream.cuda_stream), 1, 1)
+            src, dst = i32(E_local), i32(E_local)
+            gen.gen_rmat(scale, 1, 0, src, dst, thr)
+            B = gen.compute_block_size_pairs(src)   # compute_block_size (csr.hpp:77-88) on the base graph
+            off = torch.empty(V + 1, dtype=torch.int64, device=dev)
+            csr_dst = i32(E_local)
+            gen.coo_to_csr(src, dst, V, off, csr_dst)
+            del src, dst
+            pool_blocks = int((E_local // B + V) * 1.25) + (4 * b) // B + 4096
+            bulk_ms = []
+            g = None
+            for rep in range(3):
+                if g is not None:
+                    g.close()
+                t0 = time.perf_counter()
+                g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream), V, B)
+                create_ms = (time.perf_counter() - t0) * 1e3
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                flush.zero_()
+                e0.record(stream)
+                g.bulk_init(off, csr_dst)
+                e1.record(stream)
+                stream.synchronize()
+                bulk_ms.append((create_ms, e0.elapsed_time(e1)))
+            bulk_rep = g.last_op_report()
+            st = g.stats()
+            del off, csr_dst
+            sharded = None
+        else:
+            from paper_2306_08252_b200.sharded import ShardedDynamicGraph
+            gen = DynamicGraph(GraphConfig(device=local, pool_blocks=1024, stream=stream.cuda_stream), 1, 1)
+            src, dst = i32(E_local), i32(E_local)
+            gen.gen_rmat(scale, 1, rank * E_local, src, dst, thr)
+            B = 32 if args.edge_factor == 16 else max(1, args.edge_factor * 2)
+            pool_blocks = int((E_local // B + V // world) * 1.6) + (8 * b) // B + 4096
+            t0 = time.perf_counter()
+            sharded = ShardedDynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream),
+                                          V, B, torch_stream=stream)
+            create_ms = (time.perf_counter() - t0) * 1e3
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dist.barrier(); torch.cuda.synchronize()
+            e0.record(stream)
+            sharded.insert_pairs(src, dst)
+            e1.record(stream)
+            stream.synchronize()
+            bulk_ms = [(create_ms, e0.elapsed_time(e1))]
+            g = sharded.local
+            bulk_rep = g.last_op_report()
+            st = g.stats()
+            del src, dst
+
+        # ---- update batches (device + pinned host copies) ---------------------------------------
+        nb = K + W
+        batches = []
+        for i in range(nb):
+            s, d = i32(b), i32(b)
+            gen.gen_rmat(scale, 2, (i * world + rank) * b, s, d, thr)
+            batches.append((s, d))
+        stream.synchronize()
+        host_batches = []
+        if not args.no_e2e:
+            for s, d in batches:
+                hs = torch.empty(b, dtype=torch.int32).pin_memory()
+                hd = torch.empty(b, dtype=torch.int32).pin_memory()
+                hs.copy_(s); hd.copy_(d)
+                host_batches.append((hs.numpy().view(np.uint32), hd.numpy().view(np.uint32)))
+        target = sharded if sharded is not None else g
+
+        def step(i, host=False):
+            s, d = (host_batches if host else batches)[i]
+            target.insert_pairs(s, d)
+            r_ins = g.last_op_report()
+            target.delete_pairs(s, d)
+            return r_ins, g.last_op_report()
+
+        def timed_pass(host: bool):
+            """W warm-up + K timed steps; returns (sum of per-step device ms, per-step list, reports)."""
+            for i in range(W):
+                step(i, host)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            per, reps = [], []
+            t_wall = time.perf_counter()
+            for i in range(W, W + K):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                reps.append(step(i, host))
+                e1.record(stream)
+                e1.synchronize()
+                per.append(e0.elapsed_time(e1))
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            wall = (time.perf_counter() - t_wall) * 1e3
+            total = torch.tensor([sum(per)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(total, op=dist.ReduceOp.MAX)
+            return float(total.item()), per, reps, wall
+
+        # split insert / delete device times (one extra untimed-for-the-metric pass of event pairs)
+        def split_pass():
+            ins = dele = 0.0
+            for i in range(W, W + K):
+                s, d = batches[i]
+                flush.zero_()
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(stream); target.insert_pairs(s, d); e1.record(stream)
+                target.delete_pairs(s, d); e2.record(stream); e2.synchronize()
+                ins += e0.elapsed_time(e1); dele += e1.elapsed_time(e2)
+            return ins, dele
+
+        clocks = ClockSampler(local)
+        clocks.start()
+        total_ms, per_step, reps, wall_ms = timed_pass(host=False)
+        clock_rec = clocks.stop()
+        launches = sum(r[0]["kernel_launches"] + r[1]["kernel_launches"] for r in reps)
+        ins_ms, del_ms = split_pass()
+        e2e = None
+        if not args.no_e2e:
+            e2e_ms, _, _, _ = timed_pass(host=True)
+            e2e = {"value": 2 * b * world * K / (e2e_ms * 1e-3) / 1e6, "unit": UNIT,
+                   "ms_per_step": e2e_ms / K,
+                   "h2d_bytes_per_step": 2 * 8 * b, "d2h_bytes_per_step": 2 * STATUS_BYTES,
+                   "api": "DynamicGraph.insert_pairs/delete_pairs -> dg_insert_batch_coo/dg_delete_batch_coo(DG_MEM_HOST), pinned host batches"}
+
+        # ---- per-kernel timing pass (CUDA events around every launch) ---------------------------
+        roofline, kernels = None, None
+        if not args.no_profile:
+            g.profile_enable(True)
+            prof_reps = [step(i) for i in range(W, W + K)]
+            g.profile_enable(False)
+            prof = g.profile_report()
+            tot = sum(ms for ms, _ in prof.values()) or 1.0
+            kernels = {k: {"ms_per_step": ms / K, "launches_per_step": n / K, "share": ms / tot}
+                       for k, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+            top = max(prof.items(), key=lambda kv: kv[1][0])
+            name, (ms, n) = top
+            sort_passes = math.ceil(scale / 8) + math.ceil(scale / 8)
+            # delete-side kernels use the delete report, insert-side the insert report
+            ins_side = name.startswith("append_kernel")
+            per_launch = [kernel_bytes(name, r[0] if ins_side else r[1], B, sort_passes) for r in prof_reps]
+            if per_launch[0] is not None and n:
+                launches_per_op = n / (K * (2 if name.startswith(("sort_", "scan_", "pack_")) else 1))
+                bytes_launch = sum(per_launch) / len(per_launch)
+                if name.startswith("scan_kernel"):
+                    bytes_launch = bytes_launch  # upper bound: the largest scan of the op
+                avg_ms = ms / n
+                ach = bytes_launch / (avg_ms * 1e-3) / 1e9
+                roofline = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                            "frac": ach / hbm_peak, "traffic": None, "peak_source": peak_src,
+                            "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
+                            "launches_per_step": n / K, "share_of_step": ms / tot}
+
+        final_st = g.stats()
+        digest = g.digest()
+
+    value = 2 * b * world * K / (total_ms * 1e-3) / 1e6
+    r_ins, r_del = reps[-1]
+    # op-level algorithmic bytes: insert 12b + 32T; delete 8b + 4S + S/8 + 32T
+    a_ins = 12 * r_ins["batch_entries"] + 32 * r_ins["touched_sources"]
+    a_del = 8 * r_del["batch_entries"] + 4 * r_del["slots_scanned"] + r_del["slots_scanned"] / 8 + 32 * r_del["touched_sources"]
+    a_bulk = 8 * (V // world + 1) + 4 * bulk_rep["batch_entries"] * 2 + 16 * (V // world) + 8 * st["pool_blocks_in_use"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic", "config": workload_config(args, world, B),
+        "insert_medges_s": b * world * K / (ins_ms * 1e-3) / 1e6, "delete_medges_s": b * world * K / (del_ms * 1e-3) / 1e6,
+        "insert_ms": ins_ms / K, "delete_ms": del_ms / K,
+        "bulk_init_ms": min(m for _, m in bulk_ms), "create_ms": min(c for c, _ in bulk_ms),
+        "op_hbm": {"insert_gbs": a_ins / (ins_ms / K * 1e-3) / 1e9, "delete_gbs": a_del / (del_ms / K * 1e-3) / 1e9,
+                   "bulk_init_gbs": a_bulk / (min(m for _, m in bulk_ms) * 1e-3) / 1e9, "peak_gbs": hbm_peak},
+        "op_report": {"insert": r_ins, "delete": r_del},
+        "graph": {"active_edges": final_st["active_edges"], "blocks_in_use": final_st["pool_blocks_in_use"],
+                  "max_degree": final_st["max_degree"], "digest": f"{digest[0]:016x}"},
+        "wall_ms_per_step": wall_ms / K,
+        "clocks": clock_rec, "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = cpu_reference_run(args.scale, args.edge_factor, args.batch, 1, args.cpu_steps, os.cpu_count() or 1)
+            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                     "insert_medges_s", "delete_medges_s", "bulk_insert_ms", "init_ms")}
+        except Exception as e:  # the baseline is reported, never required for the CUDA number
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_b200_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
