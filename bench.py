@@ -45,7 +45,7 @@ if str(ROOT) not in sys.path:
 
 METRIC = "batch edge insert+delete throughput (batch=1M, R-MAT s22)"
 UNIT = "Medges/s"
-STATUS_BYTES = 152  # sizeof(DeviceState) + sizeof(OpState): the per-op D2H status read (csrc/dg_api.cu op_end)
+STATUS_BYTES = 200  # sizeof(DeviceState) + sizeof(OpState): the per-op D2H status read (csrc/dg_api.cu op_end)
 
 
 def parse_args():
@@ -57,6 +57,8 @@ def parse_args():
     ap.add_argument("--scale", type=int, default=22, help="R-MAT scale per GPU (22 = BASELINE config[1])")
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--batch", type=int, default=1_000_000)
+    ap.add_argument("--block-size", type=int, default=32,
+                    help="edge-block size B; 32 = one 128-byte line (0 = the reference's compute_block_size rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -121,38 +123,40 @@ class ClockSampler:
 # --------------------------------------------------------------------------------------
 # algorithmic bytes per kernel launch
 # --------------------------------------------------------------------------------------
-def kernel_bytes(name: str, rep: dict, B: int, sort_passes: int) -> float | None:
-    """Algorithmic HBM bytes of ONE launch of `name` inside a delete (or insert) op.
+def kernel_bytes(name: str, rep: dict, B: int) -> float | None:
+    """Algorithmic HBM bytes of ONE launch of `name`.
 
     b = batch entries, T = touched sources, W = blocks of touched chains,
     S = slots of touched chains, M = compaction moves (all from dg_last_op_report)."""
     b, T = rep["batch_entries"], rep["touched_sources"]
     W, S, M = rep["blocks_scanned"], rep["slots_scanned"], rep["moved"]
-    if name.startswith("match_kernel"):
-        return 4 * S + 8 * W + 8 * b + 4 * T            # slab slots + worklist (handle, run) + sorted keys + counters
-    if name.startswith("classify_kernel"):
-        return 4 * S + 8 * W + 12 * M                    # re-read of matched chains + hole/survivor records
+    SL = rep.get("slots_scanned_long", 0)
+    if name.startswith("match_long"):
+        return 4 * SL + 8 * (SL // B) + 8 * b            # slab slots of long chains + worklist handles + masks + targets
+    if name.startswith("match_small"):
+        return 4 * (S - SL) + 12 * W + 8 * b + 4 * T     # slab slots + worklist (handle, run) + mask + targets + counters
+    if name.startswith("delete_holes_kernel"):
+        return 12 * W + 8 * M + 32 * T                   # worklist + masks, hole records, per-source repair
+    if name.startswith("delete_moves_kernel"):
+        return 8 * W + 16 * M
     if name.startswith("sort_pass_kernel"):
         return 16 * b                                    # 8 B key read + 8 B key write
-    if name.startswith("sort_hist_kernel"):
-        return 8 * b
     if name.startswith("pack_coo_kernel"):
         return 16 * b                                    # 2 x u32 in, u64 key out
     if name.startswith("scan_kernel"):
-        return 16 * b
-    if name.startswith("enumerate_walk_kernel"):
+        return 16 * b                                    # the largest scan of an op (run detection over the keys)
+    if name.startswith("enumerate_"):
         return 12 * W + 12 * T                           # next[] reads + worklist writes
     if name.startswith("append_kernel"):
-        return 12 * b + 32 * T
-    if name.startswith("finalize_delete_kernel"):
-        return 16 * M + 32 * T
+        return 12 * b + 32 * T + 4 * (T + b // B)
     return None
 
 
 # --------------------------------------------------------------------------------------
 # CPU baseline (reference arm and the cpu_baseline leg)
 # --------------------------------------------------------------------------------------
-def cpu_reference_run(scale: int, edge_factor: int, batch: int, warmup: int, steps: int, threads: int):
+def cpu_reference_run(scale: int, edge_factor: int, batch: int, warmup: int, steps: int, threads: int,
+                      block_size: int = 32):
     """Times the reference's CPU implementation of the step on this host.
 
     Uses oracle/_ref/libdyngraph_ref.so (the unmodified reference headers behind
@@ -177,8 +181,8 @@ def cpu_reference_run(scale: int, edge_factor: int, batch: int, warmup: int, ste
         return s, d
 
     bs, bd = gen(1, 0, E)
-    B = 32
-    if ref is not None:
+    B = block_size
+    if B == 0 and ref is not None:
         out = C.c_uint32()
         if ref.ref_compute_block_size_coo(V, C.c_void_p(bs.ctypes.data), C.c_void_p(bd.ctypes.data), E, C.byref(out)) == 0:
             B = int(out.value)
@@ -218,7 +222,7 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    r = cpu_reference_run(args.scale, args.edge_factor, args.batch, args.warmup, args.steps, threads)
+    r = cpu_reference_run(args.scale, args.edge_factor, args.batch, args.warmup, args.steps, threads, args.block_size)
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
@@ -296,7 +300,8 @@ def run_b200_arm(args):
             gen = DynamicGraph(GraphConfig(device=local, pool_blocks=1024, stream=stream.cuda_stream), 1, 1)
             src, dst = i32(E_local), i32(E_local)
             gen.gen_rmat(scale, 1, 0, src, dst, thr)
-            B = gen.compute_block_size_pairs(src)   # compute_block_size (csr.hpp:77-88) on the base graph
+            # 0 => compute_block_size (csr.hpp:77-88) on the base graph
+            B = args.block_size or gen.compute_block_size_pairs(src)
             off = torch.empty(V + 1, dtype=torch.int64, device=dev)
             csr_dst = i32(E_local)
             gen.coo_to_csr(src, dst, V, off, csr_dst)
@@ -319,6 +324,14 @@ def run_b200_arm(args):
                 bulk_ms.append((create_ms, e0.elapsed_time(e1)))
             bulk_rep = g.last_op_report()
             st = g.stats()
+            bulk_kernels = None
+            if not args.no_profile:   # one more, untimed, build with per-kernel events
+                g.close()
+                g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream), V, B)
+                g.profile_enable(True)
+                g.bulk_init(off, csr_dst)
+                g.profile_enable(False)
+                bulk_kernels = {k: round(ms * 1e3, 1) for k, (ms, _) in g.profile_report().items()}
             del off, csr_dst
             sharded = None
         else:
@@ -326,7 +339,7 @@ def run_b200_arm(args):
             gen = DynamicGraph(GraphConfig(device=local, pool_blocks=1024, stream=stream.cuda_stream), 1, 1)
             src, dst = i32(E_local), i32(E_local)
             gen.gen_rmat(scale, 1, rank * E_local, src, dst, thr)
-            B = 32 if args.edge_factor == 16 else max(1, args.edge_factor * 2)
+            B = args.block_size or 2 * args.edge_factor
             pool_blocks = int((E_local // B + V // world) * 1.6) + (8 * b) // B + 4096
             t0 = time.perf_counter()
             sharded = ShardedDynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream),
@@ -339,6 +352,7 @@ def run_b200_arm(args):
             e1.record(stream)
             stream.synchronize()
             bulk_ms = [(create_ms, e0.elapsed_time(e1))]
+            bulk_kernels = None
             g = sharded.local
             bulk_rep = g.last_op_report()
             st = g.stats()
@@ -409,7 +423,6 @@ def run_b200_arm(args):
         clocks = ClockSampler(local)
         clocks.start()
         total_ms, per_step, reps, wall_ms = timed_pass(host=False)
-        clock_rec = clocks.stop()
         launches = sum(r[0]["kernel_launches"] + r[1]["kernel_launches"] for r in reps)
         ins_ms, del_ms = split_pass()
         e2e = None
@@ -432,15 +445,11 @@ def run_b200_arm(args):
                        for k, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
             top = max(prof.items(), key=lambda kv: kv[1][0])
             name, (ms, n) = top
-            sort_passes = math.ceil(scale / 8) + math.ceil(scale / 8)
             # delete-side kernels use the delete report, insert-side the insert report
             ins_side = name.startswith("append_kernel")
-            per_launch = [kernel_bytes(name, r[0] if ins_side else r[1], B, sort_passes) for r in prof_reps]
+            per_launch = [kernel_bytes(name, r[0] if ins_side else r[1], B) for r in prof_reps]
             if per_launch[0] is not None and n:
-                launches_per_op = n / (K * (2 if name.startswith(("sort_", "scan_", "pack_")) else 1))
                 bytes_launch = sum(per_launch) / len(per_launch)
-                if name.startswith("scan_kernel"):
-                    bytes_launch = bytes_launch  # upper bound: the largest scan of the op
                 avg_ms = ms / n
                 ach = bytes_launch / (avg_ms * 1e-3) / 1e9
                 roofline = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
@@ -448,6 +457,7 @@ def run_b200_arm(args):
                             "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
                             "launches_per_step": n / K, "share_of_step": ms / tot}
 
+        clock_rec = clocks.stop()   # sampled over the timed, split, e2e and per-kernel passes
         final_st = g.stats()
         digest = g.digest()
 
@@ -470,11 +480,11 @@ def run_b200_arm(args):
         "graph": {"active_edges": final_st["active_edges"], "blocks_in_use": final_st["pool_blocks_in_use"],
                   "max_degree": final_st["max_degree"], "digest": f"{digest[0]:016x}"},
         "wall_ms_per_step": wall_ms / K,
-        "clocks": clock_rec, "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
+        "bulk_init_kernels_us": bulk_kernels, "clocks": clock_rec, "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference_run(args.scale, args.edge_factor, args.batch, 1, args.cpu_steps, os.cpu_count() or 1)
+            r = cpu_reference_run(args.scale, args.edge_factor, args.batch, 1, args.cpu_steps, os.cpu_count() or 1, B)
             line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample",
                                                      "insert_medges_s", "delete_medges_s", "bulk_insert_ms", "init_ms")}
         except Exception as e:  # the baseline is reported, never required for the CUDA number

@@ -53,6 +53,10 @@ extern "C" {
 
 /* dg_config.flags */
 #define DG_FLAG_NO_RECLAIM 1u /* reclaim_on_delete = false (graph.hpp:26) */
+/* How a COO batch is grouped by source (default: chosen per batch from V and n):
+ * RADIX = pack keys + LSD radix sort, O(n); COUNT = per-vertex counters + scan, O(V + n). */
+#define DG_FLAG_GROUP_RADIX 2u
+#define DG_FLAG_GROUP_COUNT 4u
 
 /* reference: types.hpp:16-17 (kInvalidVertex / kNullBlock) */
 #define DG_INVALID_VERTEX 0xFFFFFFFFu
@@ -115,6 +119,7 @@ typedef struct dg_op_report {
   uint64_t matched;         /* entries removed (delete) / queries answered true */
   uint64_t moved;           /* entries moved by compaction */
   uint64_t kernel_launches; /* kernels enqueued by the op */
+  uint64_t slots_scanned_long; /* part of slots_scanned handled by the long-chain path */
 } dg_op_report;
 
 /* ---- lifecycle ------------------------------------------------------- */

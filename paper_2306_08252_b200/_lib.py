@@ -12,6 +12,8 @@ from .build import LIB_PATH
 DG_OK, DG_ERR_DATA, DG_ERR_ENGINE, DG_ERR_CUDA = 0, 2, 3, 4
 DG_MEM_HOST, DG_MEM_DEVICE = 0, 1
 DG_FLAG_NO_RECLAIM = 1
+DG_FLAG_GROUP_RADIX = 2
+DG_FLAG_GROUP_COUNT = 4
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)
@@ -46,7 +48,7 @@ class DgMemory(C.Structure):
 class DgOpReport(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "batch_entries", "touched_sources", "blocks_popped", "blocks_pushed", "slots_scanned",
-        "blocks_scanned", "matched", "moved", "kernel_launches")]
+        "blocks_scanned", "matched", "moved", "kernel_launches", "slots_scanned_long")]
 
 
 # every symbol include/dyngraph_b200.h declares: name -> (restype, argtypes)

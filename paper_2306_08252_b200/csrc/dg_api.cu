@@ -51,6 +51,7 @@ struct dg_graph {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int reclaim = 1;
+  int group_mode = 0;  // 0 auto, 1 radix sort, 2 per-vertex counting
 
   uint32_t B = 0;
   uint64_t size = 0;       // logical size
@@ -72,7 +73,6 @@ struct dg_graph {
   Workspace ws;
   // compaction scratch (grown on demand, survives workspace resets)
   unsigned long long* mv_hole = nullptr;
-  uint32_t* mv_val = nullptr;
   uint64_t mv_cap = 0;
 
   std::string last_error;
@@ -164,6 +164,8 @@ GraphView view(const dg_graph* h) {
   g.ring = h->ring;
   g.ring_cap = h->NB;
   g.B = h->B;
+  g.bsh = (h->B != 0 && (h->B & (h->B - 1)) == 0) ? (int)std::countr_zero(h->B) : -1;
+  g.mw = (h->B + 31) / 32;
   g.size = (uint32_t)h->size;
   g.dst_limit = (uint32_t)std::min<uint64_t>(h->dst_limit(), 0xFFFFFFFFull);
   g.reclaim = h->reclaim;
@@ -226,15 +228,17 @@ int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
   op.err_index = ~0ull;
   op.n_runs = n_runs;
   op.aux1 = 0;
-  op.pad[0] = n_input;  // device-resident copy of the input length for scans
+  op.n_input = n_input;  // device-resident copy of the input length for scans
+  op.n_aux = h->size + 1;
   DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
   h->launches = 0;
   h->report = dg_op_report{};
   h->report.batch_entries = n_input;
   return DG_OK;
 }
-inline const unsigned long long* d_n_input(const dg_graph* h) { return &h->d_op()->pad[0]; }
+inline const unsigned long long* d_n_input(const dg_graph* h) { return &h->d_op()->n_input; }
 inline const unsigned long long* d_n_runs(const dg_graph* h) { return &h->d_op()->n_runs; }
+inline const unsigned long long* d_n_aux(const dg_graph* h) { return &h->d_op()->n_aux; }
 
 const char* detail_text(uint32_t d) {
   switch (d) {
@@ -269,6 +273,7 @@ int op_end(dg_graph* h) {
   h->report.matched = op.matched;
   h->report.moved = op.moves;
   h->report.kernel_launches = h->launches;
+  h->report.slots_scanned_long = op.slots_long;
   if (op.err != 0) {
     h->report.blocks_popped = 0;
     return fail(h, (int)op.err,
@@ -280,13 +285,13 @@ int op_end(dg_graph* h) {
 
 // ---- scan / sort launchers -------------------------------------------------
 template <class In, class Out, class Fin>
-void launch_scan(dg_graph* h, uint64_t n_bound, const unsigned long long* n_ptr, In in, Out out,
-                 Fin fin) {
+void launch_scan(dg_graph* h, const char* name, uint64_t n_bound, const unsigned long long* n_ptr,
+                 In in, Out out, Fin fin) {
   const size_t words = scan_scratch_words(n_bound);
   unsigned long long* scratch = ws_alloc<unsigned long long>(h, words);
   cudaMemsetAsync(scratch, 0, words * sizeof(unsigned long long), h->stream);
   const unsigned tiles = (unsigned)std::max<uint64_t>(1, (n_bound + kScanTile - 1) / kScanTile);
-  DG_LAUNCH(h, "scan_kernel", scan_kernel<<<tiles, kScanThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
+  DG_LAUNCH(h, name, scan_kernel<<<tiles, kScanThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
 }
 inline size_t scan_ws_bytes(uint64_t n_bound) {
   return aligned(scan_scratch_words(n_bound) * sizeof(unsigned long long));
@@ -313,38 +318,54 @@ SortPlan make_sort_plan(int lo_bits, int hi_bits) {
 
 inline size_t sort_ws_bytes(uint64_t n, int passes) {
   return aligned((size_t)kMaxPasses * kRadix * sizeof(unsigned int)) +
-         aligned((size_t)passes * (2 + sort_tiles(n) * kRadix) * sizeof(unsigned long long));
+         aligned((size_t)std::max(passes, 1) * (2 + sort_tiles(std::max<uint64_t>(n, 1)) * kRadix) * sizeof(unsigned long long));
 }
 
+// Sort scratch: per-pass raw digit histograms + per-pass look-back status.
+struct SortScratch {
+  unsigned int* hist;
+  unsigned long long* status;
+  size_t per_pass;
+};
+// Allocates and zeroes the scratch (before the kernel that fills the histograms).
+SortScratch sort_prepare(dg_graph* h, uint64_t n, const SortPlan& plan) {
+  SortScratch sc{};
+  sc.per_pass = 2 + sort_tiles(std::max<uint64_t>(n, 1)) * kRadix;
+  sc.hist = ws_alloc<unsigned int>(h, (size_t)kMaxPasses * kRadix);
+  sc.status = ws_alloc<unsigned long long>(h, (size_t)std::max(plan.passes, 1) * sc.per_pass);
+  cudaMemsetAsync(sc.hist, 0, (size_t)kMaxPasses * kRadix * sizeof(unsigned int), h->stream);
+  cudaMemsetAsync(sc.status, 0, (size_t)std::max(plan.passes, 1) * sc.per_pass * sizeof(unsigned long long), h->stream);
+  return sc;
+}
 // Sorts keys (and values) through the passes of `plan`; *keys/*vals end up
-// pointing at the buffer holding the sorted data (a or b).
+// pointing at the buffer holding the sorted data (a or b).  hist_done: the
+// producer of the keys already accumulated the histograms into sc.hist.
 void sort_keys(dg_graph* h, unsigned long long** keys, unsigned long long** keys_alt,
-               uint32_t** vals, uint32_t** vals_alt, uint64_t n, const SortPlan& plan) {
+               uint32_t** vals, uint32_t** vals_alt, uint64_t n, const SortPlan& plan,
+               const SortScratch& sc, bool hist_done) {
   if (plan.passes == 0 || n == 0) return;
-  unsigned int* hist = ws_alloc<unsigned int>(h, (size_t)kMaxPasses * kRadix);
-  const size_t per_pass = 2 + sort_tiles(n) * kRadix;
-  unsigned long long* status = ws_alloc<unsigned long long>(h, (size_t)plan.passes * per_pass);
-  cudaMemsetAsync(hist, 0, (size_t)kMaxPasses * kRadix * sizeof(unsigned int), h->stream);
-  cudaMemsetAsync(status, 0, (size_t)plan.passes * per_pass * sizeof(unsigned long long), h->stream);
-  DG_LAUNCH(h, "sort_hist_kernel", sort_hist_kernel<<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(*keys, n, plan, hist, h->d_op()));
-  DG_LAUNCH(h, "sort_scan_hist_kernel", sort_scan_hist_kernel<<<1, kRadix, 0, h->stream>>>(hist, plan.passes, h->d_op()));
+  if (!hist_done)
+    DG_LAUNCH(h, "sort_hist_kernel", sort_hist_kernel<<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(*keys, n, plan, sc.hist, h->d_op()));
   const unsigned tiles = (unsigned)sort_tiles(n);
   for (int p = 0; p < plan.passes; ++p) {
     if (vals && *vals) {
       DG_LAUNCH(h, "sort_pass_kernel<true>", sort_pass_kernel<true><<<tiles, kSortThreads, 0, h->stream>>>(
-          *keys, *keys_alt, *vals, *vals_alt, n, plan.shift[p], plan.bits[p], hist + p * kRadix,
-          status + (size_t)p * per_pass, h->d_op()));
+          *keys, *keys_alt, *vals, *vals_alt, n, plan.shift[p], plan.bits[p], sc.hist + p * kRadix,
+          sc.status + (size_t)p * sc.per_pass, h->d_op()));
       std::swap(*vals, *vals_alt);
     } else {
       DG_LAUNCH(h, "sort_pass_kernel<false>", sort_pass_kernel<false><<<tiles, kSortThreads, 0, h->stream>>>(
-          *keys, *keys_alt, nullptr, nullptr, n, plan.shift[p], plan.bits[p], hist + p * kRadix,
-          status + (size_t)p * per_pass, h->d_op()));
+          *keys, *keys_alt, nullptr, nullptr, n, plan.shift[p], plan.bits[p], sc.hist + p * kRadix,
+          sc.status + (size_t)p * sc.per_pass, h->d_op()));
     }
     std::swap(*keys, *keys_alt);
   }
 }
 
 inline int bits_for(uint64_t max_value) { return max_value == 0 ? 0 : (int)std::bit_width(max_value); }
+// sort plan of the batch ops: group by source only (no order needed among a source's targets)
+inline SortPlan src_sort_plan(const dg_graph* h, uint64_t max_src) { return make_sort_plan(0, bits_for(max_src)); }
+
 
 // ---- pool ---------------------------------------------------------------------
 int create_pool(dg_graph* h, uint32_t B) {
@@ -383,13 +404,10 @@ int ensure_mv_scratch(dg_graph* h, uint64_t entries) {
   if (entries <= h->mv_cap) return DG_OK;
   DG_CUDA(h, cudaStreamSynchronize(h->stream));
   if (h->mv_hole) cudaFree(h->mv_hole);
-  if (h->mv_val) cudaFree(h->mv_val);
   h->mv_hole = nullptr;
-  h->mv_val = nullptr;
   h->mv_cap = 0;
   const uint64_t want = entries + entries / 4 + 1024;
-  if (cudaMalloc(&h->mv_hole, want * sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMalloc(&h->mv_val, want * sizeof(uint32_t)) != cudaSuccess) {
+  if (cudaMalloc(&h->mv_hole, want * sizeof(unsigned long long)) != cudaSuccess) {
     cudaGetLastError();
     return fail(h, DG_ERR_ENGINE, "compaction scratch: device allocation failed");
   }
@@ -418,20 +436,38 @@ struct RunBuffers {
   uint32_t* run_tail;
 };
 
+// upper bound of append units: every non-empty run has at most 1 + ceil(c / B) of them
+inline uint64_t units_bound(const dg_graph* h, uint64_t runs_bound, uint64_t n_edges) {
+  return 2 * std::min<uint64_t>(runs_bound, n_edges) + n_edges / std::max<uint32_t>(h->B, 1) + 1;
+}
+
 // plan + append over a grouped batch (COO: sorted keys + detected runs; CSR: offsets).
+// csr_path: the destination range check rides in the append pass and the
+// metadata commit is a separate kernel that only runs when nothing failed.
 void enqueue_plan_append(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n_edges,
-                         uint32_t* run_deg, uint32_t* run_tail) {
+                         uint32_t* run_deg, uint32_t* run_tail, bool csr_path) {
   GraphView g = view(h);
+  const uint64_t ub = units_bound(h, runs_bound, n_edges);
   uint32_t* unit_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   uint32_t* blk_off = ws_alloc<uint32_t>(h, runs_bound + 1);
-  launch_scan(h, runs_bound, d_n_runs(h), PlanIn{g, b, run_deg, run_tail},
-              PlanOut{unit_off, blk_off}, PlanFin{g, unit_off, h->d_op(), n_edges});
-  const uint64_t units_bound = std::min<uint64_t>(2 * n_edges, runs_bound + n_edges);
-  DG_LAUNCH(h, "append_kernel", append_kernel<<<grid_for(h, units_bound, 8), 256, 0, h->stream>>>(g, b, unit_off, blk_off,
-                                                                    run_deg, run_tail, h->d_op()));
+  uint32_t* unit_run = ws_alloc<uint32_t>(h, ub);
+  launch_scan(h, "scan_kernel<plan>", runs_bound, d_n_runs(h), PlanIn{g, b},
+              PlanOut{g, b, run_deg, run_tail, unit_off, blk_off, unit_run},
+              PlanFin{g, unit_off, h->d_op(), n_edges, csr_path ? 0 : 1});
+  const int grid = grid_for(h, ub, 8 * 32);
+  if (csr_path) {
+    DG_LAUNCH(h, "append_kernel<validate>", append_kernel<true, false><<<grid, 256, 0, h->stream>>>(
+        g, b, unit_off, blk_off, unit_run, run_deg, run_tail, h->d_op()));
+    DG_LAUNCH(h, "commit_insert_kernel", commit_insert_kernel<<<grid_for(h, runs_bound, 256), 256, 0, h->stream>>>(
+        g, b, blk_off, run_deg, h->d_op()));
+  } else {
+    DG_LAUNCH(h, "append_kernel<commit>", append_kernel<false, true><<<grid, 256, 0, h->stream>>>(
+        g, b, unit_off, blk_off, unit_run, run_deg, run_tail, h->d_op()));
+  }
 }
-inline size_t plan_append_ws(uint64_t runs_bound) {
-  return 2 * aligned((runs_bound + 1) * 4) + scan_ws_bytes(runs_bound);
+inline size_t plan_append_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n_edges) {
+  return 2 * aligned((runs_bound + 1) * 4) + aligned(units_bound(h, runs_bound, n_edges) * 4) +
+         scan_ws_bytes(runs_bound);
 }
 
 struct Worklist {
@@ -439,25 +475,152 @@ struct Worklist {
   uint32_t* wl_handle;
   uint32_t* wl_run;
   uint32_t* run_deg;
+  uint2* med_items;    // (run, chunk) items of the medium / long match tiers (nullptr without a batch)
+  uint2* long_items;
+  uint32_t* big_list;  // chains longer than kLaneWalk blocks
 };
 
-Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound, int check_alive) {
+// items: every run of a tier has at least one, plus one per full chunk of its chain
+inline uint64_t med_items_bound(const dg_graph* h, uint64_t n) {
+  return n / (kTinyTargets + 1) + h->blocks_in_use() / kMedChunk + 16;
+}
+inline uint64_t long_items_bound(const dg_graph* h, uint64_t n) {
+  return n / (kMedTargets + 1) + h->blocks_in_use() / kLongChunk + 16;
+}
+inline uint64_t big_bound(const dg_graph* h) { return h->blocks_in_use() / (kLaneWalk + 1) + 16; }
+
+// n_batch: entries of the batch the runs index into (0 = no batch: export, digest)
+Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n_batch,
+                           int check_alive) {
   GraphView g = view(h);
-  Worklist w;
+  Worklist w{};
   const uint64_t wl_cap = h->blocks_in_use();
   w.wl_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   w.run_deg = ws_alloc<uint32_t>(h, runs_bound + 1);
   w.wl_handle = ws_alloc<uint32_t>(h, wl_cap + 1);
   w.wl_run = ws_alloc<uint32_t>(h, wl_cap + 1);
-  launch_scan(h, runs_bound, d_n_runs(h), EnumIn{g, b, w.run_deg, check_alive}, EnumOut{w.wl_off},
+  if (b.run_start != nullptr) {
+    w.med_items = ws_alloc<uint2>(h, med_items_bound(h, n_batch));
+    w.long_items = ws_alloc<uint2>(h, long_items_bound(h, n_batch));
+  }
+  w.big_list = ws_alloc<uint32_t>(h, big_bound(h));
+  EnumIn in{g, b, check_alive};
+  launch_scan(h, "scan_kernel<enum>", runs_bound, d_n_runs(h), in,
+              EnumOut{in, w.run_deg, w.wl_off, w.med_items, w.long_items, w.big_list, h->d_op()},
               EnumFin{w.wl_off, h->d_op(), wl_cap});
-  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_for(h, runs_bound, 8), 256, 0, h->stream>>>(
+  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_for(h, runs_bound, 256), 256, 0, h->stream>>>(
       g, b, w.wl_off, w.wl_handle, w.wl_run, h->d_op()));
+  DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_for(h, big_bound(h), 8), 256, 0, h->stream>>>(
+      g, b, w.wl_off, w.big_list, w.wl_handle, w.wl_run, h->d_op()));
   return w;
 }
-inline size_t enumerate_ws(const dg_graph* h, uint64_t runs_bound) {
+inline size_t enumerate_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n_batch) {
   return 2 * aligned((runs_bound + 1) * 4) + 2 * aligned((h->blocks_in_use() + 1) * 4) +
-         scan_ws_bytes(runs_bound);
+         aligned(med_items_bound(h, n_batch) * 8) + aligned(long_items_bound(h, n_batch) * 8) +
+         aligned(big_bound(h) * 4) + scan_ws_bytes(runs_bound);
+}
+
+// match over an enumerated worklist: three tiers by the number of targets per source
+template <bool kIsDelete>
+void enqueue_match(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t n_batch,
+                   uint32_t* run_matched, uint32_t* wl_mask, uint8_t* hit) {
+  GraphView g = view(h);
+  const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
+  DG_LAUNCH(h, kIsDelete ? "match_tiny_kernel<delete>" : "match_tiny_kernel<query>",
+            match_tiny_kernel<kIsDelete><<<grid_for(h, wl_bound, 256), 256, 0, h->stream>>>(
+                g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
+  DG_LAUNCH(h, kIsDelete ? "match_med_kernel<delete>" : "match_med_kernel<query>",
+            match_med_kernel<kIsDelete><<<grid_for(h, med_items_bound(h, n_batch), 8), 256, 0, h->stream>>>(
+                g, b, w.wl_off, w.wl_handle, w.med_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
+  const int long_grid = (int)std::min<uint64_t>(long_items_bound(h, n_batch), (uint64_t)h->sm_count * 6);
+  DG_LAUNCH(h, kIsDelete ? "match_long_kernel<delete>" : "match_long_kernel<query>",
+            match_long_kernel<kIsDelete><<<long_grid, kLongThreads, 0, h->stream>>>(
+                g, b, w.wl_off, w.wl_handle, w.long_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
+}
+
+// ---- grouping a COO batch by source --------------------------------------------------------------
+// Two strategies behind one result (a BatchView + a bound on the runs):
+//   counting: per-vertex counters, a scan over the vertices, a scatter — O(V + n);
+//   radix:    pack 64-bit keys, LSD radix sort by source, run detection — O(n).
+struct Grouped {
+  BatchView b{};
+  uint64_t runs_bound = 0;
+  uint32_t* index = nullptr;  // original position of every grouped entry (queries)
+};
+
+inline bool use_counting(const dg_graph* h, uint64_t n) {
+  if (h->group_mode == 1) return false;
+  if (h->group_mode == 2) return true;
+  return h->size + 1 <= std::max<uint64_t>(32 * n, 1ull << 22);
+}
+
+inline size_t group_ws_bytes(const dg_graph* h, uint64_t n, bool with_index, uint64_t max_src) {
+  size_t t = 0;
+  if (use_counting(h, n)) {
+    t += aligned((h->size + 2) * 4) + 2 * aligned(n * 4) + (with_index ? aligned(n * 4) : 0);
+    t += 2 * aligned((std::min<uint64_t>(n, h->size + 1) + 1) * 4) + scan_ws_bytes(h->size + 1);
+  } else {
+    t += 2 * aligned(n * 8) + (with_index ? 2 * aligned(n * 4) : 0);
+    t += sort_ws_bytes(n, src_sort_plan(h, max_src).passes);
+    t += 2 * aligned((n + 1) * 4) + scan_ws_bytes(n);
+  }
+  return t;
+}
+
+template <int kMode>
+Grouped group_batch(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, bool with_index,
+                    uint64_t max_src) {
+  GraphView g = view(h);
+  Grouped out;
+  if (use_counting(h, n)) {
+    const uint64_t nv = h->size + 1;  // + 1: the slot unknown query sources are clamped to
+    uint32_t* cnt = ws_alloc<uint32_t>(h, nv + 1);
+    uint32_t* rank = ws_alloc<uint32_t>(h, n);
+    uint32_t* gdst = ws_alloc<uint32_t>(h, n);
+    if (with_index) out.index = ws_alloc<uint32_t>(h, n);
+    out.runs_bound = std::min<uint64_t>(n, nv);
+    uint32_t* run_start = ws_alloc<uint32_t>(h, out.runs_bound + 1);
+    uint32_t* run_src = ws_alloc<uint32_t>(h, out.runs_bound + 1);
+    cudaMemsetAsync(cnt, 0, (nv + 1) * 4, h->stream);
+    DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
+        g, d_src, d_dst, (uint32_t)n, cnt, rank, h->d_op()));
+    launch_scan(h, "scan_kernel<group>", nv, d_n_aux(h), GroupIn{cnt}, GroupOut{cnt, run_src, run_start},
+                GroupFin{run_start, h->d_op()});
+    if (with_index) {
+      DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, true><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
+          g, d_src, d_dst, (uint32_t)n, cnt, rank, gdst, out.index, h->d_op()));
+    } else {
+      DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, false><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
+          g, d_src, d_dst, (uint32_t)n, cnt, rank, gdst, nullptr, h->d_op()));
+    }
+    out.b = BatchView{nullptr, gdst, run_src, run_start};
+  } else {
+    SortPlan plan = src_sort_plan(h, max_src);
+    unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
+    unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
+    uint32_t *idx = nullptr, *idx_alt = nullptr;
+    if (with_index) {
+      idx = ws_alloc<uint32_t>(h, n);
+      idx_alt = ws_alloc<uint32_t>(h, n);
+    }
+    SortScratch sc = sort_prepare(h, n, plan);
+    if (with_index) {
+      DG_LAUNCH(h, "pack_coo_kernel", pack_coo_kernel<kMode, true><<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(
+          g, d_src, d_dst, (uint32_t)n, keys, idx, plan, sc.hist, h->d_op()));
+    } else {
+      DG_LAUNCH(h, "pack_coo_kernel", pack_coo_kernel<kMode, false><<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(
+          g, d_src, d_dst, (uint32_t)n, keys, nullptr, plan, sc.hist, h->d_op()));
+    }
+    sort_keys(h, &keys, &keys_alt, with_index ? &idx : nullptr, with_index ? &idx_alt : nullptr, n, plan, sc, true);
+    out.runs_bound = n;
+    uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
+    uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
+    launch_scan(h, "scan_kernel<runs>", n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
+                RunsFin{run_start, h->d_op(), (uint32_t)n});
+    out.b = BatchView{keys, nullptr, run_src, run_start};
+    out.index = idx;
+  }
+  return out;
 }
 
 int require_pool(dg_graph* h) {
@@ -466,39 +629,31 @@ int require_pool(dg_graph* h) {
   return DG_OK;
 }
 
-// delete tail shared by the COO and CSR paths: keys are packed and validated.
-int delete_sorted_tail(dg_graph* h, unsigned long long* keys, unsigned long long* keys_alt,
-                       uint64_t n) {
+// delete over a grouped batch (COO: group_batch; CSR: the offsets are the runs)
+int delete_grouped(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n) {
   GraphView g = view(h);
-  SortPlan plan = make_sort_plan(bits_for(h->dst_limit() - 1), bits_for(h->size - 1));
-  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
-  uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
-  uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
-  launch_scan(h, n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
-              RunsFin{run_start, h->d_op(), (uint32_t)n});
-  BatchView b{keys, nullptr, run_src, run_start};
-  Worklist w = enqueue_enumerate(h, b, n, /*check_alive=*/1);
-  uint32_t* run_matched = ws_alloc<uint32_t>(h, n + 1);
-  uint32_t* hole_cnt = ws_alloc<uint32_t>(h, n + 1);
-  uint32_t* surv_cnt = ws_alloc<uint32_t>(h, n + 1);
-  uint32_t* mv_off = ws_alloc<uint32_t>(h, n + 1);
-  cudaMemsetAsync(run_matched, 0, (n + 1) * 4, h->stream);
+  Worklist w = enqueue_enumerate(h, b, runs_bound, n, /*check_alive=*/1);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  DG_LAUNCH(h, "match_kernel<true>", match_kernel<true><<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
-      g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, nullptr, h->d_op()));
+  uint32_t* run_matched = ws_alloc<uint32_t>(h, runs_bound + 1);
+  uint32_t* hole_cnt = ws_alloc<uint32_t>(h, runs_bound + 1);
+  uint32_t* surv_cnt = ws_alloc<uint32_t>(h, runs_bound + 1);
+  uint32_t* mv_off = ws_alloc<uint32_t>(h, runs_bound + 1);
+  uint32_t* wl_mask = ws_alloc<uint32_t>(h, (wl_bound + 1) * g.mw);
+  cudaMemsetAsync(run_matched, 0, (runs_bound + 1) * 4, h->stream);
+  enqueue_match<true>(h, b, w, n, run_matched, wl_mask, nullptr);
   const size_t ws_mark = h->ws.off;
   for (int attempt = 0; attempt < 2; ++attempt) {
     h->ws.off = ws_mark;
-    cudaMemsetAsync(hole_cnt, 0, (n + 1) * 4, h->stream);
-    cudaMemsetAsync(surv_cnt, 0, (n + 1) * 4, h->stream);
-    launch_scan(h, n, d_n_runs(h), MovesIn{w.run_deg, run_matched}, MovesOut{mv_off},
+    cudaMemsetAsync(hole_cnt, 0, (runs_bound + 1) * 4, h->stream);
+    cudaMemsetAsync(surv_cnt, 0, (runs_bound + 1) * 4, h->stream);
+    launch_scan(h, "scan_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{w.run_deg, run_matched}, MovesOut{mv_off},
                 MovesFin{mv_off, h->d_op(), h->mv_cap});
-    DG_LAUNCH(h, "classify_kernel", classify_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+    DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_for(h, wl_bound, 256), 256, 0, h->stream>>>(
+        g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, wl_mask, hole_cnt,
+        h->mv_hole, h->d_op()));
+    DG_LAUNCH(h, "delete_moves_kernel", delete_moves_kernel<<<grid_for(h, wl_bound, 256), 256, 0, h->stream>>>(
         g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, hole_cnt, surv_cnt,
-        h->mv_hole, h->mv_val, h->d_op()));
-    DG_LAUNCH(h, "finalize_delete_kernel", finalize_delete_kernel<<<grid_for(h, n, 8), 256, 0, h->stream>>>(
-        g, b, w.wl_off, w.wl_handle, w.run_deg, run_matched, mv_off, hole_cnt, h->mv_hole,
-        h->mv_val, h->d_op()));
+        h->mv_hole, h->d_op()));
     const int rc = op_end(h);
     if (rc != DG_OK) return rc;
     if (h->h_blk->op.aux1 == 0) return DG_OK;
@@ -508,9 +663,10 @@ int delete_sorted_tail(dg_graph* h, unsigned long long* keys, unsigned long long
   }
   return fail(h, DG_ERR_ENGINE, "delete: compaction scratch retry failed");
 }
-inline size_t delete_tail_ws(const dg_graph* h, uint64_t n, int passes) {
-  return sort_ws_bytes(n, passes) + 2 * aligned((n + 1) * 4) + scan_ws_bytes(n) +
-         enumerate_ws(h, n) + 4 * aligned((n + 1) * 4) + scan_ws_bytes(n);
+inline size_t delete_grouped_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n) {
+  const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
+  return enumerate_ws(h, runs_bound, n) + 4 * aligned((runs_bound + 1) * 4) +
+         aligned((wl_bound + 1) * ((h->B + 31) / 32) * 4) + scan_ws_bytes(runs_bound);
 }
 
 }  // namespace
@@ -539,6 +695,7 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
   h->cfg = cfg;
   h->device = cfg.device;
   h->reclaim = (cfg.flags & DG_FLAG_NO_RECLAIM) ? 0 : 1;
+  h->group_mode = (cfg.flags & DG_FLAG_GROUP_RADIX) ? 1 : ((cfg.flags & DG_FLAG_GROUP_COUNT) ? 2 : 0);
   auto bail = [&](int code, const std::string& msg) {
     g_create_error = msg;
     dg_destroy(h);
@@ -607,7 +764,6 @@ void dg_destroy(dg_graph* h) {
   if (h->h_blk) cudaFreeHost(h->h_blk);
   cudaFree(h->ws.base);
   cudaFree(h->mv_hole);
-  cudaFree(h->mv_val);
   for (auto& sp : h->prof_open) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
   for (auto e : h->prof_pool) cudaEventDestroy(e);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -624,32 +780,23 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   if (n == 0) return DG_OK;  // EmptyBatchChangesNothing
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
-  const int src_bits = bits_for(h->size - 1);
-  SortPlan plan = make_sort_plan(0, src_bits);
+  const uint64_t rb = std::min<uint64_t>(n, h->size + 1);  // runs bound of either grouping
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
-  sz.add<unsigned long long>(n); sz.add<unsigned long long>(n);
-  sz.total += sort_ws_bytes(n, plan.passes);
-  sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1);
-  sz.total += scan_ws_bytes(n) + plan_append_ws(n);
+  sz.total += group_ws_bytes(h, n, false, h->size - 1);
+  sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1);
+  // block size may still be unknown (deferred pool): size the unit list for B = 1
+  sz.total += 2 * aligned((n + 1) * 4) + aligned((3 * n + 1) * 4) + scan_ws_bytes(n);
+  (void)rb;
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const uint32_t *d_src, *d_dst;
   if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
   if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
   if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
-  GraphView g = view(h);
-  unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
-  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
-  DG_LAUNCH(h, "pack_coo_kernel<kPackInsert, false>", pack_coo_kernel<kPackInsert, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op()));
-  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
-  uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
-  uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
-  uint32_t* run_deg = ws_alloc<uint32_t>(h, n + 1);
-  uint32_t* run_tail = ws_alloc<uint32_t>(h, n + 1);
-  launch_scan(h, n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
-              RunsFin{run_start, h->d_op(), (uint32_t)n});
+  Grouped gb = group_batch<kPackInsert>(h, d_src, d_dst, n, false, h->size - 1);
+  uint32_t* run_deg = ws_alloc<uint32_t>(h, gb.runs_bound + 1);
+  uint32_t* run_tail = ws_alloc<uint32_t>(h, gb.runs_bound + 1);
   if (h->B == 0) {
     // deferred pool: compute_block_size (csr.hpp:77-88) from this first batch
     if ((rc = op_end(h)) != DG_OK) return rc;
@@ -660,10 +807,8 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
     OpState& op = h->h_blk->op;
     op.err_index = ~0ull;
     DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
-    g = view(h);
   }
-  BatchView b{keys, nullptr, run_src, run_start};
-  enqueue_plan_append(h, b, n, n, run_deg, run_tail);
+  enqueue_plan_append(h, gb.b, gb.runs_bound, n, run_deg, run_tail, /*csr_path=*/false);
   return op_end(h);
 }
 
@@ -683,7 +828,7 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<unsigned long long>(n_offsets); sz.add<uint32_t>(n_edges); }
   sz.add<uint32_t>(V + 2); sz.add<uint32_t>(V + 1); sz.add<uint32_t>(V + 1);
-  sz.total += plan_append_ws(V);
+  sz.total += 2 * aligned((V + 1) * 4) + aligned((2 * std::min<uint64_t>(V, n_edges) + n_edges + 1) * 4) + scan_ws_bytes(V);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const unsigned long long* d_off;
@@ -697,11 +842,8 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
   uint32_t* run_tail = ws_alloc<uint32_t>(h, V + 1);
   DG_LAUNCH(h, "csr_validate_offsets_kernel", csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
       g, d_off, (uint32_t)n_offsets, n_edges, /*check_dead_source=*/1, run_start, h->d_op()));
-  if (n_edges > 0) {
-    DG_LAUNCH(h, "validate_dsts_kernel", validate_dsts_kernel<<<grid_for(h, n_edges, 256 * 4), 256, 0, h->stream>>>(
-        g, d_dst, (uint32_t)n_edges, h->d_op()));
-  }
   if (n_edges == 0 || V == 0) return op_end(h);  // validated; nothing to append
+  // (the destination range check, csr.hpp:67-72, is fused into the append pass)
   if (h->B == 0) {
     DG_LAUNCH(h, "count_nonzero_runs_kernel", count_nonzero_runs_kernel<<<grid_for(h, V, 256), 256, 0, h->stream>>>(run_start, (uint32_t)V, h->d_op()));
     if ((rc = op_end(h)) != DG_OK) return rc;
@@ -715,7 +857,7 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
     DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
   }
   BatchView b{nullptr, d_dst, nullptr, run_start};
-  enqueue_plan_append(h, b, V, n_edges, run_deg, run_tail);
+  enqueue_plan_append(h, b, V, n_edges, run_deg, run_tail, /*csr_path=*/true);
   return op_end(h);
 }
 
@@ -739,24 +881,19 @@ int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
   const bool no_pool = h->B == 0;  // no pool yet => no edges: only validation can have an effect
-  const int passes = make_sort_plan(bits_for(h->dst_limit() - 1), bits_for(h->size - 1)).passes;
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
-  sz.add<unsigned long long>(n); sz.add<unsigned long long>(n);
-  if (!no_pool) sz.total += delete_tail_ws(h, n, passes);
+  sz.total += group_ws_bytes(h, n, false, h->size - 1);
+  if (!no_pool) sz.total += delete_grouped_ws(h, n, n);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const uint32_t *d_src, *d_dst;
   if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
   if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
   if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
-  GraphView g = view(h);
-  unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
-  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
-  DG_LAUNCH(h, "pack_coo_kernel<kPackDelete, false>", pack_coo_kernel<kPackDelete, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op()));
+  Grouped gb = group_batch<kPackDelete>(h, d_src, d_dst, n, false, h->size - 1);
   if (no_pool) return op_end(h);
-  return delete_sorted_tail(h, keys, keys_alt, n);
+  return delete_grouped(h, gb.b, gb.runs_bound, n);
 }
 
 int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
@@ -770,19 +907,17 @@ int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets
   if (n_edges >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   const uint64_t V = h->size;
   const uint64_t n = n_edges;
-  const int passes = V ? make_sort_plan(bits_for(h->dst_limit() - 1), bits_for(V - 1)).passes : 0;
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<unsigned long long>(n_offsets); sz.add<uint32_t>(n); }
   sz.add<uint32_t>(V + 2);
-  sz.add<unsigned long long>(n + 1); sz.add<unsigned long long>(n + 1);
-  if (h->B) sz.total += delete_tail_ws(h, std::max<uint64_t>(n, 1), passes);
+  if (h->B) sz.total += delete_grouped_ws(h, V, n);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const unsigned long long* d_off;
   const uint32_t* d_dst;
   if ((rc = stage_in(h, reinterpret_cast<const unsigned long long*>(offsets), n_offsets, mem, &d_off)) != DG_OK) return rc;
   if ((rc = stage_in(h, destinations, n, mem, &d_dst)) != DG_OK) return rc;
-  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  if ((rc = op_begin(h, n, V)) != DG_OK) return rc;
   GraphView g = view(h);
   uint32_t* run_start = ws_alloc<uint32_t>(h, V + 2);
   DG_LAUNCH(h, "csr_validate_offsets_kernel", csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
@@ -791,11 +926,9 @@ int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets
     DG_LAUNCH(h, "validate_dsts_kernel", validate_dsts_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(g, d_dst, (uint32_t)n, h->d_op()));
   }
   if (n == 0 || V == 0 || h->B == 0) return op_end(h);
-  unsigned long long* keys = ws_alloc<unsigned long long>(h, n + 1);
-  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n + 1);
-  DG_LAUNCH(h, "csr_expand_kernel", csr_expand_kernel<<<grid_for(h, (n + 31) / 32, 8), 256, 0, h->stream>>>(
-      run_start, (uint32_t)V, d_dst, (uint32_t)n, keys, h->d_op()));
-  return delete_sorted_tail(h, keys, keys_alt, n);
+  // a CSR batch is already grouped: run r is vertex r (empty runs are skipped by the enumeration)
+  BatchView b{nullptr, d_dst, nullptr, run_start};
+  return delete_grouped(h, b, V, n);
 }
 
 // ---- query ---------------------------------------------------------------------
@@ -811,14 +944,10 @@ int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64
     else DG_CUDA(h, cudaMemsetAsync(out, 0, n, h->stream));
     return DG_OK;
   }
-  SortPlan plan = make_sort_plan(bits_for(h->dst_limit()), bits_for(h->size));
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); sz.add<uint8_t>(n); }
-  sz.add<unsigned long long>(n); sz.add<unsigned long long>(n);
-  sz.add<uint32_t>(n); sz.add<uint32_t>(n);
-  sz.total += sort_ws_bytes(n, plan.passes);
-  sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1);
-  sz.total += scan_ws_bytes(n) + enumerate_ws(h, n);
+  sz.total += group_ws_bytes(h, n, true, h->size);  // ids are clamped to size (unknown source)
+  sz.total += enumerate_ws(h, n, n);
   sz.add<uint8_t>(n);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
@@ -827,26 +956,12 @@ int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64
   if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
   uint8_t* d_out = (mem == DG_MEM_HOST) ? ws_alloc<uint8_t>(h, n) : out;
   if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
-  GraphView g = view(h);
-  unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
-  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
-  uint32_t* idx = ws_alloc<uint32_t>(h, n);
-  uint32_t* idx_alt = ws_alloc<uint32_t>(h, n);
-  DG_LAUNCH(h, "pack_coo_kernel<kPackQuery, true>", pack_coo_kernel<kPackQuery, true><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      g, d_src, d_dst, (uint32_t)n, keys, idx, h->d_op()));
-  sort_keys(h, &keys, &keys_alt, &idx, &idx_alt, n, plan);
-  uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
-  uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
-  launch_scan(h, n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
-              RunsFin{run_start, h->d_op(), (uint32_t)n});
-  BatchView b{keys, nullptr, run_src, run_start};
-  Worklist w = enqueue_enumerate(h, b, n, /*check_alive=*/1);
+  Grouped gb = group_batch<kPackQuery>(h, d_src, d_dst, n, true, h->size);
+  Worklist w = enqueue_enumerate(h, gb.b, gb.runs_bound, n, /*check_alive=*/1);
   uint8_t* hit = ws_alloc<uint8_t>(h, n);
   cudaMemsetAsync(hit, 0, n, h->stream);
-  const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  DG_LAUNCH(h, "match_kernel<false>", match_kernel<false><<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
-      g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, nullptr, hit, h->d_op()));
-  DG_LAUNCH(h, "query_scatter_kernel", query_scatter_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(hit, idx, (uint32_t)n, d_out, h->d_op()));
+  enqueue_match<false>(h, gb.b, w, n, nullptr, nullptr, hit);
+  DG_LAUNCH(h, "query_scatter_kernel", query_scatter_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(hit, gb.index, (uint32_t)n, d_out, h->d_op()));
   if (mem == DG_MEM_HOST)
     DG_CUDA(h, cudaMemcpyAsync(out, d_out, n, cudaMemcpyDeviceToHost, h->stream));
   return op_end(h);
@@ -873,7 +988,7 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
     DG_CUDA(h, cudaMemsetAsync(d_off, 0, sizeof(unsigned long long), h->stream));
     if ((rc = op_end(h)) != DG_OK) return rc;
   } else {
-    launch_scan(h, V, d_n_input(h), DegIn{h->deg}, OffsetsOut{d_off}, OffsetsFin{d_off, V, h->d_op()});
+    launch_scan(h, "scan_kernel<offsets>", V, d_n_input(h), DegIn{h->deg}, OffsetsOut{d_off}, OffsetsFin{d_off, V, h->d_op()});
     if ((rc = op_end(h)) != DG_OK) return rc;
     total = h->h_blk->op.aux0;
   }
@@ -888,7 +1003,7 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
   SortPlan plan = make_sort_plan(bits_for(h->dst_limit() - 1), bits_for(V - 1));
   WsSizer sz;
   sz.add<unsigned long long>(V + 1);
-  sz.total += enumerate_ws(h, V);
+  sz.total += enumerate_ws(h, V, 0);
   if (mem == DG_MEM_HOST) sz.add<uint32_t>(total);
   if (sorted) { sz.add<unsigned long long>(total); sz.add<unsigned long long>(total); sz.total += sort_ws_bytes(total, plan.passes); }
   // (host path: offsets were copied to the caller; re-uploaded after the workspace is re-laid out)
@@ -901,7 +1016,7 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
   if ((rc = op_begin(h, V, V)) != DG_OK) return rc;
   GraphView g = view(h);
   BatchView b{nullptr, nullptr, nullptr, nullptr};
-  Worklist w = enqueue_enumerate(h, b, V, /*check_alive=*/0);
+  Worklist w = enqueue_enumerate(h, b, V, 0, /*check_alive=*/0);
   uint32_t* d_dst = (mem == DG_MEM_HOST) ? ws_alloc<uint32_t>(h, total) : destinations;
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   if (!sorted) {
@@ -912,7 +1027,8 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
     unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, total);
     DG_LAUNCH(h, "export_copy_kernel", export_copy_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
         g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, d_off2, nullptr, keys, h->d_op()));
-    sort_keys(h, &keys, &keys_alt, nullptr, nullptr, total, plan);
+    SortScratch sc = sort_prepare(h, total, plan);
+    sort_keys(h, &keys, &keys_alt, nullptr, nullptr, total, plan, sc, false);
     DG_LAUNCH(h, "keys_low_kernel", keys_low_kernel<<<grid_for(h, total, 256 * 4), 256, 0, h->stream>>>(keys, total, d_dst));
   }
   if (mem == DG_MEM_HOST)
@@ -945,12 +1061,12 @@ int dg_digest(dg_graph* h, uint64_t* out_digest, uint64_t* out_entries) {
   if (out_digest) *out_digest = 0;
   if (out_entries) *out_entries = 0;
   if (V == 0 || h->B == 0) return DG_OK;
-  int rc = ws_reserve(h, enumerate_ws(h, V));
+  int rc = ws_reserve(h, enumerate_ws(h, V, 0));
   if (rc != DG_OK) return rc;
   if ((rc = op_begin(h, V, V)) != DG_OK) return rc;
   GraphView g = view(h);
   BatchView b{nullptr, nullptr, nullptr, nullptr};
-  Worklist w = enqueue_enumerate(h, b, V, 0);
+  Worklist w = enqueue_enumerate(h, b, V, 0, 0);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   DG_LAUNCH(h, "digest_kernel", digest_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(g, w.wl_off, w.wl_handle, w.wl_run,
                                                                  w.run_deg, h->d_op()));
@@ -1081,7 +1197,7 @@ int dg_memory_get(const dg_graph* h, dg_memory* out) {
   out->pool_bytes = h->NB ? h->blocks_in_use() * ((uint64_t)h->B * 4 + 4) : 0;
   out->queue_bytes = h->NB * 4;
   out->pool_reserved_bytes = h->NB * ((uint64_t)h->B * 4 + 4);
-  out->workspace_bytes = h->ws.cap + h->mv_cap * 12;
+  out->workspace_bytes = h->ws.cap + h->mv_cap * 8;
   return DG_OK;
 }
 
@@ -1147,12 +1263,13 @@ int dg_compute_block_size_coo(dg_graph* h, const uint32_t* src, uint64_t n, int 
   g.dst_limit = 0xFFFFFFFFu;
   unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
   unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
-  DG_LAUNCH(h, "pack_coo_kernel<kPackQuery, false>", pack_coo_kernel<kPackQuery, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      g, d_src, d_src, (uint32_t)n, keys, nullptr, h->d_op()));
-  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
+  SortScratch sc = sort_prepare(h, n, plan);
+  DG_LAUNCH(h, "pack_coo_kernel<query>", pack_coo_kernel<kPackQuery, false><<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(
+      g, d_src, d_src, (uint32_t)n, keys, nullptr, plan, sc.hist, h->d_op()));
+  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan, sc, true);
   uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
   uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
-  launch_scan(h, n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
+  launch_scan(h, "scan_kernel<runs>", n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
               RunsFin{run_start, h->d_op(), (uint32_t)n});
   if ((rc = op_end(h)) != DG_OK) return rc;
   const uint64_t T = h->h_blk->op.n_runs;
@@ -1200,9 +1317,10 @@ int dg_coo_to_csr(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_
   unsigned long long* keys = ws_alloc<unsigned long long>(h, n + 1);
   unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n + 1);
   if (n > 0) {
-    DG_LAUNCH(h, "pack_coo_kernel<kPackDelete, false>", pack_coo_kernel<kPackDelete, false><<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-        g, d_src, d_dst, (uint32_t)n, keys, nullptr, h->d_op()));
-    sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
+    SortScratch sc = sort_prepare(h, n, plan);
+    DG_LAUNCH(h, "pack_coo_kernel<delete>", pack_coo_kernel<kPackDelete, false><<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(
+        g, d_src, d_dst, (uint32_t)n, keys, nullptr, plan, sc.hist, h->d_op()));
+    sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan, sc, true);
   }
   DG_LAUNCH(h, "keys_to_offsets_kernel", keys_to_offsets_kernel<<<grid_for(h, n + 1, 256), 256, 0, h->stream>>>(
       keys, (uint32_t)n, vertex_count, reinterpret_cast<unsigned long long*>(offsets_dev),
@@ -1245,7 +1363,8 @@ int dg_route_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t
   unsigned long long* d_counts = ws_alloc<unsigned long long>(h, world + 2);
   DG_LAUNCH(h, "route_keys_kernel", route_keys_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
       src, (uint32_t)n, world, bits, (uint32_t)std::min<uint64_t>(vertex_count, 0xFFFFFFFFull), keys, h->d_op()));
-  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan);
+  SortScratch sc = sort_prepare(h, n, plan);
+  sort_keys(h, &keys, &keys_alt, nullptr, nullptr, n, plan, sc, false);
   DG_LAUNCH(h, "route_gather_kernel", route_gather_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
       keys, src, dst, (uint32_t)n, world, bits, out_src_local, out_dst, out_index, d_counts, h->d_op()));
   std::vector<unsigned long long> ends(world + 1);

@@ -62,7 +62,15 @@ struct OpState {
   unsigned long long pushed;      // blocks returned to the ring
   unsigned long long aux0;        // op-specific
   unsigned long long aux1;
-  unsigned long long pad[3];
+  unsigned long long n_input;     // device-resident copy of the input length (scan bound)
+  unsigned long long n_items;     // CTA work items of the long-chain match path
+  unsigned long long n_edges;     // entries an insert commits to active_edges
+  unsigned long long slots_long;  // part of `slots` inspected by the long-chain (shared-memory table) path
+  unsigned long long n_big;       // chains walked by a whole warp (enumerate_big_kernel)
+  unsigned long long n_med;       // warp work items of the medium match tier
+  unsigned long long n_aux;       // second device-resident scan bound (vertex count of the counting group-by)
+  unsigned int med_cursor;        // dynamic work distribution of the medium / long match tiers
+  unsigned int long_cursor;
 };
 
 __device__ __forceinline__ void set_error(OpState* op, uint32_t code, uint32_t detail,
@@ -217,26 +225,23 @@ struct SortPlan {
 
 __host__ __device__ inline size_t sort_tiles(uint64_t n) { return (n + kSortTile - 1) / kSortTile; }
 
-// Global histogram of every pass in one read of the keys.
-// hist layout: [pass][256] u32.
-__global__ void __launch_bounds__(256)
-sort_hist_kernel(const unsigned long long* __restrict__ keys, uint64_t n, SortPlan plan,
-                 unsigned int* __restrict__ hist, const OpState* __restrict__ op_guard) {
-  if (op_guard != nullptr && op_guard->err != 0) return;
-  __shared__ unsigned int s_hist[kMaxPasses * kRadix];
-  for (int i = threadIdx.x; i < plan.passes * kRadix; i += blockDim.x) s_hist[i] = 0;
-  __syncthreads();
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned long long k = keys[i];
+// Accumulates one key into the per-pass shared histograms (layout [pass][256]).
+__device__ __forceinline__ void hist_add(unsigned int* s_hist, const SortPlan& plan,
+                                         unsigned long long k) {
 #pragma unroll
-    for (int p = 0; p < kMaxPasses; ++p) {
-      if (p < plan.passes) {
-        const unsigned d = (unsigned)(k >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u);
-        atomicAdd(&s_hist[p * kRadix + d], 1u);
-      }
+  for (int p = 0; p < kMaxPasses; ++p) {
+    if (p < plan.passes) {
+      const unsigned d = (unsigned)(k >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u);
+      atomicAdd(&s_hist[p * kRadix + d], 1u);
     }
   }
+}
+__device__ __forceinline__ void hist_clear(unsigned int* s_hist, const SortPlan& plan) {
+  for (int i = threadIdx.x; i < plan.passes * kRadix; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+}
+__device__ __forceinline__ void hist_flush(const unsigned int* s_hist, const SortPlan& plan,
+                                           unsigned int* __restrict__ hist) {
   __syncthreads();
   for (int i = threadIdx.x; i < plan.passes * kRadix; i += blockDim.x) {
     const unsigned c = s_hist[i];
@@ -244,51 +249,62 @@ sort_hist_kernel(const unsigned long long* __restrict__ keys, uint64_t n, SortPl
   }
 }
 
-// Exclusive scan of each pass's 256 bins (one block, 256 threads).
-__global__ void __launch_bounds__(kRadix)
-sort_scan_hist_kernel(unsigned int* __restrict__ hist, int passes,
-                      const OpState* __restrict__ op_guard) {
+// Global histogram of every pass in one read of the keys (RAW counts; each
+// scatter pass turns its 256 counts into digit bases itself).
+// hist layout: [pass][256] u32.  Producers that already stream the keys (the
+// COO pack kernels) fold this into their own pass instead.
+__global__ void __launch_bounds__(256)
+sort_hist_kernel(const unsigned long long* __restrict__ keys, uint64_t n, SortPlan plan,
+                 unsigned int* __restrict__ hist, const OpState* __restrict__ op_guard) {
   if (op_guard != nullptr && op_guard->err != 0) return;
-  __shared__ unsigned int s_warp[kRadix / 32];
-  for (int p = 0; p < passes; ++p) {
-    const unsigned c = hist[p * kRadix + threadIdx.x];
-    unsigned incl = c;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      unsigned t = __shfl_up_sync(kFull, incl, d);
-      if (lane_id() >= d) incl += t;
-    }
-    if (lane_id() == 31) s_warp[threadIdx.x >> 5] = incl;
-    __syncthreads();
-    unsigned warp_excl = 0;
-    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) warp_excl += s_warp[w];
-    hist[p * kRadix + threadIdx.x] = warp_excl + incl - c;
-    __syncthreads();
-  }
+  __shared__ unsigned int s_hist[kMaxPasses * kRadix];
+  hist_clear(s_hist, plan);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    hist_add(s_hist, plan, keys[i]);
+  hist_flush(s_hist, plan, hist);
 }
 
 // One scatter pass.  status: [0] ticket, then per tile 256 u64 words.
-// Must be zeroed before the launch.
+// Must be zeroed before the launch.  digit_count: this pass's RAW histogram.
 template <bool kHasValues>
 __global__ void __launch_bounds__(kSortThreads)
 sort_pass_kernel(const unsigned long long* __restrict__ keys_in,
                  unsigned long long* __restrict__ keys_out,
                  const unsigned int* __restrict__ vals_in, unsigned int* __restrict__ vals_out,
-                 uint64_t n, int shift, int bits, const unsigned int* __restrict__ digit_base,
+                 uint64_t n, int shift, int bits, const unsigned int* __restrict__ digit_count,
                  unsigned long long* status, const OpState* __restrict__ op_guard) {
   if (op_guard != nullptr && op_guard->err != 0) return;
   constexpr int kWarps = kSortThreads / 32;
+  static_assert(kSortThreads == kRadix, "thread d owns digit d");
   __shared__ unsigned int s_cnt[kWarps][kRadix];  // per-warp digit counts -> exclusive offsets
   __shared__ unsigned long long s_goff[kRadix];   // global base of each digit for this tile
+  __shared__ unsigned int s_wsum[kWarps];
   __shared__ unsigned int s_tile;
   if (threadIdx.x == 0) s_tile = atomicAdd(reinterpret_cast<unsigned int*>(status), 1u);
   for (int i = threadIdx.x; i < kWarps * kRadix; i += kSortThreads) (&s_cnt[0][0])[i] = 0;
-  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  // exclusive scan of the 256 raw digit counts (thread d -> base of digit d)
+  unsigned int digit_base;
+  {
+    const unsigned c = digit_count[threadIdx.x];
+    unsigned incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    unsigned warp_excl = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) warp_excl += (w < warp) ? s_wsum[w] : 0u;
+    digit_base = warp_excl + incl - c;
+  }
   const unsigned int tile = s_tile;
   unsigned long long* tile_status = status + 2;
 
-  const int warp = threadIdx.x >> 5;
-  const int lane = lane_id();
   const unsigned lt_mask = (1u << lane) - 1u;
   const unsigned dmask = (1u << bits) - 1u;
   const uint64_t warp_base = (uint64_t)tile * kSortTile + (uint64_t)warp * (32 * kSortItems);
@@ -335,18 +351,28 @@ sort_pass_kernel(const unsigned long long* __restrict__ keys_in,
       st_volatile_u64(my, kFlagPre | tile_cnt);
     } else {
       st_volatile_u64(my, kFlagAgg | tile_cnt);
+      // look back over the predecessors, kLook status words in flight at a time
+      constexpr int kLook = 8;
       long long look = (long long)tile - 1;
-      while (true) {
-        unsigned long long w = ld_volatile_u64(tile_status + (size_t)look * kRadix + d);
-        while ((w & kFlagMask) == 0)
-          w = ld_volatile_u64(tile_status + (size_t)look * kRadix + d);
-        excl += w & kValMask;
-        if ((w & kFlagMask) == kFlagPre) break;
-        --look;
+      bool done = false;
+      while (!done) {
+        unsigned long long w[kLook];
+#pragma unroll
+        for (int q = 0; q < kLook; ++q)
+          w[q] = (look - q >= 0) ? ld_volatile_u64(tile_status + (size_t)(look - q) * kRadix + d) : kFlagPre;
+#pragma unroll
+        for (int q = 0; q < kLook; ++q) {
+          if (done) break;
+          while ((w[q] & kFlagMask) == 0)   // predecessor not published yet
+            w[q] = ld_volatile_u64(tile_status + (size_t)(look - q) * kRadix + d);
+          excl += w[q] & kValMask;
+          if ((w[q] & kFlagMask) == kFlagPre) done = true;
+        }
+        look -= kLook;
       }
       st_volatile_u64(my, kFlagPre | (excl + tile_cnt));
     }
-    s_goff[d] = (unsigned long long)digit_base[d] + excl;
+    s_goff[d] = (unsigned long long)digit_base + excl;
   }
   __syncthreads();
 #pragma unroll

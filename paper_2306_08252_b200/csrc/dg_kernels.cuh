@@ -32,6 +32,8 @@ struct GraphView {
   uint32_t* ring;
   unsigned long long ring_cap;  // == NB
   uint32_t B;
+  int bsh;             // log2(B) when B is a power of two, else -1
+  uint32_t mw;         // 32-bit match-mask words per block: ceil(B / 32)
   uint32_t size;       // logical size at launch
   uint32_t dst_limit;  // destinations must be < dst_limit (== size single-GPU)
   int reclaim;
@@ -52,6 +54,13 @@ __device__ __forceinline__ uint32_t batch_src(const BatchView& b, uint32_t r) {
   return b.run_src ? b.run_src[r] : r;
 }
 __device__ __forceinline__ uint32_t ceil_div(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+// x / B and ceil(x / B) with the shift fast path (B = 32 is the native block: one 128-byte line)
+__device__ __forceinline__ uint32_t div_b(const GraphView& g, uint32_t x) {
+  return g.bsh >= 0 ? (x >> g.bsh) : (x / g.B);
+}
+__device__ __forceinline__ uint32_t blocks_for(const GraphView& g, uint32_t x) {
+  return div_b(g, x + g.B - 1);
+}
 
 __device__ __forceinline__ unsigned long long block_reduce_sum(unsigned long long v,
                                                                unsigned long long* s_warp) {
@@ -97,11 +106,15 @@ enum PackMode : int { kPackInsert = 0, kPackDelete = 1, kPackQuery = 2 };
 // csr.hpp:67-72 (destination range), graph.hpp:322-327 (dead source on insert).
 // Query mode never fails: ids outside the graph are clamped to values no
 // stored entry can equal (graph.hpp:229 unknown source -> false).
+// The radix-sort digit histograms of the keys are accumulated in the same
+// pass (hist != nullptr), so the sort never re-reads the batch for them.
 template <int kMode, bool kWithIndex>
-__global__ void pack_coo_kernel(GraphView g, const uint32_t* __restrict__ src,
-                                const uint32_t* __restrict__ dst, uint32_t n,
-                                unsigned long long* __restrict__ keys,
-                                uint32_t* __restrict__ index, OpState* op) {
+__global__ void __launch_bounds__(256)
+pack_coo_kernel(GraphView g, const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                uint32_t n, unsigned long long* __restrict__ keys, uint32_t* __restrict__ index,
+                SortPlan plan, unsigned int* __restrict__ hist, OpState* op) {
+  __shared__ unsigned int s_hist[kMaxPasses * kRadix];
+  if (hist != nullptr) hist_clear(s_hist, plan);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint32_t s = src[i], d = dst[i];
     if (kMode == kPackQuery) {
@@ -116,8 +129,134 @@ __global__ void pack_coo_kernel(GraphView g, const uint32_t* __restrict__ src,
       }
       if (d >= g.dst_limit) set_error(op, 2, kErrDstRange, i);
     }
-    keys[i] = ((unsigned long long)s << 32) | d;
+    const unsigned long long k = ((unsigned long long)s << 32) | d;
+    keys[i] = k;
     if (kWithIndex) index[i] = i;
+    if (hist != nullptr) hist_add(s_hist, plan, k);
+  }
+  if (hist != nullptr) hist_flush(s_hist, plan, hist);
+}
+
+// ---------------------------------------------------------------------------
+// COO staging, counting variant: group the batch by source with a per-vertex
+// counter array instead of a radix sort — count, scan over the vertices,
+// scatter.  Used when the vertex count is within a small multiple of the batch
+// (the scan is O(V)); the radix path covers small batches on large graphs.
+// The order of a source's entries inside its group is the arrival order of the
+// atomics, which the multiset semantics do not observe.
+// ---------------------------------------------------------------------------
+// validate (csr.hpp:67-72, graph.hpp:322-327) + count entries per source.
+// Four entries per thread, each stage issued for all four before the next
+// (loads -> alive-bit loads -> atomics), so the dependent round trips overlap.
+constexpr int kGroupItems = 4;
+template <int kMode>
+__global__ void __launch_bounds__(256)
+group_count_kernel(GraphView g, const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                   uint32_t n, uint32_t* __restrict__ cnt, uint32_t* __restrict__ rank, OpState* op) {
+  const uint32_t base = blockIdx.x * (256 * kGroupItems) + threadIdx.x;
+  uint32_t s[kGroupItems], d[kGroupItems];
+  bool ok[kGroupItems];
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q) {
+    const uint32_t i = base + q * 256;
+    ok[q] = i < n;
+    s[q] = ok[q] ? src[i] : 0u;
+    d[q] = ok[q] ? dst[i] : 0u;
+  }
+  uint32_t aw[kGroupItems];
+  if (kMode == kPackInsert) {
+#pragma unroll
+    for (int q = 0; q < kGroupItems; ++q) aw[q] = (ok[q] && s[q] < g.size) ? g.alive[s[q] >> 5] : 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q) {
+    if (!ok[q]) continue;
+    const uint32_t i = base + q * 256;
+    if (kMode == kPackQuery) {
+      if (s[q] >= g.size) s[q] = g.size;  // cnt has size + 1 entries: the extra one collects unknown sources
+    } else {
+      if (s[q] >= g.size) {
+        set_error(op, 2, kErrSrcRange, i);
+        ok[q] = false;
+      } else if (kMode == kPackInsert && !((aw[q] >> (s[q] & 31)) & 1u)) {
+        set_error(op, 2, kErrDeadSource, i);
+        ok[q] = false;
+      }
+      if (d[q] >= g.dst_limit) {
+        set_error(op, 2, kErrDstRange, i);
+        ok[q] = false;
+      }
+    }
+  }
+  // the returned count is the entry's rank inside its source's group
+  uint32_t rk[kGroupItems];
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q)
+    if (ok[q]) rk[q] = atomicAdd(&cnt[s[q]], 1u);
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q)
+    if (ok[q]) rank[base + q * 256] = rk[q];
+}
+
+// scan over the vertices: packed value [63:32] touched sources, [31:0] entries
+struct GroupIn {
+  const uint32_t* cnt;
+  __device__ unsigned long long operator()(unsigned long long v) const {
+    const uint32_t c = cnt[v];
+    return ((unsigned long long)(c ? 1u : 0u) << 32) | c;
+  }
+};
+struct GroupOut {
+  uint32_t* cnt;        // becomes the group start of each touched source
+  uint32_t* run_src;
+  uint32_t* run_start;
+  __device__ void operator()(unsigned long long v, unsigned long long excl,
+                             unsigned long long val) const {
+    if ((uint32_t)val) {
+      const uint32_t r = (uint32_t)(excl >> 32);
+      run_src[r] = (uint32_t)v;
+      run_start[r] = (uint32_t)excl;
+      cnt[v] = (uint32_t)excl;
+    }
+  }
+};
+struct GroupFin {
+  uint32_t* run_start;
+  OpState* op;
+  __device__ void operator()(unsigned long long total) const {
+    run_start[total >> 32] = (uint32_t)total;
+    op->n_runs = total >> 32;
+  }
+};
+
+template <int kMode, bool kWithIndex>
+__global__ void __launch_bounds__(256)
+group_scatter_kernel(GraphView g, const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                     uint32_t n, const uint32_t* __restrict__ start, const uint32_t* __restrict__ rank,
+                     uint32_t* __restrict__ out_dst, uint32_t* __restrict__ out_index, OpState* op) {
+  if (op->err) return;  // a rejected batch was counted only partially
+  const uint32_t base = blockIdx.x * (256 * kGroupItems) + threadIdx.x;
+  uint32_t s[kGroupItems], d[kGroupItems], pos[kGroupItems];
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q) {
+    const uint32_t i = base + q * 256;
+    s[q] = i < n ? src[i] : 0u;
+    d[q] = i < n ? dst[i] : 0u;
+    pos[q] = i < n ? rank[i] : 0u;
+    if (kMode == kPackQuery) {
+      if (s[q] >= g.size) s[q] = g.size;
+      if (d[q] >= g.dst_limit) d[q] = g.dst_limit;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q)
+    if (base + q * 256 < n) pos[q] += start[s[q]];
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q) {
+    if (base + q * 256 < n) {
+      out_dst[pos[q]] = d[q];
+      if (kWithIndex) out_index[pos[q]] = base + q * 256;
+    }
   }
 }
 
@@ -232,35 +371,46 @@ __global__ void csr_expand_kernel(const uint32_t* __restrict__ run_start, uint32
 constexpr int kPackShift = 31;
 constexpr unsigned long long kPackLoMask = (1ull << kPackShift) - 1ull;
 
+// (The In functors of the scans are PURE loads: the scan kernel issues the 8
+// items of a thread back to back, and a store in between would serialise them.)
 struct PlanIn {
   GraphView g;
   BatchView b;
-  uint32_t* run_deg;
-  uint32_t* run_tail;
   __device__ unsigned long long operator()(unsigned long long r64) const {
     const uint32_t r = (uint32_t)r64;
     const uint32_t v = batch_src(b, r);
     const uint32_t c = b.run_start[r + 1] - b.run_start[r];
-    const uint32_t d = g.deg[v];
-    run_deg[r] = d;
-    run_tail[r] = g.tail[v];
     if (c == 0) return 0ull;
+    const uint32_t d = g.deg[v];
     // space left in the tail block == block_size - last_insert_offset (graph.hpp:149-150)
-    const uint32_t nb = ceil_div(d, g.B);
+    const uint32_t nb = blocks_for(g, d);
     const uint32_t space = nb * g.B - d;
     const uint32_t fill = min(c, space);
-    const uint32_t need = ceil_div(c - fill, g.B);  // graph.hpp:152-153
+    const uint32_t need = blocks_for(g, c - fill);  // graph.hpp:152-153
     const uint32_t units = need + (fill > 0 ? 1u : 0u);
     return ((unsigned long long)units << kPackShift) | need;
   }
 };
+// Besides the two exclusive offsets, every unit records its run so the append
+// kernel never searches (a hub's few thousand units are plain stores here).
 struct PlanOut {
+  GraphView g;
+  BatchView b;
+  uint32_t* run_deg;   // snapshots of deg/tail: append publishes the new values while other
+  uint32_t* run_tail;  // units of the same source still need the old ones
   uint32_t* unit_off;
   uint32_t* blk_off;
+  uint32_t* unit_run;
   __device__ void operator()(unsigned long long r, unsigned long long excl,
-                             unsigned long long) const {
-    unit_off[r] = (uint32_t)(excl >> kPackShift);
+                             unsigned long long v) const {
+    const uint32_t vtx = batch_src(b, (uint32_t)r);
+    run_deg[r] = g.deg[vtx];
+    run_tail[r] = g.tail[vtx];
+    const uint32_t uo = (uint32_t)(excl >> kPackShift);
+    unit_off[r] = uo;
     blk_off[r] = (uint32_t)(excl & kPackLoMask);
+    const uint32_t units = (uint32_t)(v >> kPackShift);
+    for (uint32_t j = 0; j < units; ++j) unit_run[uo + j] = (uint32_t)r;
   }
 };
 struct PlanFin {
@@ -268,12 +418,14 @@ struct PlanFin {
   uint32_t* unit_off;
   OpState* op;
   unsigned long long n_edges;
+  int commit_globals;  // COO path: validation is complete, commit here; CSR path: commit_insert_kernel
   __device__ void operator()(unsigned long long total) const {
     const unsigned long long need = total & kPackLoMask;
     const unsigned long long units = total >> kPackShift;
     unit_off[op->n_runs] = (uint32_t)units;
     op->n_units = units;
     op->total_need = need;
+    op->n_edges = n_edges;
     DeviceState* st = g.st;
     // ensure_available (block_pool.hpp:177-189): fail BEFORE any mutation
     if (need > st->rear - st->front) {
@@ -283,88 +435,208 @@ struct PlanFin {
       return;
     }
     op->front_old = st->front;
-    st->front += need;              // commit_front (block_pool.hpp:162-166)
-    st->active_edges += n_edges;    // graph.hpp:186
+    if (commit_globals) {
+      st->front += need;              // commit_front (block_pool.hpp:162-166)
+      st->active_edges += n_edges;    // graph.hpp:186
+    }
   }
 };
 
+// ring slot of queue position front_old + off, off < ring_cap (pop_range, block_pool.hpp:148-158)
+__device__ __forceinline__ uint32_t ring_at(const GraphView& g, unsigned long long base_mod,
+                                            unsigned long long off) {
+  unsigned long long i = base_mod + off;
+  if (i >= g.ring_cap) i -= g.ring_cap;
+  return g.ring[i];
+}
+
 // ---------------------------------------------------------------------------
-// insert: append (graph.hpp:333-372) — one warp per unit, a unit being either
-// the free tail of a source's last block or one fresh block.
+// insert: append (graph.hpp:333-372).  A unit is either the free tail of a
+// source's last block or one fresh block.  A warp takes 32 consecutive units:
+// each lane resolves ONE unit's metadata and links (one round of independent
+// loads for 32 units), then the warp copies the 32 units' entries with
+// coalesced loads/stores, four units in flight.
+//   kValidateDst: CSR path — the destination range check (csr.hpp:67-72) is
+//     fused into this single pass over the batch; entries land only in free
+//     slots (tail space beyond deg, blocks still owned by the queue), so a
+//     late failure leaves nothing observable and commit_insert_kernel never runs.
+//   kCommit: COO path — validation finished before the sort, so the last unit
+//     of a source publishes deg/tail here.
 // ---------------------------------------------------------------------------
+template <bool kValidateDst, bool kCommit>
 __global__ void __launch_bounds__(256)
 append_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ unit_off,
-              const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ run_deg,
-              const uint32_t* __restrict__ run_tail, const OpState* op) {
+              const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ unit_run,
+              const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ run_tail,
+              OpState* op) {
   if (op->err) return;
-  const uint32_t T = (uint32_t)op->n_runs;
   const uint32_t U = (uint32_t)op->n_units;
-  const unsigned long long front_old = op->front_old;
+  const unsigned long long base_mod = op->front_old % g.ring_cap;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
-  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
-    const uint32_t r = warp_find_run(unit_off, T, u);
-    const uint32_t j = u - unit_off[r];
-    const uint32_t v = batch_src(b, r);
-    const uint32_t rs = b.run_start[r];
-    const uint32_t c = b.run_start[r + 1] - rs;
-    const uint32_t d = run_deg[r];
-    const uint32_t nb_old = ceil_div(d, g.B);
-    const uint32_t space = nb_old * g.B - d;
-    const uint32_t fill = min(c, space);
-    const uint32_t has_fill = fill > 0 ? 1u : 0u;
-    const uint32_t need = ceil_div(c - fill, g.B);
-    uint32_t blk, off0, src0, cnt;
-    if (has_fill && j == 0) {
-      blk = run_tail[r];                 // resume at the last-insert position (graph.hpp:344-349)
-      off0 = d - (nb_old - 1) * g.B;
-      src0 = rs;
-      cnt = fill;
-    } else {
-      const uint32_t f = j - has_fill;
-      const unsigned long long pos = front_old + blk_off[r] + f;  // pop_range (block_pool.hpp:148-158)
-      blk = g.ring[pos % g.ring_cap];
-      off0 = 0;
-      src0 = rs + fill + f * g.B;
-      cnt = min(g.B, c - fill - f * g.B);
-      if (lane == 0) {
-        const uint32_t prev = (f == 0) ? (nb_old > 0 ? run_tail[r] : kNull)
-                                       : g.ring[(pos - 1) % g.ring_cap];
+  for (uint32_t u0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; u0 < U; u0 += nwarps * 32u) {
+    const uint32_t u = u0 + lane;
+    uint32_t blk = 0, off0 = 0, src0 = 0, cnt = 0;
+    if (u < U) {
+      const uint32_t r = unit_run[u];
+      const uint32_t j = u - unit_off[r];
+      const uint32_t v = batch_src(b, r);
+      const uint32_t rs = b.run_start[r];
+      const uint32_t c = b.run_start[r + 1] - rs;
+      const uint32_t d = run_deg[r];
+      const uint32_t nb_old = blocks_for(g, d);
+      const uint32_t space = nb_old * g.B - d;
+      const uint32_t fill = min(c, space);
+      const uint32_t has_fill = fill > 0 ? 1u : 0u;
+      const uint32_t need = blocks_for(g, c - fill);
+      if (has_fill && j == 0) {
+        blk = run_tail[r];                 // resume at the last-insert position (graph.hpp:344-349)
+        off0 = d - (nb_old - 1) * g.B;
+        src0 = rs;
+        cnt = fill;
+      } else {
+        const uint32_t f = j - has_fill;
+        const unsigned long long o = (unsigned long long)blk_off[r] + f;
+        blk = ring_at(g, base_mod, o);
+        off0 = 0;
+        src0 = rs + fill + f * g.B;
+        cnt = min(g.B, c - fill - f * g.B);
+        const uint32_t prev = (f == 0) ? (nb_old > 0 ? run_tail[r] : kNull) : ring_at(g, base_mod, o - 1);
         if (prev == kNull) g.head[v] = blk; else g.next[prev] = blk;
         if (f == need - 1) {
           g.next[blk] = kNull;
-          g.tail[v] = blk;
+          if (kCommit) g.tail[v] = blk;
+        }
+      }
+      if (kCommit && j == need + has_fill - 1) g.deg[v] = d + c;
+    }
+    const uint32_t nvalid = min(32u, U - u0);
+    constexpr int kFly = 8;  // units in flight per warp
+    for (uint32_t l0 = 0; l0 < nvalid; l0 += kFly) {
+      uint32_t vb[kFly], vo[kFly], vs[kFly], vc[kFly], val[kFly];
+#pragma unroll
+      for (int q = 0; q < kFly; ++q) {
+        const int l = (int)(l0 + q) & 31;
+        vb[q] = __shfl_sync(kFull, blk, l);
+        vo[q] = __shfl_sync(kFull, off0, l);
+        vs[q] = __shfl_sync(kFull, src0, l);
+        const uint32_t cq = __shfl_sync(kFull, cnt, l);
+        vc[q] = (l0 + q < nvalid) ? cq : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < kFly; ++q)
+        if ((uint32_t)lane < vc[q]) val[q] = batch_value(b, vs[q] + lane);
+#pragma unroll
+      for (int q = 0; q < kFly; ++q) {
+        if ((uint32_t)lane < vc[q]) {
+          if (kValidateDst && val[q] >= g.dst_limit) set_error(op, 2, kErrDstRange, vs[q] + lane);
+          g.slab[(unsigned long long)vb[q] * g.B + vo[q] + lane] = val[q];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kFly; ++q) {
+        for (uint32_t s = 32 + lane; s < vc[q]; s += 32) {  // blocks wider than a warp
+          const uint32_t x = batch_value(b, vs[q] + s);
+          if (kValidateDst && x >= g.dst_limit) set_error(op, 2, kErrDstRange, vs[q] + s);
+          g.slab[(unsigned long long)vb[q] * g.B + vo[q] + s] = x;
         }
       }
     }
-    uint32_t* out = g.slab + (unsigned long long)blk * g.B + off0;
-    for (uint32_t s = lane; s < cnt; s += 32) out[s] = batch_value(b, src0 + s);
-    if (lane == 0 && j == need + has_fill - 1) g.deg[v] = d + c;
+  }
+}
+
+// CSR path commit: runs only when every check passed (validate-then-mutate,
+// graph.hpp:168-171): publishes deg/tail per source and the queue front /
+// live-edge count (block_pool.hpp:162-166, graph.hpp:186).
+__global__ void __launch_bounds__(256)
+commit_insert_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ blk_off,
+                     const uint32_t* __restrict__ run_deg, OpState* op) {
+  if (op->err) return;
+  const uint32_t T = (uint32_t)op->n_runs;
+  const unsigned long long base_mod = op->front_old % g.ring_cap;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < T; r += gridDim.x * blockDim.x) {
+    const uint32_t c = b.run_start[r + 1] - b.run_start[r];
+    if (c == 0) continue;
+    const uint32_t v = batch_src(b, r);
+    const uint32_t d = run_deg[r];
+    const uint32_t nb_old = blocks_for(g, d);
+    const uint32_t fill = min(c, nb_old * g.B - d);
+    const uint32_t need = blocks_for(g, c - fill);
+    g.deg[v] = d + c;
+    if (need > 0) g.tail[v] = ring_at(g, base_mod, (unsigned long long)blk_off[r] + need - 1);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g.st->front += op->total_need;
+    g.st->active_edges += op->n_edges;
   }
 }
 
 // ---------------------------------------------------------------------------
-// chain enumeration: touched sources -> flat list of their blocks
+// chain enumeration: touched sources -> flat list of their blocks (+ the CTA
+// work items of the long-chain match path)
 // ---------------------------------------------------------------------------
+constexpr uint32_t kLaneWalk = 16;       // chains up to this many blocks are walked by one lane
+// Match tiers by the number of targets k the batch holds for a source:
+//   k <= kTinyTargets               thread-per-block register compare (match_tiny_kernel)
+//   kTinyTargets < k <= kMedTargets a warp per 32-block chunk, per-warp shared-memory table
+//   k > kMedTargets                 a CTA per 256-block chunk, CTA-wide shared-memory table
+constexpr uint32_t kTinyTargets = 8;
+constexpr uint32_t kMedTargets = 128;
+constexpr uint32_t kMedChunk = 32;       // blocks per warp item of the medium path
+// wl_run entries carry the tier in the top bit (set = NOT tiny) so the tiny
+// kernel decides from its first load; runs index fewer than 2^31 entries.
+constexpr uint32_t kTierBit = 0x80000000u;
+constexpr uint32_t kRunMask = 0x7FFFFFFFu;
+__device__ __forceinline__ uint32_t run_tag(const BatchView& b, uint32_t r) {
+  if (b.run_start == nullptr) return r;
+  return (b.run_start[r + 1] - b.run_start[r] > kTinyTargets) ? (r | kTierBit) : r;
+}
+constexpr uint32_t kLongChunk = 256;     // blocks per CTA item of the long path
+
 struct EnumIn {
   GraphView g;
   BatchView b;
-  uint32_t* run_deg;
   int check_alive;  // delete/query skip dead or unknown sources (graph.hpp:205, :229)
-  __device__ unsigned long long operator()(unsigned long long r64) const {
-    const uint32_t r = (uint32_t)r64;
+  __device__ uint32_t degree(uint32_t r) const {
+    if (b.run_start != nullptr && b.run_start[r + 1] == b.run_start[r]) return 0;  // empty run (CSR batches)
     const uint32_t v = batch_src(b, r);
     uint32_t d = 0;
     if (v < g.size && (!check_alive || bit_test(g.alive, v))) d = g.deg[v];
-    run_deg[r] = d;
-    return ceil_div(d, g.B);
+    return d;
+  }
+  __device__ unsigned long long operator()(unsigned long long r64) const {
+    return blocks_for(g, degree((uint32_t)r64));
   }
 };
+// Work lists are filled through device counters (order is irrelevant: they
+// only distribute work): chains a whole warp walks, and the (run, chunk)
+// items of the medium and long match tiers.
 struct EnumOut {
+  EnumIn in;
+  uint32_t* run_deg;
   uint32_t* wl_off;
+  uint2* med_items;    // nullptr on paths without a batch (export, digest)
+  uint2* long_items;
+  uint32_t* big_list;  // sources whose chain the whole warp walks (enumerate_big_kernel)
+  OpState* op;
   __device__ void operator()(unsigned long long r, unsigned long long excl,
-                             unsigned long long) const {
+                             unsigned long long v) const {
+    run_deg[r] = in.degree((uint32_t)r);
     wl_off[r] = (uint32_t)excl;
+    const uint32_t nblk = (uint32_t)v;
+    if (nblk > kLaneWalk) big_list[atomicAdd(&op->n_big, 1ull)] = (uint32_t)r;
+    if (med_items != nullptr && nblk > 0) {
+      const uint32_t k = in.b.run_start[r + 1] - in.b.run_start[r];
+      if (k > kMedTargets) {
+        const uint32_t n = (nblk + kLongChunk - 1) / kLongChunk;
+        const unsigned long long base = atomicAdd(&op->n_items, (unsigned long long)n);
+        for (uint32_t c = 0; c < n; ++c) long_items[base + c] = make_uint2((uint32_t)r, c);
+      } else if (k > kTinyTargets) {
+        const uint32_t n = (nblk + kMedChunk - 1) / kMedChunk;
+        const unsigned long long base = atomicAdd(&op->n_med, (unsigned long long)n);
+        for (uint32_t c = 0; c < n; ++c) med_items[base + c] = make_uint2((uint32_t)r, c);
+      }
+    }
   }
 };
 struct EnumFin {
@@ -381,38 +653,87 @@ struct EnumFin {
   }
 };
 
-// One warp per source walks the chain.  Each round trip loads next[h..h+31]
-// and confirms the longest prefix with next[h+i] == h+i+1, i.e. a run of
-// physically consecutive blocks that really are consecutive in the chain —
-// bulk-built hubs advance 32 blocks per memory latency, fragmented chains
-// degrade to one block per latency.
+// A warp takes 32 sources; chains of up to kLaneWalk blocks are walked one per
+// lane, 32 chains per memory round trip.  Longer chains were listed by the
+// scan and go to enumerate_big_kernel.
 __global__ void __launch_bounds__(256)
 enumerate_walk_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                       uint32_t* __restrict__ wl_handle, uint32_t* __restrict__ wl_run,
                       const OpState* op) {
   if (op->err) return;
   const uint32_t T = (uint32_t)op->n_runs;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int lane = lane_id();
-  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < T; r += nwarps) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < T; r += gridDim.x * blockDim.x) {
     const uint32_t base = wl_off[r];
     const uint32_t nblk = wl_off[r + 1] - base;
-    if (nblk == 0) continue;
-    const uint32_t v = batch_src(b, r);
-    uint32_t h = g.head[v];
+    if (nblk == 0 || nblk > kLaneWalk) continue;
+    uint32_t h = g.head[batch_src(b, r)];
+    const uint32_t tag = run_tag(b, r);
+    for (uint32_t k = 0; k < nblk; ++k) {
+      wl_handle[base + k] = h;
+      wl_run[base + k] = tag;
+      h = g.next[h];
+    }
+  }
+}
+
+// One warp per long chain.  Each round trip loads next[h .. h+127] and
+// confirms the longest prefix with next[h+i] == h+i+1, i.e. a run of
+// physically consecutive blocks that really are consecutive in the chain —
+// bulk-built hubs advance 128 blocks per memory latency, fragmented chains
+// degrade to one block per latency.
+__global__ void __launch_bounds__(256)
+enumerate_big_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
+                     const uint32_t* __restrict__ big_list, uint32_t* __restrict__ wl_handle,
+                     uint32_t* __restrict__ wl_run, const OpState* op) {
+  if (op->err) return;
+  const uint32_t nbig = (uint32_t)op->n_big;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nbig; i += nwarps) {
+    const uint32_t r = big_list[i];
+    const uint32_t base = wl_off[r];
+    const uint32_t nblk = wl_off[r + 1] - base;
+    uint32_t h = g.head[batch_src(b, r)];
+    const uint32_t tag = run_tag(b, r);
     uint32_t k = 0;
     while (k < nblk) {
-      const unsigned long long hh = (unsigned long long)h + lane;
-      const uint32_t nx = (hh < g.ring_cap) ? g.next[hh] : kNull;
-      const bool ok = (unsigned long long)nx == hh + 1;
-      const unsigned m = __ballot_sync(kFull, ok);
-      uint32_t len = (m == kFull) ? 32u : (uint32_t)__ffs(~m);
-      len = min(len, nblk - k);
-      if ((uint32_t)lane < len) {
-        wl_handle[base + k + lane] = (uint32_t)hh;
-        wl_run[base + k + lane] = r;
+      uint32_t nx[4];
+      unsigned m[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned long long hh = (unsigned long long)h + 32 * q + lane;
+        nx[q] = (hh < g.ring_cap) ? g.next[hh] : kNull;
       }
-      h = __shfl_sync(kFull, nx, len - 1);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned long long hh = (unsigned long long)h + 32 * q + lane;
+        m[q] = __ballot_sync(kFull, (unsigned long long)nx[q] == hh + 1);
+      }
+      // blocks h .. h+len-1 are consecutive in the chain (block h itself always counts)
+      uint32_t len = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (len == 32u * q) len += (m[q] == kFull) ? 32u : (uint32_t)__ffs(~m[q]) - 1u;
+      }
+      len = min(len + 1, 128u);      // the first non-consecutive link still names a valid successor
+      len = min(len, nblk - k);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t o = 32 * q + lane;
+        if (o < len) {
+          wl_handle[base + k + o] = h + o;
+          wl_run[base + k + o] = tag;
+        }
+      }
+      // successor of block h+len-1
+      const uint32_t last = len - 1;
+      uint32_t nh = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t t = __shfl_sync(kFull, nx[q], last & 31);
+        if ((last >> 5) == (uint32_t)q) nh = t;
+      }
+      h = nh;
       k += len;
     }
   }
@@ -420,53 +741,381 @@ enumerate_walk_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_
 
 // ---------------------------------------------------------------------------
 // delete: match + tombstone (graph.hpp:376-394) / query: match (graph.hpp:228-241)
-// one warp per edge block of a touched chain; the source's targets are a
-// dst-sorted slice of the batch, searched by binary search.
+//
+// The batch is grouped by source only (no order among a source's targets).
+//  * match_small_kernel — flat over the worklist, a warp per 32 blocks: each
+//    lane resolves one block's metadata, then the warp visits the blocks; the
+//    source's targets sit one per lane and are compared by shuffle broadcast
+//    (__ballot_sync collects the slot mask).  Sources with more than 32
+//    targets on short chains loop over groups of 32 targets.
+//  * match_long_kernel — sources with > 32 targets AND a long chain: a CTA per
+//    512-block chunk builds an open-addressing table of the targets in shared
+//    memory and probes it once per slot.
+// Delete records, per block, the bit mask of matched slots (wl_mask) so the
+// compaction never re-reads the chains.
 // ---------------------------------------------------------------------------
+// match_tiny_kernel: ONE THREAD PER BLOCK, sources with at most kTinyTargets
+// targets.  With the native block (B = 32: one 128-byte line) a thread pulls
+// its block into registers with eight independent 16-byte loads — no
+// cross-lane traffic, eight loads in flight per thread — and compares the 32
+// slots against the targets held in registers.  The match mask is built in a
+// register and stored coalesced.  Other block sizes take the scalar loop.
 template <bool kIsDelete>
 __global__ void __launch_bounds__(256)
-match_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
-             const uint32_t* __restrict__ wl_handle, const uint32_t* __restrict__ wl_run,
-             const uint32_t* __restrict__ run_deg, uint32_t* __restrict__ run_matched,
-             uint8_t* __restrict__ hit, OpState* op) {
+match_tiny_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
+                  const uint32_t* __restrict__ wl_handle, const uint32_t* __restrict__ wl_run,
+                  const uint32_t* __restrict__ run_deg, uint32_t* __restrict__ run_matched,
+                  uint32_t* __restrict__ wl_mask, uint8_t* __restrict__ hit, OpState* op) {
   if (op->err) return;
   __shared__ unsigned long long s_warp[8];
   const uint32_t W = (uint32_t)op->wl_blocks;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int lane = lane_id();
   unsigned long long slots = 0;
-  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < W; w += nwarps) {
-    const uint32_t r = wl_run[w];
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
+    const uint32_t tag = wl_run[w];
     const uint32_t h = wl_handle[w];
-    const uint32_t k = w - wl_off[r];
+    if (tag & kTierBit) continue;  // the table tiers' work
+    const uint32_t r = tag;
+    const uint32_t rs = b.run_start[r];
+    const uint32_t k = b.run_start[r + 1] - rs;
     const uint32_t d = run_deg[r];
-    const uint32_t rs = b.run_start[r], re = b.run_start[r + 1];
-    const uint32_t cnt = min(g.B, d - k * g.B);
+    const uint32_t kb = w - wl_off[r];
+    const uint32_t cnt = min(g.B, d - kb * g.B);
+    slots += cnt;
     uint32_t* blk = g.slab + (unsigned long long)h * g.B;
+    uint32_t tg[kTinyTargets];
+#pragma unroll
+    for (int j = 0; j < (int)kTinyTargets; ++j) tg[j] = ((uint32_t)j < k) ? batch_value(b, rs + j) : kTomb;
     uint32_t matched = 0;
-    for (uint32_t s0 = 0; s0 < cnt; s0 += 32) {
-      const uint32_t s = s0 + lane;
-      const bool valid = s < cnt;
-      bool found = false;
-      if (valid) {
-        const uint32_t e = blk[s];
-        const uint32_t lb = lower_bound_lo32(b.keys, rs, re, e);
-        found = lb < re && (uint32_t)b.keys[lb] == e;
-        if (found) {
-          if (kIsDelete) {
-            blk[s] = kTomb;
-          } else {
-            for (uint32_t j = lb; j < re && (uint32_t)b.keys[j] == e; ++j) hit[j] = 1;
+    if (g.B == 32) {
+      uint4 v[8];
+      const uint4* vb = reinterpret_cast<const uint4*>(blk);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = vb[i];
+      const uint32_t valid = cnt == 32 ? 0xFFFFFFFFu : ((1u << cnt) - 1u);  // slots past deg hold stale values
+      uint32_t mask = 0;
+#pragma unroll
+      for (int j = 0; j < (int)kTinyTargets; ++j) {
+        if ((uint32_t)j < k) {
+          const uint32_t t = tg[j];
+          uint32_t mj = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            mj |= (v[i].x == t ? 1u : 0u) << (4 * i);
+            mj |= (v[i].y == t ? 1u : 0u) << (4 * i + 1);
+            mj |= (v[i].z == t ? 1u : 0u) << (4 * i + 2);
+            mj |= (v[i].w == t ? 1u : 0u) << (4 * i + 3);
+          }
+          mj &= valid;
+          if (!kIsDelete && mj) hit[rs + j] = 1;
+          mask |= mj;
+        }
+      }
+      if (kIsDelete) {
+        wl_mask[w] = mask;
+        matched = __popc(mask);
+        while (mask) {
+          const uint32_t bit = __ffs(mask) - 1;
+          mask &= mask - 1;
+          blk[bit] = kTomb;
+        }
+      }
+    } else {
+      for (uint32_t s0 = 0; s0 < cnt; s0 += 32) {
+        uint32_t mask = 0;
+        const uint32_t ns = min(32u, cnt - s0);
+        for (uint32_t s = 0; s < ns; ++s) {
+          const uint32_t e = blk[s0 + s];
+          bool found = false;
+#pragma unroll
+          for (int j = 0; j < (int)kTinyTargets; ++j) {
+            if ((uint32_t)j < k && tg[j] == e) {
+              found = true;
+              if (!kIsDelete) hit[rs + j] = 1;
+            }
+          }
+          if (found) mask |= 1u << s;
+        }
+        if (kIsDelete) {
+          wl_mask[(unsigned long long)w * g.mw + (s0 >> 5)] = mask;
+          matched += __popc(mask);
+          while (mask) {
+            const uint32_t bit = __ffs(mask) - 1;
+            mask &= mask - 1;
+            blk[s0 + bit] = kTomb;
           }
         }
       }
-      if (kIsDelete) matched += __popc(__ballot_sync(kFull, found));
     }
-    if (kIsDelete && lane == 0 && matched) atomicAdd(&run_matched[r], matched);
-    if (lane == 0) slots += cnt;
+    if (kIsDelete && matched) atomicAdd(&run_matched[r], matched);
   }
   const unsigned long long t = block_reduce_sum(slots, s_warp);
   if (threadIdx.x == 0 && t) atomicAdd(&op->slots, t);
+}
+
+// Open-addressing table of u32 keys in shared memory; kTomb marks an empty slot
+// (never a valid destination id).
+__device__ __forceinline__ void table_insert(uint32_t* tab, uint32_t tmask, int hshift, uint32_t x) {
+  uint32_t pos = (x * 0x9E3779B1u) >> hshift;
+  while (true) {
+    const uint32_t old = atomicCAS(&tab[pos], kTomb, x);
+    if (old == kTomb || old == x) break;
+    pos = (pos + 1) & tmask;
+  }
+}
+// returns the slot holding x, or -1
+__device__ __forceinline__ int table_find(const uint32_t* tab, uint32_t tmask, int hshift, uint32_t x) {
+  uint32_t pos = (x * 0x9E3779B1u) >> hshift;
+  while (true) {
+    const uint32_t t = tab[pos];
+    if (t == x) return (int)pos;
+    if (t == kTomb) return -1;
+    pos = (pos + 1) & tmask;
+  }
+}
+
+// Scans up to kFly blocks of one chain against a shared-memory table: the slot
+// loads of all blocks are issued together, one slot per lane, __ballot_sync
+// collects the masks.  `hd_lane` holds the handle of block u in lane u.
+// first: this is the first (or only) table slice for these blocks, so the mask
+// words are stored rather than OR-ed.  Returns the number of matches (valid in
+// lane 0).  B = 32 (one line per block) takes the straight-line path.
+constexpr int kFly = 8;
+template <bool kIsDelete>
+__device__ __forceinline__ uint32_t table_scan(const GraphView& g, const uint32_t* tab, uint8_t* flag,
+                                               uint32_t tmask, int hshift, uint32_t hd_lane,
+                                               uint32_t ng, uint32_t d, uint32_t kb_first,
+                                               uint32_t w_first, uint32_t* __restrict__ wl_mask,
+                                               bool first, unsigned long long& slots) {
+  const int lane = lane_id();
+  uint32_t e[kFly];
+  uint32_t matched = 0;
+  if (g.B == 32) {
+    uint32_t hd[kFly];
+    // slots of the group: every block but possibly the chain's last one is full
+    const uint32_t rem = d - kb_first * 32u;            // slots from the group's first block to the chain end
+    const uint32_t gslots = min(rem, ng * 32u);
+#pragma unroll
+    for (int u = 0; u < kFly; ++u) {
+      hd[u] = __shfl_sync(kFull, hd_lane, u);
+      e[u] = ((uint32_t)(32 * u + lane) < gslots) ? g.slab[(unsigned long long)hd[u] * 32u + lane] : kTomb;
+    }
+#pragma unroll
+    for (int u = 0; u < kFly; ++u) {
+      if ((uint32_t)u >= ng) break;  // warp-uniform
+      const uint32_t ev = e[u];
+      uint32_t pos = (ev * 0x9E3779B1u) >> hshift;
+      uint32_t t = tab[pos];
+      bool found = t == ev;
+      bool pend = !found && t != kTomb;
+      if (ev == kTomb) { found = false; pend = false; }  // padding lanes / tombstones of an earlier slice
+      while (pend) {
+        pos = (pos + 1) & tmask;
+        t = tab[pos];
+        found = t == ev;
+        pend = !found && t != kTomb;
+      }
+      if (kIsDelete) {
+        const unsigned m = __ballot_sync(kFull, found);
+        if (found) g.slab[(unsigned long long)hd[u] * 32u + lane] = kTomb;
+        if (lane == 0) {
+          uint32_t* mword = &wl_mask[w_first + u];
+          *mword = first ? m : (*mword | m);   // the same warp owns this block in every slice
+        }
+        matched += __popc(m);
+      } else if (found) {
+        flag[pos] = 1;
+      }
+    }
+    if (first && lane == 0) slots += gslots;
+    return matched;
+  }
+  uint32_t cn[kFly];
+  uint32_t* blk[kFly];
+#pragma unroll
+  for (int u = 0; u < kFly; ++u) {
+    const uint32_t hd = __shfl_sync(kFull, hd_lane, u);
+    blk[u] = g.slab + (unsigned long long)hd * g.B;
+    cn[u] = ((uint32_t)u < ng) ? min(g.B, d - (kb_first + u) * g.B) : 0u;
+    e[u] = ((uint32_t)lane < cn[u]) ? blk[u][lane] : kTomb;
+  }
+#pragma unroll
+  for (int u = 0; u < kFly; ++u) {
+    if (cn[u] == 0) continue;  // warp-uniform
+    for (uint32_t s0 = 0; s0 < cn[u]; s0 += 32) {
+      const uint32_t s = s0 + lane;
+      const uint32_t ev = (s0 == 0) ? e[u] : ((s < cn[u]) ? blk[u][s] : kTomb);
+      bool found = false;
+      if (ev != kTomb) {  // padding lanes and entries tombstoned by an earlier slice
+        const int pos = table_find(tab, tmask, hshift, ev);
+        found = pos >= 0;
+        if (!kIsDelete && found) flag[pos] = 1;
+      }
+      if (kIsDelete) {
+        const unsigned m = __ballot_sync(kFull, found);
+        if (found) blk[u][s] = kTomb;
+        if (lane == 0) {
+          uint32_t* mword = &wl_mask[(unsigned long long)(w_first + u) * g.mw + (s0 >> 5)];
+          *mword = first ? m : (*mword | m);
+        }
+        matched += __popc(m);
+      }
+    }
+    if (first && lane == 0) slots += cn[u];
+  }
+  return matched;
+}
+
+// match_med_kernel: a WARP per (source, 32-block chunk) item, sources with
+// kTinyTargets < k <= kMedTargets targets; the warp keeps the source's targets
+// in its own 256-entry shared-memory table.
+constexpr uint32_t kMedTable = 512;   // >= 4 x kMedTargets: short probe sequences
+template <bool kIsDelete>
+__global__ void __launch_bounds__(256)
+match_med_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
+                 const uint32_t* __restrict__ wl_handle, const uint2* __restrict__ items,
+                 const uint32_t* __restrict__ run_deg, uint32_t* __restrict__ run_matched,
+                 uint32_t* __restrict__ wl_mask, uint8_t* __restrict__ hit, OpState* op) {
+  if (op->err) return;
+  __shared__ uint32_t s_table[8][kMedTable];
+  __shared__ uint8_t s_flag[kIsDelete ? 1 : 8][kIsDelete ? 4 : kMedTable];
+  __shared__ unsigned long long s_warp[8];
+  const uint32_t n_items = (uint32_t)op->n_med;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  uint32_t* tab = s_table[warp];
+  uint8_t* flag = s_flag[kIsDelete ? 0 : warp];
+  constexpr int hshift = 32 - 9;
+  constexpr uint32_t tmask = kMedTable - 1;
+  static_assert(kMedTable == 512, "hshift matches the table size");
+  unsigned long long slots = 0;
+  // items are handed out through a device cursor (they differ 30x in size); the next
+  // ticket is requested before the current item is processed
+  uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  while (q < n_items) {
+    uint32_t q_next = 0;
+    if (lane == 0) q_next = nwarps + atomicAdd(&op->med_cursor, 1u);
+    const uint2 it = items[q];
+    const uint32_t r = it.x, c = it.y;
+    const uint32_t rs = b.run_start[r];
+    const uint32_t k = b.run_start[r + 1] - rs;
+    const uint32_t d = run_deg[r];
+    const uint32_t nblk = blocks_for(g, d);
+    const uint32_t wbase = wl_off[r];
+    const uint32_t kb0 = c * kMedChunk;
+    const uint32_t nb = min(kMedChunk, nblk - kb0);
+    const uint32_t hd_all = ((uint32_t)lane < nb) ? wl_handle[wbase + kb0 + lane] : 0u;
+    for (uint32_t i = lane; i < kMedTable; i += 32) {
+      tab[i] = kTomb;
+      if (!kIsDelete) flag[i] = 0;
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < k; i += 32) table_insert(tab, tmask, hshift, batch_value(b, rs + i));
+    __syncwarp();
+    uint32_t matched = 0;
+    for (uint32_t i0 = 0; i0 < nb; i0 += kFly) {
+      const uint32_t hd_lane = __shfl_sync(kFull, hd_all, (i0 + lane) & 31);  // lane u <- handle of block i0+u
+      matched += table_scan<kIsDelete>(g, tab, flag, tmask, hshift, hd_lane, min((uint32_t)kFly, nb - i0), d,
+                                       kb0 + i0, wbase + kb0 + i0, wl_mask, true, slots);
+    }
+    if (kIsDelete) {
+      if (lane == 0 && matched) atomicAdd(&run_matched[r], matched);
+    } else {
+      __syncwarp();
+      for (uint32_t i = lane; i < k; i += 32) {
+        const int pos = table_find(tab, tmask, hshift, batch_value(b, rs + i));
+        if (pos >= 0 && flag[pos]) hit[rs + i] = 1;
+      }
+    }
+    __syncwarp();
+    q = __shfl_sync(kFull, q_next, 0);
+  }
+  const unsigned long long t = block_reduce_sum(slots, s_warp);
+  if (threadIdx.x == 0 && t) atomicAdd(&op->slots, t);
+}
+
+// match_long_kernel: sources with more than kMedTargets targets.  A CTA per
+// kLongChunk-block chunk builds the table of the source's targets in shared
+// memory (sized to the target count; kSliceTargets per build) and probes it
+// once per slot; warps take groups of four blocks round-robin.
+constexpr int kLongThreads = 256;
+constexpr uint32_t kTableSize = 8192;      // shared-memory table capacity (u32 keys)
+constexpr uint32_t kSliceTargets = 4096;   // targets per table build: load factor <= 0.5
+
+template <bool kIsDelete>
+__global__ void __launch_bounds__(kLongThreads)
+match_long_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
+                  const uint32_t* __restrict__ wl_handle, const uint2* __restrict__ items,
+                  const uint32_t* __restrict__ run_deg, uint32_t* __restrict__ run_matched,
+                  uint32_t* __restrict__ wl_mask, uint8_t* __restrict__ hit, OpState* op) {
+  if (op->err) return;
+  constexpr int kWarps = kLongThreads / 32;
+  __shared__ uint32_t s_table[kTableSize];
+  __shared__ uint8_t s_flag[kIsDelete ? 4 : kTableSize];
+  __shared__ unsigned long long s_warp[kWarps];
+  const uint32_t n_items = (uint32_t)op->n_items;
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  unsigned long long slots = 0;
+  __shared__ uint32_t s_next;
+  uint32_t q = blockIdx.x;
+  while (q < n_items) {
+    if (threadIdx.x == 0) s_next = gridDim.x + atomicAdd(&op->long_cursor, 1u);
+    const uint2 it = items[q];
+    const uint32_t r = it.x, c = it.y;
+    const uint32_t rs = b.run_start[r];
+    const uint32_t k = b.run_start[r + 1] - rs;
+    const uint32_t d = run_deg[r];
+    const uint32_t nblk = blocks_for(g, d);
+    const uint32_t wbase = wl_off[r];
+    const uint32_t kb0 = c * kLongChunk;
+    const uint32_t kb1 = min(nblk, kb0 + kLongChunk);
+    const uint32_t ngroups = (kb1 - kb0 + kFly - 1) / kFly;
+    unsigned long long matched = 0;
+    for (uint32_t t0 = 0; t0 < k; t0 += kSliceTargets) {
+      const uint32_t nt = min(kSliceTargets, k - t0);
+      // table of 2^tb >= 2 * nt entries (at least 64)
+      const int tb = max(6, 32 - __clz(2 * nt - 1));
+      const uint32_t tsize = 1u << tb, tmask = tsize - 1u;
+      const int hshift = 32 - tb;
+      for (uint32_t i = threadIdx.x; i < tsize; i += kLongThreads) {
+        s_table[i] = kTomb;
+        if (!kIsDelete) s_flag[i] = 0;
+      }
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < nt; i += kLongThreads)
+        table_insert(s_table, tmask, hshift, batch_value(b, rs + t0 + i));
+      __syncthreads();
+      for (uint32_t gi = warp; gi < ngroups; gi += kWarps) {
+        const uint32_t kbg = kb0 + kFly * gi;
+        const uint32_t ng = min((uint32_t)kFly, kb1 - kbg);
+        const uint32_t hd_lane = ((uint32_t)lane < ng) ? wl_handle[wbase + kbg + lane] : 0u;
+        const uint32_t mm = table_scan<kIsDelete>(g, s_table, s_flag, tmask, hshift, hd_lane, ng, d, kbg,
+                                                  wbase + kbg, wl_mask, t0 == 0, slots);
+        if (lane == 0) matched += mm;
+      }
+      __syncthreads();
+      if (!kIsDelete) {
+        for (uint32_t i = threadIdx.x; i < nt; i += kLongThreads) {
+          const int pos = table_find(s_table, tmask, hshift, batch_value(b, rs + t0 + i));
+          if (pos >= 0 && s_flag[pos]) hit[rs + t0 + i] = 1;
+        }
+        __syncthreads();
+      }
+    }
+    if (kIsDelete) {
+      const unsigned long long tm = block_reduce_sum(matched, s_warp);
+      if (threadIdx.x == 0 && tm) atomicAdd(&run_matched[r], (uint32_t)tm);
+    }
+    __syncthreads();
+    q = s_next;
+    __syncthreads();
+  }
+  const unsigned long long t = block_reduce_sum(slots, s_warp);
+  if (threadIdx.x == 0 && t) {
+    atomicAdd(&op->slots, t);
+    atomicAdd(&op->slots_long, t);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -499,117 +1148,134 @@ struct MovesFin {
   }
 };
 
-// delete: classify — holes below the new degree and survivors at/after it get
-// tickets from per-source counters (warp-aggregated); blocks past the new
-// tail are pushed to the ring rear (block_pool.hpp:192-209, warp-aggregated
-// across the CTA's freed blocks).
+// delete, step A — a thread per block of the touched chains, reading only the
+// match masks: lists the holes below the new degree (tickets from per-source
+// counters), returns blocks past the new tail to the ring rear
+// (block_pool.hpp:192-209, warp-aggregated) and, on a source's first block,
+// repairs degree / tail / head (detach_empty_tail, graph.hpp:398-414).
 __global__ void __launch_bounds__(256)
-classify_kernel(GraphView g, const uint32_t* __restrict__ wl_off,
-                const uint32_t* __restrict__ wl_handle, const uint32_t* __restrict__ wl_run,
-                const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ run_matched,
-                const uint32_t* __restrict__ mv_off, uint32_t* __restrict__ hole_cnt,
-                uint32_t* __restrict__ surv_cnt, unsigned long long* __restrict__ hole_addr,
-                uint32_t* __restrict__ moved_val, OpState* op) {
+delete_holes_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
+                    const uint32_t* __restrict__ wl_handle, const uint32_t* __restrict__ wl_run,
+                    const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ run_matched,
+                    const uint32_t* __restrict__ mv_off, const uint32_t* __restrict__ wl_mask,
+                    uint32_t* __restrict__ hole_cnt, unsigned long long* __restrict__ hole_addr,
+                    OpState* op) {
   if (op->err || op->aux1) return;
   __shared__ unsigned long long s_warp[8];
   const uint32_t W = (uint32_t)op->wl_blocks;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t Wpad = (W + 31u) & ~31u;
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
-  unsigned long long pushed = 0;
-  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < W; w += nwarps) {
-    const uint32_t r = wl_run[w];
-    const uint32_t m = run_matched[r];
-    if (m == 0) continue;
-    const uint32_t h = wl_handle[w];
-    const uint32_t k = w - wl_off[r];
-    const uint32_t d = run_deg[r];
-    const uint32_t nd = d - m;
-    const uint32_t new_nb = ceil_div(nd, g.B);
-    const uint32_t cnt = min(g.B, d - k * g.B);
-    const uint32_t mo = mv_off[r];
-    const uint32_t* blk = g.slab + (unsigned long long)h * g.B;
-    for (uint32_t s0 = 0; s0 < cnt; s0 += 32) {
-      const uint32_t s = s0 + lane;
-      const bool valid = s < cnt;
-      const uint32_t e = valid ? blk[s] : 0u;
-      const uint32_t p = k * g.B + s;
-      const bool is_hole = valid && p < nd && e == kTomb;
-      const bool is_surv = valid && p >= nd && e != kTomb;
-      const unsigned mh = __ballot_sync(kFull, is_hole);
-      const unsigned ms = __ballot_sync(kFull, is_surv);
-      if (mh) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&hole_cnt[r], (uint32_t)__popc(mh));
-        base = __shfl_sync(kFull, base, 0);
-        if (is_hole) hole_addr[mo + base + __popc(mh & lt)] = (unsigned long long)h * g.B + s;
-      }
-      if (ms) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&surv_cnt[r], (uint32_t)__popc(ms));
-        base = __shfl_sync(kFull, base, 0);
-        if (is_surv) moved_val[mo + base + __popc(ms & lt)] = e;
+  unsigned long long pushed = 0, matched = 0;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < Wpad; w += gridDim.x * blockDim.x) {
+    bool do_free = false;
+    uint32_t h = 0;
+    if (w < W) {
+      const uint32_t r = wl_run[w] & kRunMask;
+      const uint32_t m = run_matched[r];
+      if (m != 0) {
+        h = wl_handle[w];
+        const uint32_t kb = w - wl_off[r];
+        const uint32_t d = run_deg[r];
+        const uint32_t nd = d - m;
+        const uint32_t new_nb = blocks_for(g, nd);
+        const uint32_t base = kb * g.B;
+        if (base < nd) {
+          const uint32_t lim = nd - base;  // slots [0, lim) of this block stay below the new degree
+          uint32_t nh = 0;
+          for (uint32_t i = 0; i < g.mw && 32 * i < lim; ++i) {
+            uint32_t bits = wl_mask[(unsigned long long)w * g.mw + i];
+            if (lim - 32 * i < 32) bits &= (1u << (lim - 32 * i)) - 1u;
+            nh += __popc(bits);
+          }
+          if (nh) {
+            uint32_t idx = mv_off[r] + atomicAdd(&hole_cnt[r], nh);
+            for (uint32_t i = 0; i < g.mw && 32 * i < lim; ++i) {
+              uint32_t bits = wl_mask[(unsigned long long)w * g.mw + i];
+              if (lim - 32 * i < 32) bits &= (1u << (lim - 32 * i)) - 1u;
+              while (bits) {
+                const uint32_t bit = __ffs(bits) - 1;
+                bits &= bits - 1;
+                hole_addr[idx++] = (unsigned long long)h * g.B + 32 * i + bit;
+              }
+            }
+          }
+        }
+        do_free = kb >= new_nb && g.reclaim;
+        if (kb == 0) {
+          const uint32_t v = batch_src(b, r);
+          g.deg[v] = nd;
+          if (nd == 0) {
+            g.head[v] = kNull;
+            g.tail[v] = kNull;
+          } else {
+            const uint32_t t = wl_handle[wl_off[r] + new_nb - 1];
+            g.tail[v] = t;
+            g.next[t] = kNull;
+          }
+          matched += m;
+        }
       }
     }
-    if (k >= new_nb && g.reclaim) {
-      if (lane == 0) {
-        const unsigned long long pos = atomicAdd(&g.st->rear, 1ull);
-        g.ring[pos % g.ring_cap] = h;
-        ++pushed;
+    const unsigned fm = __ballot_sync(kFull, do_free);
+    if (fm) {
+      unsigned long long pos = 0;
+      const int leader = __ffs(fm) - 1;
+      if (lane == leader) {
+        pos = atomicAdd(&g.st->rear, (unsigned long long)__popc(fm));
+        pushed += __popc(fm);
       }
-    }
-  }
-  const unsigned long long t = block_reduce_sum(pushed, s_warp);
-  if (threadIdx.x == 0 && t) atomicAdd(&op->pushed, t);
-}
-
-// delete: fill holes with the tail survivors, repair degree / tail / head
-// (detach_empty_tail, graph.hpp:398-414).  One warp per touched source.
-__global__ void __launch_bounds__(256)
-finalize_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
-                       const uint32_t* __restrict__ wl_handle,
-                       const uint32_t* __restrict__ run_deg,
-                       const uint32_t* __restrict__ run_matched,
-                       const uint32_t* __restrict__ mv_off, const uint32_t* __restrict__ hole_cnt,
-                       const unsigned long long* __restrict__ hole_addr,
-                       const uint32_t* __restrict__ moved_val, OpState* op) {
-  if (op->err || op->aux1) return;
-  __shared__ unsigned long long s_warp[8];
-  const uint32_t T = (uint32_t)op->n_runs;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int lane = lane_id();
-  unsigned long long matched = 0, moves = 0;
-  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < T; r += nwarps) {
-    const uint32_t m = run_matched[r];
-    if (m == 0) continue;
-    const uint32_t v = batch_src(b, r);
-    const uint32_t nd = run_deg[r] - m;
-    const uint32_t mv = hole_cnt[r];
-    const uint32_t mo = mv_off[r];
-    for (uint32_t i = lane; i < mv; i += 32) g.slab[hole_addr[mo + i]] = moved_val[mo + i];
-    if (lane == 0) {
-      g.deg[v] = nd;
-      if (nd == 0) {
-        g.head[v] = kNull;
-        g.tail[v] = kNull;
-      } else {
-        const uint32_t t = wl_handle[wl_off[r] + ceil_div(nd, g.B) - 1];
-        g.tail[v] = t;
-        g.next[t] = kNull;
-      }
-      matched += m;
-      moves += mv;
+      pos = __shfl_sync(kFull, pos, leader);
+      if (do_free) g.ring[(pos + __popc(fm & lt)) % g.ring_cap] = h;
     }
   }
+  const unsigned long long tp = block_reduce_sum(pushed, s_warp);
   const unsigned long long tm = block_reduce_sum(matched, s_warp);
-  const unsigned long long tv = block_reduce_sum(moves, s_warp);
   if (threadIdx.x == 0) {
+    if (tp) atomicAdd(&op->pushed, tp);
     if (tm) {
       atomicAdd(&op->matched, tm);
       atomicAdd(&g.st->active_edges, (unsigned long long)(-(long long)tm));  // graph.hpp:211-213
     }
-    if (tv) atomicAdd(&op->moves, tv);
   }
+}
+
+// delete, step B — a thread per block again; only blocks reaching past the new
+// degree do anything: every live entry there takes the next hole of its source.
+__global__ void __launch_bounds__(256)
+delete_moves_kernel(GraphView g, const uint32_t* __restrict__ wl_off,
+                    const uint32_t* __restrict__ wl_handle, const uint32_t* __restrict__ wl_run,
+                    const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ run_matched,
+                    const uint32_t* __restrict__ mv_off, const uint32_t* __restrict__ hole_cnt,
+                    uint32_t* __restrict__ surv_cnt, const unsigned long long* __restrict__ hole_addr,
+                    OpState* op) {
+  if (op->err || op->aux1) return;
+  __shared__ unsigned long long s_warp[8];
+  const uint32_t W = (uint32_t)op->wl_blocks;
+  unsigned long long moves = 0;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
+    const uint32_t r = wl_run[w] & kRunMask;
+    const uint32_t m = run_matched[r];
+    if (m == 0 || hole_cnt[r] == 0) continue;
+    const uint32_t kb = w - wl_off[r];
+    const uint32_t d = run_deg[r];
+    const uint32_t nd = d - m;
+    const uint32_t base = kb * g.B;
+    const uint32_t cnt = min(g.B, d - base);
+    if (base + cnt <= nd) continue;
+    const uint32_t* blk = g.slab + (unsigned long long)wl_handle[w] * g.B;
+    const uint32_t mo = mv_off[r];
+    for (uint32_t s = (nd > base ? nd - base : 0u); s < cnt; ++s) {
+      const uint32_t e = blk[s];
+      if (e != kTomb) {
+        const uint32_t t = atomicAdd(&surv_cnt[r], 1u);
+        g.slab[hole_addr[mo + t]] = e;
+        ++moves;
+      }
+    }
+  }
+  const unsigned long long tv = block_reduce_sum(moves, s_warp);
+  if (threadIdx.x == 0 && tv) atomicAdd(&op->moves, tv);
 }
 
 // query: scatter sorted hit flags back to the caller's order
@@ -716,7 +1382,7 @@ export_copy_kernel(GraphView g, const uint32_t* __restrict__ wl_off,
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
   for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < W; w += nwarps) {
-    const uint32_t v = wl_run[w];  // runs are vertices on the export path
+    const uint32_t v = wl_run[w] & kRunMask;  // runs are vertices on the export path
     const uint32_t h = wl_handle[w];
     const uint32_t k = w - wl_off[v];
     const uint32_t cnt = min(g.B, run_deg[v] - k * g.B);
@@ -754,7 +1420,7 @@ digest_kernel(GraphView g, const uint32_t* __restrict__ wl_off,
   const int lane = lane_id();
   unsigned long long acc = 0, cntacc = 0;
   for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < W; w += nwarps) {
-    const uint32_t v = wl_run[w];
+    const uint32_t v = wl_run[w] & kRunMask;
     const uint32_t h = wl_handle[w];
     const uint32_t k = w - wl_off[v];
     const uint32_t cnt = min(g.B, run_deg[v] - k * g.B);

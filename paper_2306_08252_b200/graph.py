@@ -26,6 +26,7 @@ class GraphConfig:
     pool_blocks: int = 0         # exact block count; overrides pool_bytes
     reclaim_on_delete: bool = True
     stream: int = 0              # cudaStream_t handle; 0 => library-owned stream
+    group: str = "auto"          # how COO batches are grouped by source: "auto" | "radix" | "count"
 
 
 def _is_device(x) -> bool:
@@ -63,6 +64,7 @@ class DynamicGraph:
         c = _lib.DgConfig()
         c.device = cfg.device
         c.flags = 0 if cfg.reclaim_on_delete else _lib.DG_FLAG_NO_RECLAIM
+        c.flags |= {"auto": 0, "radix": _lib.DG_FLAG_GROUP_RADIX, "count": _lib.DG_FLAG_GROUP_COUNT}[cfg.group]
         c.pool_bytes = cfg.pool_bytes
         c.pool_blocks = cfg.pool_blocks
         c.stream = cfg.stream or None

@@ -178,9 +178,10 @@ class CpuGraph:
 class GpuGraph:
     """The product behind the same interface (status codes instead of exceptions)."""
 
-    def __init__(self, v0, block_size, pool_blocks=1 << 16, reclaim=True, **_):
+    def __init__(self, v0, block_size, pool_blocks=1 << 16, reclaim=True, group="auto", **_):
         from paper_2306_08252_b200 import DynamicGraph, GraphConfig
-        self.g = DynamicGraph(GraphConfig(pool_blocks=pool_blocks, reclaim_on_delete=reclaim), v0, block_size)
+        self.g = DynamicGraph(GraphConfig(pool_blocks=pool_blocks, reclaim_on_delete=reclaim, group=group),
+                              v0, block_size)
 
     def close(self):
         self.g.close()

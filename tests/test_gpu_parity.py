@@ -22,8 +22,12 @@ def _orc(cfg):
                     cfg.get("initial_fraction", 0.5), cfg.get("reclaim", True), 1)
 
 
-def _gpu(cfg, pool_blocks=1 << 16):
-    return GpuGraph(cfg["v0"], cfg["block_size"], pool_blocks=pool_blocks, reclaim=cfg.get("reclaim", True))
+def _gpu(cfg, pool_blocks=1 << 16, group="auto"):
+    return GpuGraph(cfg["v0"], cfg["block_size"], pool_blocks=pool_blocks, reclaim=cfg.get("reclaim", True),
+                    group=group)
+
+
+GROUPS = ("count", "radix")   # both COO grouping strategies ("auto" picks between them per batch)
 
 
 def test_cuda_library_is_the_loaded_path():
@@ -34,9 +38,10 @@ def test_cuda_library_is_the_loaded_path():
     assert "libdyngraph_b200.so" in maps
 
 
+@pytest.mark.parametrize("group", GROUPS)
 @pytest.mark.parametrize("name,cfg,script", KNOWN_ANSWER_SCRIPTS, ids=[k[0] for k in KNOWN_ANSWER_SCRIPTS])
-def test_known_answers_vs_oracle(name, cfg, script):
-    g, o = _gpu(cfg), _orc(cfg)
+def test_known_answers_vs_oracle(name, cfg, script, group):
+    g, o = _gpu(cfg, group=group), _orc(cfg)
     assert_same(run_script(g, script), run_script(o, script), name)
     g.close()
 
@@ -55,12 +60,13 @@ def test_workloads_vs_reference_golden():
         g.close()
 
 
+@pytest.mark.parametrize("group", GROUPS)
 @pytest.mark.parametrize("chunk", range(4))
-def test_random_workloads_vs_oracle(chunk):
+def test_random_workloads_vs_oracle(chunk, group):
     """verify.hpp:135-265 op mix, 25 seeds per chunk."""
     for seed in range(5000 + 25 * chunk, 5025 + 25 * chunk):
         cfg, script = make_workload(seed)
-        g, o = _gpu(cfg), _orc(cfg)
+        g, o = _gpu(cfg, group=group), _orc(cfg)
         assert_same(run_script(g, script), run_script(o, script), f"seed {seed}")
         g.close()
 
@@ -117,8 +123,9 @@ def test_compaction_scratch_regrows():
     g.close()
 
 
+@pytest.mark.parametrize("group", GROUPS)
 @pytest.mark.parametrize("block_size", [1, 3, 15, 32, 33, 64, 100])
-def test_block_sizes(block_size):
+def test_block_sizes(block_size, group):
     rng = np.random.default_rng(block_size)
     cfg = {"v0": 300, "block_size": block_size, "arena_bytes": 1 << 28}
     script = []
@@ -128,7 +135,7 @@ def test_block_sizes(block_size):
         script.append(("insert" if r % 3 != 2 else "delete", s, d))
         script.append(("check",))
     script.append(("query", rng.integers(0, 300, 5000).astype(np.uint32), rng.integers(0, 300, 5000).astype(np.uint32)))
-    g, o = _gpu(cfg, pool_blocks=1 << 18), _orc(cfg)
+    g, o = _gpu(cfg, pool_blocks=1 << 18, group=group), _orc(cfg)
     assert_same(run_script(g, script), run_script(o, script), f"B={block_size}")
     g.close()
 
