@@ -1,0 +1,210 @@
+// dyngraph_b200.hpp — C++ host-side mirror of the reference's operator API
+// over the C ABI of libdyngraph_b200.so (include/dyngraph_b200.h).
+//
+// `dyngraph_b200::DynamicGraph` has the constructor, method names, argument
+// meaning and error behaviour of `dyngraph::DynamicGraph`
+// (reference: proj/include/dyngraph/graph.hpp:80-317), so code written against
+// the reference — run_workload (io/workload.hpp:132-181), run_one_workload
+// (verify.hpp:151-242), oracle_compare (oracle.hpp:113-160) — compiles against
+// either by switching the type.  Header-only, C++17, no CUDA headers needed:
+// every method is one call into the shared library; failures come back as the
+// reference's exception classes (types.hpp:21-32).  There is NO CPU fallback:
+// if the library is missing the program does not link.
+//
+// Not mirrored (physical layout, reported rather than compared — SURVEY.md §8a):
+// arena(), dictionary(), pool(), sentinel_of(), adjacency_blocks(), plan_batch().
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "dyngraph_b200.h"
+
+namespace dyngraph_b200 {
+
+using VertexId = std::uint32_t;                       // types.hpp:11
+inline constexpr VertexId kInvalidVertex = 0xFFFFFFFFu;  // types.hpp:16
+
+// types.hpp:21-32
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DataError : public Error {
+ public:
+  using Error::Error;
+};
+class EngineError : public Error {
+ public:
+  using Error::Error;
+};
+
+enum class BatchKind { Insert, Delete };  // csr.hpp:12
+
+// csr.hpp:17-25
+struct CsrBatch {
+  BatchKind kind = BatchKind::Insert;
+  std::vector<std::uint64_t> offsets;
+  std::vector<VertexId> destinations;
+  std::uint64_t vertex_count() const { return offsets.empty() ? 0 : offsets.size() - 1; }
+  std::uint64_t edge_count() const { return destinations.size(); }
+  std::uint64_t degree(VertexId v) const { return offsets[v + 1] - offsets[v]; }
+};
+
+// csr.hpp:29-45 — stable counting sort of (source, destination) pairs
+inline CsrBatch csr_from_pairs(BatchKind kind, std::uint64_t vertex_count,
+                               const std::vector<std::pair<VertexId, VertexId>>& edges) {
+  CsrBatch b;
+  b.kind = kind;
+  b.offsets.assign(vertex_count + 1, 0);
+  for (const auto& e : edges) {
+    if (e.first >= vertex_count) throw DataError("csr batch: source out of range");
+    ++b.offsets[e.first + 1];
+  }
+  for (std::uint64_t v = 0; v < vertex_count; ++v) b.offsets[v + 1] += b.offsets[v];
+  b.destinations.resize(edges.size());
+  std::vector<std::uint64_t> cursor(b.offsets.begin(), b.offsets.end() - 1);
+  for (const auto& e : edges) b.destinations[cursor[e.first]++] = e.second;
+  return b;
+}
+
+// graph.hpp:23-28; the arena is real device memory here, so the budget is the
+// byte size of the edge-block pool (arena_bytes * pool.initial_fraction there).
+struct GraphConfig {
+  int device = 0;
+  std::uint64_t pool_bytes = 0;   // 0 => library default (1 GiB)
+  std::uint64_t pool_blocks = 0;  // exact block count; overrides pool_bytes
+  bool reclaim_on_delete = true;  // graph.hpp:26
+  void* stream = nullptr;         // cudaStream_t; nullptr => library-owned stream
+};
+
+struct GraphStats {  // graph.hpp:54-70 (reported, not compared)
+  std::uint64_t logical_size = 0, capacity = 0, alive_vertices = 0, active_edges = 0;
+  std::uint64_t adjacency_blocks = 0, occupied_slots = 0, hole_slots = 0;
+  std::uint64_t pool_blocks_created = 0, pool_blocks_in_use = 0, pool_queue_size = 0;
+  std::uint64_t max_degree = 0;
+  std::uint32_t block_size = 0;
+};
+
+class DynamicGraph {
+ public:
+  // graph.hpp:84-91
+  DynamicGraph(const GraphConfig& config, std::uint64_t initial_vertex_count, std::uint32_t block_size) {
+    dg_config c{};
+    c.device = config.device;
+    c.flags = config.reclaim_on_delete ? 0u : DG_FLAG_NO_RECLAIM;
+    c.pool_bytes = config.pool_bytes;
+    c.pool_blocks = config.pool_blocks;
+    c.stream = config.stream;
+    const int rc = dg_create(&c, initial_vertex_count, block_size, &h_);
+    if (rc != DG_OK) raise(rc, dg_last_error(nullptr));
+  }
+  ~DynamicGraph() { dg_destroy(h_); }
+  DynamicGraph(const DynamicGraph&) = delete;             // graph.hpp:93-94
+  DynamicGraph& operator=(const DynamicGraph&) = delete;
+
+  // graph.hpp:96-108
+  std::uint32_t block_size() const { return dg_block_size(h_); }
+  std::uint64_t logical_size() const { return dg_logical_size(h_); }
+  std::uint64_t vertex_capacity() const { return dg_vertex_capacity(h_); }
+  std::uint64_t alive_vertices() const { return dg_alive_vertices(h_); }
+  std::uint64_t active_edges() const { return dg_active_edges(h_); }
+  bool vertex_alive(VertexId v) const { return dg_vertex_alive(h_, v) != 0; }
+
+  // graph.hpp:167-188
+  void insert_batch(const CsrBatch& batch) {
+    if (batch.kind != BatchKind::Insert) throw DataError("plan_batch: expected an insert batch");
+    check(dg_insert_batch_csr(h_, batch.offsets.data(), batch.offsets.size(), batch.destinations.data(),
+                              batch.destinations.size(), DG_MEM_HOST));
+  }
+  // graph.hpp:195-222
+  void delete_batch(const CsrBatch& batch) {
+    if (batch.kind != BatchKind::Delete) throw DataError("delete_batch: expected a delete batch");
+    check(dg_delete_batch_csr(h_, batch.offsets.data(), batch.offsets.size(), batch.destinations.data(),
+                              batch.destinations.size(), DG_MEM_HOST));
+  }
+  // O(batch) forms of the same two operators (no V+1 offsets array)
+  void insert_pairs(const VertexId* src, const VertexId* dst, std::uint64_t n, int mem = DG_MEM_HOST) {
+    check(dg_insert_batch_coo(h_, src, dst, n, mem));
+  }
+  void delete_pairs(const VertexId* src, const VertexId* dst, std::uint64_t n, int mem = DG_MEM_HOST) {
+    check(dg_delete_batch_coo(h_, src, dst, n, mem));
+  }
+
+  // graph.hpp:228-241
+  bool query_edge(VertexId source, VertexId destination) const {
+    std::uint8_t out = 0;
+    check(dg_query_edges(h_, &source, &destination, 1, &out, DG_MEM_HOST));
+    return out != 0;
+  }
+  std::vector<std::uint8_t> query_edges(const std::vector<VertexId>& src, const std::vector<VertexId>& dst) const {
+    std::vector<std::uint8_t> out(src.size());
+    if (!src.empty()) check(dg_query_edges(h_, src.data(), dst.data(), src.size(), out.data(), DG_MEM_HOST));
+    return out;
+  }
+
+  // graph.hpp:246
+  void insert_vertices(std::uint64_t count) { check(dg_insert_vertices(h_, count)); }
+  // graph.hpp:252-276 — returns the skipped ids in encounter order
+  std::vector<VertexId> delete_vertices(const std::vector<VertexId>& ids) {
+    std::vector<VertexId> skipped(ids.size());
+    std::uint64_t ns = 0;
+    check(dg_delete_vertices(h_, ids.data(), ids.size(), skipped.data(), &ns));
+    skipped.resize(ns);
+    return skipped;
+  }
+
+  // graph.hpp:116-129 (traversal order; sorted = canonical order of oracle_compare)
+  std::vector<VertexId> active_destinations(VertexId v, bool sorted = false) const {
+    std::vector<std::uint64_t> off;
+    std::vector<VertexId> dst;
+    export_csr(off, dst, sorted);
+    if (v >= logical_size()) return {};
+    return std::vector<VertexId>(dst.begin() + off[v], dst.begin() + off[v + 1]);
+  }
+  // every vertex's active_destinations as one CSR
+  void export_csr(std::vector<std::uint64_t>& offsets, std::vector<VertexId>& destinations, bool sorted) const {
+    offsets.assign(logical_size() + 1, 0);
+    check(dg_export_csr(h_, offsets.data(), nullptr, 0, sorted ? 1 : 0, DG_MEM_HOST));
+    destinations.assign(offsets.back(), 0);
+    if (!destinations.empty())
+      check(dg_export_csr(h_, offsets.data(), destinations.data(), destinations.size(), sorted ? 1 : 0, DG_MEM_HOST));
+  }
+  // sentinel_of(v).active_edge_count for every v (graph.hpp:108)
+  std::vector<std::uint64_t> degrees() const {
+    std::vector<std::uint64_t> out(logical_size());
+    if (!out.empty()) check(dg_degrees(h_, out.data(), DG_MEM_HOST));
+    return out;
+  }
+
+  // graph.hpp:287-317
+  GraphStats stats() const {
+    dg_stats s{};
+    check(dg_stats_get(h_, &s));
+    GraphStats o;
+    o.logical_size = s.logical_size; o.capacity = s.capacity; o.alive_vertices = s.alive_vertices;
+    o.active_edges = s.active_edges; o.adjacency_blocks = s.adjacency_blocks; o.occupied_slots = s.occupied_slots;
+    o.hole_slots = s.hole_slots; o.pool_blocks_created = s.pool_blocks_created;
+    o.pool_blocks_in_use = s.pool_blocks_in_use; o.pool_queue_size = s.pool_queue_size;
+    o.max_degree = s.max_degree; o.block_size = s.block_size;
+    return o;
+  }
+
+  dg_graph* handle() const { return h_; }
+
+ private:
+  [[noreturn]] static void raise(int rc, const char* msg) {
+    const std::string m = msg ? msg : "";
+    if (rc == DG_ERR_DATA) throw DataError(m);
+    throw EngineError(m);  // resource / contract / CUDA failures
+  }
+  void check(int rc) const {
+    if (rc != DG_OK) raise(rc, dg_last_error(h_));
+  }
+  dg_graph* h_ = nullptr;
+};
+
+}  // namespace dyngraph_b200

@@ -72,3 +72,20 @@ def test_host_side_csr_helpers():
         compute_block_size(csr_from_pairs(BatchKind.Insert, 4, [], []))
     with pytest.raises(DataError):
         csr_from_pairs(BatchKind.Insert, 4, [4], [0])
+
+
+def test_cpp_mirror_header_compiles_standalone(tmp_path):
+    """include/dyngraph_b200.hpp (the C++ mirror of dyngraph::DynamicGraph) needs only a C++17 compiler."""
+    import subprocess
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "dyngraph_b200.hpp"\n'
+                   "int main() { dyngraph_b200::CsrBatch b = dyngraph_b200::csr_from_pairs("
+                   "dyngraph_b200::BatchKind::Insert, 3, {{2, 1}, {0, 2}, {2, 0}});\n"
+                   "  return (b.offsets == std::vector<std::uint64_t>{0, 1, 1, 3} && "
+                   "b.destinations == std::vector<std::uint32_t>{2, 1, 0}) ? 0 : 1; }\n")
+    exe = tmp_path / "t"
+    from paper_2306_08252_b200.build import LIB_PATH, build_library
+    build_library()
+    subprocess.run(["g++", "-std=c++17", "-Wall", "-Wextra", "-Werror", f"-I{ROOT / 'include'}", str(src), "-o", str(exe),
+                    f"-L{LIB_PATH.parent}", "-ldyngraph_b200", f"-Wl,-rpath,{LIB_PATH.parent}"], check=True)
+    assert subprocess.run([str(exe)]).returncode == 0

@@ -290,3 +290,16 @@ def test_rmat_device_generator_and_round_trip(scale, batch):
     assert np.array_equal(dst2, (ks & np.uint64(0xFFFFFFFF)).astype(np.uint32))
     assert np.array_equal(off2, np.concatenate([[0], np.cumsum(np.bincount((ks >> np.uint64(32)).astype(np.int64), minlength=V))]).astype(np.uint64))
     g.close()
+
+
+def test_cpp_dropin_against_reference_class():
+    """oracle/dropin_check.cpp: one templated workload through dyngraph::DynamicGraph (the unmodified
+    reference, compiled into the binary in the build container) and through the C++ mirror
+    include/dyngraph_b200.hpp -> C ABI -> CUDA; every compared observable must agree."""
+    import subprocess
+    exe = __import__("pathlib").Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "dropin_check"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/dropin_check not built (reference headers absent at build time)")
+    proc = subprocess.run([str(exe), "60"], capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-2000:]
+    assert "60 workloads, 0 mismatches" in proc.stdout
