@@ -145,6 +145,12 @@ def kernel_bytes(name: str, rep: dict, B: int) -> float | None:
         return 16 * b                                    # 2 x u32 in, u64 key out
     if name.startswith("scan_kernel"):
         return 16 * b                                    # the largest scan of an op (run detection over the keys)
+    if name.startswith("alloc_kernel<group"):
+        return 4 * rep.get("vertices", 0) + 40 * T       # per-vertex counters + per-run outputs
+    if name.startswith("alloc_kernel"):
+        return 24 * T
+    if name.startswith("group_"):
+        return 16 * b
     if name.startswith("enumerate_"):
         return 12 * W + 12 * T                           # next[] reads + worklist writes
     if name.startswith("append_kernel"):
@@ -307,13 +313,15 @@ def run_b200_arm(args):
             gen.coo_to_csr(src, dst, V, off, csr_dst)
             del src, dst
             pool_blocks = int((E_local // B + V) * 1.25) + (4 * b) // B + 4096
+            ws_hint = 48 * V + 8 * (E_local // B) + (64 << 20)   # scratch of the bulk build, reserved at create
             bulk_ms = []
             g = None
             for rep in range(3):
                 if g is not None:
                     g.close()
                 t0 = time.perf_counter()
-                g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream), V, B)
+                g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream,
+                                             workspace_bytes=ws_hint), V, B)
                 create_ms = (time.perf_counter() - t0) * 1e3
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 flush.zero_()
@@ -327,7 +335,8 @@ def run_b200_arm(args):
             bulk_kernels = None
             if not args.no_profile:   # one more, untimed, build with per-kernel events
                 g.close()
-                g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream), V, B)
+                g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream,
+                                             workspace_bytes=ws_hint), V, B)
                 g.profile_enable(True)
                 g.bulk_init(off, csr_dst)
                 g.profile_enable(False)

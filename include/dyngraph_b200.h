@@ -76,7 +76,8 @@ typedef struct dg_config {
   uint64_t pool_bytes;       /* 0 => 1 GiB */
   uint64_t pool_blocks;      /* if non-zero, overrides pool_bytes: exact block count */
   void* stream;              /* cudaStream_t to enqueue on; NULL => library-owned stream */
-  uint32_t reserved[8];
+  uint64_t workspace_bytes;  /* per-op scratch reserved at create (0 => grown on first use) */
+  uint32_t reserved[6];
 } dg_config;
 
 /* Replaces GraphStats (graph.hpp:54-70); reported, not compared. */

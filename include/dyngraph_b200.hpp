@@ -79,6 +79,7 @@ struct GraphConfig {
   std::uint64_t pool_blocks = 0;  // exact block count; overrides pool_bytes
   bool reclaim_on_delete = true;  // graph.hpp:26
   void* stream = nullptr;         // cudaStream_t; nullptr => library-owned stream
+  std::uint64_t workspace_bytes = 0;  // per-op scratch reserved at construction
 };
 
 struct GraphStats {  // graph.hpp:54-70 (reported, not compared)
@@ -99,6 +100,7 @@ class DynamicGraph {
     c.pool_bytes = config.pool_bytes;
     c.pool_blocks = config.pool_blocks;
     c.stream = config.stream;
+    c.workspace_bytes = config.workspace_bytes;
     const int rc = dg_create(&c, initial_vertex_count, block_size, &h_);
     if (rc != DG_OK) raise(rc, dg_last_error(nullptr));
   }

@@ -27,7 +27,8 @@ class DgConfig(C.Structure):
         ("pool_bytes", C.c_uint64),
         ("pool_blocks", C.c_uint64),
         ("stream", C.c_void_p),
-        ("reserved", C.c_uint32 * 8),
+        ("workspace_bytes", C.c_uint64),
+        ("reserved", C.c_uint32 * 6),
     ]
 
 

@@ -293,6 +293,16 @@ void launch_scan(dg_graph* h, const char* name, uint64_t n_bound, const unsigned
   const unsigned tiles = (unsigned)std::max<uint64_t>(1, (n_bound + kScanTile - 1) / kScanTile);
   DG_LAUNCH(h, name, scan_kernel<<<tiles, kScanThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
 }
+// unordered range allocation over [0, *n_ptr): see alloc_kernel
+template <class In, class Out, class Fin>
+void launch_alloc(dg_graph* h, const char* name, uint64_t n_bound, const unsigned long long* n_ptr,
+                  In in, Out out, Fin fin) {
+  unsigned long long* scratch = ws_alloc<unsigned long long>(h, kAllocScratchWords);
+  cudaMemsetAsync(scratch, 0, kAllocScratchWords * sizeof(unsigned long long), h->stream);
+  const unsigned tiles = (unsigned)std::max<uint64_t>(1, (n_bound + kAllocTile - 1) / kAllocTile);
+  DG_LAUNCH(h, name, alloc_kernel<<<tiles, kAllocThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
+}
+inline size_t alloc_ws_bytes() { return aligned(kAllocScratchWords * sizeof(unsigned long long)); }
 inline size_t scan_ws_bytes(uint64_t n_bound) {
   return aligned(scan_scratch_words(n_bound) * sizeof(unsigned long long));
 }
@@ -428,46 +438,52 @@ int stage_in(dg_graph* h, const T* p, uint64_t count, int mem, const T** out) {
   return DG_OK;
 }
 
-// ---- shared tails of the batch ops -------------------------------------------
-struct RunBuffers {
-  uint32_t* run_start;
-  uint32_t* run_src;
-  uint32_t* run_deg;
-  uint32_t* run_tail;
-};
-
+// ---- shared pieces of the batch ops ---------------------------------------------
 // upper bound of append units: every non-empty run has at most 1 + ceil(c / B) of them
-inline uint64_t units_bound(const dg_graph* h, uint64_t runs_bound, uint64_t n_edges) {
-  return 2 * std::min<uint64_t>(runs_bound, n_edges) + n_edges / std::max<uint32_t>(h->B, 1) + 1;
+inline uint64_t units_bound(uint32_t B, uint64_t runs_bound, uint64_t n_edges) {
+  return 2 * std::min<uint64_t>(runs_bound, n_edges) + n_edges / std::max<uint32_t>(B, 1) + 1;
 }
 
-// plan + append over a grouped batch (COO: sorted keys + detected runs; CSR: offsets).
-// csr_path: the destination range check rides in the append pass and the
-// metadata commit is a separate kernel that only runs when nothing failed.
-void enqueue_plan_append(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n_edges,
-                         uint32_t* run_deg, uint32_t* run_tail, bool csr_path) {
+// per-run outputs of the insert plan
+PlanArrays alloc_plan_arrays(dg_graph* h, uint64_t runs_bound, uint64_t n_edges) {
+  PlanArrays a{};
+  a.run_deg = ws_alloc<uint32_t>(h, runs_bound + 1);
+  a.run_tail = ws_alloc<uint32_t>(h, runs_bound + 1);
+  a.unit_off = ws_alloc<uint32_t>(h, runs_bound + 1);
+  a.blk_off = ws_alloc<uint32_t>(h, runs_bound + 1);
+  a.unit_run = ws_alloc<uint32_t>(h, units_bound(h->B, runs_bound, n_edges));
+  return a;
+}
+inline size_t plan_arrays_ws(uint32_t B, uint64_t runs_bound, uint64_t n_edges) {
+  return 4 * aligned((runs_bound + 1) * 4) + aligned(units_bound(B, runs_bound, n_edges) * 4) + alloc_ws_bytes();
+}
+
+// append over a planned batch.  csr_path: the destination range check rides in
+// the append pass and the metadata commit is a separate kernel that only runs
+// when nothing failed.
+void enqueue_append(dg_graph* h, const BatchView& b, const PlanArrays& a, uint64_t runs_bound,
+                    uint64_t n_edges, bool csr_path) {
   GraphView g = view(h);
-  const uint64_t ub = units_bound(h, runs_bound, n_edges);
-  uint32_t* unit_off = ws_alloc<uint32_t>(h, runs_bound + 1);
-  uint32_t* blk_off = ws_alloc<uint32_t>(h, runs_bound + 1);
-  uint32_t* unit_run = ws_alloc<uint32_t>(h, ub);
-  launch_scan(h, "scan_kernel<plan>", runs_bound, d_n_runs(h), PlanIn{g, b},
-              PlanOut{g, b, run_deg, run_tail, unit_off, blk_off, unit_run},
-              PlanFin{g, unit_off, h->d_op(), n_edges, csr_path ? 0 : 1});
-  const int grid = grid_for(h, ub, 8 * 32);
+  const int grid = grid_for(h, units_bound(h->B, runs_bound, n_edges), 8 * 32);
   if (csr_path) {
     DG_LAUNCH(h, "append_kernel<validate>", append_kernel<true, false><<<grid, 256, 0, h->stream>>>(
-        g, b, unit_off, blk_off, unit_run, run_deg, run_tail, h->d_op()));
+        g, b, a.unit_off, a.blk_off, a.unit_run, a.run_deg, a.run_tail, h->d_op()));
     DG_LAUNCH(h, "commit_insert_kernel", commit_insert_kernel<<<grid_for(h, runs_bound, 256), 256, 0, h->stream>>>(
-        g, b, blk_off, run_deg, h->d_op()));
+        g, b, a.blk_off, a.run_deg, h->d_op()));
   } else {
     DG_LAUNCH(h, "append_kernel<commit>", append_kernel<false, true><<<grid, 256, 0, h->stream>>>(
-        g, b, unit_off, blk_off, unit_run, run_deg, run_tail, h->d_op()));
+        g, b, a.unit_off, a.blk_off, a.unit_run, a.run_deg, a.run_tail, h->d_op()));
   }
 }
-inline size_t plan_append_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n_edges) {
-  return 2 * aligned((runs_bound + 1) * 4) + aligned(units_bound(h, runs_bound, n_edges) * 4) +
-         scan_ws_bytes(runs_bound);
+
+// plan + append over an already grouped batch (radix path: sorted keys + detected runs; CSR: offsets)
+void enqueue_plan_append(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n_edges,
+                         bool csr_path) {
+  GraphView g = view(h);
+  PlanArrays a = alloc_plan_arrays(h, runs_bound, n_edges);
+  launch_alloc(h, "alloc_kernel<plan>", runs_bound, d_n_runs(h), PlanIn{g, b}, PlanOut{a},
+               PlanFin{g, h->d_op(), n_edges, /*set_runs=*/0, csr_path ? 0 : 1});
+  enqueue_append(h, b, a, runs_bound, n_edges, csr_path);
 }
 
 struct Worklist {
@@ -478,6 +494,9 @@ struct Worklist {
   uint2* med_items;    // (run, chunk) items of the medium / long match tiers (nullptr without a batch)
   uint2* long_items;
   uint32_t* big_list;  // chains longer than kLaneWalk blocks
+  EnumLists lists(dg_graph* h) const {
+    return EnumLists{run_deg, wl_off, med_items, long_items, big_list, h->d_op()};
+  }
 };
 
 // items: every run of a tier has at least one, plus one per full chunk of its chain
@@ -489,35 +508,45 @@ inline uint64_t long_items_bound(const dg_graph* h, uint64_t n) {
 }
 inline uint64_t big_bound(const dg_graph* h) { return h->blocks_in_use() / (kLaneWalk + 1) + 16; }
 
-// n_batch: entries of the batch the runs index into (0 = no batch: export, digest)
-Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n_batch,
-                           int check_alive) {
-  GraphView g = view(h);
+// n_batch: entries of the batch the runs index into; has_batch false: export, digest
+Worklist alloc_worklist(dg_graph* h, uint64_t runs_bound, uint64_t n_batch, bool has_batch) {
   Worklist w{};
   const uint64_t wl_cap = h->blocks_in_use();
   w.wl_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   w.run_deg = ws_alloc<uint32_t>(h, runs_bound + 1);
   w.wl_handle = ws_alloc<uint32_t>(h, wl_cap + 1);
   w.wl_run = ws_alloc<uint32_t>(h, wl_cap + 1);
-  if (b.run_start != nullptr) {
+  if (has_batch) {
     w.med_items = ws_alloc<uint2>(h, med_items_bound(h, n_batch));
     w.long_items = ws_alloc<uint2>(h, long_items_bound(h, n_batch));
   }
   w.big_list = ws_alloc<uint32_t>(h, big_bound(h));
-  EnumIn in{g, b, check_alive};
-  launch_scan(h, "scan_kernel<enum>", runs_bound, d_n_runs(h), in,
-              EnumOut{in, w.run_deg, w.wl_off, w.med_items, w.long_items, w.big_list, h->d_op()},
-              EnumFin{w.wl_off, h->d_op(), wl_cap});
-  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_for(h, runs_bound, 256), 256, 0, h->stream>>>(
-      g, b, w.wl_off, w.wl_handle, w.wl_run, h->d_op()));
-  DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_for(h, big_bound(h), 8), 256, 0, h->stream>>>(
-      g, b, w.wl_off, w.big_list, w.wl_handle, w.wl_run, h->d_op()));
   return w;
 }
-inline size_t enumerate_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n_batch) {
+inline size_t worklist_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n_batch) {
   return 2 * aligned((runs_bound + 1) * 4) + 2 * aligned((h->blocks_in_use() + 1) * 4) +
          aligned(med_items_bound(h, n_batch) * 8) + aligned(long_items_bound(h, n_batch) * 8) +
-         aligned(big_bound(h) * 4) + scan_ws_bytes(runs_bound);
+         aligned(big_bound(h) * 4) + alloc_ws_bytes();
+}
+
+// chain walk over a planned worklist
+void enqueue_walk(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound) {
+  GraphView g = view(h);
+  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_for(h, runs_bound, 256), 256, 0, h->stream>>>(
+      g, b, w.wl_off, w.run_deg, w.wl_handle, w.wl_run, h->d_op()));
+  DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_for(h, big_bound(h), 8), 256, 0, h->stream>>>(
+      g, b, w.wl_off, w.run_deg, w.big_list, w.wl_handle, w.wl_run, h->d_op()));
+}
+
+// enumeration over an already grouped batch (radix path, CSR batches) or over every vertex (export)
+Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n_batch,
+                           int check_alive) {
+  GraphView g = view(h);
+  Worklist w = alloc_worklist(h, runs_bound, n_batch, b.run_start != nullptr);
+  launch_alloc(h, "alloc_kernel<enum>", runs_bound, d_n_runs(h), EnumIn{g, b, check_alive}, EnumOut{b, w.lists(h)},
+               EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/0});
+  enqueue_walk(h, b, w, runs_bound);
+  return w;
 }
 
 // match over an enumerated worklist: three tiers by the number of targets per source
@@ -529,36 +558,54 @@ void enqueue_match(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
   DG_LAUNCH(h, kIsDelete ? "match_tiny_kernel<delete>" : "match_tiny_kernel<query>",
             match_tiny_kernel<kIsDelete><<<grid_for(h, wl_bound, 256), 256, 0, h->stream>>>(
                 g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
+  const size_t med_smem = kIsDelete ? kMedSmemDelete : kMedSmemQuery;
+  const size_t long_smem = kIsDelete ? kLongSmemDelete : kLongSmemQuery;
+  static bool attr_done[2] = {false, false};
+  if (!attr_done[kIsDelete ? 1 : 0]) {  // opt in to > 48 KB of dynamic shared memory once per instantiation
+    cudaFuncSetAttribute(match_med_kernel<kIsDelete>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)med_smem);
+    cudaFuncSetAttribute(match_long_kernel<kIsDelete>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_smem);
+    attr_done[kIsDelete ? 1 : 0] = true;
+  }
   DG_LAUNCH(h, kIsDelete ? "match_med_kernel<delete>" : "match_med_kernel<query>",
-            match_med_kernel<kIsDelete><<<grid_for(h, med_items_bound(h, n_batch), 8), 256, 0, h->stream>>>(
+            match_med_kernel<kIsDelete><<<grid_for(h, med_items_bound(h, n_batch), 8), 256, med_smem, h->stream>>>(
                 g, b, w.wl_off, w.wl_handle, w.med_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
   const int long_grid = (int)std::min<uint64_t>(long_items_bound(h, n_batch), (uint64_t)h->sm_count * 6);
   DG_LAUNCH(h, kIsDelete ? "match_long_kernel<delete>" : "match_long_kernel<query>",
-            match_long_kernel<kIsDelete><<<long_grid, kLongThreads, 0, h->stream>>>(
+            match_long_kernel<kIsDelete><<<long_grid, kLongThreads, long_smem, h->stream>>>(
                 g, b, w.wl_off, w.wl_handle, w.long_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
 }
 
 // ---- grouping a COO batch by source --------------------------------------------------------------
-// Two strategies behind one result (a BatchView + a bound on the runs):
-//   counting: per-vertex counters, a scan over the vertices, a scatter — O(V + n);
-//   radix:    pack 64-bit keys, LSD radix sort by source, run detection — O(n).
-struct Grouped {
-  BatchView b{};
-  uint64_t runs_bound = 0;
-  uint32_t* index = nullptr;  // original position of every grouped entry (queries)
-};
-
+// Two strategies:
+//   counting: per-vertex counters (validate + count), ONE alloc pass over the
+//             vertices that hands out run slots and group slots TOGETHER WITH the
+//             op's own plan (insert: append units + queue positions; delete/query:
+//             work-list segments), then a scatter — O(V + n);
+//   radix:    pack 64-bit keys, LSD radix sort by source, run detection, then the
+//             op's plan as an alloc pass over the runs — O(n).
 inline bool use_counting(const dg_graph* h, uint64_t n) {
+  if (h->B == 0) return false;  // deferred pool: the plan needs the block size, which needs the run count first
   if (h->group_mode == 1) return false;
   if (h->group_mode == 2) return true;
   return h->size + 1 <= std::max<uint64_t>(32 * n, 1ull << 22);
 }
 
+struct Grouped {
+  BatchView b{};
+  uint64_t runs_bound = 0;
+  uint32_t* index = nullptr;  // original position of every grouped entry (queries)
+  // counting path, between count and scatter
+  uint32_t* cnt = nullptr;
+  uint32_t* rank = nullptr;
+  uint32_t* gdst = nullptr;
+  uint32_t *run_src = nullptr, *run_start = nullptr, *run_end = nullptr;
+};
+
 inline size_t group_ws_bytes(const dg_graph* h, uint64_t n, bool with_index, uint64_t max_src) {
   size_t t = 0;
   if (use_counting(h, n)) {
     t += aligned((h->size + 2) * 4) + 2 * aligned(n * 4) + (with_index ? aligned(n * 4) : 0);
-    t += 2 * aligned((std::min<uint64_t>(n, h->size + 1) + 1) * 4) + scan_ws_bytes(h->size + 1);
+    t += 3 * aligned((std::min<uint64_t>(n, h->size + 1) + 1) * 4);
   } else {
     t += 2 * aligned(n * 8) + (with_index ? 2 * aligned(n * 4) : 0);
     t += sort_ws_bytes(n, src_sort_plan(h, max_src).passes);
@@ -567,59 +614,70 @@ inline size_t group_ws_bytes(const dg_graph* h, uint64_t n, bool with_index, uin
   return t;
 }
 
+// counting path, step 1: validate + count; allocates the run arrays the op's alloc pass fills
 template <int kMode>
-Grouped group_batch(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, bool with_index,
+Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, bool with_index) {
+  GraphView g = view(h);
+  Grouped out;
+  const uint64_t nv = h->size + 1;  // + 1: the slot unknown query sources are clamped to
+  out.cnt = ws_alloc<uint32_t>(h, nv + 1);
+  out.rank = ws_alloc<uint32_t>(h, n);
+  out.gdst = ws_alloc<uint32_t>(h, n);
+  if (with_index) out.index = ws_alloc<uint32_t>(h, n);
+  out.runs_bound = std::min<uint64_t>(n, nv);
+  out.run_start = ws_alloc<uint32_t>(h, out.runs_bound + 1);
+  out.run_end = ws_alloc<uint32_t>(h, out.runs_bound + 1);
+  out.run_src = ws_alloc<uint32_t>(h, out.runs_bound + 1);
+  cudaMemsetAsync(out.cnt, 0, (nv + 1) * 4, h->stream);
+  DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
+      g, d_src, d_dst, (uint32_t)n, out.cnt, out.rank, h->d_op()));
+  out.b = BatchView{nullptr, out.gdst, out.run_src, out.run_start, out.run_end};
+  return out;
+}
+// counting path, step 3 (after the op's alloc pass turned cnt into group starts)
+template <int kMode>
+void group_scatter(dg_graph* h, const Grouped& gr, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n) {
+  GraphView g = view(h);
+  const unsigned grid = (unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems));
+  if (gr.index) {
+    DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, true><<<grid, 256, 0, h->stream>>>(
+        g, d_src, d_dst, (uint32_t)n, gr.cnt, gr.rank, gr.gdst, gr.index, h->d_op()));
+  } else {
+    DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, false><<<grid, 256, 0, h->stream>>>(
+        g, d_src, d_dst, (uint32_t)n, gr.cnt, gr.rank, gr.gdst, nullptr, h->d_op()));
+  }
+}
+
+// radix path: complete grouping (runs laid out in order: run_end == run_start + 1)
+template <int kMode>
+Grouped group_radix(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, bool with_index,
                     uint64_t max_src) {
   GraphView g = view(h);
   Grouped out;
-  if (use_counting(h, n)) {
-    const uint64_t nv = h->size + 1;  // + 1: the slot unknown query sources are clamped to
-    uint32_t* cnt = ws_alloc<uint32_t>(h, nv + 1);
-    uint32_t* rank = ws_alloc<uint32_t>(h, n);
-    uint32_t* gdst = ws_alloc<uint32_t>(h, n);
-    if (with_index) out.index = ws_alloc<uint32_t>(h, n);
-    out.runs_bound = std::min<uint64_t>(n, nv);
-    uint32_t* run_start = ws_alloc<uint32_t>(h, out.runs_bound + 1);
-    uint32_t* run_src = ws_alloc<uint32_t>(h, out.runs_bound + 1);
-    cudaMemsetAsync(cnt, 0, (nv + 1) * 4, h->stream);
-    DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
-        g, d_src, d_dst, (uint32_t)n, cnt, rank, h->d_op()));
-    launch_scan(h, "scan_kernel<group>", nv, d_n_aux(h), GroupIn{cnt}, GroupOut{cnt, run_src, run_start},
-                GroupFin{run_start, h->d_op()});
-    if (with_index) {
-      DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, true><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
-          g, d_src, d_dst, (uint32_t)n, cnt, rank, gdst, out.index, h->d_op()));
-    } else {
-      DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, false><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
-          g, d_src, d_dst, (uint32_t)n, cnt, rank, gdst, nullptr, h->d_op()));
-    }
-    out.b = BatchView{nullptr, gdst, run_src, run_start};
-  } else {
-    SortPlan plan = src_sort_plan(h, max_src);
-    unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
-    unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
-    uint32_t *idx = nullptr, *idx_alt = nullptr;
-    if (with_index) {
-      idx = ws_alloc<uint32_t>(h, n);
-      idx_alt = ws_alloc<uint32_t>(h, n);
-    }
-    SortScratch sc = sort_prepare(h, n, plan);
-    if (with_index) {
-      DG_LAUNCH(h, "pack_coo_kernel", pack_coo_kernel<kMode, true><<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(
-          g, d_src, d_dst, (uint32_t)n, keys, idx, plan, sc.hist, h->d_op()));
-    } else {
-      DG_LAUNCH(h, "pack_coo_kernel", pack_coo_kernel<kMode, false><<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(
-          g, d_src, d_dst, (uint32_t)n, keys, nullptr, plan, sc.hist, h->d_op()));
-    }
-    sort_keys(h, &keys, &keys_alt, with_index ? &idx : nullptr, with_index ? &idx_alt : nullptr, n, plan, sc, true);
-    out.runs_bound = n;
-    uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
-    uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
-    launch_scan(h, "scan_kernel<runs>", n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
-                RunsFin{run_start, h->d_op(), (uint32_t)n});
-    out.b = BatchView{keys, nullptr, run_src, run_start};
-    out.index = idx;
+  SortPlan plan = src_sort_plan(h, max_src);
+  unsigned long long* keys = ws_alloc<unsigned long long>(h, n);
+  unsigned long long* keys_alt = ws_alloc<unsigned long long>(h, n);
+  uint32_t *idx = nullptr, *idx_alt = nullptr;
+  if (with_index) {
+    idx = ws_alloc<uint32_t>(h, n);
+    idx_alt = ws_alloc<uint32_t>(h, n);
   }
+  SortScratch sc = sort_prepare(h, n, plan);
+  if (with_index) {
+    DG_LAUNCH(h, "pack_coo_kernel", pack_coo_kernel<kMode, true><<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(
+        g, d_src, d_dst, (uint32_t)n, keys, idx, plan, sc.hist, h->d_op()));
+  } else {
+    DG_LAUNCH(h, "pack_coo_kernel", pack_coo_kernel<kMode, false><<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(
+        g, d_src, d_dst, (uint32_t)n, keys, nullptr, plan, sc.hist, h->d_op()));
+  }
+  sort_keys(h, &keys, &keys_alt, with_index ? &idx : nullptr, with_index ? &idx_alt : nullptr, n, plan, sc, true);
+  out.runs_bound = n;
+  uint32_t* run_start = ws_alloc<uint32_t>(h, n + 1);
+  uint32_t* run_src = ws_alloc<uint32_t>(h, n + 1);
+  launch_scan(h, "scan_kernel<runs>", n, d_n_input(h), RunsIn{keys}, RunsOut{keys, run_start, run_src},
+              RunsFin{run_start, h->d_op(), (uint32_t)n});
+  out.b = BatchView{keys, nullptr, run_src, run_start, run_start + 1};
+  out.index = idx;
   return out;
 }
 
@@ -629,10 +687,34 @@ int require_pool(dg_graph* h) {
   return DG_OK;
 }
 
-// delete over a grouped batch (COO: group_batch; CSR: the offsets are the runs)
-int delete_grouped(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n) {
+// group + enumerate a COO batch for delete / query (either strategy)
+template <int kMode>
+Grouped group_and_enumerate(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n,
+                            bool with_index, uint64_t max_src, Worklist* w_out) {
   GraphView g = view(h);
-  Worklist w = enqueue_enumerate(h, b, runs_bound, n, /*check_alive=*/1);
+  if (use_counting(h, n)) {
+    Grouped gr = group_count<kMode>(h, d_src, d_dst, n, with_index);
+    Worklist w = alloc_worklist(h, gr.runs_bound, n, true);
+    launch_alloc(h, "alloc_kernel<group+enum>", h->size + 1, d_n_aux(h), GroupEnumIn{g, gr.cnt, 1},
+                 GroupEnumOut{gr.cnt, gr.run_src, gr.run_start, gr.run_end, w.lists(h)},
+                 EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/1});
+    group_scatter<kMode>(h, gr, d_src, d_dst, n);
+    enqueue_walk(h, gr.b, w, gr.runs_bound);
+    *w_out = w;
+    return gr;
+  }
+  Grouped gr = group_radix<kMode>(h, d_src, d_dst, n, with_index, max_src);
+  *w_out = enqueue_enumerate(h, gr.b, gr.runs_bound, n, /*check_alive=*/1);
+  return gr;
+}
+inline size_t group_enumerate_ws(const dg_graph* h, uint64_t n, bool with_index, uint64_t max_src) {
+  return group_ws_bytes(h, n, with_index, max_src) + worklist_ws(h, std::min<uint64_t>(n, h->size + 1) + 0, n) +
+         worklist_ws(h, n, n);  // either strategy's run bound
+}
+
+// delete over a grouped + enumerated batch
+int delete_matched(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound, uint64_t n) {
+  GraphView g = view(h);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   uint32_t* run_matched = ws_alloc<uint32_t>(h, runs_bound + 1);
   uint32_t* hole_cnt = ws_alloc<uint32_t>(h, runs_bound + 1);
@@ -646,8 +728,8 @@ int delete_grouped(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_
     h->ws.off = ws_mark;
     cudaMemsetAsync(hole_cnt, 0, (runs_bound + 1) * 4, h->stream);
     cudaMemsetAsync(surv_cnt, 0, (runs_bound + 1) * 4, h->stream);
-    launch_scan(h, "scan_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{w.run_deg, run_matched}, MovesOut{mv_off},
-                MovesFin{mv_off, h->d_op(), h->mv_cap});
+    launch_alloc(h, "alloc_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{w.run_deg, run_matched},
+                 MovesOut{mv_off}, MovesFin{h->d_op(), h->mv_cap});
     DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_for(h, wl_bound, 256), 256, 0, h->stream>>>(
         g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, wl_mask, hole_cnt,
         h->mv_hole, h->d_op()));
@@ -663,10 +745,9 @@ int delete_grouped(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_
   }
   return fail(h, DG_ERR_ENGINE, "delete: compaction scratch retry failed");
 }
-inline size_t delete_grouped_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n) {
+inline size_t delete_matched_ws(const dg_graph* h, uint64_t runs_bound) {
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  return enumerate_ws(h, runs_bound, n) + 4 * aligned((runs_bound + 1) * 4) +
-         aligned((wl_bound + 1) * ((h->B + 31) / 32) * 4) + scan_ws_bytes(runs_bound);
+  return 4 * aligned((runs_bound + 1) * 4) + aligned((wl_bound + 1) * ((h->B + 31) / 32) * 4) + alloc_ws_bytes();
 }
 
 }  // namespace
@@ -743,6 +824,7 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
     if (rc != DG_OK) return bail(rc, h->last_error);
   }
   if (ensure_mv_scratch(h, 1 << 16) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
+  if (cfg.workspace_bytes && ws_reserve(h, cfg.workspace_bytes) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
   e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return bail(DG_ERR_CUDA, std::string("dg_create: ") + cudaGetErrorString(e));
   *out = h;
@@ -780,23 +862,30 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   if (n == 0) return DG_OK;  // EmptyBatchChangesNothing
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
-  const uint64_t rb = std::min<uint64_t>(n, h->size + 1);  // runs bound of either grouping
+  const bool counting = use_counting(h, n);
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
   sz.total += group_ws_bytes(h, n, false, h->size - 1);
-  sz.add<uint32_t>(n + 1); sz.add<uint32_t>(n + 1);
   // block size may still be unknown (deferred pool): size the unit list for B = 1
-  sz.total += 2 * aligned((n + 1) * 4) + aligned((3 * n + 1) * 4) + scan_ws_bytes(n);
-  (void)rb;
+  sz.total += plan_arrays_ws(1, n, n);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const uint32_t *d_src, *d_dst;
   if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
   if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
   if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
-  Grouped gb = group_batch<kPackInsert>(h, d_src, d_dst, n, false, h->size - 1);
-  uint32_t* run_deg = ws_alloc<uint32_t>(h, gb.runs_bound + 1);
-  uint32_t* run_tail = ws_alloc<uint32_t>(h, gb.runs_bound + 1);
+  if (counting) {
+    GraphView g = view(h);
+    Grouped gr = group_count<kPackInsert>(h, d_src, d_dst, n, false);
+    PlanArrays a = alloc_plan_arrays(h, gr.runs_bound, n);
+    launch_alloc(h, "alloc_kernel<group+plan>", h->size + 1, d_n_aux(h), GroupPlanIn{g, gr.cnt},
+                 GroupPlanOut{gr.cnt, gr.run_src, gr.run_start, gr.run_end, a},
+                 PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/1});
+    group_scatter<kPackInsert>(h, gr, d_src, d_dst, n);
+    enqueue_append(h, gr.b, a, gr.runs_bound, n, /*csr_path=*/false);
+    return op_end(h);
+  }
+  Grouped gr = group_radix<kPackInsert>(h, d_src, d_dst, n, false, h->size - 1);
   if (h->B == 0) {
     // deferred pool: compute_block_size (csr.hpp:77-88) from this first batch
     if ((rc = op_end(h)) != DG_OK) return rc;
@@ -808,7 +897,7 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
     op.err_index = ~0ull;
     DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
   }
-  enqueue_plan_append(h, gb.b, gb.runs_bound, n, run_deg, run_tail, /*csr_path=*/false);
+  enqueue_plan_append(h, gr.b, gr.runs_bound, n, /*csr_path=*/false);
   return op_end(h);
 }
 
@@ -827,8 +916,8 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
   const uint64_t V = h->size;
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<unsigned long long>(n_offsets); sz.add<uint32_t>(n_edges); }
-  sz.add<uint32_t>(V + 2); sz.add<uint32_t>(V + 1); sz.add<uint32_t>(V + 1);
-  sz.total += 2 * aligned((V + 1) * 4) + aligned((2 * std::min<uint64_t>(V, n_edges) + n_edges + 1) * 4) + scan_ws_bytes(V);
+  sz.add<uint32_t>(V + 2);
+  sz.total += plan_arrays_ws(1, V, n_edges);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const unsigned long long* d_off;
@@ -838,8 +927,6 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
   if ((rc = op_begin(h, n_edges, V)) != DG_OK) return rc;
   GraphView g = view(h);
   uint32_t* run_start = ws_alloc<uint32_t>(h, V + 2);
-  uint32_t* run_deg = ws_alloc<uint32_t>(h, V + 1);
-  uint32_t* run_tail = ws_alloc<uint32_t>(h, V + 1);
   DG_LAUNCH(h, "csr_validate_offsets_kernel", csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
       g, d_off, (uint32_t)n_offsets, n_edges, /*check_dead_source=*/1, run_start, h->d_op()));
   if (n_edges == 0 || V == 0) return op_end(h);  // validated; nothing to append
@@ -856,8 +943,8 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
     op.aux0 = 0;
     DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
   }
-  BatchView b{nullptr, d_dst, nullptr, run_start};
-  enqueue_plan_append(h, b, V, n_edges, run_deg, run_tail, /*csr_path=*/true);
+  BatchView b{nullptr, d_dst, nullptr, run_start, run_start + 1};
+  enqueue_plan_append(h, b, V, n_edges, /*csr_path=*/true);
   return op_end(h);
 }
 
@@ -883,17 +970,21 @@ int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   const bool no_pool = h->B == 0;  // no pool yet => no edges: only validation can have an effect
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
-  sz.total += group_ws_bytes(h, n, false, h->size - 1);
-  if (!no_pool) sz.total += delete_grouped_ws(h, n, n);
+  if (no_pool) sz.total += group_ws_bytes(h, n, false, h->size - 1);
+  else sz.total += group_enumerate_ws(h, n, false, h->size - 1) + delete_matched_ws(h, n);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const uint32_t *d_src, *d_dst;
   if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
   if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
   if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
-  Grouped gb = group_batch<kPackDelete>(h, d_src, d_dst, n, false, h->size - 1);
-  if (no_pool) return op_end(h);
-  return delete_grouped(h, gb.b, gb.runs_bound, n);
+  if (no_pool) {  // validation only (radix path packs + validates; B == 0 never takes the counting path)
+    group_radix<kPackDelete>(h, d_src, d_dst, n, false, h->size - 1);
+    return op_end(h);
+  }
+  Worklist w;
+  Grouped gr = group_and_enumerate<kPackDelete>(h, d_src, d_dst, n, false, h->size - 1, &w);
+  return delete_matched(h, gr.b, w, gr.runs_bound, n);
 }
 
 int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
@@ -910,7 +1001,7 @@ int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<unsigned long long>(n_offsets); sz.add<uint32_t>(n); }
   sz.add<uint32_t>(V + 2);
-  if (h->B) sz.total += delete_grouped_ws(h, V, n);
+  if (h->B) sz.total += worklist_ws(h, V, n) + delete_matched_ws(h, V);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const unsigned long long* d_off;
@@ -927,8 +1018,9 @@ int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets
   }
   if (n == 0 || V == 0 || h->B == 0) return op_end(h);
   // a CSR batch is already grouped: run r is vertex r (empty runs are skipped by the enumeration)
-  BatchView b{nullptr, d_dst, nullptr, run_start};
-  return delete_grouped(h, b, V, n);
+  BatchView b{nullptr, d_dst, nullptr, run_start, run_start + 1};
+  Worklist w = enqueue_enumerate(h, b, V, n, /*check_alive=*/1);
+  return delete_matched(h, b, w, V, n);
 }
 
 // ---- query ---------------------------------------------------------------------
@@ -946,8 +1038,7 @@ int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64
   }
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); sz.add<uint8_t>(n); }
-  sz.total += group_ws_bytes(h, n, true, h->size);  // ids are clamped to size (unknown source)
-  sz.total += enumerate_ws(h, n, n);
+  sz.total += group_enumerate_ws(h, n, true, h->size);  // ids are clamped to size (unknown source)
   sz.add<uint8_t>(n);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
@@ -956,8 +1047,8 @@ int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64
   if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
   uint8_t* d_out = (mem == DG_MEM_HOST) ? ws_alloc<uint8_t>(h, n) : out;
   if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
-  Grouped gb = group_batch<kPackQuery>(h, d_src, d_dst, n, true, h->size);
-  Worklist w = enqueue_enumerate(h, gb.b, gb.runs_bound, n, /*check_alive=*/1);
+  Worklist w;
+  Grouped gb = group_and_enumerate<kPackQuery>(h, d_src, d_dst, n, true, h->size, &w);
   uint8_t* hit = ws_alloc<uint8_t>(h, n);
   cudaMemsetAsync(hit, 0, n, h->stream);
   enqueue_match<false>(h, gb.b, w, n, nullptr, nullptr, hit);
@@ -1003,7 +1094,7 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
   SortPlan plan = make_sort_plan(bits_for(h->dst_limit() - 1), bits_for(V - 1));
   WsSizer sz;
   sz.add<unsigned long long>(V + 1);
-  sz.total += enumerate_ws(h, V, 0);
+  sz.total += worklist_ws(h, V, 0);
   if (mem == DG_MEM_HOST) sz.add<uint32_t>(total);
   if (sorted) { sz.add<unsigned long long>(total); sz.add<unsigned long long>(total); sz.total += sort_ws_bytes(total, plan.passes); }
   // (host path: offsets were copied to the caller; re-uploaded after the workspace is re-laid out)
@@ -1015,7 +1106,7 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
   }
   if ((rc = op_begin(h, V, V)) != DG_OK) return rc;
   GraphView g = view(h);
-  BatchView b{nullptr, nullptr, nullptr, nullptr};
+  BatchView b{nullptr, nullptr, nullptr, nullptr, nullptr};
   Worklist w = enqueue_enumerate(h, b, V, 0, /*check_alive=*/0);
   uint32_t* d_dst = (mem == DG_MEM_HOST) ? ws_alloc<uint32_t>(h, total) : destinations;
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
@@ -1061,11 +1152,11 @@ int dg_digest(dg_graph* h, uint64_t* out_digest, uint64_t* out_entries) {
   if (out_digest) *out_digest = 0;
   if (out_entries) *out_entries = 0;
   if (V == 0 || h->B == 0) return DG_OK;
-  int rc = ws_reserve(h, enumerate_ws(h, V, 0));
+  int rc = ws_reserve(h, worklist_ws(h, V, 0));
   if (rc != DG_OK) return rc;
   if ((rc = op_begin(h, V, V)) != DG_OK) return rc;
   GraphView g = view(h);
-  BatchView b{nullptr, nullptr, nullptr, nullptr};
+  BatchView b{nullptr, nullptr, nullptr, nullptr, nullptr};
   Worklist w = enqueue_enumerate(h, b, V, 0, 0);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   DG_LAUNCH(h, "digest_kernel", digest_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(g, w.wl_off, w.wl_handle, w.wl_run,

@@ -209,6 +209,109 @@ scan_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* sc
 }
 
 // ===========================================================================
+// Unordered range allocation ("atomic scan")
+// ===========================================================================
+// Most prefix sums of the batch ops only hand out DISJOINT RANGES (queue
+// positions, work-list segments, scratch segments, group slots): order between
+// tiles is irrelevant.  alloc_kernel keeps the exclusive scan inside a tile
+// and replaces the look-back chain by one atomicAdd per tile and word on a
+// global cursor, so tiles never wait for each other.  Two 64-bit words are
+// scanned at once (callers pack two 32-bit quantities into each).
+//   In(i)                         -> Sum2 (PURE loads; see scan_kernel)
+//   Out(i, excl.a, excl.b, value) -> per element
+//   Fin(total.a, total.b)         -> once, by the last tile to finish
+// scratch: [0] cursor a, [1] cursor b, [2] finished tiles; zeroed before launch.
+struct Sum2 {
+  unsigned long long a, b;
+};
+constexpr size_t kAllocScratchWords = 4;
+constexpr int kAllocThreads = 256;
+constexpr int kAllocItems = 4;
+constexpr int kAllocTile = kAllocThreads * kAllocItems;
+
+// In::Aux is a small per-element payload In fills next to the sums (values it
+// already loaded) and Out receives back, so Out never re-loads them.  In must
+// use predicated loads (`x = c ? p[i] : 0`), not branches: the kernel issues a
+// thread's items back to back and a branch would serialise their latencies.
+template <class In, class Out, class Fin>
+__global__ void __launch_bounds__(kAllocThreads, 4)
+alloc_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* scratch,
+             const OpState* __restrict__ op_guard, In in, Out out, Fin fin) {
+  if (op_guard != nullptr && op_guard->err != 0) return;
+  __shared__ Sum2 s_warp[kAllocThreads / 32];
+  __shared__ Sum2 s_base;
+  const unsigned long long n = *n_ptr;
+  const unsigned long long num_tiles = (n + kAllocTile - 1) / kAllocTile;
+  const unsigned int tile = blockIdx.x;
+  if (tile >= num_tiles) {
+    if (n == 0 && tile == 0 && threadIdx.x == 0) fin(0ull, 0ull);
+    return;
+  }
+  const unsigned long long base = (unsigned long long)tile * kAllocTile +
+                                  (unsigned long long)threadIdx.x * kAllocItems;
+  Sum2 v[kAllocItems];
+  typename In::Aux aux[kAllocItems];
+  Sum2 thread_sum{0ull, 0ull};
+#pragma unroll
+  for (int j = 0; j < kAllocItems; ++j) {
+    const unsigned long long i = base + j;
+    v[j] = in(i < n ? i : n - 1, aux[j]);   // clamped index keeps the loads unconditional
+    if (i >= n) v[j] = Sum2{0ull, 0ull};
+    thread_sum.a += v[j].a;
+    thread_sum.b += v[j].b;
+  }
+  Sum2 incl = thread_sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long ta = __shfl_up_sync(kFull, incl.a, d);
+    const unsigned long long tb = __shfl_up_sync(kFull, incl.b, d);
+    if (lane_id() >= d) {
+      incl.a += ta;
+      incl.b += tb;
+    }
+  }
+  const int warp = threadIdx.x >> 5;
+  if (lane_id() == 31) s_warp[warp] = incl;
+  __syncthreads();
+  Sum2 warp_excl{0ull, 0ull}, tile_sum{0ull, 0ull};
+#pragma unroll
+  for (int w = 0; w < kAllocThreads / 32; ++w) {
+    const Sum2 sw = s_warp[w];
+    if (w < warp) {
+      warp_excl.a += sw.a;
+      warp_excl.b += sw.b;
+    }
+    tile_sum.a += sw.a;
+    tile_sum.b += sw.b;
+  }
+  if (threadIdx.x == 0) {
+    Sum2 bs{0ull, 0ull};
+    if (tile_sum.a) bs.a = atomicAdd(&scratch[0], tile_sum.a);
+    if (tile_sum.b) bs.b = atomicAdd(&scratch[1], tile_sum.b);
+    s_base = bs;
+  }
+  __syncthreads();
+  Sum2 run{s_base.a + warp_excl.a + (incl.a - thread_sum.a), s_base.b + warp_excl.b + (incl.b - thread_sum.b)};
+#pragma unroll
+  for (int j = 0; j < kAllocItems; ++j) {
+    const unsigned long long i = base + j;
+    if (i < n) out(i, run.a, run.b, v[j], aux[j]);
+    run.a += v[j].a;
+    run.b += v[j].b;
+  }
+  // (off the tile's critical path) the last tile to get here sees every tile's
+  // contribution to the cursors: thread 0's cursor atomics precede its fence
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long done = atomicAdd(&scratch[2], 1ull);
+    if (done == num_tiles - 1) {
+      __threadfence();
+      fin(ld_volatile_u64(&scratch[0]), ld_volatile_u64(&scratch[1]));
+    }
+  }
+}
+
+// ===========================================================================
 // Onesweep radix sort (u64 keys, optional u32 values)
 // ===========================================================================
 constexpr int kSortThreads = 256;

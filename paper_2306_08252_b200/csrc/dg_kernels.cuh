@@ -44,7 +44,8 @@ struct BatchView {
   const unsigned long long* keys;  // sorted (src<<32|dst), or nullptr on the CSR path
   const uint32_t* dsts;            // CSR path values, or nullptr
   const uint32_t* run_src;         // nullptr => run r is vertex r
-  const uint32_t* run_start;       // [T + 1]
+  const uint32_t* run_start;       // first entry of run r
+  const uint32_t* run_end;         // one past its last entry (== run_start + 1 when runs are laid out in order)
 };
 
 __device__ __forceinline__ uint32_t batch_value(const BatchView& b, uint32_t i) {
@@ -52,6 +53,9 @@ __device__ __forceinline__ uint32_t batch_value(const BatchView& b, uint32_t i) 
 }
 __device__ __forceinline__ uint32_t batch_src(const BatchView& b, uint32_t r) {
   return b.run_src ? b.run_src[r] : r;
+}
+__device__ __forceinline__ uint32_t run_len(const BatchView& b, uint32_t r) {
+  return b.run_end[r] - b.run_start[r];
 }
 __device__ __forceinline__ uint32_t ceil_div(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
 // x / B and ceil(x / B) with the shift fast path (B = 32 is the native block: one 128-byte line)
@@ -74,6 +78,43 @@ __device__ __forceinline__ unsigned long long block_reduce_sum(unsigned long lon
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_warp[w];
   return t;  // valid in thread 0
 }
+
+// ---- asynchronous global -> shared staging (LDGSTS) -------------------------------
+// The match kernels stage up to 32 edge blocks of 128 bytes per warp in shared
+// memory: the copies are all issued before anything waits (no registers tied
+// up, no unrolled code), then a rolled loop consumes them.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+// Stages blocks u in [0, 32) whose bit is set in `want` (B = 32): handle of
+// block u in lane u; 8 lanes move one 128-byte block, 4 blocks per instruction.
+// Layout: the 16-byte chunk c of block u sits at chunk position (c + u) & 7 of
+// row u, so that afterwards LANE u can read ITS block with eight conflict-free
+// 16-byte shared loads (block_chunk) — the compare then runs one block per
+// lane with no cross-lane traffic.
+__device__ __forceinline__ void stage_blocks32(const GraphView& g, uint32_t (*dst)[32], uint32_t hd_lane,
+                                               unsigned want) {
+  const int lane = lane_id();
+  const int sub = lane >> 3, c = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int u = 4 * i + sub;
+    const uint32_t hu = __shfl_sync(kFull, hd_lane, u);
+    if ((want >> u) & 1u) cp_async16(&dst[u][((c + u) & 7) * 4], g.slab + (unsigned long long)hu * 32u + c * 4);
+  }
+}
+__device__ __forceinline__ uint4 block_chunk(uint32_t (*stg)[32], int u, int c) {
+  return *reinterpret_cast<const uint4*>(&stg[u][((c + u) & 7) * 4]);
+}
+__device__ __forceinline__ uint32_t block_slot(uint32_t (*stg)[32], int u, uint32_t s) {
+  return stg[u][((((s >> 2) + u) & 7) << 2) | (s & 3)];
+}
+// second, independent hash for the membership filters
+__device__ __forceinline__ uint32_t filter_hash(uint32_t x, int bits) { return (x * 0x85EBCA6Bu) >> (32 - bits); }
 
 // ---------------------------------------------------------------------------
 // init
@@ -197,37 +238,6 @@ group_count_kernel(GraphView g, const uint32_t* __restrict__ src, const uint32_t
   for (int q = 0; q < kGroupItems; ++q)
     if (ok[q]) rank[base + q * 256] = rk[q];
 }
-
-// scan over the vertices: packed value [63:32] touched sources, [31:0] entries
-struct GroupIn {
-  const uint32_t* cnt;
-  __device__ unsigned long long operator()(unsigned long long v) const {
-    const uint32_t c = cnt[v];
-    return ((unsigned long long)(c ? 1u : 0u) << 32) | c;
-  }
-};
-struct GroupOut {
-  uint32_t* cnt;        // becomes the group start of each touched source
-  uint32_t* run_src;
-  uint32_t* run_start;
-  __device__ void operator()(unsigned long long v, unsigned long long excl,
-                             unsigned long long val) const {
-    if ((uint32_t)val) {
-      const uint32_t r = (uint32_t)(excl >> 32);
-      run_src[r] = (uint32_t)v;
-      run_start[r] = (uint32_t)excl;
-      cnt[v] = (uint32_t)excl;
-    }
-  }
-};
-struct GroupFin {
-  uint32_t* run_start;
-  OpState* op;
-  __device__ void operator()(unsigned long long total) const {
-    run_start[total >> 32] = (uint32_t)total;
-    op->n_runs = total >> 32;
-  }
-};
 
 template <int kMode, bool kWithIndex>
 __global__ void __launch_bounds__(256)
@@ -365,64 +375,106 @@ __global__ void csr_expand_kernel(const uint32_t* __restrict__ run_start, uint32
 }
 
 // ---------------------------------------------------------------------------
-// insert: plan (graph.hpp:135-160) as a scan over touched sources
+// insert: plan (graph.hpp:135-160).  Everything the plan hands out is a
+// disjoint range (append units, queue positions, and — on the counting path —
+// run slots and group slots), so it runs as ONE alloc_kernel pass:
+//   word a = [63:32] touched sources (runs), [31:0] batch entries
+//   word b = [63:32] append units,           [31:0] fresh blocks
+// (The In functors are PURE loads: the kernel issues a thread's 8 items back to
+// back, and a store in between would serialise them.)
 // ---------------------------------------------------------------------------
-// Packed scan value: [61:31] append units, [30:0] fresh blocks.
-constexpr int kPackShift = 31;
-constexpr unsigned long long kPackLoMask = (1ull << kPackShift) - 1ull;
+__device__ __forceinline__ unsigned long long plan_word(const GraphView& g, uint32_t d, uint32_t c) {
+  // space left in the tail block == block_size - last_insert_offset (graph.hpp:149-150)
+  const uint32_t nb = blocks_for(g, d);
+  const uint32_t space = nb * g.B - d;
+  const uint32_t fill = min(c, space);
+  const uint32_t need = blocks_for(g, c - fill);  // graph.hpp:152-153
+  const uint32_t units = need + (fill > 0 ? 1u : 0u);
+  return ((unsigned long long)units << 32) | need;
+}
 
-// (The In functors of the scans are PURE loads: the scan kernel issues the 8
-// items of a thread back to back, and a store in between would serialise them.)
-struct PlanIn {
-  GraphView g;
-  BatchView b;
-  __device__ unsigned long long operator()(unsigned long long r64) const {
-    const uint32_t r = (uint32_t)r64;
-    const uint32_t v = batch_src(b, r);
-    const uint32_t c = b.run_start[r + 1] - b.run_start[r];
-    if (c == 0) return 0ull;
-    const uint32_t d = g.deg[v];
-    // space left in the tail block == block_size - last_insert_offset (graph.hpp:149-150)
-    const uint32_t nb = blocks_for(g, d);
-    const uint32_t space = nb * g.B - d;
-    const uint32_t fill = min(c, space);
-    const uint32_t need = blocks_for(g, c - fill);  // graph.hpp:152-153
-    const uint32_t units = need + (fill > 0 ? 1u : 0u);
-    return ((unsigned long long)units << kPackShift) | need;
-  }
+struct PlanAux {
+  uint32_t d, tail;  // degree / tail block of the source before the batch
 };
-// Besides the two exclusive offsets, every unit records its run so the append
-// kernel never searches (a hub's few thousand units are plain stores here).
-struct PlanOut {
-  GraphView g;
-  BatchView b;
+struct PlanArrays {
   uint32_t* run_deg;   // snapshots of deg/tail: append publishes the new values while other
   uint32_t* run_tail;  // units of the same source still need the old ones
   uint32_t* unit_off;
   uint32_t* blk_off;
-  uint32_t* unit_run;
-  __device__ void operator()(unsigned long long r, unsigned long long excl,
-                             unsigned long long v) const {
-    const uint32_t vtx = batch_src(b, (uint32_t)r);
-    run_deg[r] = g.deg[vtx];
-    run_tail[r] = g.tail[vtx];
-    const uint32_t uo = (uint32_t)(excl >> kPackShift);
+  uint32_t* unit_run;  // every unit records its run so the append kernel never searches
+  __device__ void write(uint32_t r, const PlanAux& x, unsigned long long excl_b, unsigned long long val_b) const {
+    run_deg[r] = x.d;
+    run_tail[r] = x.tail;
+    const uint32_t uo = (uint32_t)(excl_b >> 32);
     unit_off[r] = uo;
-    blk_off[r] = (uint32_t)(excl & kPackLoMask);
-    const uint32_t units = (uint32_t)(v >> kPackShift);
-    for (uint32_t j = 0; j < units; ++j) unit_run[uo + j] = (uint32_t)r;
+    blk_off[r] = (uint32_t)excl_b;
+    const uint32_t units = (uint32_t)(val_b >> 32);
+    for (uint32_t j = 0; j < units; ++j) unit_run[uo + j] = r;
+  }
+};
+
+// plan over already-grouped runs (radix path, CSR batches)
+struct PlanIn {
+  using Aux = PlanAux;
+  GraphView g;
+  BatchView b;
+  __device__ Sum2 operator()(unsigned long long r64, Aux& x) const {
+    const uint32_t r = (uint32_t)r64;
+    const uint32_t c = run_len(b, r);
+    const uint32_t v = batch_src(b, r);
+    x.d = c ? g.deg[v] : 0u;
+    x.tail = c ? g.tail[v] : kNull;
+    return Sum2{0ull, c ? plan_word(g, x.d, c) : 0ull};
+  }
+};
+struct PlanOut {
+  PlanArrays arr;
+  __device__ void operator()(unsigned long long r, unsigned long long, unsigned long long excl_b,
+                             Sum2 v, const PlanAux& x) const {
+    arr.write((uint32_t)r, x, excl_b, v.b);
+  }
+};
+// plan fused with the counting group-by: one pass over the vertices
+struct GroupPlanIn {
+  using Aux = PlanAux;
+  GraphView g;
+  const uint32_t* cnt;
+  __device__ Sum2 operator()(unsigned long long v, Aux& x) const {
+    const uint32_t c = cnt[v];
+    x.d = c ? g.deg[v] : 0u;
+    x.tail = c ? g.tail[v] : kNull;
+    return Sum2{c ? ((1ull << 32) | c) : 0ull, c ? plan_word(g, x.d, c) : 0ull};
+  }
+};
+struct GroupPlanOut {
+  uint32_t* cnt;        // becomes the group start of each touched source
+  uint32_t* run_src;
+  uint32_t* run_start;
+  uint32_t* run_end;
+  PlanArrays arr;
+  __device__ void operator()(unsigned long long v, unsigned long long excl_a, unsigned long long excl_b,
+                             Sum2 val, const PlanAux& x) const {
+    const uint32_t c = (uint32_t)val.a;
+    if (c == 0) return;
+    const uint32_t r = (uint32_t)(excl_a >> 32);
+    const uint32_t es = (uint32_t)excl_a;
+    run_src[r] = (uint32_t)v;
+    run_start[r] = es;
+    run_end[r] = es + c;
+    cnt[v] = es;
+    arr.write(r, x, excl_b, val.b);
   }
 };
 struct PlanFin {
   GraphView g;
-  uint32_t* unit_off;
   OpState* op;
   unsigned long long n_edges;
+  int set_runs;        // counting path: the pass also counted the runs
   int commit_globals;  // COO path: validation is complete, commit here; CSR path: commit_insert_kernel
-  __device__ void operator()(unsigned long long total) const {
-    const unsigned long long need = total & kPackLoMask;
-    const unsigned long long units = total >> kPackShift;
-    unit_off[op->n_runs] = (uint32_t)units;
+  __device__ void operator()(unsigned long long total_a, unsigned long long total_b) const {
+    const unsigned long long need = total_b & 0xFFFFFFFFull;
+    const unsigned long long units = total_b >> 32;
+    if (set_runs) op->n_runs = total_a >> 32;
     op->n_units = units;
     op->total_need = need;
     op->n_edges = n_edges;
@@ -482,7 +534,7 @@ append_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ unit_off,
       const uint32_t j = u - unit_off[r];
       const uint32_t v = batch_src(b, r);
       const uint32_t rs = b.run_start[r];
-      const uint32_t c = b.run_start[r + 1] - rs;
+      const uint32_t c = b.run_end[r] - rs;
       const uint32_t d = run_deg[r];
       const uint32_t nb_old = blocks_for(g, d);
       const uint32_t space = nb_old * g.B - d;
@@ -555,7 +607,7 @@ commit_insert_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ blk_
   const uint32_t T = (uint32_t)op->n_runs;
   const unsigned long long base_mod = op->front_old % g.ring_cap;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < T; r += gridDim.x * blockDim.x) {
-    const uint32_t c = b.run_start[r + 1] - b.run_start[r];
+    const uint32_t c = run_len(b, r);
     if (c == 0) continue;
     const uint32_t v = batch_src(b, r);
     const uint32_t d = run_deg[r];
@@ -589,64 +641,112 @@ constexpr uint32_t kTierBit = 0x80000000u;
 constexpr uint32_t kRunMask = 0x7FFFFFFFu;
 __device__ __forceinline__ uint32_t run_tag(const BatchView& b, uint32_t r) {
   if (b.run_start == nullptr) return r;
-  return (b.run_start[r + 1] - b.run_start[r] > kTinyTargets) ? (r | kTierBit) : r;
+  return (run_len(b, r) > kTinyTargets) ? (r | kTierBit) : r;
 }
 constexpr uint32_t kLongChunk = 256;     // blocks per CTA item of the long path
 
-struct EnumIn {
-  GraphView g;
-  BatchView b;
-  int check_alive;  // delete/query skip dead or unknown sources (graph.hpp:205, :229)
-  __device__ uint32_t degree(uint32_t r) const {
-    if (b.run_start != nullptr && b.run_start[r + 1] == b.run_start[r]) return 0;  // empty run (CSR batches)
-    const uint32_t v = batch_src(b, r);
-    uint32_t d = 0;
-    if (v < g.size && (!check_alive || bit_test(g.alive, v))) d = g.deg[v];
-    return d;
-  }
-  __device__ unsigned long long operator()(unsigned long long r64) const {
-    return blocks_for(g, degree((uint32_t)r64));
-  }
-};
-// Work lists are filled through device counters (order is irrelevant: they
-// only distribute work): chains a whole warp walks, and the (run, chunk)
-// items of the medium and long match tiers.
-struct EnumOut {
-  EnumIn in;
+// Enumeration plan: work-list segments are disjoint ranges too (alloc_kernel):
+//   word a = [63:32] touched sources (counting path only), [31:0] batch entries
+//   word b = blocks of the touched chains
+// The match tiers' (run, chunk) items and the long-chain list are filled
+// through device counters (order is irrelevant: they only distribute work).
+struct EnumLists {
   uint32_t* run_deg;
   uint32_t* wl_off;
   uint2* med_items;    // nullptr on paths without a batch (export, digest)
   uint2* long_items;
   uint32_t* big_list;  // sources whose chain the whole warp walks (enumerate_big_kernel)
   OpState* op;
-  __device__ void operator()(unsigned long long r, unsigned long long excl,
-                             unsigned long long v) const {
-    run_deg[r] = in.degree((uint32_t)r);
-    wl_off[r] = (uint32_t)excl;
-    const uint32_t nblk = (uint32_t)v;
-    if (nblk > kLaneWalk) big_list[atomicAdd(&op->n_big, 1ull)] = (uint32_t)r;
+  __device__ void write(uint32_t r, uint32_t d, uint32_t nblk, uint32_t k, unsigned long long excl_b) const {
+    run_deg[r] = d;
+    wl_off[r] = (uint32_t)excl_b;
+    if (nblk > kLaneWalk) big_list[atomicAdd(&op->n_big, 1ull)] = r;
     if (med_items != nullptr && nblk > 0) {
-      const uint32_t k = in.b.run_start[r + 1] - in.b.run_start[r];
       if (k > kMedTargets) {
         const uint32_t n = (nblk + kLongChunk - 1) / kLongChunk;
         const unsigned long long base = atomicAdd(&op->n_items, (unsigned long long)n);
-        for (uint32_t c = 0; c < n; ++c) long_items[base + c] = make_uint2((uint32_t)r, c);
+        for (uint32_t c = 0; c < n; ++c) long_items[base + c] = make_uint2(r, c);
       } else if (k > kTinyTargets) {
         const uint32_t n = (nblk + kMedChunk - 1) / kMedChunk;
         const unsigned long long base = atomicAdd(&op->n_med, (unsigned long long)n);
-        for (uint32_t c = 0; c < n; ++c) med_items[base + c] = make_uint2((uint32_t)r, c);
+        for (uint32_t c = 0; c < n; ++c) med_items[base + c] = make_uint2(r, c);
       }
     }
   }
 };
+// degree of a touched vertex as delete/query see it: dead or unknown sources have
+// none (graph.hpp:205, :229).  Predicated, independent loads (see alloc_kernel).
+__device__ __forceinline__ uint32_t live_degree(const GraphView& g, uint32_t v, bool wanted, int check_alive) {
+  const bool in_range = wanted && v < g.size;
+  const uint32_t d = in_range ? g.deg[v] : 0u;
+  const uint32_t aw = (in_range && check_alive) ? g.alive[v >> 5] : 0xFFFFFFFFu;
+  return ((aw >> (v & 31)) & 1u) ? d : 0u;
+}
+struct EnumAux {
+  uint32_t d;
+};
+
+// over already-grouped runs (radix path, CSR batches, export: runs = vertices)
+struct EnumIn {
+  using Aux = EnumAux;
+  GraphView g;
+  BatchView b;
+  int check_alive;
+  __device__ Sum2 operator()(unsigned long long r64, Aux& x) const {
+    const uint32_t r = (uint32_t)r64;
+    const bool wanted = b.run_start == nullptr || run_len(b, r) != 0;  // empty runs: CSR batches
+    x.d = live_degree(g, batch_src(b, r), wanted, check_alive);
+    return Sum2{0ull, blocks_for(g, x.d)};
+  }
+};
+struct EnumOut {
+  BatchView b;
+  EnumLists lists;
+  __device__ void operator()(unsigned long long r, unsigned long long, unsigned long long excl_b,
+                             Sum2 v, const EnumAux& x) const {
+    const uint32_t k = b.run_start != nullptr ? run_len(b, (uint32_t)r) : 0u;
+    lists.write((uint32_t)r, x.d, (uint32_t)v.b, k, excl_b);
+  }
+};
+// fused with the counting group-by: one pass over the vertices
+struct GroupEnumIn {
+  using Aux = EnumAux;
+  GraphView g;
+  const uint32_t* cnt;
+  int check_alive;
+  __device__ Sum2 operator()(unsigned long long v, Aux& x) const {
+    const uint32_t c = cnt[v];
+    x.d = live_degree(g, (uint32_t)v, c != 0, check_alive);
+    return Sum2{c ? ((1ull << 32) | c) : 0ull, blocks_for(g, x.d)};
+  }
+};
+struct GroupEnumOut {
+  uint32_t* cnt;
+  uint32_t* run_src;
+  uint32_t* run_start;
+  uint32_t* run_end;
+  EnumLists lists;
+  __device__ void operator()(unsigned long long v, unsigned long long excl_a, unsigned long long excl_b,
+                             Sum2 val, const EnumAux& x) const {
+    const uint32_t c = (uint32_t)val.a;
+    if (c == 0) return;
+    const uint32_t r = (uint32_t)(excl_a >> 32);
+    const uint32_t es = (uint32_t)excl_a;
+    run_src[r] = (uint32_t)v;
+    run_start[r] = es;
+    run_end[r] = es + c;
+    cnt[v] = es;
+    lists.write(r, x.d, (uint32_t)val.b, c, excl_b);
+  }
+};
 struct EnumFin {
-  uint32_t* wl_off;
   OpState* op;
   unsigned long long wl_cap;
-  __device__ void operator()(unsigned long long total) const {
-    wl_off[op->n_runs] = (uint32_t)total;
-    op->wl_blocks = total;
-    if (total > wl_cap) {  // cannot happen: wl_cap >= blocks in use (host mirror)
+  int set_runs;
+  __device__ void operator()(unsigned long long total_a, unsigned long long total_b) const {
+    if (set_runs) op->n_runs = total_a >> 32;
+    op->wl_blocks = total_b;
+    if (total_b > wl_cap) {  // cannot happen: wl_cap >= blocks in use (host mirror)
       op->err = 3;
       op->err_detail = kErrScratch;
     }
@@ -658,13 +758,13 @@ struct EnumFin {
 // scan and go to enumerate_big_kernel.
 __global__ void __launch_bounds__(256)
 enumerate_walk_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
-                      uint32_t* __restrict__ wl_handle, uint32_t* __restrict__ wl_run,
-                      const OpState* op) {
+                      const uint32_t* __restrict__ run_deg, uint32_t* __restrict__ wl_handle,
+                      uint32_t* __restrict__ wl_run, const OpState* op) {
   if (op->err) return;
   const uint32_t T = (uint32_t)op->n_runs;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < T; r += gridDim.x * blockDim.x) {
     const uint32_t base = wl_off[r];
-    const uint32_t nblk = wl_off[r + 1] - base;
+    const uint32_t nblk = blocks_for(g, run_deg[r]);
     if (nblk == 0 || nblk > kLaneWalk) continue;
     uint32_t h = g.head[batch_src(b, r)];
     const uint32_t tag = run_tag(b, r);
@@ -683,8 +783,8 @@ enumerate_walk_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_
 // degrade to one block per latency.
 __global__ void __launch_bounds__(256)
 enumerate_big_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
-                     const uint32_t* __restrict__ big_list, uint32_t* __restrict__ wl_handle,
-                     uint32_t* __restrict__ wl_run, const OpState* op) {
+                     const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ big_list,
+                     uint32_t* __restrict__ wl_handle, uint32_t* __restrict__ wl_run, const OpState* op) {
   if (op->err) return;
   const uint32_t nbig = (uint32_t)op->n_big;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -692,7 +792,7 @@ enumerate_big_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_o
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nbig; i += nwarps) {
     const uint32_t r = big_list[i];
     const uint32_t base = wl_off[r];
-    const uint32_t nblk = wl_off[r + 1] - base;
+    const uint32_t nblk = blocks_for(g, run_deg[r]);
     uint32_t h = g.head[batch_src(b, r)];
     const uint32_t tag = run_tag(b, r);
     uint32_t k = 0;
@@ -754,12 +854,15 @@ enumerate_big_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_o
 // Delete records, per block, the bit mask of matched slots (wl_mask) so the
 // compaction never re-reads the chains.
 // ---------------------------------------------------------------------------
-// match_tiny_kernel: ONE THREAD PER BLOCK, sources with at most kTinyTargets
-// targets.  With the native block (B = 32: one 128-byte line) a thread pulls
-// its block into registers with eight independent 16-byte loads — no
-// cross-lane traffic, eight loads in flight per thread — and compares the 32
-// slots against the targets held in registers.  The match mask is built in a
-// register and stored coalesced.  Other block sizes take the scalar loop.
+// match_tiny_kernel: sources with at most kTinyTargets targets.
+//   B = 32 (one 128-byte line per block): a WARP per 32 consecutive worklist
+//   blocks.  Metadata phase: one lane per block (tier tag, handle, source's
+//   targets -> the warp's shared-memory strip).  Load phase: the tiny blocks are
+//   loaded one slot per lane, all (up to 32) coalesced loads issued before the
+//   first compare.  Compare phase: per block, the <= 8 targets are broadcast
+//   reads from the strip; __ballot_sync builds the match mask, lane u keeps
+//   block u's mask so masks and counters leave coalesced.
+//   Other block sizes: one thread per block, scalar loop.
 template <bool kIsDelete>
 __global__ void __launch_bounds__(256)
 match_tiny_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
@@ -768,58 +871,98 @@ match_tiny_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                   uint32_t* __restrict__ wl_mask, uint8_t* __restrict__ hit, OpState* op) {
   if (op->err) return;
   __shared__ unsigned long long s_warp[8];
+  __shared__ __align__(16) uint32_t s_slots[8][32][32];  // [warp][block][slot]
   const uint32_t W = (uint32_t)op->wl_blocks;
   unsigned long long slots = 0;
-  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
-    const uint32_t tag = wl_run[w];
-    const uint32_t h = wl_handle[w];
-    if (tag & kTierBit) continue;  // the table tiers' work
-    const uint32_t r = tag;
-    const uint32_t rs = b.run_start[r];
-    const uint32_t k = b.run_start[r + 1] - rs;
-    const uint32_t d = run_deg[r];
-    const uint32_t kb = w - wl_off[r];
-    const uint32_t cnt = min(g.B, d - kb * g.B);
-    slots += cnt;
-    uint32_t* blk = g.slab + (unsigned long long)h * g.B;
-    uint32_t tg[kTinyTargets];
+  if (g.B == 32) {
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = lane_id();
+    uint32_t(*stg)[32] = s_slots[threadIdx.x >> 5];
+    for (uint32_t w0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; w0 < W; w0 += nwarps * 32u) {
+      // ---- metadata: lane = block
+      const uint32_t w = w0 + lane;
+      uint32_t tag = kTierBit, h = 0;
+      if (w < W) {
+        tag = wl_run[w];
+        h = wl_handle[w];
+      }
+      const bool tiny = !(tag & kTierBit);
+      const unsigned tmask32 = __ballot_sync(kFull, tiny);
+      if (tmask32 == 0) continue;
+      // ---- stage: every tiny block of the group in flight at once
+      stage_blocks32(g, stg, h, tmask32);
+      uint32_t r = 0, rs = 0, k = 0, cnt = 0;
+      uint32_t tg[kTinyTargets];
+      if (tiny) {
+        r = tag;
+        rs = b.run_start[r];
+        k = b.run_end[r] - rs;
+        cnt = min(32u, run_deg[r] - (w - wl_off[r]) * 32u);
+      }
 #pragma unroll
-    for (int j = 0; j < (int)kTinyTargets; ++j) tg[j] = ((uint32_t)j < k) ? batch_value(b, rs + j) : kTomb;
-    uint32_t matched = 0;
-    if (g.B == 32) {
-      uint4 v[8];
-      const uint4* vb = reinterpret_cast<const uint4*>(blk);
+      for (int j = 0; j < (int)kTinyTargets; ++j) tg[j] = ((uint32_t)j < k) ? batch_value(b, rs + j) : kTomb;
+      slots += cnt;
+      cp_async_wait_all();
+      __syncwarp();
+      // ---- compare: lane = block.  Pass 1 tests every slot against a 64-bit filter of the lane's
+      // targets (6 instructions per slot); pass 2 compares only the few candidates exactly.
+      if (tiny) {
+        unsigned long long filt = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = vb[i];
-      const uint32_t valid = cnt == 32 ? 0xFFFFFFFFu : ((1u << cnt) - 1u);  // slots past deg hold stale values
-      uint32_t mask = 0;
+        for (int j = 0; j < (int)kTinyTargets; ++j)
+          if ((uint32_t)j < k) filt |= 1ull << filter_hash(tg[j], 6);
+        uint32_t cand = 0;
 #pragma unroll
-      for (int j = 0; j < (int)kTinyTargets; ++j) {
-        if ((uint32_t)j < k) {
-          const uint32_t t = tg[j];
-          uint32_t mj = 0;
+        for (int c = 0; c < 8; ++c) {
+          const uint4 v = block_chunk(stg, lane, c);
+          cand |= (uint32_t)((filt >> filter_hash(v.x, 6)) & 1ull) << (4 * c);
+          cand |= (uint32_t)((filt >> filter_hash(v.y, 6)) & 1ull) << (4 * c + 1);
+          cand |= (uint32_t)((filt >> filter_hash(v.z, 6)) & 1ull) << (4 * c + 2);
+          cand |= (uint32_t)((filt >> filter_hash(v.w, 6)) & 1ull) << (4 * c + 3);
+        }
+        cand &= cnt == 32 ? 0xFFFFFFFFu : ((1u << cnt) - 1u);  // slots past deg hold stale values
+        uint32_t mask = 0;
+        while (cand) {
+          const uint32_t bit = __ffs(cand) - 1;
+          cand &= cand - 1;
+          const uint32_t e = block_slot(stg, lane, bit);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            mj |= (v[i].x == t ? 1u : 0u) << (4 * i);
-            mj |= (v[i].y == t ? 1u : 0u) << (4 * i + 1);
-            mj |= (v[i].z == t ? 1u : 0u) << (4 * i + 2);
-            mj |= (v[i].w == t ? 1u : 0u) << (4 * i + 3);
+          for (int j = 0; j < (int)kTinyTargets; ++j) {
+            if ((uint32_t)j < k && e == tg[j]) {
+              mask |= 1u << bit;
+              if (!kIsDelete) hit[rs + j] = 1;
+            }
           }
-          mj &= valid;
-          if (!kIsDelete && mj) hit[rs + j] = 1;
-          mask |= mj;
+        }
+        if (kIsDelete) {
+          wl_mask[w] = mask;
+          if (mask) atomicAdd(&run_matched[r], (uint32_t)__popc(mask));
+          while (mask) {
+            const uint32_t bit = __ffs(mask) - 1;
+            mask &= mask - 1;
+            g.slab[(unsigned long long)h * 32u + bit] = kTomb;
+          }
         }
       }
-      if (kIsDelete) {
-        wl_mask[w] = mask;
-        matched = __popc(mask);
-        while (mask) {
-          const uint32_t bit = __ffs(mask) - 1;
-          mask &= mask - 1;
-          blk[bit] = kTomb;
-        }
-      }
-    } else {
+      __syncwarp();
+    }
+  } else {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
+      const uint32_t tag = wl_run[w];
+      const uint32_t h = wl_handle[w];
+      if (tag & kTierBit) continue;  // the table tiers' work
+      const uint32_t r = tag;
+      const uint32_t rs = b.run_start[r];
+      const uint32_t k = b.run_end[r] - rs;
+      const uint32_t d = run_deg[r];
+      const uint32_t kb = w - wl_off[r];
+      const uint32_t cnt = min(g.B, d - kb * g.B);
+      slots += cnt;
+      uint32_t* blk = g.slab + (unsigned long long)h * g.B;
+      uint32_t tg[kTinyTargets];
+#pragma unroll
+      for (int j = 0; j < (int)kTinyTargets; ++j) tg[j] = ((uint32_t)j < k) ? batch_value(b, rs + j) : kTomb;
+      uint32_t matched = 0;
       for (uint32_t s0 = 0; s0 < cnt; s0 += 32) {
         uint32_t mask = 0;
         const uint32_t ns = min(32u, cnt - s0);
@@ -845,8 +988,8 @@ match_tiny_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
           }
         }
       }
+      if (kIsDelete && matched) atomicAdd(&run_matched[r], matched);
     }
-    if (kIsDelete && matched) atomicAdd(&run_matched[r], matched);
   }
   const unsigned long long t = block_reduce_sum(slots, s_warp);
   if (threadIdx.x == 0 && t) atomicAdd(&op->slots, t);
@@ -854,7 +997,10 @@ match_tiny_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
 
 // Open-addressing table of u32 keys in shared memory; kTomb marks an empty slot
 // (never a valid destination id).
-__device__ __forceinline__ void table_insert(uint32_t* tab, uint32_t tmask, int hshift, uint32_t x) {
+__device__ __forceinline__ void table_insert(uint32_t* tab, uint32_t tmask, int hshift, uint32_t* bm,
+                                             int bm_bits, uint32_t x) {
+  const uint32_t hb = filter_hash(x, bm_bits);
+  atomicOr(&bm[hb >> 5], 1u << (hb & 31));
   uint32_t pos = (x * 0x9E3779B1u) >> hshift;
   while (true) {
     const uint32_t old = atomicCAS(&tab[pos], kTomb, x);
@@ -873,94 +1019,118 @@ __device__ __forceinline__ int table_find(const uint32_t* tab, uint32_t tmask, i
   }
 }
 
-// Scans up to kFly blocks of one chain against a shared-memory table: the slot
-// loads of all blocks are issued together, one slot per lane, __ballot_sync
-// collects the masks.  `hd_lane` holds the handle of block u in lane u.
-// first: this is the first (or only) table slice for these blocks, so the mask
-// words are stored rather than OR-ed.  Returns the number of matches (valid in
-// lane 0).  B = 32 (one line per block) takes the straight-line path.
-constexpr int kFly = 8;
+// Scans up to 32 blocks of one chain against a shared-memory table.  `hd_lane`
+// holds the handle of block u in lane u.  first: this is the first (or only)
+// table slice for these blocks, so the mask words are stored rather than OR-ed.
+// Returns the number of matches (valid in every lane).
+//   B = 32 (one line per block): ALL blocks of the group are staged in the warp's
+//   shared-memory strip `stg` with asynchronous copies (up to 32 x 128 bytes in
+//   flight per warp), then a rolled loop probes one slot per lane and collects a
+//   __ballot_sync mask per block; lane u keeps block u's mask so the masks leave
+//   coalesced.
+//   Other block sizes: scalar-per-block loop, 8 blocks at a time.
 template <bool kIsDelete>
 __device__ __forceinline__ uint32_t table_scan(const GraphView& g, const uint32_t* tab, uint8_t* flag,
-                                               uint32_t tmask, int hshift, uint32_t hd_lane,
-                                               uint32_t ng, uint32_t d, uint32_t kb_first,
-                                               uint32_t w_first, uint32_t* __restrict__ wl_mask,
-                                               bool first, unsigned long long& slots) {
+                                               uint32_t tmask, int hshift, const uint32_t* bm, int bm_bits,
+                                               uint32_t (*stg)[32],
+                                               uint32_t hd_lane, uint32_t ng, uint32_t d,
+                                               uint32_t kb_first, uint32_t w_first,
+                                               uint32_t* __restrict__ wl_mask, bool first,
+                                               unsigned long long& slots) {
   const int lane = lane_id();
-  uint32_t e[kFly];
   uint32_t matched = 0;
   if (g.B == 32) {
-    uint32_t hd[kFly];
     // slots of the group: every block but possibly the chain's last one is full
     const uint32_t rem = d - kb_first * 32u;            // slots from the group's first block to the chain end
     const uint32_t gslots = min(rem, ng * 32u);
+    stage_blocks32(g, stg, hd_lane, ng >= 32 ? 0xFFFFFFFFu : ((1u << ng) - 1u));
+    cp_async_wait_all();
+    __syncwarp();
+    // lane = block.  Pass 1 tests the lane's 32 slots against the bitmap filter of the targets;
+    // pass 2 probes the table only for the candidates.
+    uint32_t mask = 0;
+    if ((uint32_t)lane < ng) {
+      const uint32_t cnt = min(32u, gslots - 32u * lane);
+      uint32_t cand = 0;
 #pragma unroll
-    for (int u = 0; u < kFly; ++u) {
-      hd[u] = __shfl_sync(kFull, hd_lane, u);
-      e[u] = ((uint32_t)(32 * u + lane) < gslots) ? g.slab[(unsigned long long)hd[u] * 32u + lane] : kTomb;
-    }
+      for (int c = 0; c < 8; ++c) {
+        const uint4 v = block_chunk(stg, lane, c);
+        const uint32_t evs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int u = 0; u < kFly; ++u) {
-      if ((uint32_t)u >= ng) break;  // warp-uniform
-      const uint32_t ev = e[u];
-      uint32_t pos = (ev * 0x9E3779B1u) >> hshift;
-      uint32_t t = tab[pos];
-      bool found = t == ev;
-      bool pend = !found && t != kTomb;
-      if (ev == kTomb) { found = false; pend = false; }  // padding lanes / tombstones of an earlier slice
-      while (pend) {
-        pos = (pos + 1) & tmask;
-        t = tab[pos];
-        found = t == ev;
-        pend = !found && t != kTomb;
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t hb = filter_hash(evs[i], bm_bits);
+          cand |= ((bm[hb >> 5] >> (hb & 31)) & 1u) << (4 * c + i);
+        }
+      }
+      cand &= cnt == 32 ? 0xFFFFFFFFu : ((1u << cnt) - 1u);  // stale padding
+      while (cand) {
+        const uint32_t bit = __ffs(cand) - 1;
+        cand &= cand - 1;
+        const uint32_t ev = block_slot(stg, lane, bit);
+        if (ev == kTomb) continue;  // tombstone of an earlier slice
+        uint32_t pos = (ev * 0x9E3779B1u) >> hshift;
+        uint32_t t = tab[pos];
+        while (t != ev && t != kTomb) {
+          pos = (pos + 1) & tmask;
+          t = tab[pos];
+        }
+        if (t == ev) {
+          mask |= 1u << bit;
+          if (!kIsDelete) flag[pos] = 1;
+        }
       }
       if (kIsDelete) {
-        const unsigned m = __ballot_sync(kFull, found);
-        if (found) g.slab[(unsigned long long)hd[u] * 32u + lane] = kTomb;
-        if (lane == 0) {
-          uint32_t* mword = &wl_mask[w_first + u];
-          *mword = first ? m : (*mword | m);   // the same warp owns this block in every slice
+        if (first) wl_mask[w_first + lane] = mask;
+        else if (mask) wl_mask[w_first + lane] |= mask;  // the same warp owns these blocks in every slice
+        uint32_t m2 = mask;
+        while (m2) {
+          const uint32_t bit = __ffs(m2) - 1;
+          m2 &= m2 - 1;
+          g.slab[(unsigned long long)hd_lane * 32u + bit] = kTomb;
         }
-        matched += __popc(m);
-      } else if (found) {
-        flag[pos] = 1;
       }
     }
+    matched = __popc(mask);
+#pragma unroll
+    for (int dlt = 16; dlt > 0; dlt >>= 1) matched += __shfl_xor_sync(kFull, matched, dlt);
     if (first && lane == 0) slots += gslots;
+    __syncwarp();  // the staging strip is reused by the caller's next group
     return matched;
   }
-  uint32_t cn[kFly];
-  uint32_t* blk[kFly];
+  for (uint32_t u0 = 0; u0 < ng; u0 += 8) {
+    uint32_t e[8], cn[8];
+    uint32_t* blk[8];
 #pragma unroll
-  for (int u = 0; u < kFly; ++u) {
-    const uint32_t hd = __shfl_sync(kFull, hd_lane, u);
-    blk[u] = g.slab + (unsigned long long)hd * g.B;
-    cn[u] = ((uint32_t)u < ng) ? min(g.B, d - (kb_first + u) * g.B) : 0u;
-    e[u] = ((uint32_t)lane < cn[u]) ? blk[u][lane] : kTomb;
-  }
-#pragma unroll
-  for (int u = 0; u < kFly; ++u) {
-    if (cn[u] == 0) continue;  // warp-uniform
-    for (uint32_t s0 = 0; s0 < cn[u]; s0 += 32) {
-      const uint32_t s = s0 + lane;
-      const uint32_t ev = (s0 == 0) ? e[u] : ((s < cn[u]) ? blk[u][s] : kTomb);
-      bool found = false;
-      if (ev != kTomb) {  // padding lanes and entries tombstoned by an earlier slice
-        const int pos = table_find(tab, tmask, hshift, ev);
-        found = pos >= 0;
-        if (!kIsDelete && found) flag[pos] = 1;
-      }
-      if (kIsDelete) {
-        const unsigned m = __ballot_sync(kFull, found);
-        if (found) blk[u][s] = kTomb;
-        if (lane == 0) {
-          uint32_t* mword = &wl_mask[(unsigned long long)(w_first + u) * g.mw + (s0 >> 5)];
-          *mword = first ? m : (*mword | m);
-        }
-        matched += __popc(m);
-      }
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t hd = __shfl_sync(kFull, hd_lane, (u0 + u) & 31);
+      blk[u] = g.slab + (unsigned long long)hd * g.B;
+      cn[u] = (u0 + u < ng) ? min(g.B, d - (kb_first + u0 + u) * g.B) : 0u;
+      e[u] = ((uint32_t)lane < cn[u]) ? blk[u][lane] : kTomb;
     }
-    if (first && lane == 0) slots += cn[u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (cn[u] == 0) continue;  // warp-uniform
+      for (uint32_t s0 = 0; s0 < cn[u]; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const uint32_t ev = (s0 == 0) ? e[u] : ((s < cn[u]) ? blk[u][s] : kTomb);
+        bool found = false;
+        if (ev != kTomb) {  // padding lanes and entries tombstoned by an earlier slice
+          const int pos = table_find(tab, tmask, hshift, ev);
+          found = pos >= 0;
+          if (!kIsDelete && found) flag[pos] = 1;
+        }
+        if (kIsDelete) {
+          const unsigned m = __ballot_sync(kFull, found);
+          if (found) blk[u][s] = kTomb;
+          if (lane == 0) {
+            uint32_t* mword = &wl_mask[(unsigned long long)(w_first + u0 + u) * g.mw + (s0 >> 5)];
+            *mword = first ? m : (*mword | m);
+          }
+          matched += __popc(m);
+        }
+      }
+      if (first && lane == 0) slots += cn[u];
+    }
   }
   return matched;
 }
@@ -969,6 +1139,10 @@ __device__ __forceinline__ uint32_t table_scan(const GraphView& g, const uint32_
 // kTinyTargets < k <= kMedTargets targets; the warp keeps the source's targets
 // in its own 256-entry shared-memory table.
 constexpr uint32_t kMedTable = 512;   // >= 4 x kMedTargets: short probe sequences
+// dynamic shared memory: per warp a table, a staging strip and (query) flags
+constexpr int kMedFilterBits = 12;     // 4096-bit membership filter per warp: <= 3% false positives
+constexpr size_t kMedSmemDelete = 8 * (kMedTable * 4 + 32 * 32 * 4 + (1u << kMedFilterBits) / 8);
+constexpr size_t kMedSmemQuery = kMedSmemDelete + 8 * kMedTable;
 template <bool kIsDelete>
 __global__ void __launch_bounds__(256)
 match_med_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
@@ -976,15 +1150,16 @@ match_med_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                  const uint32_t* __restrict__ run_deg, uint32_t* __restrict__ run_matched,
                  uint32_t* __restrict__ wl_mask, uint8_t* __restrict__ hit, OpState* op) {
   if (op->err) return;
-  __shared__ uint32_t s_table[8][kMedTable];
-  __shared__ uint8_t s_flag[kIsDelete ? 1 : 8][kIsDelete ? 4 : kMedTable];
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ unsigned long long s_warp[8];
   const uint32_t n_items = (uint32_t)op->n_med;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
-  uint32_t* tab = s_table[warp];
-  uint8_t* flag = s_flag[kIsDelete ? 0 : warp];
+  uint32_t(*stg)[32] = reinterpret_cast<uint32_t(*)[32]>(dyn_smem + (size_t)warp * 32 * 32 * 4);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(dyn_smem + 8 * 32 * 32 * 4) + warp * kMedTable;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(dyn_smem + 8 * (32 * 32 * 4 + kMedTable * 4)) + warp * ((1u << kMedFilterBits) / 32);
+  uint8_t* flag = dyn_smem + kMedSmemDelete + (kIsDelete ? 0 : warp * kMedTable);
   constexpr int hshift = 32 - 9;
   constexpr uint32_t tmask = kMedTable - 1;
   static_assert(kMedTable == 512, "hshift matches the table size");
@@ -998,7 +1173,7 @@ match_med_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
     const uint2 it = items[q];
     const uint32_t r = it.x, c = it.y;
     const uint32_t rs = b.run_start[r];
-    const uint32_t k = b.run_start[r + 1] - rs;
+    const uint32_t k = b.run_end[r] - rs;
     const uint32_t d = run_deg[r];
     const uint32_t nblk = blocks_for(g, d);
     const uint32_t wbase = wl_off[r];
@@ -1009,15 +1184,13 @@ match_med_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
       tab[i] = kTomb;
       if (!kIsDelete) flag[i] = 0;
     }
+    for (uint32_t i = lane; i < (1u << kMedFilterBits) / 32; i += 32) bm[i] = 0;
     __syncwarp();
-    for (uint32_t i = lane; i < k; i += 32) table_insert(tab, tmask, hshift, batch_value(b, rs + i));
+    for (uint32_t i = lane; i < k; i += 32)
+      table_insert(tab, tmask, hshift, bm, kMedFilterBits, batch_value(b, rs + i));
     __syncwarp();
-    uint32_t matched = 0;
-    for (uint32_t i0 = 0; i0 < nb; i0 += kFly) {
-      const uint32_t hd_lane = __shfl_sync(kFull, hd_all, (i0 + lane) & 31);  // lane u <- handle of block i0+u
-      matched += table_scan<kIsDelete>(g, tab, flag, tmask, hshift, hd_lane, min((uint32_t)kFly, nb - i0), d,
-                                       kb0 + i0, wbase + kb0 + i0, wl_mask, true, slots);
-    }
+    const uint32_t matched = table_scan<kIsDelete>(g, tab, flag, tmask, hshift, bm, kMedFilterBits, stg, hd_all, nb,
+                                                   d, kb0, wbase + kb0, wl_mask, true, slots);
     if (kIsDelete) {
       if (lane == 0 && matched) atomicAdd(&run_matched[r], matched);
     } else {
@@ -1041,6 +1214,9 @@ match_med_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
 constexpr int kLongThreads = 256;
 constexpr uint32_t kTableSize = 8192;      // shared-memory table capacity (u32 keys)
 constexpr uint32_t kSliceTargets = 4096;   // targets per table build: load factor <= 0.5
+constexpr int kLongFilterBits = 16;    // 64K-bit membership filter per CTA: <= 6% false positives per slice
+constexpr size_t kLongSmemDelete = (kLongThreads / 32) * 32 * 32 * 4 + kTableSize * 4 + (1u << kLongFilterBits) / 8;
+constexpr size_t kLongSmemQuery = kLongSmemDelete + kTableSize;
 
 template <bool kIsDelete>
 __global__ void __launch_bounds__(kLongThreads)
@@ -1050,9 +1226,12 @@ match_long_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                   uint32_t* __restrict__ wl_mask, uint8_t* __restrict__ hit, OpState* op) {
   if (op->err) return;
   constexpr int kWarps = kLongThreads / 32;
-  __shared__ uint32_t s_table[kTableSize];
-  __shared__ uint8_t s_flag[kIsDelete ? 4 : kTableSize];
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ unsigned long long s_warp[kWarps];
+  uint32_t(*stg)[32] = reinterpret_cast<uint32_t(*)[32]>(dyn_smem + (size_t)(threadIdx.x >> 5) * 32 * 32 * 4);
+  uint32_t* s_table = reinterpret_cast<uint32_t*>(dyn_smem + kWarps * 32 * 32 * 4);
+  uint32_t* s_bm = s_table + kTableSize;
+  uint8_t* s_flag = dyn_smem + kLongSmemDelete;
   const uint32_t n_items = (uint32_t)op->n_items;
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
@@ -1064,13 +1243,13 @@ match_long_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
     const uint2 it = items[q];
     const uint32_t r = it.x, c = it.y;
     const uint32_t rs = b.run_start[r];
-    const uint32_t k = b.run_start[r + 1] - rs;
+    const uint32_t k = b.run_end[r] - rs;
     const uint32_t d = run_deg[r];
     const uint32_t nblk = blocks_for(g, d);
     const uint32_t wbase = wl_off[r];
     const uint32_t kb0 = c * kLongChunk;
     const uint32_t kb1 = min(nblk, kb0 + kLongChunk);
-    const uint32_t ngroups = (kb1 - kb0 + kFly - 1) / kFly;
+    const uint32_t ngroups = (kb1 - kb0 + 31) / 32;
     unsigned long long matched = 0;
     for (uint32_t t0 = 0; t0 < k; t0 += kSliceTargets) {
       const uint32_t nt = min(kSliceTargets, k - t0);
@@ -1082,16 +1261,17 @@ match_long_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
         s_table[i] = kTomb;
         if (!kIsDelete) s_flag[i] = 0;
       }
+      for (uint32_t i = threadIdx.x; i < (1u << kLongFilterBits) / 32; i += kLongThreads) s_bm[i] = 0;
       __syncthreads();
       for (uint32_t i = threadIdx.x; i < nt; i += kLongThreads)
-        table_insert(s_table, tmask, hshift, batch_value(b, rs + t0 + i));
+        table_insert(s_table, tmask, hshift, s_bm, kLongFilterBits, batch_value(b, rs + t0 + i));
       __syncthreads();
       for (uint32_t gi = warp; gi < ngroups; gi += kWarps) {
-        const uint32_t kbg = kb0 + kFly * gi;
-        const uint32_t ng = min((uint32_t)kFly, kb1 - kbg);
+        const uint32_t kbg = kb0 + 32 * gi;
+        const uint32_t ng = min(32u, kb1 - kbg);
         const uint32_t hd_lane = ((uint32_t)lane < ng) ? wl_handle[wbase + kbg + lane] : 0u;
-        const uint32_t mm = table_scan<kIsDelete>(g, s_table, s_flag, tmask, hshift, hd_lane, ng, d, kbg,
-                                                  wbase + kbg, wl_mask, t0 == 0, slots);
+        const uint32_t mm = table_scan<kIsDelete>(g, s_table, s_flag, tmask, hshift, s_bm, kLongFilterBits, stg,
+                                                  hd_lane, ng, d, kbg, wbase + kbg, wl_mask, t0 == 0, slots);
         if (lane == 0) matched += mm;
       }
       __syncthreads();
@@ -1121,28 +1301,28 @@ match_long_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
 // ---------------------------------------------------------------------------
 // delete: compaction plan — per source, moves <= min(matched, new degree)
 // ---------------------------------------------------------------------------
+struct NoAux {};
 struct MovesIn {
+  using Aux = NoAux;
   const uint32_t* run_deg;
   const uint32_t* run_matched;
-  __device__ unsigned long long operator()(unsigned long long r) const {
+  __device__ Sum2 operator()(unsigned long long r, Aux&) const {
     const uint32_t m = run_matched[r];
     const uint32_t nd = run_deg[r] - m;
-    return min(m, nd);
+    return Sum2{0ull, min(m, nd)};
   }
 };
 struct MovesOut {
   uint32_t* mv_off;
-  __device__ void operator()(unsigned long long r, unsigned long long excl,
-                             unsigned long long) const {
-    mv_off[r] = (uint32_t)excl;
+  __device__ void operator()(unsigned long long r, unsigned long long, unsigned long long excl_b,
+                             Sum2, const NoAux&) const {
+    mv_off[r] = (uint32_t)excl_b;
   }
 };
 struct MovesFin {
-  uint32_t* mv_off;
   OpState* op;
   unsigned long long mv_cap;
-  __device__ void operator()(unsigned long long total) const {
-    mv_off[op->n_runs] = (uint32_t)total;
+  __device__ void operator()(unsigned long long, unsigned long long total) const {
     op->aux0 = total;                      // scratch entries needed
     op->aux1 = total > mv_cap ? 1ull : 0ull;  // host grows the scratch and re-runs the tail
   }

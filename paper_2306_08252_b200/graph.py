@@ -27,6 +27,7 @@ class GraphConfig:
     reclaim_on_delete: bool = True
     stream: int = 0              # cudaStream_t handle; 0 => library-owned stream
     group: str = "auto"          # how COO batches are grouped by source: "auto" | "radix" | "count"
+    workspace_bytes: int = 0     # per-op scratch reserved at construction (0 => grown on first use)
 
 
 def _is_device(x) -> bool:
@@ -68,6 +69,7 @@ class DynamicGraph:
         c.pool_bytes = cfg.pool_bytes
         c.pool_blocks = cfg.pool_blocks
         c.stream = cfg.stream or None
+        c.workspace_bytes = cfg.workspace_bytes
         self._h = C.c_void_p()
         rc = self._lib.dg_create(C.byref(c), initial_vertex_count, block_size, C.byref(self._h))
         if rc != 0:

@@ -20,9 +20,14 @@ for b in blocks[:1] if len(sys.argv) <= 3 else blocks:
     hdr = b["hdr"]
     si = hdr.index("# Samples")
     stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
-    src = [r for r in b["lines"] if r[0] != ""]   # cuda source rows
-    tot = sum(int(r[si] or 0) for r in src) or 1
+    def num(x):
+        try:
+            return int(x)
+        except ValueError:
+            return 0
+    src = [r for r in b["lines"] if r[0] != "" and len(r) > si]   # cuda source rows
+    tot = sum(num(r[si]) for r in src) or 1
     print("==", b["name"][:90], "samples", tot)
-    for r in sorted(src, key=lambda r: -int(r[si] or 0))[:top]:
-        st = sorted(((int(r[i] or 0), hdr[i]) for i in stall_cols), reverse=True)[:3]
-        print(f"{int(r[si])/tot:6.1%} L{r[0]:>4} {r[1].strip()[:80]:80s} {' '.join(f'{n}:{c}' for c, n in st if c)}")
+    for r in sorted(src, key=lambda r: -num(r[si]))[:top]:
+        st = sorted(((num(r[i]), hdr[i]) for i in stall_cols), reverse=True)[:3]
+        print(f"{num(r[si])/tot:6.1%} L{r[0]:>4} {r[1].strip()[:80]:80s} {' '.join(f'{n}:{c}' for c, n in st if c)}")
