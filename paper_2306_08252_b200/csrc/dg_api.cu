@@ -587,7 +587,7 @@ inline bool use_counting(const dg_graph* h, uint64_t n) {
   if (h->B == 0) return false;  // deferred pool: the plan needs the block size, which needs the run count first
   if (h->group_mode == 1) return false;
   if (h->group_mode == 2) return true;
-  return h->size + 1 <= std::max<uint64_t>(32 * n, 1ull << 22);
+  return h->size <= std::max<uint64_t>(64 * n, 1ull << 22);  // the counter array is cleared per batch
 }
 
 struct Grouped {
@@ -595,6 +595,8 @@ struct Grouped {
   uint64_t runs_bound = 0;
   uint32_t* index = nullptr;  // original position of every grouped entry (queries)
   // counting path, between count and scatter
+  GroupIndex gi{};
+  uint64_t cnt_words = 0;
   uint32_t* cnt = nullptr;
   uint32_t* rank = nullptr;
   uint32_t* gdst = nullptr;
@@ -604,7 +606,7 @@ struct Grouped {
 inline size_t group_ws_bytes(const dg_graph* h, uint64_t n, bool with_index, uint64_t max_src) {
   size_t t = 0;
   if (use_counting(h, n)) {
-    t += aligned((h->size + 2) * 4) + 2 * aligned(n * 4) + (with_index ? aligned(n * 4) : 0);
+    t += aligned((std::bit_ceil(std::max<uint64_t>(h->size, 1)) + 2) * 4) + 2 * aligned(n * 4) + (with_index ? aligned(n * 4) : 0);
     t += 3 * aligned((std::min<uint64_t>(n, h->size + 1) + 1) * 4);
   } else {
     t += 2 * aligned(n * 8) + (with_index ? 2 * aligned(n * 4) : 0);
@@ -620,7 +622,10 @@ Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, u
   GraphView g = view(h);
   Grouped out;
   const uint64_t nv = h->size + 1;  // + 1: the slot unknown query sources are clamped to
-  out.cnt = ws_alloc<uint32_t>(h, nv + 1);
+  const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
+  out.gi = GroupIndex{(uint32_t)(cap - 1), (uint32_t)h->size};
+  out.cnt_words = cap + 1;
+  out.cnt = ws_alloc<uint32_t>(h, cap + 2);
   out.rank = ws_alloc<uint32_t>(h, n);
   out.gdst = ws_alloc<uint32_t>(h, n);
   if (with_index) out.index = ws_alloc<uint32_t>(h, n);
@@ -628,9 +633,9 @@ Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, u
   out.run_start = ws_alloc<uint32_t>(h, out.runs_bound + 1);
   out.run_end = ws_alloc<uint32_t>(h, out.runs_bound + 1);
   out.run_src = ws_alloc<uint32_t>(h, out.runs_bound + 1);
-  cudaMemsetAsync(out.cnt, 0, (nv + 1) * 4, h->stream);
+  cudaMemsetAsync(out.cnt, 0, (cap + 1) * 4, h->stream);
   DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
-      g, d_src, d_dst, (uint32_t)n, out.cnt, out.rank, h->d_op()));
+      g, out.gi, d_src, d_dst, (uint32_t)n, out.cnt, out.rank, h->d_op()));
   out.b = BatchView{nullptr, out.gdst, out.run_src, out.run_start, out.run_end};
   return out;
 }
@@ -641,10 +646,10 @@ void group_scatter(dg_graph* h, const Grouped& gr, const uint32_t* d_src, const 
   const unsigned grid = (unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems));
   if (gr.index) {
     DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, true><<<grid, 256, 0, h->stream>>>(
-        g, d_src, d_dst, (uint32_t)n, gr.cnt, gr.rank, gr.gdst, gr.index, h->d_op()));
+        g, gr.gi, d_src, d_dst, (uint32_t)n, gr.cnt, gr.rank, gr.gdst, gr.index, h->d_op()));
   } else {
     DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, false><<<grid, 256, 0, h->stream>>>(
-        g, d_src, d_dst, (uint32_t)n, gr.cnt, gr.rank, gr.gdst, nullptr, h->d_op()));
+        g, gr.gi, d_src, d_dst, (uint32_t)n, gr.cnt, gr.rank, gr.gdst, nullptr, h->d_op()));
   }
 }
 
@@ -695,8 +700,8 @@ Grouped group_and_enumerate(dg_graph* h, const uint32_t* d_src, const uint32_t* 
   if (use_counting(h, n)) {
     Grouped gr = group_count<kMode>(h, d_src, d_dst, n, with_index);
     Worklist w = alloc_worklist(h, gr.runs_bound, n, true);
-    launch_alloc(h, "alloc_kernel<group+enum>", h->size + 1, d_n_aux(h), GroupEnumIn{g, gr.cnt, 1},
-                 GroupEnumOut{gr.cnt, gr.run_src, gr.run_start, gr.run_end, w.lists(h)},
+    launch_alloc(h, "alloc_kernel<group+enum>", n, d_n_input(h), GroupEnumIn{g, gr.gi, d_src, gr.rank, gr.cnt, 1},
+                 GroupEnumOut{g, gr.gi, d_src, gr.cnt, gr.run_src, gr.run_start, gr.run_end, w.lists(h)},
                  EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/1});
     group_scatter<kMode>(h, gr, d_src, d_dst, n);
     enqueue_walk(h, gr.b, w, gr.runs_bound);
@@ -878,8 +883,8 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
     GraphView g = view(h);
     Grouped gr = group_count<kPackInsert>(h, d_src, d_dst, n, false);
     PlanArrays a = alloc_plan_arrays(h, gr.runs_bound, n);
-    launch_alloc(h, "alloc_kernel<group+plan>", h->size + 1, d_n_aux(h), GroupPlanIn{g, gr.cnt},
-                 GroupPlanOut{gr.cnt, gr.run_src, gr.run_start, gr.run_end, a},
+    launch_alloc(h, "alloc_kernel<group+plan>", n, d_n_input(h), GroupPlanIn{g, gr.gi, d_src, gr.rank, gr.cnt},
+                 GroupPlanOut{gr.gi, d_src, gr.cnt, gr.run_src, gr.run_start, gr.run_end, a},
                  PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/1});
     group_scatter<kPackInsert>(h, gr, d_src, d_dst, n);
     enqueue_append(h, gr.b, a, gr.runs_bound, n, /*csr_path=*/false);
