@@ -45,7 +45,7 @@ if str(ROOT) not in sys.path:
 
 METRIC = "batch edge insert+delete throughput (batch=1M, R-MAT s22)"
 UNIT = "Medges/s"
-STATUS_BYTES = 200  # sizeof(DeviceState) + sizeof(OpState): the per-op D2H status read (csrc/dg_api.cu op_end)
+STATUS_BYTES = 208  # sizeof(DeviceState) + sizeof(OpState): the per-op D2H status read (csrc/dg_api.cu op_end)
 
 
 def parse_args():
@@ -130,11 +130,14 @@ def kernel_bytes(name: str, rep: dict, B: int) -> float | None:
     S = slots of touched chains, M = compaction moves (all from dg_last_op_report)."""
     b, T = rep["batch_entries"], rep["touched_sources"]
     W, S, M = rep["blocks_scanned"], rep["slots_scanned"], rep["moved"]
-    SL = rep.get("slots_scanned_long", 0)
+    SL, ST = rep.get("slots_scanned_long", 0), rep.get("slots_scanned_tiny", 0)
     if name.startswith("match_long"):
-        return 4 * SL + 8 * (SL // B) + 8 * b            # slab slots of long chains + worklist handles + masks + targets
-    if name.startswith("match_small"):
-        return 4 * (S - SL) + 12 * W + 8 * b + 4 * T     # slab slots + worklist (handle, run) + mask + targets + counters
+        return 4 * SL + 8 * (SL // B) + 8 * b            # slab slots of the tier + handles + masks + targets
+    if name.startswith("match_med"):
+        SM = S - SL - ST
+        return 4 * SM + 8 * (SM // B) + 8 * b
+    if name.startswith("match_tiny"):
+        return 4 * ST + 12 * W + 8 * b + 4 * T           # slab slots + every block's (tag, handle) + mask + targets
     if name.startswith("delete_holes_kernel"):
         return 12 * W + 8 * M + 32 * T                   # worklist + masks, hole records, per-source repair
     if name.startswith("delete_moves_kernel"):
@@ -153,8 +156,8 @@ def kernel_bytes(name: str, rep: dict, B: int) -> float | None:
         return 16 * b
     if name.startswith("enumerate_"):
         return 12 * W + 12 * T                           # next[] reads + worklist writes
-    if name.startswith("append_kernel"):
-        return 12 * b + 32 * T + 4 * (T + b // B)
+    if name.startswith("append_"):
+        return 16 * b + 32 * T + 4 * (T + b // B)
     return None
 
 
@@ -455,7 +458,7 @@ def run_b200_arm(args):
             top = max(prof.items(), key=lambda kv: kv[1][0])
             name, (ms, n) = top
             # delete-side kernels use the delete report, insert-side the insert report
-            ins_side = name.startswith("append_kernel")
+            ins_side = name.startswith(("append_", "alloc_kernel<group+plan"))
             per_launch = [kernel_bytes(name, r[0] if ins_side else r[1], B) for r in prof_reps]
             if per_launch[0] is not None and n:
                 bytes_launch = sum(per_launch) / len(per_launch)

@@ -120,7 +120,8 @@ typedef struct dg_op_report {
   uint64_t matched;         /* entries removed (delete) / queries answered true */
   uint64_t moved;           /* entries moved by compaction */
   uint64_t kernel_launches; /* kernels enqueued by the op */
-  uint64_t slots_scanned_long; /* part of slots_scanned handled by the long-chain path */
+  uint64_t slots_scanned_long; /* part of slots_scanned handled by the CTA-table tier (k > 128 targets) */
+  uint64_t slots_scanned_tiny; /* part handled by the register-compare tier (k <= 8 targets) */
 } dg_op_report;
 
 /* ---- lifecycle ------------------------------------------------------- */

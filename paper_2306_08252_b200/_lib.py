@@ -49,7 +49,7 @@ class DgMemory(C.Structure):
 class DgOpReport(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "batch_entries", "touched_sources", "blocks_popped", "blocks_pushed", "slots_scanned",
-        "blocks_scanned", "matched", "moved", "kernel_launches", "slots_scanned_long")]
+        "blocks_scanned", "matched", "moved", "kernel_launches", "slots_scanned_long", "slots_scanned_tiny")]
 
 
 # every symbol include/dyngraph_b200.h declares: name -> (restype, argtypes)

@@ -274,6 +274,7 @@ int op_end(dg_graph* h) {
   h->report.moved = op.moves;
   h->report.kernel_launches = h->launches;
   h->report.slots_scanned_long = op.slots_long;
+  h->report.slots_scanned_tiny = op.slots_tiny;
   if (op.err != 0) {
     h->report.blocks_popped = 0;
     return fail(h, (int)op.err,
@@ -299,8 +300,15 @@ void launch_alloc(dg_graph* h, const char* name, uint64_t n_bound, const unsigne
                   In in, Out out, Fin fin) {
   unsigned long long* scratch = ws_alloc<unsigned long long>(h, kAllocScratchWords);
   cudaMemsetAsync(scratch, 0, kAllocScratchWords * sizeof(unsigned long long), h->stream);
-  const unsigned tiles = (unsigned)std::max<uint64_t>(1, (n_bound + kAllocTile - 1) / kAllocTile);
-  DG_LAUNCH(h, name, alloc_kernel<<<tiles, kAllocThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
+  if (n_bound > (2u << 20)) {
+    constexpr int kTile = kAllocThreads * kAllocItemsLarge;
+    const unsigned tiles = (unsigned)((n_bound + kTile - 1) / kTile);
+    DG_LAUNCH(h, name, alloc_kernel<kAllocItemsLarge><<<tiles, kAllocThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
+  } else {
+    constexpr int kTile = kAllocThreads * kAllocItemsSmall;
+    const unsigned tiles = (unsigned)std::max<uint64_t>(1, (n_bound + kTile - 1) / kTile);
+    DG_LAUNCH(h, name, alloc_kernel<kAllocItemsSmall><<<tiles, kAllocThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
+  }
 }
 inline size_t alloc_ws_bytes() { return aligned(kAllocScratchWords * sizeof(unsigned long long)); }
 inline size_t scan_ws_bytes(uint64_t n_bound) {
@@ -870,9 +878,14 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   const bool counting = use_counting(h, n);
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
-  sz.total += group_ws_bytes(h, n, false, h->size - 1);
-  // block size may still be unknown (deferred pool): size the unit list for B = 1
-  sz.total += plan_arrays_ws(1, n, n);
+  if (counting) {
+    const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
+    sz.total += aligned((cap + 2) * 4) + aligned(n * 4) + aligned((cap + 2) * 16) + alloc_ws_bytes();
+  } else {
+    sz.total += group_ws_bytes(h, n, false, h->size - 1);
+    // block size may still be unknown (deferred pool): size the unit list for B = 1
+    sz.total += plan_arrays_ws(1, n, n);
+  }
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const uint32_t *d_src, *d_dst;
@@ -880,14 +893,21 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
   if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
   if (counting) {
+    // count -> plan (one alloc pass over the entries) -> entry-parallel append: no grouped copy
     GraphView g = view(h);
-    Grouped gr = group_count<kPackInsert>(h, d_src, d_dst, n, false);
-    PlanArrays a = alloc_plan_arrays(h, gr.runs_bound, n);
-    launch_alloc(h, "alloc_kernel<group+plan>", n, d_n_input(h), GroupPlanIn{g, gr.gi, d_src, gr.rank, gr.cnt},
-                 GroupPlanOut{gr.gi, d_src, gr.cnt, gr.run_src, gr.run_start, gr.run_end, a},
-                 PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/1});
-    group_scatter<kPackInsert>(h, gr, d_src, d_dst, n);
-    enqueue_append(h, gr.b, a, gr.runs_bound, n, /*csr_path=*/false);
+    const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
+    GroupIndex gi{(uint32_t)(cap - 1), (uint32_t)h->size};
+    uint32_t* cnt = ws_alloc<uint32_t>(h, cap + 2);
+    uint32_t* rank = ws_alloc<uint32_t>(h, n);
+    uint4* info = ws_alloc<uint4>(h, cap + 2);
+    cudaMemsetAsync(cnt, 0, (cap + 1) * 4, h->stream);
+    const unsigned grid = (unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems));
+    DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kPackInsert><<<grid, 256, 0, h->stream>>>(
+        g, gi, d_src, d_dst, (uint32_t)n, cnt, rank, h->d_op()));
+    launch_alloc(h, "alloc_kernel<group+plan>", n, d_n_input(h), GroupPlanIn{g, gi, d_src, rank, cnt},
+                 GroupPlanOut{gi, d_src, info}, PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/1});
+    DG_LAUNCH(h, "append_entries_kernel", append_entries_kernel<<<grid, 256, 0, h->stream>>>(
+        g, gi, d_src, d_dst, rank, (uint32_t)n, info, h->d_op()));
     return op_end(h);
   }
   Grouped gr = group_radix<kPackInsert>(h, d_src, d_dst, n, false, h->size - 1);
@@ -922,7 +942,7 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<unsigned long long>(n_offsets); sz.add<uint32_t>(n_edges); }
   sz.add<uint32_t>(V + 2);
-  sz.total += plan_arrays_ws(1, V, n_edges);
+  sz.total += plan_arrays_ws(h->B ? h->B : 1, V, n_edges);  // deferred pool: size the unit list for B = 1
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const unsigned long long* d_off;

@@ -71,6 +71,7 @@ struct OpState {
   unsigned long long n_aux;       // second device-resident scan bound (vertex count of the counting group-by)
   unsigned int med_cursor;        // dynamic work distribution of the medium / long match tiers
   unsigned int long_cursor;
+  unsigned long long slots_tiny;  // part of `slots` inspected by the register-compare tier
 };
 
 __device__ __forceinline__ void set_error(OpState* op, uint32_t code, uint32_t detail,
@@ -226,18 +227,19 @@ struct Sum2 {
 };
 constexpr size_t kAllocScratchWords = 4;
 constexpr int kAllocThreads = 256;
-constexpr int kAllocItems = 4;
-constexpr int kAllocTile = kAllocThreads * kAllocItems;
+constexpr int kAllocItemsSmall = 4;    // batches: more tiles, shorter per-tile latency chain
+constexpr int kAllocItemsLarge = 4;    // vertex-sized passes (16 items per thread measured 1.8x slower)
 
 // In::Aux is a small per-element payload In fills next to the sums (values it
 // already loaded) and Out receives back, so Out never re-loads them.  In must
 // use predicated loads (`x = c ? p[i] : 0`), not branches: the kernel issues a
 // thread's items back to back and a branch would serialise their latencies.
-template <class In, class Out, class Fin>
-__global__ void __launch_bounds__(kAllocThreads, 4)
+template <int kAllocItems, class In, class Out, class Fin>
+__global__ void __launch_bounds__(kAllocThreads, kAllocItems <= 4 ? 4 : 2)
 alloc_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* scratch,
              const OpState* __restrict__ op_guard, In in, Out out, Fin fin) {
   if (op_guard != nullptr && op_guard->err != 0) return;
+  constexpr int kAllocTile = kAllocThreads * kAllocItems;
   __shared__ Sum2 s_warp[kAllocThreads / 32];
   __shared__ Sum2 s_base;
   const unsigned long long n = *n_ptr;

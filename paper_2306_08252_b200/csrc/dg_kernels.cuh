@@ -451,8 +451,15 @@ struct PlanOut {
 };
 // plan fused with the counting group-by: one pass over the batch ENTRIES.  The
 // entry that drew rank 0 in group_count_kernel speaks for its source: it reads
-// the source's count and state and takes the source's run slot, group slot,
-// append units and queue positions — no pass over the vertices.
+// the source's count and state and takes the source's queue positions — no
+// pass over the vertices, no run list.  What the append needs per source goes
+// to `info`, indexed like the counters.
+struct SourceInfo {   // 16 bytes, one gather per entry in append_entries_kernel
+  uint32_t d;         // degree before the batch
+  uint32_t tail;      // tail block before the batch
+  uint32_t blk_off;   // first queue position (relative to the old front) of its fresh blocks
+  uint32_t c;         // entries the batch holds for it
+};
 struct GroupPlanIn {
   using Aux = PlanAux;
   GraphView g;
@@ -466,29 +473,18 @@ struct GroupPlanIn {
     const uint32_t c = rep ? cnt[gi(s)] : 0u;
     x.d = rep ? g.deg[s] : 0u;
     x.tail = rep ? g.tail[s] : kNull;
-    return Sum2{c ? ((1ull << 32) | c) : 0ull, c ? plan_word(g, x.d, c) : 0ull};
+    return Sum2{c ? ((1ull << 32) | c) : 0ull, c ? (plan_word(g, x.d, c) & 0xFFFFFFFFull) : 0ull};
   }
 };
 struct GroupPlanOut {
   GroupIndex gi;
   const uint32_t* src;
-  uint32_t* cnt;        // becomes the group start of each touched source
-  uint32_t* run_src;
-  uint32_t* run_start;
-  uint32_t* run_end;
-  PlanArrays arr;
-  __device__ void operator()(unsigned long long i, unsigned long long excl_a, unsigned long long excl_b,
+  uint4* info;
+  __device__ void operator()(unsigned long long i, unsigned long long, unsigned long long excl_b,
                              Sum2 val, const PlanAux& x) const {
     const uint32_t c = (uint32_t)val.a;
     if (c == 0) return;
-    const uint32_t v = src[i];
-    const uint32_t r = (uint32_t)(excl_a >> 32);
-    const uint32_t es = (uint32_t)excl_a;
-    run_src[r] = v;
-    run_start[r] = es;
-    run_end[r] = es + c;
-    cnt[gi(v)] = es;
-    arr.write(r, x, excl_b, val.b);
+    info[gi(src[i])] = make_uint4(x.d, x.tail, (uint32_t)excl_b, c);
   }
 };
 struct PlanFin {
@@ -589,7 +585,7 @@ append_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ unit_off,
       if (kCommit && j == need + has_fill - 1) g.deg[v] = d + c;
     }
     const uint32_t nvalid = min(32u, U - u0);
-    constexpr int kFly = 8;  // units in flight per warp
+    constexpr int kFly = 8;  // units in flight per warp (16 measured slower: registers)
     for (uint32_t l0 = 0; l0 < nvalid; l0 += kFly) {
       uint32_t vb[kFly], vo[kFly], vs[kFly], vc[kFly], val[kFly];
 #pragma unroll
@@ -618,6 +614,66 @@ append_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ unit_off,
           if (kValidateDst && x >= g.dst_limit) set_error(op, 2, kErrDstRange, vs[q] + s);
           g.slab[(unsigned long long)vb[q] * g.B + vo[q] + s] = x;
         }
+      }
+    }
+  }
+}
+
+// insert, counting path: append straight from the COO batch, one thread per
+// ENTRY, four entries per thread with each stage issued for all four (entry ->
+// source info gather -> queue handle -> slab store).  The entry's rank inside
+// its source fixes its slot: position = old degree + rank.  The entry landing in
+// slot 0 of a fresh block links that block; the last entry publishes degree and
+// tail (graph.hpp:333-372 without a grouped copy of the batch and without a
+// unit list).
+__global__ void __launch_bounds__(256)
+append_entries_kernel(GraphView g, GroupIndex gi, const uint32_t* __restrict__ src,
+                      const uint32_t* __restrict__ dst, const uint32_t* __restrict__ rank, uint32_t n,
+                      const uint4* __restrict__ info, OpState* op) {
+  if (op->err) return;
+  const unsigned long long base_mod = op->front_old % g.ring_cap;
+  const uint32_t base = blockIdx.x * (256 * kGroupItems) + threadIdx.x;
+  uint32_t s[kGroupItems], d[kGroupItems], rk[kGroupItems];
+  uint4 in[kGroupItems];
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q) {
+    const uint32_t i = base + q * 256;
+    s[q] = i < n ? src[i] : 0u;
+    d[q] = i < n ? dst[i] : 0u;
+    rk[q] = i < n ? rank[i] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q) in[q] = (base + q * 256 < n) ? info[gi(s[q])] : make_uint4(0, 0, 0, 0);
+  uint32_t blk[kGroupItems], prev[kGroupItems], slot[kGroupItems];
+  bool fresh[kGroupItems];
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q) {
+    const uint32_t d_old = in[q].x;
+    const uint32_t nb_old = blocks_for(g, d_old);
+    const uint32_t p = d_old + rk[q];
+    const uint32_t kb = div_b(g, p);
+    slot[q] = p - kb * g.B;
+    fresh[q] = kb >= nb_old;
+    blk[q] = in[q].y;   // the old tail block (the only old block with room: chains are compact)
+    prev[q] = kNull;
+    if (base + q * 256 < n && fresh[q]) {
+      const unsigned long long o = (unsigned long long)in[q].z + (kb - nb_old);
+      blk[q] = ring_at(g, base_mod, o);
+      if (slot[q] == 0) prev[q] = (kb == nb_old) ? (nb_old > 0 ? in[q].y : kNull) : ring_at(g, base_mod, o - 1);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kGroupItems; ++q) {
+    if (base + q * 256 >= n) continue;
+    g.slab[(unsigned long long)blk[q] * g.B + slot[q]] = d[q];
+    if (fresh[q] && slot[q] == 0) {
+      if (prev[q] == kNull) g.head[s[q]] = blk[q]; else g.next[prev[q]] = blk[q];
+    }
+    if (rk[q] == in[q].w - 1) {   // the source's last entry
+      g.deg[s[q]] = in[q].x + in[q].w;
+      if (fresh[q]) {
+        g.next[blk[q]] = kNull;
+        g.tail[s[q]] = blk[q];
       }
     }
   }
@@ -1027,7 +1083,10 @@ match_tiny_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
     }
   }
   const unsigned long long t = block_reduce_sum(slots, s_warp);
-  if (threadIdx.x == 0 && t) atomicAdd(&op->slots, t);
+  if (threadIdx.x == 0 && t) {
+    atomicAdd(&op->slots, t);
+    atomicAdd(&op->slots_tiny, t);
+  }
 }
 
 // Open-addressing table of u32 keys in shared memory; kTomb marks an empty slot
@@ -1377,8 +1436,10 @@ delete_holes_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_of
                     OpState* op) {
   if (op->err || op->aux1) return;
   __shared__ unsigned long long s_warp[8];
+  __shared__ uint32_t s_cnt[8];
+  __shared__ unsigned long long s_ring_base;
   const uint32_t W = (uint32_t)op->wl_blocks;
-  const uint32_t Wpad = (W + 31u) & ~31u;
+  const uint32_t Wpad = (W + 255u) & ~255u;   // CTA-uniform trip count (barriers inside)
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   unsigned long long pushed = 0, matched = 0;
@@ -1432,17 +1493,25 @@ delete_holes_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_of
         }
       }
     }
+    // blocks past the new tail go back to the ring rear: one cursor bump per CTA iteration
     const unsigned fm = __ballot_sync(kFull, do_free);
-    if (fm) {
-      unsigned long long pos = 0;
-      const int leader = __ffs(fm) - 1;
-      if (lane == leader) {
-        pos = atomicAdd(&g.st->rear, (unsigned long long)__popc(fm));
-        pushed += __popc(fm);
+    const int wid = threadIdx.x >> 5;
+    if (lane == 0) s_cnt[wid] = __popc(fm);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t c = s_cnt[i];
+        s_cnt[i] = tot;
+        tot += c;
       }
-      pos = __shfl_sync(kFull, pos, leader);
-      if (do_free) g.ring[(pos + __popc(fm & lt)) % g.ring_cap] = h;
+      s_ring_base = tot ? atomicAdd(&g.st->rear, (unsigned long long)tot) : 0ull;
+      pushed += tot;
     }
+    __syncthreads();
+    if (do_free) g.ring[(s_ring_base + s_cnt[wid] + __popc(fm & lt)) % g.ring_cap] = h;
+    __syncthreads();
   }
   const unsigned long long tp = block_reduce_sum(pushed, s_warp);
   const unsigned long long tm = block_reduce_sum(matched, s_warp);
