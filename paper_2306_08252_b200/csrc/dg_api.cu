@@ -75,6 +75,15 @@ struct dg_graph {
   unsigned long long* mv_hole = nullptr;
   uint64_t mv_cap = 0;
 
+  // independent kernels of one op (chain walks, the match tiers) run side by side on two
+  // auxiliary streams between a fork and a join on the op's stream
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  bool forked = false;
+  // alloc_kernel cursors carved from a buffer an earlier memset of the op already zeroed
+  unsigned long long* pre_zero = nullptr;
+  int pre_zero_left = 0;
+
   std::string last_error;
   dg_op_report report{};
   uint64_t launches = 0;
@@ -221,6 +230,27 @@ inline int grid_for(const dg_graph* h, uint64_t items, int per_block) {
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
 }
 
+// ---- fork / join of independent kernels ------------------------------------------
+// Between fork() and join() lane(h, i) names stream i of {op stream, aux 0, aux 1}.
+// With per-kernel profiling on, everything stays on the op stream so the event
+// brackets keep measuring single kernels.
+void fork(dg_graph* h) {
+  if (h->profiling || h->aux[0] == nullptr) return;
+  cudaEventRecord(h->ev_fork, h->stream);
+  cudaStreamWaitEvent(h->aux[0], h->ev_fork, 0);
+  cudaStreamWaitEvent(h->aux[1], h->ev_fork, 0);
+  h->forked = true;
+}
+inline cudaStream_t lane(const dg_graph* h, int i) { return (h->forked && i > 0) ? h->aux[i - 1] : h->stream; }
+void join(dg_graph* h) {
+  if (!h->forked) return;
+  for (int i = 0; i < 2; ++i) {
+    cudaEventRecord(h->ev_join[i], h->aux[i]);
+    cudaStreamWaitEvent(h->stream, h->ev_join[i], 0);
+  }
+  h->forked = false;
+}
+
 // ---- op bracket -----------------------------------------------------------
 int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
   OpState& op = h->h_blk->op;
@@ -232,6 +262,7 @@ int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
   op.n_aux = h->size + 1;
   DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
   h->launches = 0;
+  h->pre_zero_left = 0;
   h->report = dg_op_report{};
   h->report.batch_entries = n_input;
   return DG_OK;
@@ -298,8 +329,15 @@ void launch_scan(dg_graph* h, const char* name, uint64_t n_bound, const unsigned
 template <class In, class Out, class Fin>
 void launch_alloc(dg_graph* h, const char* name, uint64_t n_bound, const unsigned long long* n_ptr,
                   In in, Out out, Fin fin) {
-  unsigned long long* scratch = ws_alloc<unsigned long long>(h, kAllocScratchWords);
-  cudaMemsetAsync(scratch, 0, kAllocScratchWords * sizeof(unsigned long long), h->stream);
+  unsigned long long* scratch;
+  if (h->pre_zero_left > 0) {
+    scratch = h->pre_zero;
+    h->pre_zero += kAllocScratchWords;
+    --h->pre_zero_left;
+  } else {
+    scratch = ws_alloc<unsigned long long>(h, kAllocScratchWords);
+    cudaMemsetAsync(scratch, 0, kAllocScratchWords * sizeof(unsigned long long), h->stream);
+  }
   if (n_bound > (2u << 20)) {
     constexpr int kTile = kAllocThreads * kAllocItemsLarge;
     const unsigned tiles = (unsigned)((n_bound + kTile - 1) / kTile);
@@ -540,10 +578,11 @@ inline size_t worklist_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n_bat
 // chain walk over a planned worklist
 void enqueue_walk(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound) {
   GraphView g = view(h);
-  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_for(h, runs_bound, 256), 256, 0, h->stream>>>(
-      g, b, w.wl_off, w.run_deg, w.wl_handle, w.wl_run, h->d_op()));
-  DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_for(h, big_bound(h), 8), 256, 0, h->stream>>>(
+  // (inside a fork: the long-chain walk starts first, it is the critical path)
+  DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_for(h, big_bound(h), 8), 256, 0, lane(h, 1)>>>(
       g, b, w.wl_off, w.run_deg, w.big_list, w.wl_handle, w.wl_run, h->d_op()));
+  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_for(h, runs_bound, 256), 256, 0, lane(h, 2)>>>(
+      g, b, w.wl_off, w.run_deg, w.wl_handle, w.wl_run, h->d_op()));
 }
 
 // enumeration over an already grouped batch (radix path, CSR batches) or over every vertex (export)
@@ -553,7 +592,9 @@ Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound,
   Worklist w = alloc_worklist(h, runs_bound, n_batch, b.run_start != nullptr);
   launch_alloc(h, "alloc_kernel<enum>", runs_bound, d_n_runs(h), EnumIn{g, b, check_alive}, EnumOut{b, w.lists(h)},
                EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/0});
+  fork(h);
   enqueue_walk(h, b, w, runs_bound);
+  join(h);
   return w;
 }
 
@@ -563,9 +604,6 @@ void enqueue_match(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
                    uint32_t* run_matched, uint32_t* wl_mask, uint8_t* hit) {
   GraphView g = view(h);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  DG_LAUNCH(h, kIsDelete ? "match_tiny_kernel<delete>" : "match_tiny_kernel<query>",
-            match_tiny_kernel<kIsDelete><<<grid_for(h, wl_bound, 256), 256, 0, h->stream>>>(
-                g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
   const size_t med_smem = kIsDelete ? kMedSmemDelete : kMedSmemQuery;
   const size_t long_smem = kIsDelete ? kLongSmemDelete : kLongSmemQuery;
   static bool attr_done[2] = {false, false};
@@ -574,13 +612,20 @@ void enqueue_match(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
     cudaFuncSetAttribute(match_long_kernel<kIsDelete>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_smem);
     attr_done[kIsDelete ? 1 : 0] = true;
   }
-  DG_LAUNCH(h, kIsDelete ? "match_med_kernel<delete>" : "match_med_kernel<query>",
-            match_med_kernel<kIsDelete><<<grid_for(h, med_items_bound(h, n_batch), 8), 256, med_smem, h->stream>>>(
-                g, b, w.wl_off, w.wl_handle, w.med_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
-  const int long_grid = (int)std::min<uint64_t>(long_items_bound(h, n_batch), (uint64_t)h->sm_count * 6);
+  // the tiers touch disjoint blocks: side by side, heaviest items first
+  fork(h);
+  const int long_grid = (int)std::min<uint64_t>(long_items_bound(h, n_batch), (uint64_t)h->sm_count * 3);
   DG_LAUNCH(h, kIsDelete ? "match_long_kernel<delete>" : "match_long_kernel<query>",
-            match_long_kernel<kIsDelete><<<long_grid, kLongThreads, long_smem, h->stream>>>(
+            match_long_kernel<kIsDelete><<<long_grid, kLongThreads, long_smem, lane(h, 1)>>>(
                 g, b, w.wl_off, w.wl_handle, w.long_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
+  const int med_grid = (int)std::min<uint64_t>(grid_for(h, med_items_bound(h, n_batch), 8), (uint64_t)h->sm_count * 4);
+  DG_LAUNCH(h, kIsDelete ? "match_med_kernel<delete>" : "match_med_kernel<query>",
+            match_med_kernel<kIsDelete><<<med_grid, 256, med_smem, lane(h, 2)>>>(
+                g, b, w.wl_off, w.wl_handle, w.med_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
+  DG_LAUNCH(h, kIsDelete ? "match_tiny_kernel<delete>" : "match_tiny_kernel<query>",
+            match_tiny_kernel<kIsDelete><<<grid_for(h, wl_bound, 256), 256, 0, lane(h, 0)>>>(
+                g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
+  join(h);
 }
 
 // ---- grouping a COO batch by source --------------------------------------------------------------
@@ -614,7 +659,7 @@ struct Grouped {
 inline size_t group_ws_bytes(const dg_graph* h, uint64_t n, bool with_index, uint64_t max_src) {
   size_t t = 0;
   if (use_counting(h, n)) {
-    t += aligned((std::bit_ceil(std::max<uint64_t>(h->size, 1)) + 2) * 4) + 2 * aligned(n * 4) + (with_index ? aligned(n * 4) : 0);
+    t += aligned((std::bit_ceil(std::max<uint64_t>(h->size, 1)) + 4 + 4 * kAllocScratchWords) * 4) + 2 * aligned(n * 4) + (with_index ? aligned(n * 4) : 0);
     t += 3 * aligned((std::min<uint64_t>(n, h->size + 1) + 1) * 4);
   } else {
     t += 2 * aligned(n * 8) + (with_index ? 2 * aligned(n * 4) : 0);
@@ -633,7 +678,9 @@ Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, u
   const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
   out.gi = GroupIndex{(uint32_t)(cap - 1), (uint32_t)h->size};
   out.cnt_words = cap + 1;
-  out.cnt = ws_alloc<uint32_t>(h, cap + 2);
+  // the counters and the op's alloc_kernel cursors are zeroed by ONE memset
+  const uint64_t cnt_words = (cap + 3) & ~1ull;  // even: the 64-bit cursors follow
+  out.cnt = ws_alloc<uint32_t>(h, cnt_words + 2 * 2 * kAllocScratchWords);
   out.rank = ws_alloc<uint32_t>(h, n);
   out.gdst = ws_alloc<uint32_t>(h, n);
   if (with_index) out.index = ws_alloc<uint32_t>(h, n);
@@ -641,7 +688,9 @@ Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, u
   out.run_start = ws_alloc<uint32_t>(h, out.runs_bound + 1);
   out.run_end = ws_alloc<uint32_t>(h, out.runs_bound + 1);
   out.run_src = ws_alloc<uint32_t>(h, out.runs_bound + 1);
-  cudaMemsetAsync(out.cnt, 0, (cap + 1) * 4, h->stream);
+  cudaMemsetAsync(out.cnt, 0, (cnt_words + 2 * 2 * kAllocScratchWords) * 4, h->stream);
+  h->pre_zero = reinterpret_cast<unsigned long long*>(out.cnt + cnt_words);
+  h->pre_zero_left = 2;
   DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
       g, out.gi, d_src, d_dst, (uint32_t)n, out.cnt, out.rank, h->d_op()));
   out.b = BatchView{nullptr, out.gdst, out.run_src, out.run_start, out.run_end};
@@ -711,8 +760,10 @@ Grouped group_and_enumerate(dg_graph* h, const uint32_t* d_src, const uint32_t* 
     launch_alloc(h, "alloc_kernel<group+enum>", n, d_n_input(h), GroupEnumIn{g, gr.gi, d_src, gr.rank, gr.cnt, 1},
                  GroupEnumOut{g, gr.gi, d_src, gr.cnt, gr.run_src, gr.run_start, gr.run_end, w.lists(h)},
                  EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/1});
+    fork(h);   // the scatter and the two chain walks are independent
     group_scatter<kMode>(h, gr, d_src, d_dst, n);
     enqueue_walk(h, gr.b, w, gr.runs_bound);
+    join(h);
     *w_out = w;
     return gr;
   }
@@ -729,18 +780,18 @@ inline size_t group_enumerate_ws(const dg_graph* h, uint64_t n, bool with_index,
 int delete_matched(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound, uint64_t n) {
   GraphView g = view(h);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  uint32_t* run_matched = ws_alloc<uint32_t>(h, runs_bound + 1);
-  uint32_t* hole_cnt = ws_alloc<uint32_t>(h, runs_bound + 1);
-  uint32_t* surv_cnt = ws_alloc<uint32_t>(h, runs_bound + 1);
+  uint32_t* zeroed = ws_alloc<uint32_t>(h, 3 * (runs_bound + 1));  // one memset for the three counters
+  uint32_t* run_matched = zeroed;
+  uint32_t* hole_cnt = zeroed + (runs_bound + 1);
+  uint32_t* surv_cnt = zeroed + 2 * (runs_bound + 1);
   uint32_t* mv_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   uint32_t* wl_mask = ws_alloc<uint32_t>(h, (wl_bound + 1) * g.mw);
-  cudaMemsetAsync(run_matched, 0, (runs_bound + 1) * 4, h->stream);
+  cudaMemsetAsync(zeroed, 0, 3 * (runs_bound + 1) * 4, h->stream);
   enqueue_match<true>(h, b, w, n, run_matched, wl_mask, nullptr);
   const size_t ws_mark = h->ws.off;
   for (int attempt = 0; attempt < 2; ++attempt) {
     h->ws.off = ws_mark;
-    cudaMemsetAsync(hole_cnt, 0, (runs_bound + 1) * 4, h->stream);
-    cudaMemsetAsync(surv_cnt, 0, (runs_bound + 1) * 4, h->stream);
+    if (attempt > 0) cudaMemsetAsync(hole_cnt, 0, 2 * (runs_bound + 1) * 4, h->stream);
     launch_alloc(h, "alloc_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{w.run_deg, run_matched},
                  MovesOut{mv_off}, MovesFin{h->d_op(), h->mv_cap});
     DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_for(h, wl_bound, 256), 256, 0, h->stream>>>(
@@ -837,6 +888,13 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
     if (rc != DG_OK) return bail(rc, h->last_error);
   }
   if (ensure_mv_scratch(h, 1 << 16) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
+  for (int i = 0; i < 2; ++i) {
+    if (cudaStreamCreateWithFlags(&h->aux[i], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
+      return bail(DG_ERR_CUDA, "dg_create: auxiliary stream");
+  }
+  if (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+    return bail(DG_ERR_CUDA, "dg_create: auxiliary stream");
   if (cfg.workspace_bytes && ws_reserve(h, cfg.workspace_bytes) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
   e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return bail(DG_ERR_CUDA, std::string("dg_create: ") + cudaGetErrorString(e));
@@ -859,6 +917,11 @@ void dg_destroy(dg_graph* h) {
   if (h->h_blk) cudaFreeHost(h->h_blk);
   cudaFree(h->ws.base);
   cudaFree(h->mv_hole);
+  for (int i = 0; i < 2; ++i) {
+    if (h->aux[i]) { cudaStreamSynchronize(h->aux[i]); cudaStreamDestroy(h->aux[i]); }
+    if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
+  }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   for (auto& sp : h->prof_open) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
   for (auto e : h->prof_pool) cudaEventDestroy(e);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -880,7 +943,7 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
   if (counting) {
     const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
-    sz.total += aligned((cap + 2) * 4) + aligned(n * 4) + aligned((cap + 2) * 16) + alloc_ws_bytes();
+    sz.total += aligned((cap + 4 + 2 * kAllocScratchWords) * 4) + aligned(n * 4) + aligned((cap + 2) * 16) + alloc_ws_bytes();
   } else {
     sz.total += group_ws_bytes(h, n, false, h->size - 1);
     // block size may still be unknown (deferred pool): size the unit list for B = 1
@@ -897,10 +960,13 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
     GraphView g = view(h);
     const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
     GroupIndex gi{(uint32_t)(cap - 1), (uint32_t)h->size};
-    uint32_t* cnt = ws_alloc<uint32_t>(h, cap + 2);
+    const uint64_t cnt_words = (cap + 3) & ~1ull;  // even: the 64-bit cursors follow
+    uint32_t* cnt = ws_alloc<uint32_t>(h, cnt_words + 2 * kAllocScratchWords);
     uint32_t* rank = ws_alloc<uint32_t>(h, n);
     uint4* info = ws_alloc<uint4>(h, cap + 2);
-    cudaMemsetAsync(cnt, 0, (cap + 1) * 4, h->stream);
+    cudaMemsetAsync(cnt, 0, (cnt_words + 2 * kAllocScratchWords) * 4, h->stream);  // counters + the alloc cursors
+    h->pre_zero = reinterpret_cast<unsigned long long*>(cnt + cnt_words);
+    h->pre_zero_left = 1;
     const unsigned grid = (unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems));
     DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kPackInsert><<<grid, 256, 0, h->stream>>>(
         g, gi, d_src, d_dst, (uint32_t)n, cnt, rank, h->d_op()));
