@@ -1,0 +1,13 @@
+#!/bin/bash
+# Round artefacts: parity tests, full bench (with cpu baseline), reference arm, C3 bench, ncu launch list, ncu full of top kernels.
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest_rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench_rc=$?"; tail -3 gpurun_out/bench.err
+python scripts/show_bench.py gpurun_out/bench.json | head -12
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref_rc=$?"; cut -c1-300 gpurun_out/bench_ref.json
+timeout 900 python bench.py --scale 24 --batch 10000000 --steps 5 --warmup 2 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo "c3_rc=$?"; tail -3 gpurun_out/bench_c3.err
+python scripts/show_bench.py gpurun_out/bench_c3.json | head -9
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+  python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-profile > gpurun_out/ncu_bench.log 2>&1; echo "ncu_list_rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"match_med|match_tiny|match_long" -s 3 -c 3 -o gpurun_out/prof_match -f \
+  python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-profile > gpurun_out/ncu_match.log 2>&1; echo "ncu_full_rc=$?"

@@ -303,3 +303,91 @@ def test_cpp_dropin_against_reference_class():
     proc = subprocess.run([str(exe), "60"], capture_output=True, text=True, timeout=600)
     assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-2000:]
     assert "60 workloads, 0 mismatches" in proc.stdout
+
+
+def test_config5_mixed_stream_latency_regime():
+    """BASELINE config 5: interleaved insert / delete / query stream with vertex add / remove and block
+    reclamation, batch sizes 1K-100K (verify.hpp:179-259 op mix), full parity with the oracle."""
+    rng = np.random.default_rng(0x5EED)
+    V0 = 1 << 16
+    cfg = {"v0": V0, "block_size": 16, "arena_bytes": 1 << 30, "reclaim": True}
+    from paper_2306_08252_b200 import rmat
+    bs, bd = rmat.rmat_edges(16, 1, 0, 16 * V0)
+    script = [("insert", bs, bd), ("check",)]
+    size, alive = V0, np.ones(V0 + 4096, bool)
+    log_s, log_d = [bs], [bd]
+    for step in range(40):
+        roll = int(rng.integers(0, 100))
+        n = int(rng.choice([1000, 3000, 10000, 30000, 100000]))
+        if roll < 55:
+            al = np.flatnonzero(alive[:size]).astype(np.uint32)
+            s = al[rng.integers(0, len(al), n)]
+            d = rng.integers(0, size, n).astype(np.uint32)
+            script.append(("insert", s, d))
+            log_s.append(s); log_d.append(d)
+        elif roll < 80:
+            src = rng.integers(0, len(log_s))
+            pick = rng.integers(0, len(log_s[src]), n)
+            s, d = log_s[src][pick].copy(), log_d[src][pick].copy()
+            arb = rng.integers(0, 10, n) >= 7
+            s[arb] = rng.integers(0, size, int(arb.sum())).astype(np.uint32)
+            d[arb] = rng.integers(0, size, int(arb.sum())).astype(np.uint32)
+            script.append(("delete", s, d))
+        elif roll < 90 and size + 64 < len(alive):
+            cnt = int(1 + rng.integers(0, 64))
+            script.append(("add_vertices", cnt))
+            size += cnt
+        else:
+            ids = rng.integers(0, size, int(1 + rng.integers(0, 4))).astype(np.uint32)
+            script.append(("del_vertices", ids))
+            alive[ids] = False
+        if step % 5 == 4:
+            qs = np.concatenate([log_s[-1][:2000], rng.integers(0, size + 3, 1000).astype(np.uint32)])
+            qd = np.concatenate([log_d[-1][:2000], rng.integers(0, size + 3, 1000).astype(np.uint32)])
+            script += [("query", qs, qd), ("check",)]
+    g, o = _gpu(cfg, pool_blocks=1 << 19), _orc(cfg)
+    assert_same(run_script(g, script), run_script(o, script), "config 5 mixed stream")
+    st = g.g.stats()
+    assert st["hole_slots"] == 0 and st["pool_blocks_in_use"] == st["adjacency_blocks"]
+    g.close()
+
+
+@pytest.mark.parametrize("group", GROUPS)
+def test_config3_skewed_rmat_hubs_and_queue_pressure(group):
+    """BASELINE config 3 shape at a test-sized scale (the full s24 / 10M run is bench.py --scale 24
+    --batch 10000000): skewed R-MAT (a=.57) whose hubs grow chains of thousands of blocks, a pool sized
+    so the batches only fit because deletes return their blocks, and size-independent properties:
+    digest linearity, insert -> delete round trip, degrees, pool conservation."""
+    import torch
+    from paper_2306_08252_b200 import DynamicGraph, GraphConfig, rmat
+    scale, batch, B = 18, 2_000_000, 32
+    V, E = 1 << scale, 16 << scale
+    thr = rmat.thresholds()
+    hs, hd = rmat.rmat_edges(scale, 1, 0, E, thr)
+    deg = np.bincount(hs, minlength=V)
+    base_blocks = int(((deg + B - 1) // B).sum())
+    g = DynamicGraph(GraphConfig(pool_blocks=base_blocks + batch // B + V // 4, group=group), V, B)
+    order = np.argsort(hs, kind="stable")
+    off = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
+    g.bulk_init(off, hd[order])
+    assert g.stats()["pool_blocks_in_use"] == base_blocks and g.stats()["max_degree"] == deg.max()
+    assert g.stats()["max_degree"] > 1000 * B // 8   # hubs: chains of hundreds of blocks at this scale
+    d0 = _np_digest(hs, hd)
+    assert g.digest() == (d0, E)
+    base_keys = (hs.astype(np.uint64) << np.uint64(32)) | hd
+    free_before = g.stats()["pool_queue_size"]
+    for i in range(4):   # 4 x 2M inserts through a pool with room for ~1.1 batches
+        bs, bd = rmat.rmat_edges(scale, 2, i * batch, batch, thr)
+        g.insert_pairs(torch.from_numpy(bs.view(np.int32)).cuda(), torch.from_numpy(bd.view(np.int32)).cuda())
+        assert g.digest() == ((d0 + _np_digest(bs, bd)) % (1 << 64), E + batch), i
+        assert g.query_edges(bs[:5000], bd[:5000]).all()
+        g.delete_pairs(bs, bd)
+        keep = ~np.isin(base_keys, (bs.astype(np.uint64) << np.uint64(32)) | bd)
+        hs, hd, base_keys = hs[keep], hd[keep], base_keys[keep]
+        d0, E = _np_digest(hs, hd), int(keep.sum())
+        assert g.digest() == (d0, E), i
+        assert np.array_equal(g.degrees(), np.bincount(hs, minlength=V).astype(np.uint64))
+        st = g.stats()
+        assert st["hole_slots"] == 0 and st["pool_blocks_in_use"] == st["adjacency_blocks"]
+        assert st["pool_queue_size"] >= free_before   # emptied blocks came back
+    g.close()
