@@ -88,7 +88,7 @@ SIGNATURES = {
                               C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
     "dg_coo_to_csr": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_uint64,
                                 C.c_void_p, C.c_void_p]),
-    "dg_route_coo": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
+    "dg_route_coo": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64,
                                C.c_void_p, C.c_void_p, C.c_void_p, u64p]),
     "dg_owner_perm": (C.c_uint32, [C.c_uint32, C.c_uint32]),
     "dg_owner_perm_inv": (C.c_uint32, [C.c_uint32, C.c_uint32]),

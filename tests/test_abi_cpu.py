@@ -89,3 +89,16 @@ def test_cpp_mirror_header_compiles_standalone(tmp_path):
     subprocess.run(["g++", "-std=c++17", "-Wall", "-Wextra", "-Werror", f"-I{ROOT / 'include'}", str(src), "-o", str(exe),
                     f"-L{LIB_PATH.parent}", "-ldyngraph_b200", f"-Wl,-rpath,{LIB_PATH.parent}"], check=True)
     assert subprocess.run([str(exe)]).returncode == 0
+
+
+def test_ctypes_signatures_match_header_arity():
+    """Every ctypes signature has as many arguments as the header's prototype (a missing one
+    shifts every later pointer)."""
+    from paper_2306_08252_b200 import _lib
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    protos = dict(re.findall(r"\b(dg_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", text))
+    assert len(protos) >= 30
+    for name, args in protos.items():
+        args = args.strip()
+        n = 0 if args in ("", "void") else args.count(",") + 1
+        assert len(_lib.SIGNATURES[name][1]) == n, (name, n, len(_lib.SIGNATURES[name][1]))

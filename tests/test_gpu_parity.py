@@ -391,3 +391,74 @@ def test_config3_skewed_rmat_hubs_and_queue_pressure(group):
         assert st["hole_slots"] == 0 and st["pool_blocks_in_use"] == st["adjacency_blocks"]
         assert st["pool_queue_size"] >= free_before   # emptied blocks came back
     g.close()
+
+
+def _sharded_world1(port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2306_08252_b200 import GraphConfig
+        from paper_2306_08252_b200.sharded import ShardedDynamicGraph
+        rng = np.random.default_rng(9)
+        V = 3000
+        sg = ShardedDynamicGraph(GraphConfig(pool_blocks=1 << 15), V, 8)
+        orc = CpuGraph(load_oracle(), "orc", V, 8, 1 << 28)
+        dev = lambda a: torch.from_numpy(a.view(np.int32)).cuda()
+        log = []
+        for it in range(6):
+            s = (rng.zipf(1.4, 20000) % V).astype(np.uint32)
+            d = rng.integers(0, V, 20000).astype(np.uint32)
+            if it % 3 == 2:
+                s[:8000], d[:8000] = log[-1][0][:8000], log[-1][1][:8000]
+                sg.delete_pairs(dev(s), dev(d)); orc.delete_pairs(s, d)
+            else:
+                sg.insert_pairs(dev(s), dev(d)); orc.insert_pairs(s, d)
+            log.append((s, d))
+            assert sg.active_edges() == orc.active_edges()
+        qs = np.concatenate([log[0][0][:3000], rng.integers(0, V + 5, 2000).astype(np.uint32)])
+        qd = np.concatenate([log[0][1][:3000], rng.integers(0, V + 5, 2000).astype(np.uint32)])
+        ans = sg.query_edges(dev(qs), dev(qd)).cpu().numpy()
+        assert np.array_equal(ans, orc.query(qs, qd))
+        # the shard holds local ids perm(v): map back and compare the canonical state
+        off, dst = sg.local.export_csr(sorted=True)
+        lib = sg._lib
+        ooff, odst = orc.export_csr(sorted=True)
+        for lid in range(len(off) - 1):
+            v = lib.dg_owner_perm_inv(lid, sg.bits)
+            got = dst[int(off[lid]):int(off[lid + 1])]
+            want = odst[int(ooff[v]):int(ooff[v + 1])] if v < V else np.zeros(0, np.uint32)
+            assert np.array_equal(got, want), (lid, v)
+        d_s, n_s = sg.digest()
+        off2, dst2 = orc.export_csr(sorted=False)
+        srcs = np.repeat(np.arange(V, dtype=np.uint32), np.diff(off2.astype(np.int64)))
+        assert (d_s, n_s) == (_np_digest(srcs, dst2), len(dst2))
+        try:
+            sg.insert_pairs(dev(np.array([V + 7], np.uint32)), dev(np.array([0], np.uint32)))
+            q.put("no error raised for an out-of-range source")
+            return
+        except Exception as e:
+            assert "DataError" in type(e).__name__, type(e)
+        q.put("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_store_world_size_1_on_gpu():
+    """The multi-GPU host layer end to end on the one GPU available: dg_route_coo on the device,
+    NCCL all-to-all (world 1), permuted local ids, answers routed back, status agreement."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_sharded_world1, args=(port, q))
+    p.start()
+    p.join(timeout=300)
+    assert p.exitcode == 0
+    assert q.get(timeout=5) == "ok"
