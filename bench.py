@@ -258,7 +258,8 @@ def workload_config(args, world: int, B: int) -> dict:
         "workload": f"R-MAT scale {scale} (a,b,c,d=.57,.19,.19,.05; V={1 << scale}, base E={args.edge_factor << scale}) "
                     f"bulk init + per step: insert batch={args.batch * world} then delete the same batch",
         "batch": args.batch * world, "scale": scale, "edge_factor": args.edge_factor, "block_size": B,
-        "parallelism": "single GPU" if world == 1 else f"source-hash partition over {world} GPUs + NCCL all-to-all routing",
+        "parallelism": "single GPU" if world == 1 else
+        f"source-hash partition over {world} GPUs, fused owner-routing + exchange kernel over peer memory (NVLink P2P)",
         "l2": "256 MiB memset between steps (untimed) flushes L2; distinct batch every step",
     }
 
@@ -359,8 +360,11 @@ def run_b200_arm(args):
             B = args.block_size or 2 * args.edge_factor
             pool_blocks = int((E_local // B + V // world) * 1.6) + (8 * b) // B + 4096
             t0 = time.perf_counter()
+            # fused owner-routing + exchange over peer memory; the receive buffer holds one round (the
+            # bulk build goes through it in one piece): 1.25x the per-rank share + slack
             sharded = ShardedDynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream),
-                                          V, B, torch_stream=stream)
+                                          V, B, torch_stream=stream, exchange=os.environ.get("DG_EXCHANGE", "p2p"),
+                                          exchange_capacity=int(1.25 * max(E_local, b)) + (1 << 20))
             create_ms = (time.perf_counter() - t0) * 1e3
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             dist.barrier(); torch.cuda.synchronize()

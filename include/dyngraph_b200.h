@@ -303,6 +303,43 @@ int dg_route_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t
                  uint32_t world, uint32_t bits, uint64_t vertex_count, uint32_t* out_src_local,
                  uint32_t* out_dst, uint32_t* out_index, uint64_t* counts_host);
 
+/*
+ * Fused routing + exchange over peer memory (NVLink P2P): instead of
+ * partition -> count exchange -> NCCL all-to-all, ONE kernel computes every
+ * pair's owner and stores it straight into the owner's receive buffer
+ * (peer-mapped through CUDA IPC), reserving slots with a warp-aggregated
+ * system-scope atomicAdd on the owner's cursor.  A collective barrier (any
+ * all-reduce, e.g. the status agreement) then publishes the round.
+ *
+ * Round protocol, every rank:  dg_exchange_reset -> barrier -> dg_exchange_push_coo
+ * -> dg_synchronize -> barrier -> dg_exchange_received -> local batch op on the
+ * received DEVICE arrays.  Queries additionally carry (origin rank, origin index)
+ * and return their answers with dg_exchange_push_answers into the origin's
+ * answer buffer -> barrier -> dg_exchange_answers.
+ */
+typedef struct dg_exchange dg_exchange;
+#define DG_IPC_HANDLE_BYTES 64
+
+/* capacity: most entries this rank can receive (and most answers it can get back) in one round */
+int dg_exchange_create(dg_graph* h, uint32_t rank, uint32_t world, uint64_t capacity, dg_exchange** out);
+void dg_exchange_destroy(dg_exchange* x);
+/* IPC handle of this rank's buffers (64 bytes) — all-gather it, then hand every peer's to set_peer */
+int dg_exchange_ipc_handle(dg_exchange* x, void* handle_out);
+int dg_exchange_set_peer(dg_exchange* x, uint32_t peer_rank, const void* handle);
+int dg_exchange_reset(dg_exchange* x);
+/* validates src < vertex_count (DG_ERR_DATA, nothing pushed), else pushes (local src id, global dst,
+ * origin index) of every pair to its owner.  src/dst: DEVICE arrays. */
+int dg_exchange_push_coo(dg_exchange* x, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t bits,
+                         uint64_t vertex_count);
+/* after the barrier: what this rank received (DEVICE arrays owned by the exchange) */
+int dg_exchange_received(dg_exchange* x, uint64_t* n, uint32_t** src_local, uint32_t** dst,
+                         uint32_t** origin_index, uint32_t** origin_rank);
+/* answers[i] (DEVICE, one per received entry) go to answer slot origin_index[i] of rank origin_rank[i] */
+int dg_exchange_push_answers(dg_exchange* x, const uint8_t* answers, uint64_t n);
+/* after the barrier: the first n answers this rank got back (indexed by the position in its own
+ * query batch), copied to `out` (host or device per `mem`) */
+int dg_exchange_answers(dg_exchange* x, uint8_t* out, uint64_t n, int mem);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,6 +14,7 @@ DG_MEM_HOST, DG_MEM_DEVICE = 0, 1
 DG_FLAG_NO_RECLAIM = 1
 DG_FLAG_GROUP_RADIX = 2
 DG_FLAG_GROUP_COUNT = 4
+DG_IPC_HANDLE_BYTES = 64
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)
@@ -93,6 +94,16 @@ SIGNATURES = {
     "dg_owner_perm": (C.c_uint32, [C.c_uint32, C.c_uint32]),
     "dg_owner_perm_inv": (C.c_uint32, [C.c_uint32, C.c_uint32]),
     "dg_set_dst_limit": (C.c_int, [_H, C.c_uint64]),
+    "dg_exchange_create": (C.c_int, [_H, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "dg_exchange_destroy": (None, [C.c_void_p]),
+    "dg_exchange_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dg_exchange_set_peer": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "dg_exchange_reset": (C.c_int, [C.c_void_p]),
+    "dg_exchange_push_coo": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64]),
+    "dg_exchange_received": (C.c_int, [C.c_void_p, u64p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                       C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "dg_exchange_push_answers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "dg_exchange_answers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int]),
 }
 
 _lib = None

@@ -1557,4 +1557,173 @@ int dg_route_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t
   return DG_OK;
 }
 
+// ---- fused routing + exchange over peer memory ------------------------------------------------
+struct dg_exchange {
+  dg_graph* h = nullptr;
+  uint32_t rank = 0, world = 1;
+  uint64_t capacity = 0;
+  char* base = nullptr;          // this rank's buffers (one cudaMalloc: IPC-exportable)
+  size_t bytes = 0;
+  void* peer_base[kMaxPeers] = {};  // opened IPC mappings (nullptr for self / not set)
+  PeerBuffers pb{};
+};
+
+namespace {
+struct ExchangeLayout {
+  size_t cursor, src, dst, idx, from, ans, total;
+};
+ExchangeLayout exchange_layout(uint64_t cap) {
+  ExchangeLayout l{};
+  size_t off = 0;
+  l.cursor = off; off += 256;
+  l.src = off; off += aligned(cap * 4);
+  l.dst = off; off += aligned(cap * 4);
+  l.idx = off; off += aligned(cap * 4);
+  l.from = off; off += aligned(cap * 4);
+  l.ans = off; off += aligned(cap);
+  l.total = off;
+  return l;
+}
+void exchange_bind(dg_exchange* x, uint32_t peer, char* base) {
+  const ExchangeLayout l = exchange_layout(x->capacity);
+  x->pb.cursor[peer] = reinterpret_cast<unsigned long long*>(base + l.cursor);
+  x->pb.src[peer] = reinterpret_cast<uint32_t*>(base + l.src);
+  x->pb.dst[peer] = reinterpret_cast<uint32_t*>(base + l.dst);
+  x->pb.idx[peer] = reinterpret_cast<uint32_t*>(base + l.idx);
+  x->pb.from[peer] = reinterpret_cast<uint32_t*>(base + l.from);
+  x->pb.ans[peer] = reinterpret_cast<uint8_t*>(base + l.ans);
+}
+}  // namespace
+
+int dg_exchange_create(dg_graph* h, uint32_t rank, uint32_t world, uint64_t capacity, dg_exchange** out) {
+  if (!h || !out) return DG_ERR_DATA;
+  *out = nullptr;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (world == 0 || world > (uint32_t)kMaxPeers || rank >= world)
+    return fail(h, DG_ERR_DATA, "exchange: world must be in [1, 16] and rank < world");
+  if (capacity == 0 || capacity >= (1ull << 31)) return fail(h, DG_ERR_DATA, "exchange: bad capacity");
+  dg_exchange* x = new (std::nothrow) dg_exchange();
+  if (!x) return fail(h, DG_ERR_ENGINE, "exchange: out of host memory");
+  x->h = h;
+  x->rank = rank;
+  x->world = world;
+  x->capacity = capacity;
+  x->bytes = exchange_layout(capacity).total;
+  if (cudaMalloc(&x->base, x->bytes) != cudaSuccess) {
+    cudaGetLastError();
+    delete x;
+    return fail(h, DG_ERR_ENGINE, "exchange: device allocation failed");
+  }
+  cudaMemsetAsync(x->base, 0, 256, h->stream);
+  x->pb.capacity = capacity;
+  x->pb.world = world;
+  x->pb.rank = rank;
+  exchange_bind(x, rank, x->base);
+  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  *out = x;
+  return DG_OK;
+}
+
+void dg_exchange_destroy(dg_exchange* x) {
+  if (!x) return;
+  cudaSetDevice(x->h->device);
+  cudaStreamSynchronize(x->h->stream);
+  for (int p = 0; p < kMaxPeers; ++p)
+    if (x->peer_base[p]) cudaIpcCloseMemHandle(x->peer_base[p]);
+  cudaFree(x->base);
+  cudaGetLastError();
+  delete x;
+}
+
+int dg_exchange_ipc_handle(dg_exchange* x, void* handle_out) {
+  if (!x || !handle_out) return DG_ERR_DATA;
+  static_assert(sizeof(cudaIpcMemHandle_t) == DG_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaSetDevice(x->h->device);
+  cudaIpcMemHandle_t hd;
+  DG_CUDA(x->h, cudaIpcGetMemHandle(&hd, x->base));
+  std::memcpy(handle_out, &hd, sizeof(hd));
+  return DG_OK;
+}
+
+int dg_exchange_set_peer(dg_exchange* x, uint32_t peer_rank, const void* handle) {
+  if (!x || !handle) return DG_ERR_DATA;
+  if (peer_rank >= x->world) return fail(x->h, DG_ERR_DATA, "exchange: peer rank out of range");
+  if (peer_rank == x->rank) return DG_OK;  // own buffers are bound at creation
+  cudaSetDevice(x->h->device);
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, sizeof(hd));
+  void* p = nullptr;
+  DG_CUDA(x->h, cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+  x->peer_base[peer_rank] = p;
+  exchange_bind(x, peer_rank, static_cast<char*>(p));
+  return DG_OK;
+}
+
+int dg_exchange_reset(dg_exchange* x) {
+  if (!x) return DG_ERR_DATA;
+  cudaSetDevice(x->h->device);
+  DG_CUDA(x->h, cudaMemsetAsync(x->base, 0, 256, x->h->stream));
+  DG_CUDA(x->h, cudaStreamSynchronize(x->h->stream));
+  return DG_OK;
+}
+
+int dg_exchange_push_coo(dg_exchange* x, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t bits,
+                         uint64_t vertex_count) {
+  if (!x) return DG_ERR_DATA;
+  dg_graph* h = x->h;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  if (bits > 32 || vertex_count > (bits >= 32 ? (1ull << 32) : (1ull << bits)))
+    return fail(h, DG_ERR_DATA, "exchange: vertex_count exceeds 2^bits");
+  for (uint32_t p = 0; p < x->world; ++p)
+    if (x->pb.cursor[p] == nullptr) return fail(h, DG_ERR_ENGINE, "exchange: peer " + std::to_string(p) + " not set");
+  if (n == 0) return DG_OK;
+  int rc;
+  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  DG_LAUNCH(h, "exchange_validate_kernel", exchange_validate_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      src, (uint32_t)n, (uint32_t)std::min<uint64_t>(vertex_count, 0xFFFFFFFFull), h->d_op()));
+  DG_LAUNCH(h, "exchange_push_kernel", exchange_push_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      x->pb, src, dst, (uint32_t)n, bits, h->d_op()));
+  return op_end(h);
+}
+
+int dg_exchange_received(dg_exchange* x, uint64_t* n, uint32_t** src_local, uint32_t** dst,
+                         uint32_t** origin_index, uint32_t** origin_rank) {
+  if (!x || !n) return DG_ERR_DATA;
+  cudaSetDevice(x->h->device);
+  unsigned long long c = 0;
+  DG_CUDA(x->h, cudaMemcpy(&c, x->base, sizeof(c), cudaMemcpyDeviceToHost));
+  if (c > x->capacity) return fail(x->h, DG_ERR_ENGINE, "exchange: receive buffer overflow");
+  *n = c;
+  if (src_local) *src_local = x->pb.src[x->rank];
+  if (dst) *dst = x->pb.dst[x->rank];
+  if (origin_index) *origin_index = x->pb.idx[x->rank];
+  if (origin_rank) *origin_rank = x->pb.from[x->rank];
+  return DG_OK;
+}
+
+int dg_exchange_push_answers(dg_exchange* x, const uint8_t* answers, uint64_t n) {
+  if (!x) return DG_ERR_DATA;
+  dg_graph* h = x->h;
+  cudaSetDevice(h->device);
+  if (n == 0) return DG_OK;
+  DG_LAUNCH(h, "exchange_answers_kernel", exchange_answers_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+      x->pb, answers, x->pb.idx[x->rank], x->pb.from[x->rank], (uint32_t)n));
+  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  return DG_OK;
+}
+
+int dg_exchange_answers(dg_exchange* x, uint8_t* out, uint64_t n, int mem) {
+  if (!x || (!out && n)) return DG_ERR_DATA;
+  if (n > x->capacity) return fail(x->h, DG_ERR_DATA, "exchange: more answers than the buffer holds");
+  cudaSetDevice(x->h->device);
+  if (n == 0) return DG_OK;
+  DG_CUDA(x->h, cudaMemcpyAsync(out, x->pb.ans[x->rank], n,
+                                mem == DG_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, x->h->stream));
+  DG_CUDA(x->h, cudaStreamSynchronize(x->h->stream));
+  return DG_OK;
+}
+
 }  // extern "C"

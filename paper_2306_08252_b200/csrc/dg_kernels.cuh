@@ -1861,4 +1861,71 @@ __global__ void route_gather_kernel(const unsigned long long* __restrict__ keys,
   }
 }
 
+// ---------------------------------------------------------------------------
+// K11, fused: owner computation + exchange over peer memory.  The receive
+// buffers of every rank are mapped into this process (CUDA IPC over NVLink);
+// a warp groups its 32 pairs by owner (__match_any_sync), the group leader
+// reserves slots with ONE system-scope atomicAdd on the owner's cursor, and
+// the lanes store their records straight into the owner's buffers.
+// ---------------------------------------------------------------------------
+constexpr int kMaxPeers = 16;
+struct PeerBuffers {
+  unsigned long long* cursor[kMaxPeers];
+  uint32_t* src[kMaxPeers];
+  uint32_t* dst[kMaxPeers];
+  uint32_t* idx[kMaxPeers];
+  uint32_t* from[kMaxPeers];
+  uint8_t* ans[kMaxPeers];
+  unsigned long long capacity;
+  uint32_t world, rank;
+};
+
+__global__ void __launch_bounds__(256)
+exchange_validate_kernel(const uint32_t* __restrict__ src, uint32_t n, uint32_t vertex_count, OpState* op) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (src[i] >= vertex_count) set_error(op, 2, kErrSrcRange, i);
+}
+
+__global__ void __launch_bounds__(256)
+exchange_push_kernel(PeerBuffers pb, const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                     uint32_t n, uint32_t bits, OpState* op) {
+  if (op->err) return;  // a rejected batch pushes nothing
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t npad = (n + 31u) & ~31u;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < npad; i += gridDim.x * blockDim.x) {
+    const bool valid = i < n;
+    uint32_t owner = 0xFFFFFFFFu, local = 0, d = 0;
+    if (valid) {
+      const uint32_t p = owner_perm(src[i], bits);
+      owner = p % pb.world;
+      local = p / pb.world;
+      d = dst[i];
+    }
+    const unsigned peers = __match_any_sync(kFull, owner);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long base = 0;
+    if (valid && lane == leader) base = atomicAdd_system(pb.cursor[owner], (unsigned long long)__popc(peers));
+    base = __shfl_sync(kFull, base, leader);
+    if (valid) {
+      const unsigned long long pos = base + __popc(peers & lt);
+      if (pos < pb.capacity) {
+        pb.src[owner][pos] = local;
+        pb.dst[owner][pos] = d;
+        pb.idx[owner][pos] = i;
+        pb.from[owner][pos] = pb.rank;
+      } else {
+        set_error(op, 3, kErrScratch, i);  // receive buffer of `owner` is full
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+exchange_answers_kernel(PeerBuffers pb, const uint8_t* __restrict__ answers, const uint32_t* __restrict__ idx,
+                        const uint32_t* __restrict__ from, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    pb.ans[from[i]][idx[i]] = answers[i];
+}
+
 }  // namespace dg

@@ -7,11 +7,21 @@ equal low bits carry ~44 % of the edges, so `v mod world` would be badly skewed.
 Each rank owns an ordinary single-GPU `DynamicGraph` (its own dictionary, block
 pool and free ring) over its local ids; destinations stay GLOBAL ids.
 
-Every batch op is
-  1. `dg_route_coo`   — owner-bucket partition on the device (send side),
-  2. a count exchange + payload all-to-all (`torch.distributed`, NCCL over NVLink),
-  3. the single-GPU op on what was received,
-and queries send their 1-byte answers back through the reverse all-to-all.
+Every batch op routes its pairs to the owners, then runs the single-GPU op on
+what was received; queries send their 1-byte answers back.  Two exchanges:
+
+  exchange="p2p"  (default when every peer is reachable over CUDA IPC / NVLink)
+      ONE kernel (`dg_exchange_push_coo`) computes each pair's owner and stores
+      it straight into the owner's receive buffer (peer-mapped memory, slots
+      reserved with a warp-aggregated system-scope atomicAdd on the owner's
+      cursor) — routing and transfer fused, no pack / count exchange / unpack.
+      The status all-reduce that agrees on validation doubles as the barrier
+      that publishes the round.  Answers go back the same way
+      (`dg_exchange_push_answers`).
+  exchange="nccl"
+      `dg_route_coo` (owner-bucket partition on the device) -> count exchange ->
+      payload all-to-all (`torch.distributed`) -> reverse all-to-all for answers.
+
 Validation failures are agreed with one all-reduce(MAX) BEFORE any rank mutates
 (batch atomicity, reference graph.hpp:168-171).
 
@@ -103,7 +113,7 @@ class ShardedDynamicGraph:
     """The operator API of DynamicGraph over `world` source-partitioned GPUs."""
 
     def __init__(self, config: GraphConfig | None, vertex_count: int, block_size: int,
-                 torch_stream=None, group=None):
+                 torch_stream=None, group=None, exchange: str = "p2p", exchange_capacity: int = 1 << 22):
         import torch
         import torch.distributed as dist
 
@@ -123,9 +133,60 @@ class ShardedDynamicGraph:
         if rc != 0:
             raise DataError("dst limit")
         self._lib = lib
+        self._x = None
+        if exchange == "p2p":
+            self._setup_p2p(int(exchange_capacity))
 
     def close(self):
+        if self._x is not None:
+            self._lib.dg_exchange_destroy(self._x)
+            self._x = None
         self.local.close()
+
+    # -- fused routing + exchange over peer memory ----------------------------------------------------
+    def _setup_p2p(self, capacity: int):
+        import torch.distributed as dist
+
+        x = C.c_void_p()
+        rc = self._lib.dg_exchange_create(self.local._h, self.rank, self.world, capacity, C.byref(x))
+        if agree_status(rc, self.device, self.group) != 0:
+            raise EngineError("sharded store: could not create the peer-memory exchange buffers")
+        handle = C.create_string_buffer(_lib.DG_IPC_HANDLE_BYTES)
+        self.local._check(self._lib.dg_exchange_ipc_handle(x, handle))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=self.group)
+        rc = 0
+        for peer, raw in enumerate(handles):
+            if peer != self.rank:
+                rc = max(rc, self._lib.dg_exchange_set_peer(x, peer, C.create_string_buffer(raw, len(raw))))
+        if agree_status(rc, self.device, self.group) != 0:
+            self._lib.dg_exchange_destroy(x)
+            raise EngineError("sharded store: a peer's exchange buffer could not be mapped (CUDA IPC); "
+                              "use exchange='nccl'")
+        self._x = x
+
+    def _push(self, src, dst):
+        """One exchange round; returns (n_received, src_ptr, dst_ptr, idx_ptr, from_ptr)."""
+        lib = self._lib
+        rc = lib.dg_exchange_reset(self._x)
+        agree_status(rc, self.device, self.group)     # barrier: every cursor is zero before anyone pushes
+        rc = lib.dg_exchange_push_coo(self._x, C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()), src.numel(),
+                                      self.bits, self.vertex_count)
+        rc = agree_status(rc, self.device, self.group)  # barrier: every push has landed (each rank synchronised)
+        if rc != 0:
+            raise _STATUS_EXC.get(rc, Error)("sharded batch: a rank rejected the batch while routing "
+                                              "(source id out of range or receive buffer full)")
+        n = C.c_uint64()
+        ps, pd, pi, pf = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        self.local._check(lib.dg_exchange_received(self._x, C.byref(n), C.byref(ps), C.byref(pd), C.byref(pi), C.byref(pf)))
+        return int(n.value), ps, pd, pi, pf
+
+    def _apply_ptr(self, fn, ps, pd, n):
+        code = fn(self.local._h, ps, pd, n, _lib.DG_MEM_DEVICE) if n else 0
+        msg = self._lib.dg_last_error(self.local._h).decode(errors="replace") if code else ""
+        agreed = agree_status(code, self.device, self.group)
+        if agreed != 0:
+            raise _STATUS_EXC.get(agreed, Error)(msg or "sharded batch: rejected on another rank")
 
     # -- routing -------------------------------------------------------------------------------------
     def _route(self, src, dst):
@@ -169,11 +230,17 @@ class ShardedDynamicGraph:
 
     # -- operator API (graph.hpp:167-241) ------------------------------------------------------------------
     def insert_pairs(self, src, dst):
+        if self._x is not None:
+            n, ps, pd, _, _ = self._push(src, dst)
+            return self._apply_ptr(self._lib.dg_insert_batch_coo, ps, pd, n)
         s, d, _, counts = self._route(src, dst)
         (rs, rd), _ = self._exchange([s, d], counts)
         self._apply(self.local.insert_pairs, rs, rd)
 
     def delete_pairs(self, src, dst):
+        if self._x is not None:
+            n, ps, pd, _, _ = self._push(src, dst)
+            return self._apply_ptr(self._lib.dg_delete_batch_coo, ps, pd, n)
         s, d, _, counts = self._route(src, dst)
         (rs, rd), _ = self._exchange([s, d], counts)
         self._apply(self.local.delete_pairs, rs, rd)
@@ -186,6 +253,16 @@ class ShardedDynamicGraph:
         # unknown sources answer 0 (graph.hpp:229): clamp them to a vertex id and mask afterwards
         known = (src.to(torch.int64) & 0xFFFFFFFF) < self.vertex_count
         src_c = torch.where(known, src, torch.zeros_like(src))
+        if self._x is not None:
+            nr, ps, pd, _, _ = self._push(src_c, dst)
+            ans = torch.zeros(max(nr, 1), dtype=torch.uint8, device=self.device)
+            rc = self._lib.dg_query_edges(self.local._h, ps, pd, nr, C.c_void_p(ans.data_ptr()), _lib.DG_MEM_DEVICE) if nr else 0
+            rc = max(rc, self._lib.dg_exchange_push_answers(self._x, C.c_void_p(ans.data_ptr()), nr))
+            if agree_status(rc, self.device, self.group) != 0:   # barrier: every answer has landed
+                raise EngineError("sharded query failed on a rank")
+            out = torch.empty(n, dtype=torch.uint8, device=self.device)
+            self.local._check(self._lib.dg_exchange_answers(self._x, C.c_void_p(out.data_ptr()), n, _lib.DG_MEM_DEVICE))
+            return out * known.to(torch.uint8)
         s, d, idx, counts = self._route(src_c, dst)
         (rs, rd), recv_counts = self._exchange([s, d], counts)
         ans = self.local.query_edges(rs, rd) if rs.numel() else torch.empty(0, dtype=torch.uint8, device=self.device)

@@ -393,7 +393,7 @@ def test_config3_skewed_rmat_hubs_and_queue_pressure(group):
     g.close()
 
 
-def _sharded_world1(port, q):
+def _sharded_world1(port, q, exchange):
     import os
     import torch
     import torch.distributed as dist
@@ -405,7 +405,7 @@ def _sharded_world1(port, q):
         from paper_2306_08252_b200.sharded import ShardedDynamicGraph
         rng = np.random.default_rng(9)
         V = 3000
-        sg = ShardedDynamicGraph(GraphConfig(pool_blocks=1 << 15), V, 8)
+        sg = ShardedDynamicGraph(GraphConfig(pool_blocks=1 << 15), V, 8, exchange=exchange, exchange_capacity=1 << 16)
         orc = CpuGraph(load_oracle(), "orc", V, 8, 1 << 28)
         dev = lambda a: torch.from_numpy(a.view(np.int32)).cuda()
         log = []
@@ -447,9 +447,11 @@ def _sharded_world1(port, q):
         dist.destroy_process_group()
 
 
-def test_sharded_store_world_size_1_on_gpu():
-    """The multi-GPU host layer end to end on the one GPU available: dg_route_coo on the device,
-    NCCL all-to-all (world 1), permuted local ids, answers routed back, status agreement."""
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+def test_sharded_store_world_size_1_on_gpu(exchange):
+    """The multi-GPU host layer end to end on the one GPU available, with both exchanges: the fused
+    push kernel into (own) peer-mapped buffers, and dg_route_coo + NCCL all-to-all (world 1);
+    permuted local ids, answers routed back, status agreement."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as sck:
@@ -457,7 +459,7 @@ def test_sharded_store_world_size_1_on_gpu():
         port = sck.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    p = ctx.Process(target=_sharded_world1, args=(port, q))
+    p = ctx.Process(target=_sharded_world1, args=(port, q, exchange))
     p.start()
     p.join(timeout=300)
     assert p.exitcode == 0
