@@ -282,8 +282,11 @@ def run_b200_arm(args):
             raise SystemExit("bench.py --gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    force_sharded = bool(os.environ.get("DG_FORCE_SHARDED"))   # exercise the multi-GPU path on one GPU
+    if world > 1 or force_sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
     from paper_2306_08252_b200 import DynamicGraph, GraphConfig, rmat
     from paper_2306_08252_b200._lib import load
@@ -311,7 +314,7 @@ def run_b200_arm(args):
             return torch.empty(n, dtype=torch.int32, device=dev)
 
         # ---- graph construction + bulk init (timed) --------------------------------------
-        if world == 1:
+        if world == 1 and not os.environ.get("DG_FORCE_SHARDED"):
             gen = DynamicGraph(GraphConfig(device=local, pool_blocks=1024, stream=stream.cuda_stream), 1, 1)
             src, dst = i32(E_local), i32(E_local)
             gen.gen_rmat(scale, 1, 0, src, dst, thr)
@@ -396,12 +399,15 @@ def run_b200_arm(args):
                 host_batches.append((hs.numpy().view(np.uint32), hd.numpy().view(np.uint32)))
         target = sharded if sharded is not None else g
 
-        def step(i, host=False):
+        def step(i, host=False, reports=False):
             s, d = (host_batches if host else batches)[i]
+            if host and sharded is not None:   # the sharded API takes device tensors: the H2D copy is explicit
+                s = torch.from_numpy(s.view(np.int32)).to(dev, non_blocking=True)
+                d = torch.from_numpy(d.view(np.int32)).to(dev, non_blocking=True)
             target.insert_pairs(s, d)
-            r_ins = g.last_op_report()
+            r_ins = g.last_op_report() if reports else None   # (kept out of the timed passes: host work between ops)
             target.delete_pairs(s, d)
-            return r_ins, g.last_op_report()
+            return r_ins, (g.last_op_report() if reports else None)
 
         def timed_pass(host: bool):
             """W warm-up + K timed steps; returns (sum of per-step device ms, per-step list, reports)."""
@@ -443,7 +449,8 @@ def run_b200_arm(args):
 
         clocks = ClockSampler(local)
         clocks.start()
-        total_ms, per_step, reps, wall_ms = timed_pass(host=False)
+        total_ms, per_step, _, wall_ms = timed_pass(host=False)
+        reps = [step(i, reports=True) for i in range(W, W + K)]   # same batches again, untimed: op reports
         launches = sum(r[0]["kernel_launches"] + r[1]["kernel_launches"] for r in reps)
         ins_ms, del_ms = split_pass()
         e2e = None
@@ -458,7 +465,7 @@ def run_b200_arm(args):
         roofline, kernels = None, None
         if not args.no_profile:
             g.profile_enable(True)
-            prof_reps = [step(i) for i in range(W, W + K)]
+            prof_reps = [step(i, reports=True) for i in range(W, W + K)]
             g.profile_enable(False)
             prof = g.profile_report()
             tot = sum(ms for ms, _ in prof.values()) or 1.0
@@ -519,7 +526,7 @@ def run_b200_arm(args):
                                     "sample": f"failed: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or force_sharded:
         dist.destroy_process_group()
     return 0
 

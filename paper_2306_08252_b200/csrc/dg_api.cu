@@ -606,12 +606,9 @@ void enqueue_match(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   const size_t med_smem = kIsDelete ? kMedSmemDelete : kMedSmemQuery;
   const size_t long_smem = kIsDelete ? kLongSmemDelete : kLongSmemQuery;
-  static bool attr_done[2] = {false, false};
-  if (!attr_done[kIsDelete ? 1 : 0]) {  // opt in to > 48 KB of dynamic shared memory once per instantiation
-    cudaFuncSetAttribute(match_med_kernel<kIsDelete>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)med_smem);
-    cudaFuncSetAttribute(match_long_kernel<kIsDelete>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_smem);
-    attr_done[kIsDelete ? 1 : 0] = true;
-  }
+  // opt in to > 48 KB of dynamic shared memory (per device: cheap enough to repeat)
+  cudaFuncSetAttribute(match_med_kernel<kIsDelete>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)med_smem);
+  cudaFuncSetAttribute(match_long_kernel<kIsDelete>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_smem);
   // the tiers touch disjoint blocks: side by side, heaviest items first
   fork(h);
   const int long_grid = (int)std::min<uint64_t>(long_items_bound(h, n_batch), (uint64_t)h->sm_count * 3);
@@ -1675,6 +1672,8 @@ int dg_exchange_push_coo(dg_exchange* x, const uint32_t* src, const uint32_t* ds
   h->last_error.clear();
   cudaSetDevice(h->device);
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  if (n > x->capacity)  // origin indices address the origin's answer buffer
+    return fail(h, DG_ERR_ENGINE, "exchange: batch larger than the exchange capacity");
   if (bits > 32 || vertex_count > (bits >= 32 ? (1ull << 32) : (1ull << bits)))
     return fail(h, DG_ERR_DATA, "exchange: vertex_count exceeds 2^bits");
   for (uint32_t p = 0; p < x->world; ++p)

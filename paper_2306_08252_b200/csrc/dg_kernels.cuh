@@ -1238,7 +1238,7 @@ constexpr int kMedFilterBits = 12;     // 4096-bit membership filter per warp: <
 constexpr size_t kMedSmemDelete = 8 * (kMedTable * 4 + 32 * 32 * 4 + (1u << kMedFilterBits) / 8);
 constexpr size_t kMedSmemQuery = kMedSmemDelete + 8 * kMedTable;
 template <bool kIsDelete>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 match_med_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                  const uint32_t* __restrict__ wl_handle, const uint2* __restrict__ items,
                  const uint32_t* __restrict__ run_deg, uint32_t* __restrict__ run_matched,
