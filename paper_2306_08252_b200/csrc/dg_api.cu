@@ -1004,8 +1004,14 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
   const uint64_t V = h->size;
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<unsigned long long>(n_offsets); sz.add<uint32_t>(n_edges); }
-  sz.add<uint32_t>(V + 2);
-  sz.total += plan_arrays_ws(h->B ? h->B : 1, V, n_edges);  // deferred pool: size the unit list for B = 1
+  if (h->B == 32) {
+    sz.add<uint32_t>(V + 1);
+    sz.add<CsrItem>(3 * (n_edges / kCsrHeavy) + 16);
+    sz.total += alloc_ws_bytes();
+  } else {
+    sz.add<uint32_t>(V + 2);
+    sz.total += plan_arrays_ws(h->B ? h->B : 1, V, n_edges);  // deferred pool: size the unit list for B = 1
+  }
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
   const unsigned long long* d_off;
@@ -1014,6 +1020,36 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
   if ((rc = stage_in(h, destinations, n_edges, mem, &d_dst)) != DG_OK) return rc;
   if ((rc = op_begin(h, n_edges, V)) != DG_OK) return rc;
   GraphView g = view(h);
+  if (h->B == 32 && n_edges > 0 && V > 0) {
+    // native block size: plan (offset validation fused) + one TMA-staged append pass that also
+    // validates the destinations and publishes deg/tail/front; rollback kernel on a late failure
+    const uint64_t items_cap = 3 * (n_edges / kCsrHeavy) + 16;
+    uint32_t* blk_off = ws_alloc<uint32_t>(h, V + 1);
+    CsrItem* items = ws_alloc<CsrItem>(h, items_cap);
+    launch_alloc(h, "alloc_kernel<csr plan>", V, d_n_runs(h), CsrPlanIn{g, d_off, (uint32_t)V, n_edges, h->d_op()},
+                 CsrPlanOut{blk_off, items, items_cap}, CsrPlanFin{g, h->d_op(), n_edges});
+    static int csr_ctas_per_sm = 0;
+    if (csr_ctas_per_sm == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&csr_ctas_per_sm, csr_append_kernel, kCsrWarps * 32, 0);
+      csr_ctas_per_sm = std::max(1, csr_ctas_per_sm);
+    }
+    const uint64_t groups = (V + 31) / 32 + items_cap;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((groups + kCsrWarps - 1) / kCsrWarps, (uint64_t)h->sm_count * csr_ctas_per_sm));
+    DG_LAUNCH(h, "csr_append_kernel", csr_append_kernel<<<grid, kCsrWarps * 32, 0, h->stream>>>(
+        g, d_off, d_dst, (uint32_t)V, blk_off, items, h->d_op()));
+    rc = op_end(h);
+    if (rc != DG_OK && h->h_blk->op.committed) {
+      const std::string msg = h->last_error;
+      csr_rollback_kernel<<<grid_for(h, V, 256), 256, 0, h->stream>>>(g, d_off, (uint32_t)V, h->d_op());
+      DG_CUDA(h, cudaMemcpyAsync(&h->h_blk->st, h->d_state(), sizeof(DeviceState), cudaMemcpyDeviceToHost, h->stream));
+      DG_CUDA(h, cudaStreamSynchronize(h->stream));
+      h->front = h->h_blk->st.front;
+      h->rear = h->h_blk->st.rear;
+      h->active_edges = h->h_blk->st.active_edges;
+      h->last_error = msg;
+    }
+    return rc;
+  }
   uint32_t* run_start = ws_alloc<uint32_t>(h, V + 2);
   DG_LAUNCH(h, "csr_validate_offsets_kernel", csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
       g, d_off, (uint32_t)n_offsets, n_edges, /*check_dead_source=*/1, run_start, h->d_op()));

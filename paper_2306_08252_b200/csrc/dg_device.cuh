@@ -72,6 +72,8 @@ struct OpState {
   unsigned int med_cursor;        // dynamic work distribution of the medium / long match tiers
   unsigned int long_cursor;
   unsigned long long slots_tiny;  // part of `slots` inspected by the register-compare tier
+  unsigned int plan_ok;           // CSR insert: the plan pass finished without an error (immutable afterwards)
+  unsigned int committed;         // CSR insert: the append pass ran and published deg/tail/front (rollback needed on error)
 };
 
 __device__ __forceinline__ void set_error(OpState* op, uint32_t code, uint32_t detail,

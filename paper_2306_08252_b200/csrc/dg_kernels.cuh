@@ -706,6 +706,411 @@ commit_insert_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ blk_
 }
 
 // ---------------------------------------------------------------------------
+// CSR insert / bulk init, native block size (B = 32): plan + ONE append pass.
+//
+//   csr plan   (alloc_kernel<CsrPlan*>) one pass over the vertices: validates the
+//              offsets (csr.hpp:49-66, graph.hpp:322-327), computes the fresh
+//              blocks every source needs (plan_batch, graph.hpp:135-160), hands
+//              out queue positions, and lists (vertex, 32-unit chunk) items for
+//              sources with more than kCsrHeavy entries.
+//   csr append (csr_append_kernel) a warp owns 32 consecutive vertices: their
+//              entries are ONE contiguous range of the batch, staged into the
+//              warp's shared-memory buffer by a TMA bulk copy
+//              (cp.async.bulk global -> shared, completion on an mbarrier) while
+//              the lanes resolve queue handles and links; the units (tail fill
+//              or one fresh block) are then written as full-sector 128-byte
+//              stores straight from shared memory.  Heavy sources are split into
+//              items of 32 units so a hub is spread over the whole grid.
+//              The destination range check (csr.hpp:67-72) rides in this pass and
+//              deg/tail/front are published by it; if a bad destination shows up
+//              the host runs csr_rollback_kernel, so a rejected batch still
+//              leaves the graph unchanged (graph.hpp:168-171).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kCsrStage = 1024;   // entries staged per round (4 KB per warp)
+constexpr uint32_t kCsrHeavy = 128;    // sources with more entries become items of up to 32 units (balance: hubs spread over the grid)
+constexpr int kCsrWarps = 8;
+
+struct CsrItem {       // 16 bytes: one 32-unit chunk of a heavy source
+  uint32_t v, chunk, d, tail;   // d / tail: the source's state BEFORE the batch
+};
+
+struct CsrPlanAux {
+  uint32_t c, d, tail;
+};
+struct CsrPlanIn {
+  using Aux = CsrPlanAux;
+  GraphView g;
+  const unsigned long long* off;
+  uint32_t V;
+  unsigned long long n_edges;
+  OpState* op;
+  __device__ Sum2 operator()(unsigned long long v64, Aux& x) const {
+    const uint32_t v = (uint32_t)v64;
+    const unsigned long long o0 = off[v], o1 = off[v + 1];
+    bool ok = true;
+    if (v == 0 && o0 != 0) { set_error(op, 2, kErrOffsetsStart, 0); ok = false; }
+    if (v + 1 == V && o1 != n_edges) { set_error(op, 2, kErrOffsetsEnd, V); ok = false; }
+    if (o1 < o0) { set_error(op, 2, kErrOffsetsMonotone, v + 1); ok = false; }
+    if (o1 > n_edges) ok = false;   // (non-monotone or bad end: reported where it happens)
+    const uint32_t c = ok ? (uint32_t)(o1 - o0) : 0u;
+    if (c > 0 && !bit_test(g.alive, v)) set_error(op, 2, kErrDeadSource, v);
+    x.c = c;
+    x.d = c ? g.deg[v] : 0u;
+    x.tail = (c > kCsrHeavy) ? g.tail[v] : kNull;
+    const unsigned long long w = c ? plan_word(g, x.d, c) : 0ull;
+    const uint32_t units = (uint32_t)(w >> 32);
+    const uint32_t items = (c > kCsrHeavy) ? (units + 31u) / 32u : 0u;
+    return Sum2{items, w & 0xFFFFFFFFull};
+  }
+};
+struct CsrPlanOut {
+  uint32_t* blk_off;
+  CsrItem* items;
+  unsigned long long items_cap;
+  __device__ void operator()(unsigned long long v, unsigned long long excl_a, unsigned long long excl_b,
+                             Sum2 val, const CsrPlanAux& x) const {
+    blk_off[v] = (uint32_t)excl_b;
+    const uint32_t n_it = (uint32_t)val.a;
+    if (n_it == 0 || excl_a + n_it > items_cap) return;   // (overflow only with broken offsets: already an error)
+    for (uint32_t k = 0; k < n_it; ++k) items[excl_a + k] = CsrItem{(uint32_t)v, k, x.d, x.tail};
+  }
+};
+struct CsrPlanFin {
+  GraphView g;
+  OpState* op;
+  unsigned long long n_edges;
+  __device__ void operator()(unsigned long long total_a, unsigned long long total_b) const {
+    if (op->err) return;
+    op->n_items = total_a;
+    op->total_need = total_b;
+    op->n_edges = n_edges;
+    DeviceState* st = g.st;
+    if (total_b > st->rear - st->front) {   // ensure_available (block_pool.hpp:177-189)
+      op->err = 3;
+      op->err_detail = kErrPoolUnderflow;
+      op->err_index = total_b - (st->rear - st->front);
+      return;
+    }
+    op->front_old = st->front;
+    op->plan_ok = 1;
+  }
+};
+
+// ---- mbarrier + TMA bulk copy (global -> shared) ---------------------------------
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+// bytes: multiple of 16; both addresses 16-byte aligned
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem_dst)),
+               "l"(gmem_src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+// Stages batch entries [e0, e1) (e1 - e0 <= kCsrStage) into `stage`; returns the
+// index in `stage` of entry e0.  The 16-byte-aligned interior goes through one
+// TMA bulk copy (waited for with csr_stage_wait), the unaligned tail (<= 3
+// entries) and ranges inside a single 16-byte chunk through the lanes.
+__device__ __forceinline__ uint32_t csr_stage_issue(uint32_t* stage, unsigned long long* bar, const uint32_t* __restrict__ dsts,
+                                                    unsigned long long e0, unsigned long long e1, bool& armed) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(dsts + e0);
+  const uintptr_t a1 = reinterpret_cast<uintptr_t>(dsts + e1);
+  const uintptr_t A = a0 & ~(uintptr_t)15, Z = a1 & ~(uintptr_t)15;
+  const uint32_t lead = (uint32_t)((a0 - A) >> 2);
+  armed = Z > A;
+  const int lane = lane_id();
+  if (armed && lane == 0) {
+    const unsigned bytes = (unsigned)(Z - A);
+    mbar_expect_tx(bar, bytes);
+    tma_load_1d(stage, reinterpret_cast<const void*>(A), bytes, bar);
+  }
+  // the rest: [max(a0, Z), a1) — at most 3 entries
+  const uintptr_t t0 = a0 > Z ? a0 : Z;
+  const uint32_t nt = (uint32_t)((a1 - t0) >> 2);
+  if ((uint32_t)lane < nt) stage[((t0 - A) >> 2) + lane] = *reinterpret_cast<const uint32_t*>(t0 + 4u * lane);
+  return lead;
+}
+
+// One batch of up to 32 append units, one per lane (blk / off0 / srel / cnt; cnt = 0: no unit),
+// written from the staging buffer.  Fresh blocks (off0 == 0) go out FOUR PER INSTRUCTION: eight
+// lanes own one block, each lane a 16-byte quarter-sector-aligned chunk (st.global.v4), padded
+// with kTomb up to the next 32-byte sector so no partial sector is ever written.  Slots beyond a
+// unit's entries are free slots of that block (nothing reads past deg), so padding is invisible.
+// Tail fills (off0 != 0, at most one per source) take a scalar path.  Returns through `bad` the
+// smallest batch index of an out-of-range destination seen by this lane (csr.hpp:67-72).
+__device__ __forceinline__ void csr_write_units(const GraphView& g, const uint32_t* stage, uint32_t nunits, uint32_t blk,
+                                                uint32_t off0, uint32_t srel, uint32_t cnt,
+                                                unsigned long long stage_entry0, unsigned long long& bad) {
+  const int lane = lane_id();
+  const int sub = lane >> 3, c8 = lane & 7;
+  const bool is_fill = cnt > 0 && off0 != 0;
+  // [11:0] srel, [17:12] cnt, [23:18] padded end (0 for fills and empty lanes: skipped by the fast loop)
+  const uint32_t pad_end = (cnt > 0 && !is_fill) ? min(32u, (cnt + 7u) & ~7u) : 0u;
+  const uint32_t pack = srel | (cnt << 12) | (pad_end << 18);
+  const uint32_t limit = g.dst_limit;
+  for (uint32_t q0 = 0; q0 < nunits; q0 += 4) {
+    const uint32_t bq = __shfl_sync(kFull, blk, q0 + sub);
+    const uint32_t pq = __shfl_sync(kFull, pack, q0 + sub);
+    const uint32_t sq = pq & 0xFFFu, cq = (pq >> 12) & 63u, pe = pq >> 18;
+    const uint32_t s0 = 4u * c8;
+    if (s0 < pe) {
+      const uint32_t* src = stage + sq + s0;
+      uint4 v;
+      v.x = src[0]; v.y = src[1]; v.z = src[2]; v.w = src[3];
+      const uint32_t nv = cq - min(cq, s0);   // valid words of this chunk (>= 4: all)
+      if (nv < 4) {
+        if (nv < 1) v.x = kTomb;
+        if (nv < 2) v.y = kTomb;
+        if (nv < 3) v.z = kTomb;
+        v.w = kTomb;
+      }
+      // padding is kTomb >= limit: only real entries can be reported, and they are checked by value
+      const bool b0 = v.x >= limit && nv > 0, b1 = v.y >= limit && nv > 1, b2 = v.z >= limit && nv > 2, b3 = v.w >= limit && nv > 3;
+      if (b0 | b1 | b2 | b3) {
+        const unsigned long long e = stage_entry0 + sq + s0 + (b0 ? 0u : b1 ? 1u : b2 ? 2u : 3u);
+        bad = min(bad, e);
+      }
+      *reinterpret_cast<uint4*>(g.slab + (unsigned long long)bq * 32u + s0) = v;
+    }
+  }
+  unsigned fills = __ballot_sync(kFull, is_fill);
+  while (fills) {
+    const int q = __ffs(fills) - 1;
+    fills &= fills - 1;
+    const uint32_t bq = __shfl_sync(kFull, blk, q);
+    const uint32_t oq = __shfl_sync(kFull, off0, q);
+    const uint32_t sq = __shfl_sync(kFull, srel, q);
+    const uint32_t cq = __shfl_sync(kFull, cnt, q);
+    if ((uint32_t)lane < cq) {
+      const uint32_t val = stage[sq + lane];
+      if (val >= limit) bad = min(bad, stage_entry0 + sq + lane);
+      g.slab[(unsigned long long)bq * 32u + oq + lane] = val;
+    }
+  }
+}
+
+// Unit j of a source with c batch entries, degree d and tail block tl before the batch, first
+// queue position bo: resolves its block, links it, and returns where its entries sit.
+// src_rel0: index in the staging buffer of the source's first batch entry.
+__device__ __forceinline__ void csr_resolve_unit(const GraphView& g, unsigned long long base_mod, uint32_t v, uint32_t j,
+                                                 uint32_t c, uint32_t d, uint32_t tl, uint32_t bo, uint32_t src_rel0,
+                                                 uint32_t& blk, uint32_t& off0, uint32_t& srel, uint32_t& cnt) {
+  const uint32_t nb_old = (d + 31u) >> 5;
+  const uint32_t space = nb_old * 32u - d;
+  const uint32_t fill = min(c, space);
+  const uint32_t has_fill = fill > 0 ? 1u : 0u;
+  const uint32_t need = (c - fill + 31u) >> 5;
+  if (has_fill && j == 0) {
+    blk = tl;                      // resume at the last-insert position (graph.hpp:344-349)
+    off0 = d - (nb_old - 1u) * 32u;
+    srel = src_rel0;
+    cnt = fill;
+  } else {
+    const uint32_t f = j - has_fill;
+    const unsigned long long o = (unsigned long long)bo + f;
+    blk = ring_at(g, base_mod, o);
+    off0 = 0;
+    srel = src_rel0 + fill + f * 32u;
+    cnt = min(32u, c - fill - f * 32u);
+    const uint32_t prev = (f == 0) ? (nb_old > 0 ? tl : kNull) : ring_at(g, base_mod, o - 1);
+    if (prev == kNull) g.head[v] = blk; else g.next[prev] = blk;
+    if (f == need - 1) g.next[blk] = kNull;
+  }
+}
+
+__global__ void __launch_bounds__(kCsrWarps * 32)
+csr_append_kernel(GraphView g, const unsigned long long* __restrict__ off, const uint32_t* __restrict__ dsts, uint32_t V,
+                  const uint32_t* __restrict__ blk_off, const CsrItem* __restrict__ items, OpState* op) {
+  if (!op->plan_ok) return;
+  __shared__ __align__(16) uint32_t s_stage[kCsrWarps][kCsrStage + 40];   // + alignment lead (<= 3) + the padded read of the last unit
+  __shared__ unsigned long long s_bar[kCsrWarps];
+  __shared__ uint8_t s_owner[kCsrWarps][256];   // <= 32 x (ceil(kCsrHeavy / 32) + 1) units per round
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  uint32_t* stage = s_stage[warp];
+  unsigned long long* bar = &s_bar[warp];
+  uint8_t* owner = s_owner[warp];
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    op->committed = 1;
+    g.st->front += op->total_need;         // commit_front (block_pool.hpp:162-166)
+    g.st->active_edges += op->n_edges;     // graph.hpp:186
+  }
+  unsigned phase = 0;
+  unsigned long long bad = ~0ull;   // smallest out-of-range destination index this lane saw
+  const unsigned long long base_mod = op->front_old % g.ring_cap;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+
+  // ---- heavy sources first: item = 32 consecutive units of one source
+  const uint32_t n_items = (uint32_t)op->n_items;
+  for (uint32_t it = gw; it < n_items; it += nwarps) {
+    const CsrItem item = items[it];
+    const unsigned long long o0 = off[item.v];
+    const uint32_t c = (uint32_t)(off[item.v + 1] - o0);
+    const uint32_t bo = blk_off[item.v];
+    const uint32_t nb_old = (item.d + 31u) >> 5;
+    const uint32_t fill = min(c, nb_old * 32u - item.d);
+    const uint32_t has_fill = fill > 0 ? 1u : 0u;
+    const uint32_t nu = ((c - fill + 31u) >> 5) + has_fill;
+    const uint32_t j0 = item.chunk * 32u;
+    const uint32_t nunits = min(32u, nu - j0);
+    // entries of units [j0, j0 + nunits)
+    const uint32_t f0 = j0 == 0 ? 0u : fill + (j0 - has_fill) * 32u;
+    const uint32_t j1 = j0 + nunits;
+    const uint32_t f1 = min(c, fill + (j1 - has_fill) * 32u);
+    bool armed;
+    const uint32_t lead = csr_stage_issue(stage, bar, dsts, o0 + f0, o0 + f1, armed);
+    uint32_t blk = 0, o_ = 0, srel = 0, cnt = 0;
+    if ((uint32_t)lane < nunits)
+      csr_resolve_unit(g, base_mod, item.v, j0 + lane, c, item.d, item.tail, bo, lead - f0, blk, o_, srel, cnt);
+    if (armed) { mbar_wait(bar, phase); phase ^= 1u; }
+    __syncwarp();
+    csr_write_units(g, stage, nunits, blk, o_, srel, cnt, o0 + f0 - lead, bad);
+    __syncwarp();
+  }
+
+  // ---- groups of 32 consecutive vertices
+  const uint32_t ngroups = (V + 31u) / 32u;
+  for (uint32_t grp = gw; grp < ngroups; grp += nwarps) {
+    const uint32_t v = grp * 32u + lane;
+    const bool valid = v < V;
+    const unsigned long long o0 = valid ? off[v] : 0ull;
+    const unsigned long long o1 = valid ? off[v + 1] : o0;
+    const uint32_t c = (uint32_t)(o1 - o0);
+    uint32_t d = 0, tl = kNull, bo = 0;
+    if (c > 0) {
+      d = g.deg[v];
+      tl = g.tail[v];
+      bo = blk_off[v];
+    }
+    const uint32_t nb_old = (d + 31u) >> 5;
+    const uint32_t fill = min(c, nb_old * 32u - d);
+    const uint32_t has_fill = fill > 0 ? 1u : 0u;
+    const uint32_t need = (c - fill + 31u) >> 5;
+    const bool heavy = c > kCsrHeavy;
+    const bool light = c > 0 && !heavy;
+    // publish the source's new state (insert_adjacency, graph.hpp:367-371)
+    if (c > 0) {
+      g.deg[v] = d + c;
+      if (need > 0) g.tail[v] = ring_at(g, base_mod, (unsigned long long)bo + need - 1);
+    }
+    const unsigned lightmask = __ballot_sync(kFull, light);
+    if (lightmask == 0) continue;
+    const unsigned heavymask = __ballot_sync(kFull, heavy);
+    const uint32_t cl = light ? c : 0u;
+    uint32_t cincl = cl;
+#pragma unroll
+    for (int dl = 1; dl < 32; dl <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, cincl, dl);
+      if (lane >= dl) cincl += t;
+    }
+    const uint32_t nu = light ? need + has_fill : 0u;
+    uint32_t pos = 0;
+    while (pos < 32) {
+      const unsigned rem = lightmask & (0xFFFFFFFFu << pos);
+      if (rem == 0) break;
+      const int a = __ffs(rem) - 1;
+      const uint32_t cbase = __shfl_sync(kFull, cincl - cl, a);
+      const unsigned hv_after = heavymask & (0xFFFFFFFFu << a);
+      const int hb = hv_after ? __ffs(hv_after) - 1 : 32;
+      const bool okl = valid && lane >= a && lane < hb && (cincl - cbase) <= kCsrStage;
+      const unsigned okmask = __ballot_sync(kFull, okl);
+      const int lb = a + __popc(okmask);   // the eligible lanes are a contiguous run starting at a
+      const unsigned long long e0 = __shfl_sync(kFull, o0, a);
+      const unsigned long long e1 = __shfl_sync(kFull, o1, lb - 1);
+      bool armed;
+      const uint32_t lead = csr_stage_issue(stage, bar, dsts, e0, e1, armed);
+      const bool in_round = lane >= a && lane < lb;
+      const uint32_t nur = in_round ? nu : 0u;
+      uint32_t uincl = nur;
+#pragma unroll
+      for (int dl = 1; dl < 32; dl <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, uincl, dl);
+        if (lane >= dl) uincl += t;
+      }
+      const uint32_t uexcl = uincl - nur;
+      const uint32_t U = __shfl_sync(kFull, uincl, 31);
+      for (uint32_t j = 0; j < nur; ++j) owner[uexcl + j] = (uint8_t)lane;
+      __syncwarp();
+      bool waited = !armed;
+      for (uint32_t ub = 0; ub < U; ub += 32) {
+        const uint32_t u = ub + lane;
+        const int L = (u < U) ? owner[u] : 0;
+        const unsigned long long oL = __shfl_sync(kFull, o0, L);
+        const uint32_t cL = __shfl_sync(kFull, c, L);
+        const uint32_t dL = __shfl_sync(kFull, d, L);
+        const uint32_t tlL = __shfl_sync(kFull, tl, L);
+        const uint32_t boL = __shfl_sync(kFull, bo, L);
+        const uint32_t ueL = __shfl_sync(kFull, uexcl, L);
+        uint32_t blk = 0, o_ = 0, srel = 0, cnt = 0;
+        if (u < U)
+          csr_resolve_unit(g, base_mod, grp * 32u + L, u - ueL, cL, dL, tlL, boL, (uint32_t)(oL - e0) + lead, blk, o_, srel, cnt);
+        if (!waited) { mbar_wait(bar, phase); phase ^= 1u; waited = true; }
+        __syncwarp();
+        csr_write_units(g, stage, min(32u, U - ub), blk, o_, srel, cnt, e0 - lead, bad);
+      }
+      if (!waited) { mbar_wait(bar, phase); phase ^= 1u; }   // (U == 0 cannot happen for light lanes; keeps the phase in step)
+      __syncwarp();
+      pos = (uint32_t)lb;
+    }
+  }
+  if (bad != ~0ull) set_error(op, 2, kErrDstRange, bad);
+}
+
+// Error path of the fused CSR append: a destination failed the range check after
+// deg/tail/front were published.  Restores every source's degree and tail (the old
+// tail is re-found by walking the chain) and the global counters, so the rejected
+// batch leaves the graph unchanged (graph.hpp:168-171).
+__global__ void __launch_bounds__(256)
+csr_rollback_kernel(GraphView g, const unsigned long long* __restrict__ off, uint32_t V, OpState* op) {
+  if (!op->committed) return;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    const uint32_t c = (uint32_t)(off[v + 1] - off[v]);
+    if (c == 0) continue;
+    const uint32_t d = g.deg[v] - c;
+    const uint32_t nb_old = (d + 31u) >> 5;
+    const uint32_t fill = min(c, nb_old * 32u - d);
+    g.deg[v] = d;
+    if (c > fill) {   // fresh blocks were linked: the tail moved
+      uint32_t t = kNull;
+      if (nb_old > 0) {
+        t = g.head[v];
+        for (uint32_t k = 1; k < nb_old; ++k) t = g.next[t];
+        g.next[t] = kNull;
+      } else {
+        g.head[v] = kNull;
+      }
+      g.tail[v] = t;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g.st->front -= op->total_need;
+    g.st->active_edges -= op->n_edges;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // chain enumeration: touched sources -> flat list of their blocks (+ the CTA
 // work items of the long-chain match path)
 // ---------------------------------------------------------------------------
