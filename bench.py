@@ -45,7 +45,7 @@ if str(ROOT) not in sys.path:
 
 METRIC = "batch edge insert+delete throughput (batch=1M, R-MAT s22)"
 UNIT = "Medges/s"
-STATUS_BYTES = 208  # sizeof(DeviceState) + sizeof(OpState): the per-op D2H status read (csrc/dg_api.cu op_end)
+STATUS_BYTES = 224  # sizeof(DeviceState) + sizeof(OpState): the per-op D2H status read (csrc/dg_api.cu op_end)
 
 
 def parse_args():

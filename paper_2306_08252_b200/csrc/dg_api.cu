@@ -256,6 +256,7 @@ int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
   OpState& op = h->h_blk->op;
   std::memset(&op, 0, sizeof(op));
   op.err_index = ~0ull;
+  op.bad_index = ~0ull;
   op.n_runs = n_runs;
   op.aux1 = 0;
   op.n_input = n_input;  // device-resident copy of the input length for scans
@@ -1026,8 +1027,10 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
     const uint64_t items_cap = 3 * (n_edges / kCsrHeavy) + 16;
     uint32_t* blk_off = ws_alloc<uint32_t>(h, V + 1);
     CsrItem* items = ws_alloc<CsrItem>(h, items_cap);
-    launch_alloc(h, "alloc_kernel<csr plan>", V, d_n_runs(h), CsrPlanIn{g, d_off, (uint32_t)V, n_edges, h->d_op()},
-                 CsrPlanOut{blk_off, items, items_cap}, CsrPlanFin{g, h->d_op(), n_edges});
+    unsigned long long* plan_scratch = ws_alloc<unsigned long long>(h, kAllocScratchWords);
+    cudaMemsetAsync(plan_scratch, 0, kAllocScratchWords * sizeof(unsigned long long), h->stream);
+    DG_LAUNCH(h, "csr_plan_kernel", csr_plan_kernel<<<(unsigned)((V + kCsrPlanTile - 1) / kCsrPlanTile), 256, 0, h->stream>>>(
+        g, d_off, (uint32_t)V, n_edges, blk_off, items, items_cap, plan_scratch, h->d_op()));
     static int csr_ctas_per_sm = 0;
     if (csr_ctas_per_sm == 0) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&csr_ctas_per_sm, csr_append_kernel, kCsrWarps * 32, 0);
@@ -1036,7 +1039,7 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
     const uint64_t groups = (V + 31) / 32 + items_cap;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((groups + kCsrWarps - 1) / kCsrWarps, (uint64_t)h->sm_count * csr_ctas_per_sm));
     DG_LAUNCH(h, "csr_append_kernel", csr_append_kernel<<<grid, kCsrWarps * 32, 0, h->stream>>>(
-        g, d_off, d_dst, (uint32_t)V, blk_off, items, h->d_op()));
+        g, d_off, d_dst, (uint32_t)V, blk_off, items, n_edges, plan_scratch, h->d_op()));
     rc = op_end(h);
     if (rc != DG_OK && h->h_blk->op.committed) {
       const std::string msg = h->last_error;

@@ -87,6 +87,10 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem_src) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
@@ -516,10 +520,15 @@ struct PlanFin {
   }
 };
 
-// ring slot of queue position front_old + off, off < ring_cap (pop_range, block_pool.hpp:148-158)
+// ring slot of queue position front_old + off, off < ring_cap (pop_range, block_pool.hpp:148-158).
+// lap0: front_old < ring_cap, i.e. the queue is still in its first lap.  Positions below ring_cap
+// were written once by ring_fill_kernel (ring[p] = p) and are only overwritten by pushes at
+// positions >= ring_cap, so there the handle IS the position: no load, no dependent latency
+// (a fresh pool behaves like a bump allocator until the first wrap).
 __device__ __forceinline__ uint32_t ring_at(const GraphView& g, unsigned long long base_mod,
-                                            unsigned long long off) {
+                                            unsigned long long off, bool lap0 = false) {
   unsigned long long i = base_mod + off;
+  if (lap0 && i < g.ring_cap) return (uint32_t)i;
   if (i >= g.ring_cap) i -= g.ring_cap;
   return g.ring[i];
 }
@@ -632,6 +641,7 @@ append_entries_kernel(GraphView g, GroupIndex gi, const uint32_t* __restrict__ s
                       const uint4* __restrict__ info, OpState* op) {
   if (op->err) return;
   const unsigned long long base_mod = op->front_old % g.ring_cap;
+  const bool lap0 = op->front_old < g.ring_cap;
   const uint32_t base = blockIdx.x * (256 * kGroupItems) + threadIdx.x;
   uint32_t s[kGroupItems], d[kGroupItems], rk[kGroupItems];
   uint4 in[kGroupItems];
@@ -658,8 +668,8 @@ append_entries_kernel(GraphView g, GroupIndex gi, const uint32_t* __restrict__ s
     prev[q] = kNull;
     if (base + q * 256 < n && fresh[q]) {
       const unsigned long long o = (unsigned long long)in[q].z + (kb - nb_old);
-      blk[q] = ring_at(g, base_mod, o);
-      if (slot[q] == 0) prev[q] = (kb == nb_old) ? (nb_old > 0 ? in[q].y : kNull) : ring_at(g, base_mod, o - 1);
+      blk[q] = ring_at(g, base_mod, o, lap0);
+      if (slot[q] == 0) prev[q] = (kb == nb_old) ? (nb_old > 0 ? in[q].y : kNull) : ring_at(g, base_mod, o - 1, lap0);
     }
   }
 #pragma unroll
@@ -730,71 +740,92 @@ constexpr uint32_t kCsrStage = 1024;   // entries staged per round (4 KB per war
 constexpr uint32_t kCsrHeavy = 128;    // sources with more entries become items of up to 32 units (balance: hubs spread over the grid)
 constexpr int kCsrWarps = 8;
 
-struct CsrItem {       // 16 bytes: one 32-unit chunk of a heavy source
-  uint32_t v, chunk, d, tail;   // d / tail: the source's state BEFORE the batch
+struct __align__(16) CsrItem {   // 32 bytes: one 32-unit chunk of a heavy source, self-contained (one load)
+  uint32_t v, chunk, d, tail;    // d / tail: the source's state BEFORE the batch
+  unsigned long long o0;         // first batch entry of the source
+  uint32_t c, bo;                // its batch entries / first queue position
 };
 
-struct CsrPlanAux {
-  uint32_t c, d, tail;
-};
-struct CsrPlanIn {
-  using Aux = CsrPlanAux;
-  GraphView g;
-  const unsigned long long* off;
-  uint32_t V;
-  unsigned long long n_edges;
-  OpState* op;
-  __device__ Sum2 operator()(unsigned long long v64, Aux& x) const {
-    const uint32_t v = (uint32_t)v64;
-    const unsigned long long o0 = off[v], o1 = off[v + 1];
-    bool ok = true;
-    if (v == 0 && o0 != 0) { set_error(op, 2, kErrOffsetsStart, 0); ok = false; }
-    if (v + 1 == V && o1 != n_edges) { set_error(op, 2, kErrOffsetsEnd, V); ok = false; }
-    if (o1 < o0) { set_error(op, 2, kErrOffsetsMonotone, v + 1); ok = false; }
-    if (o1 > n_edges) ok = false;   // (non-monotone or bad end: reported where it happens)
-    const uint32_t c = ok ? (uint32_t)(o1 - o0) : 0u;
-    if (c > 0 && !bit_test(g.alive, v)) set_error(op, 2, kErrDeadSource, v);
-    x.c = c;
-    x.d = c ? g.deg[v] : 0u;
-    x.tail = (c > kCsrHeavy) ? g.tail[v] : kNull;
-    const unsigned long long w = c ? plan_word(g, x.d, c) : 0ull;
-    const uint32_t units = (uint32_t)(w >> 32);
-    const uint32_t items = (c > kCsrHeavy) ? (units + 31u) / 32u : 0u;
-    return Sum2{items, w & 0xFFFFFFFFull};
+// Plan pass: one thread handles kCsrPlanItems vertices, strided by the CTA size so every load is
+// coalesced.  Fresh blocks and heavy items are two 32-bit counts packed in ONE 64-bit word
+// ([63:32] items, [31:0] blocks): one CTA scan, one atomicAdd per tile on the packed cursor
+// (ranges only need to be disjoint, not ordered).  There is no finishing step here: the append
+// pass reads the packed totals itself, so no tile ever waits on a fence.
+// scratch: [0] packed cursor, [1] finished CTAs of the append pass; zeroed before the launch.
+constexpr int kCsrPlanItems = 8;
+constexpr int kCsrPlanTile = 256 * kCsrPlanItems;
+__global__ void __launch_bounds__(256)
+csr_plan_kernel(GraphView g, const unsigned long long* __restrict__ off, uint32_t V, unsigned long long n_edges,
+                uint32_t* __restrict__ blk_off, CsrItem* __restrict__ items, unsigned long long items_cap,
+                unsigned long long* scratch, OpState* op) {
+  __shared__ unsigned long long s_warp[8];
+  __shared__ unsigned long long s_base;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t v0 = blockIdx.x * kCsrPlanTile + threadIdx.x;
+  unsigned long long o0[kCsrPlanItems], o1[kCsrPlanItems];
+  uint32_t dg[kCsrPlanItems], aw[kCsrPlanItems];
+#pragma unroll
+  for (int j = 0; j < kCsrPlanItems; ++j) {   // every load independent of the others
+    const uint32_t v = v0 + j * 256;
+    const bool in = v < V;
+    o0[j] = in ? off[v] : 0ull;
+    o1[j] = in ? off[v + 1] : 0ull;
+    dg[j] = in ? g.deg[v] : 0u;
+    aw[j] = in ? g.alive[v >> 5] : 0xFFFFFFFFu;
   }
-};
-struct CsrPlanOut {
-  uint32_t* blk_off;
-  CsrItem* items;
-  unsigned long long items_cap;
-  __device__ void operator()(unsigned long long v, unsigned long long excl_a, unsigned long long excl_b,
-                             Sum2 val, const CsrPlanAux& x) const {
-    blk_off[v] = (uint32_t)excl_b;
-    const uint32_t n_it = (uint32_t)val.a;
-    if (n_it == 0 || excl_a + n_it > items_cap) return;   // (overflow only with broken offsets: already an error)
-    for (uint32_t k = 0; k < n_it; ++k) items[excl_a + k] = CsrItem{(uint32_t)v, k, x.d, x.tail};
-  }
-};
-struct CsrPlanFin {
-  GraphView g;
-  OpState* op;
-  unsigned long long n_edges;
-  __device__ void operator()(unsigned long long total_a, unsigned long long total_b) const {
-    if (op->err) return;
-    op->n_items = total_a;
-    op->total_need = total_b;
-    op->n_edges = n_edges;
-    DeviceState* st = g.st;
-    if (total_b > st->rear - st->front) {   // ensure_available (block_pool.hpp:177-189)
-      op->err = 3;
-      op->err_detail = kErrPoolUnderflow;
-      op->err_index = total_b - (st->rear - st->front);
-      return;
+  unsigned long long w[kCsrPlanItems], sum = 0;
+  uint32_t cc[kCsrPlanItems];
+#pragma unroll
+  for (int j = 0; j < kCsrPlanItems; ++j) {
+    const uint32_t v = v0 + j * 256;
+    bool ok = v < V;
+    if (ok) {   // csr.hpp:49-66, graph.hpp:322-327
+      if (v == 0 && o0[j] != 0) { set_error(op, 2, kErrOffsetsStart, 0); ok = false; }
+      if (v + 1 == V && o1[j] != n_edges) { set_error(op, 2, kErrOffsetsEnd, V); ok = false; }
+      if (o1[j] < o0[j]) { set_error(op, 2, kErrOffsetsMonotone, v + 1); ok = false; }
+      if (o1[j] > n_edges) ok = false;   // (non-monotone or bad end: reported where it happens)
     }
-    op->front_old = st->front;
-    op->plan_ok = 1;
+    const uint32_t c = ok ? (uint32_t)(o1[j] - o0[j]) : 0u;
+    if (c > 0 && !((aw[j] >> (v & 31)) & 1u)) set_error(op, 2, kErrDeadSource, v);
+    cc[j] = c;
+    const unsigned long long pw = c ? plan_word(g, dg[j], c) : 0ull;   // [63:32] units, [31:0] fresh blocks
+    const uint32_t n_it = (c > kCsrHeavy) ? ((uint32_t)(pw >> 32) + 31u) / 32u : 0u;
+    w[j] = ((unsigned long long)n_it << 32) | (pw & 0xFFFFFFFFull);
+    sum += w[j];
   }
-};
+  unsigned long long incl = sum;
+#pragma unroll
+  for (int dl = 1; dl < 32; dl <<= 1) {
+    const unsigned long long t = __shfl_up_sync(kFull, incl, dl);
+    if (lane >= dl) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  unsigned long long warp_excl = 0, tile_sum = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const unsigned long long sw = s_warp[k];
+    if (k < warp) warp_excl += sw;
+    tile_sum += sw;
+  }
+  if (threadIdx.x == 0) s_base = tile_sum ? atomicAdd(&scratch[0], tile_sum) : 0ull;
+  __syncthreads();
+  unsigned long long run = s_base + warp_excl + (incl - sum);
+#pragma unroll
+  for (int j = 0; j < kCsrPlanItems; ++j) {
+    const uint32_t v = v0 + j * 256;
+    if (v < V) {
+      blk_off[v] = (uint32_t)run;
+      const uint32_t n_it = (uint32_t)(w[j] >> 32);
+      const unsigned long long ib = run >> 32;
+      if (n_it != 0 && ib + n_it <= items_cap) {   // (overflow only with broken offsets: already an error)
+        const uint32_t tl = g.tail[v];
+        for (uint32_t k = 0; k < n_it; ++k) items[ib + k] = CsrItem{v, k, dg[j], tl, o0[j], cc[j], (uint32_t)run};
+      }
+    }
+    run += w[j];
+  }
+}
 
 // ---- mbarrier + TMA bulk copy (global -> shared) ---------------------------------
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -843,7 +874,7 @@ __device__ __forceinline__ uint32_t csr_stage_issue(uint32_t* stage, unsigned lo
   // the rest: [max(a0, Z), a1) — at most 3 entries
   const uintptr_t t0 = a0 > Z ? a0 : Z;
   const uint32_t nt = (uint32_t)((a1 - t0) >> 2);
-  if ((uint32_t)lane < nt) stage[((t0 - A) >> 2) + lane] = *reinterpret_cast<const uint32_t*>(t0 + 4u * lane);
+  if ((uint32_t)lane < nt) cp_async4(&stage[((t0 - A) >> 2) + lane], reinterpret_cast<const void*>(t0 + 4u * lane));
   return lead;
 }
 
@@ -874,14 +905,12 @@ __device__ __forceinline__ void csr_write_units(const GraphView& g, const uint32
       uint4 v;
       v.x = src[0]; v.y = src[1]; v.z = src[2]; v.w = src[3];
       const uint32_t nv = cq - min(cq, s0);   // valid words of this chunk (>= 4: all)
-      if (nv < 4) {
-        if (nv < 1) v.x = kTomb;
-        if (nv < 2) v.y = kTomb;
-        if (nv < 3) v.z = kTomb;
-        v.w = kTomb;
-      }
-      // padding is kTomb >= limit: only real entries can be reported, and they are checked by value
+      // branch-free: out-of-range test on the real entries, then kTomb padding (selects)
       const bool b0 = v.x >= limit && nv > 0, b1 = v.y >= limit && nv > 1, b2 = v.z >= limit && nv > 2, b3 = v.w >= limit && nv > 3;
+      if (nv < 1) v.x = kTomb;
+      if (nv < 2) v.y = kTomb;
+      if (nv < 3) v.z = kTomb;
+      if (nv < 4) v.w = kTomb;
       if (b0 | b1 | b2 | b3) {
         const unsigned long long e = stage_entry0 + sq + s0 + (b0 ? 0u : b1 ? 1u : b2 ? 2u : 3u);
         bad = min(bad, e);
@@ -908,7 +937,7 @@ __device__ __forceinline__ void csr_write_units(const GraphView& g, const uint32
 // Unit j of a source with c batch entries, degree d and tail block tl before the batch, first
 // queue position bo: resolves its block, links it, and returns where its entries sit.
 // src_rel0: index in the staging buffer of the source's first batch entry.
-__device__ __forceinline__ void csr_resolve_unit(const GraphView& g, unsigned long long base_mod, uint32_t v, uint32_t j,
+__device__ __forceinline__ void csr_resolve_unit(const GraphView& g, unsigned long long base_mod, bool lap0, uint32_t v, uint32_t j,
                                                  uint32_t c, uint32_t d, uint32_t tl, uint32_t bo, uint32_t src_rel0,
                                                  uint32_t& blk, uint32_t& off0, uint32_t& srel, uint32_t& cnt) {
   const uint32_t nb_old = (d + 31u) >> 5;
@@ -924,20 +953,62 @@ __device__ __forceinline__ void csr_resolve_unit(const GraphView& g, unsigned lo
   } else {
     const uint32_t f = j - has_fill;
     const unsigned long long o = (unsigned long long)bo + f;
-    blk = ring_at(g, base_mod, o);
+    blk = ring_at(g, base_mod, o, lap0);
     off0 = 0;
     srel = src_rel0 + fill + f * 32u;
     cnt = min(32u, c - fill - f * 32u);
-    const uint32_t prev = (f == 0) ? (nb_old > 0 ? tl : kNull) : ring_at(g, base_mod, o - 1);
+    const uint32_t prev = (f == 0) ? (nb_old > 0 ? tl : kNull) : ring_at(g, base_mod, o - 1, lap0);
     if (prev == kNull) g.head[v] = blk; else g.next[prev] = blk;
     if (f == need - 1) g.next[blk] = kNull;
   }
 }
 
-__global__ void __launch_bounds__(kCsrWarps * 32)
+// Work unit w of the append pass: w < n_items is heavy item w, otherwise vertex group w - n_items.
+// Its metadata is two 16-byte registers, loaded one unit ahead of its use:
+//   item : a = {v, chunk, d, tail}           b = {o0.lo, o0.hi, c, bo}
+//   group: a = {o0.lo, o0.hi, o1.lo, o1.hi}  b = {d, tail, bo, -} of the lane's vertex
+struct CsrWork {
+  uint4 a, b;
+};
+__device__ __forceinline__ CsrWork csr_load_work(const GraphView& g, const unsigned long long* __restrict__ off,
+                                                 const uint32_t* __restrict__ blk_off, const CsrItem* __restrict__ items,
+                                                 uint32_t V, uint32_t n_items, uint32_t w, uint32_t total) {
+  CsrWork r{make_uint4(0, 0, 0, 0), make_uint4(0, kNull, 0, 0)};
+  if (w >= total) return r;
+  if (w < n_items) {
+    const uint4* p = reinterpret_cast<const uint4*>(items + w);
+    r.a = p[0];
+    r.b = p[1];
+  } else {
+    const uint32_t v = (w - n_items) * 32u + lane_id();
+    if (v < V) {   // five independent loads
+      const unsigned long long o0 = off[v], o1 = off[v + 1];
+      r.a = make_uint4((uint32_t)o0, (uint32_t)(o0 >> 32), (uint32_t)o1, (uint32_t)(o1 >> 32));
+      r.b = make_uint4(g.deg[v], g.tail[v], blk_off[v], 0u);
+    }
+  }
+  return r;
+}
+
+__global__ void __launch_bounds__(kCsrWarps * 32, 4)
 csr_append_kernel(GraphView g, const unsigned long long* __restrict__ off, const uint32_t* __restrict__ dsts, uint32_t V,
-                  const uint32_t* __restrict__ blk_off, const CsrItem* __restrict__ items, OpState* op) {
-  if (!op->plan_ok) return;
+                  const uint32_t* __restrict__ blk_off, const CsrItem* __restrict__ items, unsigned long long n_edges,
+                  unsigned long long* scratch, OpState* op) {
+  // op->err can only hold a PLAN error here: this pass reports bad destinations through
+  // op->bad_index and turns them into an error once every CTA has finished.
+  if (op->err) return;
+  const unsigned long long plan_tot = scratch[0];            // [63:32] heavy items, [31:0] fresh blocks
+  const unsigned long long need = plan_tot & 0xFFFFFFFFull;
+  const unsigned long long front_old = g.st->front;           // (published by the last CTA only)
+  if (need > g.st->rear - front_old) {                        // ensure_available (block_pool.hpp:177-189)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      op->err_detail = kErrPoolUnderflow;
+      op->err_index = need - (g.st->rear - front_old);
+      __threadfence();
+      op->err = 3;
+    }
+    return;
+  }
   __shared__ __align__(16) uint32_t s_stage[kCsrWarps][kCsrStage + 40];   // + alignment lead (<= 3) + the padded read of the last unit
   __shared__ unsigned long long s_bar[kCsrWarps];
   __shared__ uint8_t s_owner[kCsrWarps][256];   // <= 32 x (ceil(kCsrHeavy / 32) + 1) units per round
@@ -951,131 +1022,163 @@ csr_append_kernel(GraphView g, const unsigned long long* __restrict__ off, const
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    op->committed = 1;
-    g.st->front += op->total_need;         // commit_front (block_pool.hpp:162-166)
-    g.st->active_edges += op->n_edges;     // graph.hpp:186
-  }
   unsigned phase = 0;
   unsigned long long bad = ~0ull;   // smallest out-of-range destination index this lane saw
-  const unsigned long long base_mod = op->front_old % g.ring_cap;
+  const unsigned long long base_mod = front_old % g.ring_cap;
+  const bool lap0 = front_old < g.ring_cap;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t n_items = (uint32_t)(plan_tot >> 32);
+  const uint32_t total = n_items + (V + 31u) / 32u;
 
-  // ---- heavy sources first: item = 32 consecutive units of one source
-  const uint32_t n_items = (uint32_t)op->n_items;
-  for (uint32_t it = gw; it < n_items; it += nwarps) {
-    const CsrItem item = items[it];
-    const unsigned long long o0 = off[item.v];
-    const uint32_t c = (uint32_t)(off[item.v + 1] - o0);
-    const uint32_t bo = blk_off[item.v];
-    const uint32_t nb_old = (item.d + 31u) >> 5;
-    const uint32_t fill = min(c, nb_old * 32u - item.d);
-    const uint32_t has_fill = fill > 0 ? 1u : 0u;
-    const uint32_t nu = ((c - fill + 31u) >> 5) + has_fill;
-    const uint32_t j0 = item.chunk * 32u;
-    const uint32_t nunits = min(32u, nu - j0);
-    // entries of units [j0, j0 + nunits)
-    const uint32_t f0 = j0 == 0 ? 0u : fill + (j0 - has_fill) * 32u;
-    const uint32_t j1 = j0 + nunits;
-    const uint32_t f1 = min(c, fill + (j1 - has_fill) * 32u);
-    bool armed;
-    const uint32_t lead = csr_stage_issue(stage, bar, dsts, o0 + f0, o0 + f1, armed);
-    uint32_t blk = 0, o_ = 0, srel = 0, cnt = 0;
-    if ((uint32_t)lane < nunits)
-      csr_resolve_unit(g, base_mod, item.v, j0 + lane, c, item.d, item.tail, bo, lead - f0, blk, o_, srel, cnt);
-    if (armed) { mbar_wait(bar, phase); phase ^= 1u; }
-    __syncwarp();
-    csr_write_units(g, stage, nunits, blk, o_, srel, cnt, o0 + f0 - lead, bad);
-    __syncwarp();
-  }
-
-  // ---- groups of 32 consecutive vertices
-  const uint32_t ngroups = (V + 31u) / 32u;
-  for (uint32_t grp = gw; grp < ngroups; grp += nwarps) {
-    const uint32_t v = grp * 32u + lane;
-    const bool valid = v < V;
-    const unsigned long long o0 = valid ? off[v] : 0ull;
-    const unsigned long long o1 = valid ? off[v + 1] : o0;
-    const uint32_t c = (uint32_t)(o1 - o0);
-    uint32_t d = 0, tl = kNull, bo = 0;
-    if (c > 0) {
-      d = g.deg[v];
-      tl = g.tail[v];
-      bo = blk_off[v];
-    }
-    const uint32_t nb_old = (d + 31u) >> 5;
-    const uint32_t fill = min(c, nb_old * 32u - d);
-    const uint32_t has_fill = fill > 0 ? 1u : 0u;
-    const uint32_t need = (c - fill + 31u) >> 5;
-    const bool heavy = c > kCsrHeavy;
-    const bool light = c > 0 && !heavy;
-    // publish the source's new state (insert_adjacency, graph.hpp:367-371)
-    if (c > 0) {
-      g.deg[v] = d + c;
-      if (need > 0) g.tail[v] = ring_at(g, base_mod, (unsigned long long)bo + need - 1);
-    }
-    const unsigned lightmask = __ballot_sync(kFull, light);
-    if (lightmask == 0) continue;
-    const unsigned heavymask = __ballot_sync(kFull, heavy);
-    const uint32_t cl = light ? c : 0u;
-    uint32_t cincl = cl;
-#pragma unroll
-    for (int dl = 1; dl < 32; dl <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, cincl, dl);
-      if (lane >= dl) cincl += t;
-    }
-    const uint32_t nu = light ? need + has_fill : 0u;
-    uint32_t pos = 0;
-    while (pos < 32) {
-      const unsigned rem = lightmask & (0xFFFFFFFFu << pos);
-      if (rem == 0) break;
-      const int a = __ffs(rem) - 1;
-      const uint32_t cbase = __shfl_sync(kFull, cincl - cl, a);
-      const unsigned hv_after = heavymask & (0xFFFFFFFFu << a);
-      const int hb = hv_after ? __ffs(hv_after) - 1 : 32;
-      const bool okl = valid && lane >= a && lane < hb && (cincl - cbase) <= kCsrStage;
-      const unsigned okmask = __ballot_sync(kFull, okl);
-      const int lb = a + __popc(okmask);   // the eligible lanes are a contiguous run starting at a
-      const unsigned long long e0 = __shfl_sync(kFull, o0, a);
-      const unsigned long long e1 = __shfl_sync(kFull, o1, lb - 1);
+  // Work units (heavy items first, then vertex groups) differ 30x in size, so warps take them in
+  // chunks of kCsrChunk consecutive units from a device cursor (one same-address atomic per chunk:
+  // ~0.5 G/s of those is all the L2 gives).  The next chunk's ticket is requested when a chunk
+  // starts and the next unit's metadata is loaded one unit ahead: neither is ever waited for.
+  constexpr uint32_t kCsrChunk = 4;
+  uint32_t w_cur = gw * kCsrChunk, w_nxt = w_cur + 1;
+  uint32_t ticket = 0;
+  CsrWork nxt = csr_load_work(g, off, blk_off, items, V, n_items, w_cur, total);
+  while (w_cur < total) {
+    if ((w_cur % kCsrChunk) == 0 && lane == 0) ticket = nwarps + atomicAdd(&op->med_cursor, 1u);
+    if ((w_nxt % kCsrChunk) == 0) w_nxt = __shfl_sync(kFull, ticket, 0) * kCsrChunk;
+    const CsrWork cur = nxt;
+    nxt = csr_load_work(g, off, blk_off, items, V, n_items, w_nxt, total);
+    if (w_cur < n_items) {
+      // ---- heavy item: 32 consecutive units of one source
+      const uint32_t v = cur.a.x, chunk = cur.a.y, d = cur.a.z, tl = cur.a.w;
+      const unsigned long long o0 = ((unsigned long long)cur.b.y << 32) | cur.b.x;
+      const uint32_t c = cur.b.z, bo = cur.b.w;
+      const uint32_t nb_old = (d + 31u) >> 5;
+      const uint32_t fill = min(c, nb_old * 32u - d);
+      const uint32_t has_fill = fill > 0 ? 1u : 0u;
+      const uint32_t nu = ((c - fill + 31u) >> 5) + has_fill;
+      const uint32_t j0 = chunk * 32u;
+      const uint32_t nunits = min(32u, nu - j0);
+      // entries of units [j0, j0 + nunits)
+      const uint32_t f0 = j0 == 0 ? 0u : fill + (j0 - has_fill) * 32u;
+      const uint32_t j1 = j0 + nunits;
+      const uint32_t f1 = min(c, fill + (j1 - has_fill) * 32u);
       bool armed;
-      const uint32_t lead = csr_stage_issue(stage, bar, dsts, e0, e1, armed);
-      const bool in_round = lane >= a && lane < lb;
-      const uint32_t nur = in_round ? nu : 0u;
-      uint32_t uincl = nur;
+      const uint32_t lead = csr_stage_issue(stage, bar, dsts, o0 + f0, o0 + f1, armed);
+      uint32_t blk = 0, o_ = 0, srel = 0, cnt = 0;
+      if ((uint32_t)lane < nunits)
+        csr_resolve_unit(g, base_mod, lap0, v, j0 + lane, c, d, tl, bo, lead - f0, blk, o_, srel, cnt);
+      cp_async_wait_all();
+      if (armed) { mbar_wait(bar, phase); phase ^= 1u; }
+      __syncwarp();
+      csr_write_units(g, stage, nunits, blk, o_, srel, cnt, o0 + f0 - lead, bad);
+      __syncwarp();
+    } else {
+      // ---- group of 32 consecutive vertices, one per lane
+      const uint32_t grp = w_cur - n_items;
+      const uint32_t v = grp * 32u + lane;
+      const bool valid = v < V;
+      const unsigned long long o0 = ((unsigned long long)cur.a.y << 32) | cur.a.x;
+      const unsigned long long o1 = ((unsigned long long)cur.a.w << 32) | cur.a.z;
+      const uint32_t c = (uint32_t)(o1 - o0);
+      const uint32_t d = c ? cur.b.x : 0u, tl = cur.b.y, bo = cur.b.z;
+      const uint32_t nb_old = (d + 31u) >> 5;
+      const uint32_t fill = min(c, nb_old * 32u - d);
+      const uint32_t has_fill = fill > 0 ? 1u : 0u;
+      const uint32_t need = (c - fill + 31u) >> 5;
+      const bool heavy = c > kCsrHeavy;
+      const bool light = c > 0 && !heavy;
+      // the source's new state (insert_adjacency, graph.hpp:367-371): the tail handle is requested
+      // now and published at the end of the group, off the critical path
+      if (c > 0) g.deg[v] = d + c;
+      uint32_t tail_new = kNull;
+      if (need > 0) tail_new = ring_at(g, base_mod, (unsigned long long)bo + need - 1, lap0);
+      const unsigned lightmask = __ballot_sync(kFull, light);
+      if (lightmask != 0) {
+        const unsigned heavymask = __ballot_sync(kFull, heavy);
+        const uint32_t cl = light ? c : 0u;
+        uint32_t cincl = cl;
 #pragma unroll
-      for (int dl = 1; dl < 32; dl <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, uincl, dl);
-        if (lane >= dl) uincl += t;
+        for (int dl = 1; dl < 32; dl <<= 1) {
+          const uint32_t t = __shfl_up_sync(kFull, cincl, dl);
+          if (lane >= dl) cincl += t;
+        }
+        const uint32_t nu = light ? need + has_fill : 0u;
+        uint32_t pos = 0;
+        while (pos < 32) {
+          const unsigned rem = lightmask & (0xFFFFFFFFu << pos);
+          if (rem == 0) break;
+          const int a = __ffs(rem) - 1;
+          const uint32_t cbase = __shfl_sync(kFull, cincl - cl, a);
+          const unsigned hv_after = heavymask & (0xFFFFFFFFu << a);
+          const int hb = hv_after ? __ffs(hv_after) - 1 : 32;
+          const bool okl = valid && lane >= a && lane < hb && (cincl - cbase) <= kCsrStage;
+          const unsigned okmask = __ballot_sync(kFull, okl);
+          const int lb = a + __popc(okmask);   // the eligible lanes are a contiguous run starting at a
+          const unsigned long long e0 = __shfl_sync(kFull, o0, a);
+          const unsigned long long e1 = __shfl_sync(kFull, o1, lb - 1);
+          bool armed;
+          const uint32_t lead = csr_stage_issue(stage, bar, dsts, e0, e1, armed);
+          const bool in_round = lane >= a && lane < lb;
+          const uint32_t nur = in_round ? nu : 0u;
+          uint32_t uincl = nur;
+#pragma unroll
+          for (int dl = 1; dl < 32; dl <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, uincl, dl);
+            if (lane >= dl) uincl += t;
+          }
+          const uint32_t uexcl = uincl - nur;
+          const uint32_t U = __shfl_sync(kFull, uincl, 31);
+          for (uint32_t j = 0; j < nur; ++j) owner[uexcl + j] = (uint8_t)lane;
+          __syncwarp();
+          bool waited = false;
+          for (uint32_t ub = 0; ub < U; ub += 32) {
+            const uint32_t u = ub + lane;
+            const int L = (u < U) ? owner[u] : 0;
+            const unsigned long long oL = __shfl_sync(kFull, o0, L);
+            const uint32_t cL = __shfl_sync(kFull, c, L);
+            const uint32_t dL = __shfl_sync(kFull, d, L);
+            const uint32_t tlL = __shfl_sync(kFull, tl, L);
+            const uint32_t boL = __shfl_sync(kFull, bo, L);
+            const uint32_t ueL = __shfl_sync(kFull, uexcl, L);
+            uint32_t blk = 0, o_ = 0, srel = 0, cnt = 0;
+            if (u < U)
+              csr_resolve_unit(g, base_mod, lap0, grp * 32u + L, u - ueL, cL, dL, tlL, boL, (uint32_t)(oL - e0) + lead, blk, o_, srel, cnt);
+            if (!waited) {
+              cp_async_wait_all();
+              if (armed) { mbar_wait(bar, phase); phase ^= 1u; }
+              waited = true;
+            }
+            __syncwarp();
+            csr_write_units(g, stage, min(32u, U - ub), blk, o_, srel, cnt, e0 - lead, bad);
+          }
+          __syncwarp();
+          pos = (uint32_t)lb;
+        }
       }
-      const uint32_t uexcl = uincl - nur;
-      const uint32_t U = __shfl_sync(kFull, uincl, 31);
-      for (uint32_t j = 0; j < nur; ++j) owner[uexcl + j] = (uint8_t)lane;
-      __syncwarp();
-      bool waited = !armed;
-      for (uint32_t ub = 0; ub < U; ub += 32) {
-        const uint32_t u = ub + lane;
-        const int L = (u < U) ? owner[u] : 0;
-        const unsigned long long oL = __shfl_sync(kFull, o0, L);
-        const uint32_t cL = __shfl_sync(kFull, c, L);
-        const uint32_t dL = __shfl_sync(kFull, d, L);
-        const uint32_t tlL = __shfl_sync(kFull, tl, L);
-        const uint32_t boL = __shfl_sync(kFull, bo, L);
-        const uint32_t ueL = __shfl_sync(kFull, uexcl, L);
-        uint32_t blk = 0, o_ = 0, srel = 0, cnt = 0;
-        if (u < U)
-          csr_resolve_unit(g, base_mod, grp * 32u + L, u - ueL, cL, dL, tlL, boL, (uint32_t)(oL - e0) + lead, blk, o_, srel, cnt);
-        if (!waited) { mbar_wait(bar, phase); phase ^= 1u; waited = true; }
-        __syncwarp();
-        csr_write_units(g, stage, min(32u, U - ub), blk, o_, srel, cnt, e0 - lead, bad);
+      if (need > 0) g.tail[v] = tail_new;
+    }
+    w_cur = w_nxt;
+    w_nxt = w_cur + 1;
+  }
+  if (bad != ~0ull) atomicMin(&op->bad_index, bad);
+  // the last CTA to finish publishes the queue front / live-edge count and the verdict
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&scratch[1], 1ull) == gridDim.x - 1) {
+      __threadfence();
+      op->total_need = need;
+      op->n_items = n_items;
+      op->n_edges = n_edges;
+      op->front_old = front_old;
+      g.st->front = front_old + need;      // commit_front (block_pool.hpp:162-166)
+      g.st->active_edges += n_edges;       // graph.hpp:186
+      op->committed = 1;
+      const unsigned long long b = ld_volatile_u64(&op->bad_index);
+      if (b != ~0ull) {
+        op->err_detail = kErrDstRange;
+        op->err_index = b;
+        op->err = 2;
       }
-      if (!waited) { mbar_wait(bar, phase); phase ^= 1u; }   // (U == 0 cannot happen for light lanes; keeps the phase in step)
-      __syncwarp();
-      pos = (uint32_t)lb;
     }
   }
-  if (bad != ~0ull) set_error(op, 2, kErrDstRange, bad);
 }
 
 // Error path of the fused CSR append: a destination failed the range check after
@@ -1084,7 +1187,7 @@ csr_append_kernel(GraphView g, const unsigned long long* __restrict__ off, const
 // batch leaves the graph unchanged (graph.hpp:168-171).
 __global__ void __launch_bounds__(256)
 csr_rollback_kernel(GraphView g, const unsigned long long* __restrict__ off, uint32_t V, OpState* op) {
-  if (!op->committed) return;
+  if (!op->committed) return;   // (the append pass never ran: nothing was published)
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
     const uint32_t c = (uint32_t)(off[v + 1] - off[v]);
     if (c == 0) continue;
