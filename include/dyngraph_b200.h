@@ -340,6 +340,27 @@ int dg_exchange_push_answers(dg_exchange* x, const uint8_t* answers, uint64_t n)
  * query batch), copied to `out` (host or device per `mem`) */
 int dg_exchange_answers(dg_exchange* x, uint8_t* out, uint64_t n, int mem);
 
+/* ---- host -> device batch ingest (nothing in the reference) ----------
+ *
+ * The reference harness hands insert_batch / delete_batch one host batch after the other
+ * (io/workload.hpp:141-155).  On the GPU the PCIe copy of a 1M-entry batch (8 MB) costs as much as
+ * the op, so an ingest queue keeps `depth` device slots and copies batch k+1 on its own stream
+ * while batch k executes:
+ *     dg_ingest_stage_coo(q, batch[0]) ;
+ *     for k: dg_ingest_stage_coo(q, batch[k+1]) ; dg_ingest_insert(q, slot[k]) ;
+ * `src`/`dst` are HOST arrays (pinned memory makes the copy asynchronous) that must stay valid
+ * until the slot's op returns.  The ops are dg_insert_batch_coo / dg_delete_batch_coo on the
+ * staged device copy: same validation, same status codes, graph unchanged on failure.
+ */
+typedef struct dg_ingest dg_ingest;
+int dg_ingest_create(dg_graph* h, uint64_t max_entries, uint32_t depth, dg_ingest** out);
+void dg_ingest_destroy(dg_ingest* q);
+/* enqueue the copy of a host COO batch into the next free slot; *slot receives its index */
+int dg_ingest_stage_coo(dg_ingest* q, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t* slot);
+/* run the op on a staged slot (waits for its copy on the graph's stream); frees the slot */
+int dg_ingest_insert(dg_ingest* q, uint32_t slot);
+int dg_ingest_delete(dg_ingest* q, uint32_t slot);
+
 #ifdef __cplusplus
 }
 #endif

@@ -104,6 +104,11 @@ SIGNATURES = {
                                        C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "dg_exchange_push_answers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "dg_exchange_answers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int]),
+    "dg_ingest_create": (C.c_int, [_H, C.c_uint64, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "dg_ingest_destroy": (None, [C.c_void_p]),
+    "dg_ingest_stage_coo": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, u32p]),
+    "dg_ingest_insert": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "dg_ingest_delete": (C.c_int, [C.c_void_p, C.c_uint32]),
 }
 
 _lib = None

@@ -1764,4 +1764,98 @@ int dg_exchange_answers(dg_exchange* x, uint8_t* out, uint64_t n, int mem) {
   return DG_OK;
 }
 
+// ---- host -> device batch ingest ----------------------------------------------
+// The reference harness feeds batches one after the other (io/workload.hpp:141-155).  At ~0.1-0.3 ms
+// of device time per 1M-entry batch the 8 MB PCIe copy of a batch costs as much as the op itself,
+// so the copy of batch k+1 runs on its own stream while batch k executes: a small ring of device
+// slots, one copy-done event per slot the op stream waits on, one slot-free event the copy stream
+// waits on before a slot is overwritten.
+struct dg_ingest {
+  dg_graph* h = nullptr;
+  uint64_t capacity = 0;   // entries per slot
+  uint32_t depth = 0;
+  cudaStream_t copy = nullptr;
+  std::vector<uint32_t*> src, dst;
+  std::vector<uint64_t> n;
+  std::vector<cudaEvent_t> filled, freed;
+  std::vector<int> state;  // 0 free, 1 staged
+  uint32_t next = 0;
+};
+
+int dg_ingest_create(dg_graph* h, uint64_t max_entries, uint32_t depth, dg_ingest** out) {
+  if (!h || !out || depth == 0 || max_entries == 0) return fail(h, DG_ERR_DATA, "ingest: bad arguments");
+  *out = nullptr;
+  cudaSetDevice(h->device);
+  dg_ingest* q = new (std::nothrow) dg_ingest();
+  if (!q) return fail(h, DG_ERR_ENGINE, "ingest: out of host memory");
+  q->h = h;
+  q->capacity = max_entries;
+  q->depth = depth;
+  bool ok = cudaStreamCreateWithFlags(&q->copy, cudaStreamNonBlocking) == cudaSuccess;
+  for (uint32_t i = 0; ok && i < depth; ++i) {
+    uint32_t *s = nullptr, *d = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ok = cudaMalloc(&s, max_entries * 4) == cudaSuccess && cudaMalloc(&d, max_entries * 4) == cudaSuccess &&
+         cudaEventCreateWithFlags(&a, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&b, cudaEventDisableTiming) == cudaSuccess;
+    q->src.push_back(s); q->dst.push_back(d); q->filled.push_back(a); q->freed.push_back(b);
+    q->n.push_back(0); q->state.push_back(0);
+  }
+  if (!ok) {
+    cudaGetLastError();
+    dg_ingest_destroy(q);
+    return fail(h, DG_ERR_ENGINE, "ingest: device allocation failed");
+  }
+  *out = q;
+  return DG_OK;
+}
+
+void dg_ingest_destroy(dg_ingest* q) {
+  if (!q) return;
+  cudaSetDevice(q->h->device);
+  if (q->copy) { cudaStreamSynchronize(q->copy); cudaStreamDestroy(q->copy); }
+  for (auto p : q->src) cudaFree(p);
+  for (auto p : q->dst) cudaFree(p);
+  for (auto e : q->filled) if (e) cudaEventDestroy(e);
+  for (auto e : q->freed) if (e) cudaEventDestroy(e);
+  cudaGetLastError();
+  delete q;
+}
+
+int dg_ingest_stage_coo(dg_ingest* q, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t* slot_out) {
+  if (!q || !slot_out || (n && (!src || !dst))) return DG_ERR_DATA;
+  dg_graph* h = q->h;
+  cudaSetDevice(h->device);
+  if (n > q->capacity) return fail(h, DG_ERR_DATA, "ingest: batch larger than the slot capacity");
+  const uint32_t s = q->next;
+  if (q->state[s] != 0) return fail(h, DG_ERR_ENGINE, "ingest: every slot holds a staged batch (run one first)");
+  // the op that last read this slot must have finished before the slot is overwritten
+  DG_CUDA(h, cudaStreamWaitEvent(q->copy, q->freed[s], 0));
+  if (n) {
+    DG_CUDA(h, cudaMemcpyAsync(q->src[s], src, n * 4, cudaMemcpyHostToDevice, q->copy));
+    DG_CUDA(h, cudaMemcpyAsync(q->dst[s], dst, n * 4, cudaMemcpyHostToDevice, q->copy));
+  }
+  DG_CUDA(h, cudaEventRecord(q->filled[s], q->copy));
+  q->n[s] = n;
+  q->state[s] = 1;
+  q->next = (s + 1) % q->depth;
+  *slot_out = s;
+  return DG_OK;
+}
+
+static int ingest_run(dg_ingest* q, uint32_t slot, bool is_insert) {
+  if (!q || slot >= q->depth) return DG_ERR_DATA;
+  dg_graph* h = q->h;
+  cudaSetDevice(h->device);
+  if (q->state[slot] != 1) return fail(h, DG_ERR_DATA, "ingest: slot holds no staged batch");
+  DG_CUDA(h, cudaStreamWaitEvent(h->stream, q->filled[slot], 0));
+  const int rc = is_insert ? dg_insert_batch_coo(h, q->src[slot], q->dst[slot], q->n[slot], DG_MEM_DEVICE)
+                           : dg_delete_batch_coo(h, q->src[slot], q->dst[slot], q->n[slot], DG_MEM_DEVICE);
+  cudaEventRecord(q->freed[slot], h->stream);
+  q->state[slot] = 0;
+  return rc;
+}
+int dg_ingest_insert(dg_ingest* q, uint32_t slot) { return ingest_run(q, slot, true); }
+int dg_ingest_delete(dg_ingest* q, uint32_t slot) { return ingest_run(q, slot, false); }
+
 }  // extern "C"

@@ -752,7 +752,7 @@ struct __align__(16) CsrItem {   // 32 bytes: one 32-unit chunk of a heavy sourc
 // (ranges only need to be disjoint, not ordered).  There is no finishing step here: the append
 // pass reads the packed totals itself, so no tile ever waits on a fence.
 // scratch: [0] packed cursor, [1] finished CTAs of the append pass; zeroed before the launch.
-constexpr int kCsrPlanItems = 8;
+constexpr int kCsrPlanItems = 4;
 constexpr int kCsrPlanTile = 256 * kCsrPlanItems;
 __global__ void __launch_bounds__(256)
 csr_plan_kernel(GraphView g, const unsigned long long* __restrict__ off, uint32_t V, unsigned long long n_edges,

@@ -207,6 +207,12 @@ class DynamicGraph:
                                                  C.c_void_p(skipped.ctypes.data), C.byref(ns)))
         return [int(x) for x in skipped[: ns.value]]
 
+    # -- pipelined host batches ------------------------------------------------------------------
+    def ingest(self, max_entries: int, depth: int = 2) -> "BatchIngest":
+        """Ingest queue for a stream of HOST batches: the copy of the next batch overlaps the
+        current op (the loop of io/workload.hpp:141-155, with the PCIe copy taken off its path)."""
+        return BatchIngest(self, max_entries, depth)
+
     # -- reports -----------------------------------------------------------------------------
     def stats(self) -> dict:
         st = _lib.DgStats()
@@ -256,3 +262,67 @@ class DynamicGraph:
         s, d = self._pair_args(src, dst)
         o, dd = _Arg(offsets_dev, np.uint64), _Arg(destinations_dev, np.uint32)
         self._check(self._lib.dg_coo_to_csr(self._h, s.ptr, d.ptr, s.n, s.mem, vertex_count, o.ptr, dd.ptr))
+
+
+class BatchIngest:
+    """`submit("insert" | "delete", src, dst)` applies host batches in order, exactly like calling
+    insert_pairs / delete_pairs one after the other, but keeps up to `depth - 1` later batches in
+    flight to the device while an op runs.  A failing batch raises from the submit / flush call that
+    executes it; later staged batches are dropped (the reference loop would have stopped there too).
+    Host arrays must stay alive until their op ran (pinned memory makes the copy asynchronous)."""
+
+    def __init__(self, graph: DynamicGraph, max_entries: int, depth: int = 2):
+        self._g = graph
+        self._lib = graph._lib
+        self._max_entries = max_entries
+        self._depth = depth
+        self._q = None
+        self._open()
+        self._pending = []   # (kind, slot, keep-alive arrays)
+
+    def _open(self):
+        q = C.c_void_p()
+        self._g._check(self._lib.dg_ingest_create(self._g._h, self._max_entries, self._depth, C.byref(q)))
+        self._q = q
+
+    def close(self):
+        if self._q:
+            self._lib.dg_ingest_destroy(self._q)
+            self._q = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _run_oldest(self):
+        kind, slot, _keep = self._pending.pop(0)
+        fn = self._lib.dg_ingest_insert if kind == "insert" else self._lib.dg_ingest_delete
+        rc = fn(self._q, slot)
+        if rc != 0:
+            self._pending.clear()
+            self._lib.dg_ingest_destroy(self._q)   # drop whatever is still staged
+            self._open()
+            self._g._check(rc)
+        return rc
+
+    def submit(self, kind: str, src, dst):
+        if kind not in ("insert", "delete"):
+            raise DataError("ingest: kind must be 'insert' or 'delete'")
+        s = np.ascontiguousarray(src, dtype=np.uint32)
+        d = np.ascontiguousarray(dst, dtype=np.uint32)
+        if s.size != d.size:
+            raise DataError("pairs: src/dst must have equal length")
+        if len(self._pending) == self._depth:
+            self._run_oldest()
+        slot = C.c_uint32()
+        self._g._check(self._lib.dg_ingest_stage_coo(self._q, C.c_void_p(s.ctypes.data), C.c_void_p(d.ctypes.data),
+                                                     s.size, C.byref(slot)))
+        self._pending.append((kind, int(slot.value), (s, d)))
+        if len(self._pending) == self._depth:   # keep depth - 1 copies in flight behind the running op
+            self._run_oldest()
+
+    def flush(self):
+        while self._pending:
+            self._run_oldest()

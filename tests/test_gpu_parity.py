@@ -261,6 +261,45 @@ def test_device_resident_batches():
     assert g.active_edges() == o.active_edges()
 
 
+def test_pipelined_ingest_matches_sequential_ops():
+    """dg_ingest_*: host batches applied through the double-buffered ingest queue give the same
+    graph as insert_pairs / delete_pairs one after the other; a rejected batch raises from the
+    call that executes it and leaves the graph as the reference would (graph.hpp:168-171)."""
+    from paper_2306_08252_b200 import DataError, DynamicGraph, GraphConfig
+    rng = np.random.default_rng(21)
+    V = 4000
+    g = DynamicGraph(GraphConfig(pool_blocks=1 << 16), V, 32)
+    o = CpuGraph(load_oracle(), "orc", V, 32, 1 << 28)
+    q = g.ingest(max_entries=30000, depth=3)
+    ops = []
+    for i in range(9):
+        s = (rng.zipf(1.3, 30000) % V).astype(np.uint32)
+        d = rng.integers(0, V, 30000).astype(np.uint32)
+        ops.append(("insert" if i % 3 != 2 else "delete", s, d))
+    for kind, s, d in ops:
+        q.submit(kind, s, d)
+        (o.insert_pairs if kind == "insert" else o.delete_pairs)(s, d)
+    q.flush()
+    assert g.active_edges() == o.active_edges()
+    a, b = g.export_csr(), o.export_csr()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    # a bad batch in the middle of the stream
+    good = ops[0]
+    bad_d = good[2].copy(); bad_d[17] = V + 1
+    q.submit("insert", good[1], good[2])
+    with pytest.raises(DataError):
+        q.submit("insert", good[1], bad_d)
+        q.submit("insert", good[1], good[2])
+        q.flush()
+    o.insert_pairs(good[1], good[2])
+    assert g.active_edges() == o.active_edges()
+    q.submit("delete", good[1], good[2]); q.flush()
+    o.delete_pairs(good[1], good[2])
+    a, b = g.export_csr(), o.export_csr()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    q.close(); g.close()
+
+
 def test_config1_uniform_2p16_1m():
     """BASELINE config 1: synth_uniform(65536, 1e6, 0xbeef), bulk init, 10 x 10K inserts then
     the same batches as deletes, 100K queries — full parity with the oracle."""
