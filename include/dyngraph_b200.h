@@ -77,7 +77,18 @@ typedef struct dg_config {
   uint64_t pool_blocks;      /* if non-zero, overrides pool_bytes: exact block count */
   void* stream;              /* cudaStream_t to enqueue on; NULL => library-owned stream */
   uint64_t workspace_bytes;  /* per-op scratch reserved at create (0 => grown on first use) */
-  uint32_t reserved[6];
+  /* Edge-queue growth (GrowthPolicy, block_pool.hpp:18-29; commit_front / ensure_available /
+   * try_grow, :162-189, :252-264).  pool_max_blocks plays the arena's role: the most blocks the
+   * pool may ever hold.  0 (or <= the initial count) => fixed pool, underflow is an engine error.
+   * Otherwise the pool grows by growth_fraction of its capacity whenever cumulative consumption
+   * reaches trigger_fraction of it (checked after every insert) and on demand when a batch needs
+   * more blocks than are queued; device memory is committed in place (CUDA virtual memory
+   * management: the address range is reserved once, physical chunks are mapped as the pool
+   * grows, nothing is copied). */
+  uint64_t pool_max_blocks;
+  float trigger_fraction;    /* 0 => 0.8 */
+  float growth_fraction;     /* 0 => 0.25 */
+  uint32_t reserved[2];
 } dg_config;
 
 /* Replaces GraphStats (graph.hpp:54-70); reported, not compared. */
@@ -96,7 +107,7 @@ typedef struct dg_stats {
   uint64_t queue_rear;
   uint64_t max_degree;
   uint32_t block_size;
-  uint32_t reserved;
+  uint32_t growth_count;       /* growth rounds so far (block_pool.hpp growth_count()) */
 } dg_stats;
 
 /* Replaces MemoryBreakdown (graph.hpp:43-52) with real device allocations. */

@@ -29,7 +29,10 @@ class DgConfig(C.Structure):
         ("pool_blocks", C.c_uint64),
         ("stream", C.c_void_p),
         ("workspace_bytes", C.c_uint64),
-        ("reserved", C.c_uint32 * 6),
+        ("pool_max_blocks", C.c_uint64),
+        ("trigger_fraction", C.c_float),
+        ("growth_fraction", C.c_float),
+        ("reserved", C.c_uint32 * 2),
     ]
 
 
@@ -38,7 +41,7 @@ class DgStats(C.Structure):
         "logical_size", "capacity", "alive_vertices", "active_edges", "adjacency_blocks",
         "occupied_slots", "hole_slots", "pool_blocks_created", "pool_blocks_in_use",
         "pool_queue_size", "queue_front", "queue_rear", "max_degree")] + [
-        ("block_size", C.c_uint32), ("reserved", C.c_uint32)]
+        ("block_size", C.c_uint32), ("growth_count", C.c_uint32)]
 
 
 class DgMemory(C.Structure):

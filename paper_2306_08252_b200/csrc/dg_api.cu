@@ -6,6 +6,7 @@
 // OpState::err on the device and every later kernel of the op starts with
 // `if (op->err) return;` (validate-then-mutate, reference graph.hpp:168-171).
 // The op ends with one 256-byte read-back of {DeviceState, OpState}.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -42,6 +43,87 @@ inline size_t aligned(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 thread_local std::string g_create_error;
 
+// ---- device memory committed in place (CUDA virtual memory management) -------------------------
+// The growing pool arrays (slab, next links) reserve their address range for the largest pool
+// once; physical chunks are mapped behind the committed part as the pool grows, so device
+// pointers stay valid and nothing is copied.  The driver entry points are looked up at run
+// time (cudaGetDriverEntryPoint): the library does not link against libcuda.
+struct DrvApi {
+  CUresult (*getGranularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*addressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*addressFree)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  bool ok = false;
+};
+const DrvApi& drv() {
+  static DrvApi api = [] {
+    DrvApi a;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess && *fn;
+    };
+    a.ok = get("cuMemGetAllocationGranularity", (void**)&a.getGranularity) && get("cuMemAddressReserve", (void**)&a.addressReserve) &&
+           get("cuMemAddressFree", (void**)&a.addressFree) && get("cuMemCreate", (void**)&a.create) &&
+           get("cuMemRelease", (void**)&a.release) && get("cuMemMap", (void**)&a.map) && get("cuMemUnmap", (void**)&a.unmap) &&
+           get("cuMemSetAccess", (void**)&a.setAccess);
+    cudaGetLastError();
+    return a;
+  }();
+  return api;
+}
+struct VmRange {
+  CUdeviceptr base = 0;
+  size_t reserved = 0, mapped = 0, gran = 0;
+  int device = 0;
+  std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> chunks;
+  bool reserve(int dev, size_t max_bytes) {
+    const DrvApi& d = drv();
+    if (!d.ok) return false;
+    device = dev;
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = dev;
+    if (d.getGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || gran == 0) return false;
+    reserved = (max_bytes + gran - 1) / gran * gran;
+    return d.addressReserve(&base, reserved, 0, 0, 0) == CUDA_SUCCESS;
+  }
+  // commit at least `bytes` in total
+  bool commit(size_t bytes) {
+    const DrvApi& d = drv();
+    const size_t want = std::min(reserved, (bytes + gran - 1) / gran * gran);
+    if (want <= mapped) return bytes <= mapped;
+    const size_t add = want - mapped;
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    CUmemGenericAllocationHandle hdl;
+    if (d.create(&hdl, add, &prop, 0) != CUDA_SUCCESS) return false;
+    if (d.map(base + mapped, add, 0, hdl, 0) != CUDA_SUCCESS) { d.release(hdl); return false; }
+    CUmemAccessDesc acc{};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (d.setAccess(base + mapped, add, &acc, 1) != CUDA_SUCCESS) { d.unmap(base + mapped, add); d.release(hdl); return false; }
+    chunks.emplace_back(hdl, add);
+    mapped = want;
+    return bytes <= mapped;
+  }
+  void destroy() {
+    const DrvApi& d = drv();
+    if (!base) return;
+    size_t off = 0;
+    for (auto& c : chunks) { d.unmap(base + off, c.second); d.release(c.first); off += c.second; }
+    d.addressFree(base, reserved);
+    chunks.clear();
+    base = 0; reserved = mapped = 0;
+  }
+};
+
 }  // namespace
 
 struct dg_graph {
@@ -65,6 +147,14 @@ struct dg_graph {
   // pool
   uint32_t *slab = nullptr, *next = nullptr, *ring = nullptr;
   uint64_t NB = 0;
+  // growth (GrowthPolicy, block_pool.hpp:18-29)
+  uint64_t nb_max = 0;          // most blocks the pool may hold; <= NB: fixed pool
+  double trigger = 0.8, growth = 0.25;
+  uint64_t consumed = 0;        // cumulative pops (block_pool.hpp consumed())
+  uint32_t growth_count = 0;
+  uint64_t ring_identity = 0;   // ring[p] == p for queue positions below this
+  bool pool_vm = false;         // slab / next live in VmRanges
+  VmRange vm_slab, vm_next;
 
   DevBlock* d_blk = nullptr;  // device
   DevBlock* h_blk = nullptr;  // pinned host mirror
@@ -85,6 +175,7 @@ struct dg_graph {
   int pre_zero_left = 0;
 
   std::string last_error;
+  uint64_t last_shortfall = 0;  // blocks the last rejected insert was short of (0: it was not a pool underflow)
   dg_op_report report{};
   uint64_t launches = 0;
 
@@ -172,6 +263,7 @@ GraphView view(const dg_graph* h) {
   g.next = h->next;
   g.ring = h->ring;
   g.ring_cap = h->NB;
+  g.ring_identity = h->ring_identity;
   g.B = h->B;
   g.bsh = (h->B != 0 && (h->B & (h->B - 1)) == 0) ? (int)std::countr_zero(h->B) : -1;
   g.mw = (h->B + 31) / 32;
@@ -309,6 +401,7 @@ int op_end(dg_graph* h) {
   h->report.slots_scanned_tiny = op.slots_tiny;
   if (op.err != 0) {
     h->report.blocks_popped = 0;
+    if (op.err_detail == kErrPoolUnderflow) h->last_shortfall = op.err_index;
     return fail(h, (int)op.err,
                 std::string(op.err == DG_ERR_DATA ? "csr batch: " : "block pool: ") +
                     detail_text(op.err_detail) + " (index " + std::to_string(op.err_index) + ")");
@@ -432,8 +525,29 @@ int create_pool(dg_graph* h, uint32_t B) {
                                    : (h->cfg.pool_bytes ? h->cfg.pool_bytes : (1ull << 30)) / per_block;
   if (nb == 0) return fail(h, DG_ERR_ENGINE, "block pool: arena cannot host a single edge block");
   if (nb >= (1ull << 31)) nb = (1ull << 31) - 1;
-  cudaError_t e;
-  if ((e = cudaMalloc(&h->slab, nb * B * sizeof(uint32_t))) != cudaSuccess ||
+  h->nb_max = std::min<uint64_t>(h->cfg.pool_max_blocks, (1ull << 31) - 1);
+  cudaError_t e = cudaSuccess;
+  if (h->nb_max > nb) {
+    // growing pool: reserve the address range of the largest pool, commit the initial part
+    const bool ok = h->vm_slab.reserve(h->device, h->nb_max * B * sizeof(uint32_t)) && h->vm_slab.commit(nb * B * sizeof(uint32_t)) &&
+                    h->vm_next.reserve(h->device, h->nb_max * sizeof(uint32_t)) && h->vm_next.commit(nb * sizeof(uint32_t));
+    if (!ok) {
+      h->vm_slab.destroy();
+      h->vm_next.destroy();
+      return fail(h, DG_ERR_ENGINE, "block pool: cannot reserve / commit device memory for a growing pool");
+    }
+    h->pool_vm = true;
+    h->slab = reinterpret_cast<uint32_t*>(h->vm_slab.base);
+    h->next = reinterpret_cast<uint32_t*>(h->vm_next.base);
+    if ((e = cudaMalloc(&h->ring, nb * sizeof(uint32_t))) != cudaSuccess) {
+      cudaGetLastError();
+      h->vm_slab.destroy();
+      h->vm_next.destroy();
+      h->slab = h->next = nullptr;
+      h->pool_vm = false;
+      return fail(h, DG_ERR_ENGINE, std::string("block pool: device allocation failed: ") + cudaGetErrorString(e));
+    }
+  } else if ((e = cudaMalloc(&h->slab, nb * B * sizeof(uint32_t))) != cudaSuccess ||
       (e = cudaMalloc(&h->next, nb * sizeof(uint32_t))) != cudaSuccess ||
       (e = cudaMalloc(&h->ring, nb * sizeof(uint32_t))) != cudaSuccess) {
     cudaGetLastError();
@@ -442,6 +556,7 @@ int create_pool(dg_graph* h, uint32_t B) {
     h->slab = h->next = h->ring = nullptr;
     return fail(h, DG_ERR_ENGINE, std::string("block pool: device allocation failed: ") + cudaGetErrorString(e));
   }
+  h->ring_identity = nb;
   h->B = B;
   h->NB = nb;
   DG_LAUNCH(h, "ring_fill_kernel", ring_fill_kernel<<<grid_for(h, nb, 256 * 4), 256, 0, h->stream>>>(h->ring, nb));
@@ -455,6 +570,67 @@ int create_pool(dg_graph* h, uint32_t B) {
   h->front = 0;
   h->rear = nb;
   return DG_OK;
+}
+
+// One growth round (try_grow, block_pool.hpp:252-264): growth_fraction of the capacity, clamped to
+// what the budget still allows.  Returns false when the pool cannot grow any further.
+bool try_grow(dg_graph* h) {
+  if (!h->pool_vm || h->NB >= h->nb_max) return false;
+  uint64_t want = (uint64_t)((double)h->NB * h->growth);
+  if (want == 0) want = 1;
+  const uint64_t grant = std::min<uint64_t>(want, h->nb_max - h->NB);
+  const uint64_t nb_new = h->NB + grant;
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return false;
+  if (!h->vm_slab.commit(nb_new * h->B * sizeof(uint32_t)) || !h->vm_next.commit(nb_new * sizeof(uint32_t))) return false;
+  uint32_t* ring_new = nullptr;
+  if (cudaMalloc(&ring_new, nb_new * sizeof(uint32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  ring_relayout_kernel<<<grid_for(h, (h->rear - h->front) + grant, 256), 256, 0, h->stream>>>(
+      h->ring, h->NB, ring_new, nb_new, h->front, h->rear, (uint32_t)h->NB, grant);
+  cudaMemsetAsync(h->next + h->NB, 0xFF, grant * sizeof(uint32_t), h->stream);
+  if (h->rear == h->ring_identity) h->ring_identity += grant;   // nothing was ever recycled: still a bump allocator
+  h->rear += grant;
+  h->h_blk->st.front = h->front;
+  h->h_blk->st.rear = h->rear;
+  h->h_blk->st.active_edges = h->active_edges;
+  cudaMemcpyAsync(h->d_state(), &h->h_blk->st, sizeof(DeviceState), cudaMemcpyHostToDevice, h->stream);
+  cudaStreamSynchronize(h->stream);
+  cudaFree(h->ring);
+  h->ring = ring_new;
+  h->NB = nb_new;
+  ++h->growth_count;
+  return cudaGetLastError() == cudaSuccess;
+}
+
+// commit_front's growth rule (block_pool.hpp:162-172): after a batch popped `popped` blocks, grow
+// once if cumulative consumption reached trigger_fraction of the capacity.
+void after_pop(dg_graph* h, uint64_t popped) {
+  h->consumed += popped;
+  if (h->pool_vm && h->NB > 0 && (double)h->consumed / (double)h->NB >= h->trigger) try_grow(h);
+}
+
+// ensure_available (block_pool.hpp:177-189) for a batch that was rejected for `shortfall` missing
+// blocks: grows until the queue covers it; false (nothing changed) when the budget cannot.
+bool grow_for_shortfall(dg_graph* h, uint64_t shortfall) {
+  if (!h->pool_vm || h->nb_max - h->NB < shortfall) return false;
+  const uint64_t target = (h->rear - h->front) + shortfall;
+  while (h->rear - h->front < target)
+    if (!try_grow(h)) return false;
+  return true;
+}
+
+// ensure_available + commit_front around an insert (block_pool.hpp:162-189): a batch rejected for a
+// pool underflow left the graph untouched, so when the growth budget covers the shortfall the pool
+// grows and the batch runs again; after a successful batch the trigger rule may grow the pool.
+template <class F>
+int insert_with_growth(dg_graph* h, F&& run) {
+  int rc = run();
+  if (!h) return rc;
+  if (rc == DG_ERR_ENGINE && h->last_shortfall != 0 && grow_for_shortfall(h, h->last_shortfall)) rc = run();
+  if (rc == DG_OK) after_pop(h, h->report.blocks_popped);
+  return rc;
 }
 
 int ensure_mv_scratch(dg_graph* h, uint64_t entries) {
@@ -839,6 +1015,12 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
   h->device = cfg.device;
   h->reclaim = (cfg.flags & DG_FLAG_NO_RECLAIM) ? 0 : 1;
   h->group_mode = (cfg.flags & DG_FLAG_GROUP_RADIX) ? 1 : ((cfg.flags & DG_FLAG_GROUP_COUNT) ? 2 : 0);
+  if (cfg.trigger_fraction > 0.f) h->trigger = cfg.trigger_fraction;
+  if (cfg.growth_fraction > 0.f) h->growth = cfg.growth_fraction;
+  if (h->trigger > 1.0 || h->growth > 1.0 || cfg.trigger_fraction < 0.f || cfg.growth_fraction < 0.f) {
+    delete h;
+    return fail(nullptr, DG_ERR_DATA, "growth policy: fractions must be in (0, 1]");   // block_pool.hpp:23-28
+  }
   auto bail = [&](int code, const std::string& msg) {
     g_create_error = msg;
     dg_destroy(h);
@@ -908,8 +1090,13 @@ void dg_destroy(dg_graph* h) {
   cudaFree(h->tail);
   cudaFree(h->deg);
   cudaFree(h->alive);
-  cudaFree(h->slab);
-  cudaFree(h->next);
+  if (h->pool_vm) {
+    h->vm_slab.destroy();
+    h->vm_next.destroy();
+  } else {
+    cudaFree(h->slab);
+    cudaFree(h->next);
+  }
   cudaFree(h->ring);
   cudaFree(h->d_blk);
   if (h->h_blk) cudaFreeHost(h->h_blk);
@@ -928,10 +1115,11 @@ void dg_destroy(dg_graph* h) {
 }
 
 // ---- insert -------------------------------------------------------------------
-int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
-                        int mem) {
+static int insert_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                           int mem) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
+  h->last_shortfall = 0;
   cudaSetDevice(h->device);
   if (n == 0) return DG_OK;  // EmptyBatchChangesNothing
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
@@ -990,11 +1178,17 @@ int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   return op_end(h);
 }
 
+int dg_insert_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                        int mem) {
+  return insert_with_growth(h, [&] { return insert_coo_impl(h, src, dst, n, mem); });
+}
+
 static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
                            const uint32_t* destinations, uint64_t n_edges, int mem,
                            bool require_empty) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
+  h->last_shortfall = 0;
   cudaSetDevice(h->device);
   if (n_offsets != h->size + 1)  // csr.hpp:50-53
     return fail(h, DG_ERR_DATA, "csr batch: offsets length " + std::to_string(n_offsets) +
@@ -1077,12 +1271,12 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
 
 int dg_insert_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
                         const uint32_t* destinations, uint64_t n_edges, int mem) {
-  return insert_csr_impl(h, offsets, n_offsets, destinations, n_edges, mem, false);
+  return insert_with_growth(h, [&] { return insert_csr_impl(h, offsets, n_offsets, destinations, n_edges, mem, false); });
 }
 
 int dg_bulk_init_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
                      const uint32_t* destinations, uint64_t n_edges, int mem) {
-  return insert_csr_impl(h, offsets, n_offsets, destinations, n_edges, mem, true);
+  return insert_with_growth(h, [&] { return insert_csr_impl(h, offsets, n_offsets, destinations, n_edges, mem, true); });
 }
 
 // ---- delete -------------------------------------------------------------------
@@ -1405,6 +1599,7 @@ int dg_stats_get(dg_graph* h, dg_stats* out) {
   out->queue_front = h->front;
   out->queue_rear = h->rear;
   out->block_size = h->B;
+  out->growth_count = h->growth_count;
   return DG_OK;
 }
 
@@ -1414,7 +1609,7 @@ int dg_memory_get(const dg_graph* h, dg_memory* out) {
   out->sentinel_bytes = h->capacity * 8;
   out->pool_bytes = h->NB ? h->blocks_in_use() * ((uint64_t)h->B * 4 + 4) : 0;
   out->queue_bytes = h->NB * 4;
-  out->pool_reserved_bytes = h->NB * ((uint64_t)h->B * 4 + 4);
+  out->pool_reserved_bytes = h->pool_vm ? h->vm_slab.mapped + h->vm_next.mapped : h->NB * ((uint64_t)h->B * 4 + 4);   // committed device memory
   out->workspace_bytes = h->ws.cap + h->mv_cap * 8;
   return DG_OK;
 }

@@ -31,6 +31,7 @@ struct GraphView {
   uint32_t* next;
   uint32_t* ring;
   unsigned long long ring_cap;  // == NB
+  unsigned long long ring_identity;  // ring[p] == p for every queue position p below this (never-recycled prefix)
   uint32_t B;
   int bsh;             // log2(B) when B is a power of two, else -1
   uint32_t mw;         // 32-bit match-mask words per block: ceil(B / 32)
@@ -128,6 +129,20 @@ __global__ void ring_fill_kernel(uint32_t* __restrict__ ring, unsigned long long
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
        i += (unsigned long long)gridDim.x * blockDim.x)
     ring[i] = (uint32_t)i;
+}
+
+// Pool growth (try_grow, block_pool.hpp:252-264): the queue window [front, rear) moves to a ring
+// of the new capacity and the `grant` new handles are pushed behind it.
+__global__ void ring_relayout_kernel(const uint32_t* __restrict__ old_ring, unsigned long long old_cap,
+                                     uint32_t* __restrict__ new_ring, unsigned long long new_cap,
+                                     unsigned long long front, unsigned long long rear,
+                                     uint32_t first_new, unsigned long long grant) {
+  const unsigned long long live = rear - front;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < live + grant;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long pos = front + i;
+    new_ring[pos % new_cap] = i < live ? old_ring[pos % old_cap] : first_new + (uint32_t)(i - live);
+  }
 }
 
 // vertex_dictionary.hpp:84-91 (append_slots): fresh alive vertices with empty
@@ -521,14 +536,14 @@ struct PlanFin {
 };
 
 // ring slot of queue position front_old + off, off < ring_cap (pop_range, block_pool.hpp:148-158).
-// lap0: front_old < ring_cap, i.e. the queue is still in its first lap.  Positions below ring_cap
-// were written once by ring_fill_kernel (ring[p] = p) and are only overwritten by pushes at
-// positions >= ring_cap, so there the handle IS the position: no load, no dependent latency
-// (a fresh pool behaves like a bump allocator until the first wrap).
+// lap0: front_old < ring_identity, i.e. the queue still serves never-recycled handles.  Positions
+// below ring_identity were written once (ring[p] = p, ring_fill_kernel / pool growth) and can only
+// be overwritten by pushes a full lap later, so there the handle IS the position: no load, no
+// dependent latency (a fresh pool behaves like a bump allocator until its first wrap).
 __device__ __forceinline__ uint32_t ring_at(const GraphView& g, unsigned long long base_mod,
                                             unsigned long long off, bool lap0 = false) {
   unsigned long long i = base_mod + off;
-  if (lap0 && i < g.ring_cap) return (uint32_t)i;
+  if (lap0 && i < g.ring_identity) return (uint32_t)i;
   if (i >= g.ring_cap) i -= g.ring_cap;
   return g.ring[i];
 }
@@ -641,7 +656,7 @@ append_entries_kernel(GraphView g, GroupIndex gi, const uint32_t* __restrict__ s
                       const uint4* __restrict__ info, OpState* op) {
   if (op->err) return;
   const unsigned long long base_mod = op->front_old % g.ring_cap;
-  const bool lap0 = op->front_old < g.ring_cap;
+  const bool lap0 = op->front_old < g.ring_identity;
   const uint32_t base = blockIdx.x * (256 * kGroupItems) + threadIdx.x;
   uint32_t s[kGroupItems], d[kGroupItems], rk[kGroupItems];
   uint4 in[kGroupItems];
@@ -1025,7 +1040,7 @@ csr_append_kernel(GraphView g, const unsigned long long* __restrict__ off, const
   unsigned phase = 0;
   unsigned long long bad = ~0ull;   // smallest out-of-range destination index this lane saw
   const unsigned long long base_mod = front_old % g.ring_cap;
-  const bool lap0 = front_old < g.ring_cap;
+  const bool lap0 = front_old < g.ring_identity;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t n_items = (uint32_t)(plan_tot >> 32);

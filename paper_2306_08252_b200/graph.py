@@ -28,6 +28,10 @@ class GraphConfig:
     stream: int = 0              # cudaStream_t handle; 0 => library-owned stream
     group: str = "auto"          # how COO batches are grouped by source: "auto" | "radix" | "count"
     workspace_bytes: int = 0     # per-op scratch reserved at construction (0 => grown on first use)
+    # GrowthPolicy (block_pool.hpp:18-29): pool_max_blocks is the arena's role (0 => fixed pool)
+    pool_max_blocks: int = 0
+    trigger_fraction: float = 0.0   # 0 => 0.8
+    growth_fraction: float = 0.0    # 0 => 0.25
 
 
 def _is_device(x) -> bool:
@@ -70,6 +74,9 @@ class DynamicGraph:
         c.pool_blocks = cfg.pool_blocks
         c.stream = cfg.stream or None
         c.workspace_bytes = cfg.workspace_bytes
+        c.pool_max_blocks = cfg.pool_max_blocks
+        c.trigger_fraction = cfg.trigger_fraction
+        c.growth_fraction = cfg.growth_fraction
         self._h = C.c_void_p()
         rc = self._lib.dg_create(C.byref(c), initial_vertex_count, block_size, C.byref(self._h))
         if rc != 0:

@@ -300,6 +300,74 @@ def test_pipelined_ingest_matches_sequential_ops():
     q.close(); g.close()
 
 
+def test_edge_queue_growth_policy():
+    """GrowthPolicy on real device memory (block_pool.hpp:162-189, :252-264; the reference's own
+    numbers: proj/tests/block_pool_test.cpp:107-162).  1000 blocks, trigger 0.8, growth 0.25:
+    consuming 800 grows the pool by 250; a batch larger than the queue grows it on demand before
+    anything is mutated; beyond pool_max_blocks the batch is rejected and the graph is unchanged."""
+    from paper_2306_08252_b200 import DynamicGraph, EngineError, GraphConfig
+    V, B = 2000, 4
+    g = DynamicGraph(GraphConfig(pool_blocks=1000, pool_max_blocks=1287), V, B)
+    o = CpuGraph(load_oracle(), "orc", V, B, 1 << 28)
+    st = g.stats()
+    assert st["pool_blocks_created"] == 1000 and st["growth_count"] == 0
+    # 799 sources x 4 entries = 799 blocks: below the trigger
+    s = np.repeat(np.arange(799, dtype=np.uint32), 4); d = (s + 1) % V
+    g.insert_pairs(s, d); o.insert_pairs(s, d)
+    assert g.stats()["pool_blocks_created"] == 1000
+    # one more block: 800 / 1000 >= 0.8 -> +250
+    s1 = np.full(4, 799, np.uint32); d1 = np.arange(4, dtype=np.uint32)
+    g.insert_pairs(s1, d1); o.insert_pairs(s1, d1)
+    st = g.stats()
+    assert st["pool_blocks_created"] == 1250 and st["growth_count"] == 1 and st["pool_queue_size"] == 450
+    # 480 fresh blocks > 450 queued: ensure_available grows (capped at 1287: +37) before the batch runs
+    s2 = np.repeat(np.arange(800, 1280, dtype=np.uint32), 4); d2 = (s2 * 7) % V
+    g.insert_pairs(s2, d2); o.insert_pairs(s2, d2)
+    st = g.stats()
+    assert st["pool_blocks_created"] == 1287 and st["pool_blocks_in_use"] == 1280 and st["growth_count"] == 2
+    assert g.memory()["pool_reserved_bytes"] >= 1287 * (B * 4 + 4)
+    # 8 more blocks cannot be provided: rejected, nothing changes
+    s3 = np.repeat(np.arange(1280, 1288, dtype=np.uint32), 4); d3 = s3 % 5
+    before = g.digest()
+    with pytest.raises(EngineError):
+        g.insert_pairs(s3, d3)
+    assert g.digest() == before and g.stats()["pool_blocks_in_use"] == 1280
+    # deletes hand blocks back; the recycled handles are served after the grown ones
+    g.delete_pairs(s, d); o.delete_pairs(s, d)
+    g.insert_pairs(s3, d3); o.insert_pairs(s3, d3)
+    a, b = g.export_csr(), o.export_csr()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert g.active_edges() == o.active_edges()
+    g.close()
+
+
+def test_growing_pool_random_workloads_match_oracle():
+    """A pool that starts tiny and grows through the trigger / on-demand rules must give the same
+    graphs as the oracle on the random op mix (verify.hpp:135-265), COO and CSR inserts, B = 32."""
+    from paper_2306_08252_b200 import BatchKind, DynamicGraph, GraphConfig, csr_from_pairs
+    rng = np.random.default_rng(99)
+    V = 5000
+    g = DynamicGraph(GraphConfig(pool_blocks=64, pool_max_blocks=1 << 16), V, 32)
+    o = CpuGraph(load_oracle(), "orc", V, 32, 1 << 30)
+    for r in range(12):
+        s = (rng.zipf(1.3, 20000) % V).astype(np.uint32)
+        d = rng.integers(0, V, 20000).astype(np.uint32)
+        if r % 4 == 3:
+            g.delete_pairs(s[:10000], d[:10000]); o.delete_pairs(s[:10000], d[:10000])
+        elif r % 4 == 1:
+            b = csr_from_pairs(BatchKind.Insert, V, s, d)
+            g.insert_batch(b); o.insert_csr(b.offsets, b.destinations)
+        else:
+            g.insert_pairs(s, d); o.insert_pairs(s, d)
+        assert g.active_edges() == o.active_edges()
+    a, b = g.export_csr(), o.export_csr()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert g.stats()["growth_count"] > 3
+    q = rng.integers(0, V, 5000).astype(np.uint32)
+    assert np.array_equal(np.asarray(g.query_edges(q, q[::-1].copy())), np.asarray(o.query(q, q[::-1].copy())))
+    g.close()
+
+
 def test_config1_uniform_2p16_1m():
     """BASELINE config 1: synth_uniform(65536, 1e6, 0xbeef), bulk init, 10 x 10K inserts then
     the same batches as deletes, 100K queries — full parity with the oracle."""
