@@ -577,7 +577,11 @@ void orc_gen_rmat(uint32_t scale, uint64_t seed, uint64_t first, uint64_t n, uin
 /* std::mt19937_64 (the engine behind synth_uniform, io/synthetic.hpp:19-25):
  * the published MT19937-64 recurrence, restated so config 1's exact input
  * (synth_uniform(65536, 1000000, 0xbeef), acceptance_test.cpp:241) can be
- * regenerated where the reference is absent.  Pairs are in generation order. */
+ * regenerated where the reference is absent.  Pairs are in generation order.
+ * NOTE: the reference writes `edges.emplace_back(rng() % V, rng() % V)`; the order of the two
+ * draws is unspecified in C++ and g++ (the only toolchain the reference builds with here)
+ * evaluates the arguments right to left, so the FIRST draw of a pair is the DESTINATION.
+ * Pinned against dyngraph::io::synth_uniform itself (tests/golden/ref_io.npz). */
 void orc_synth_uniform_pairs(uint64_t v, uint64_t e, uint64_t seed, uint32_t* src, uint32_t* dst) {
   enum { NN = 312, MM = 156 };
   static const uint64_t MATRIX_A = 0xB5026F5AA96619E9ull, UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
@@ -598,6 +602,6 @@ void orc_synth_uniform_pairs(uint64_t v, uint64_t e, uint64_t seed, uint32_t* sr
     x ^= (x << 17) & 0x71D67FFFEDA60000ull;
     x ^= (x << 37) & 0xFFF7EEE000000000ull;
     x ^= (x >> 43);
-    if ((k & 1) == 0) src[k >> 1] = (uint32_t)(x % v); else dst[k >> 1] = (uint32_t)(x % v);
+    if ((k & 1) == 0) dst[k >> 1] = (uint32_t)(x % v); else src[k >> 1] = (uint32_t)(x % v);
   }
 }

@@ -200,15 +200,98 @@ int ref_compute_block_size_coo(std::uint64_t v, const std::uint32_t* src, const 
   }
 }
 
-// synth_uniform (io/synthetic.hpp:19-25) as COO in generation order, for golden inputs
+// synth_uniform (io/synthetic.hpp:19-25) as COO in generation order, for golden inputs.  The
+// reference's `emplace_back(rng() % V, rng() % V)` leaves the order of the two draws unspecified;
+// g++ evaluates right to left, so the first draw is the destination (make_golden.py checks this
+// against dyngraph::io::synth_uniform itself).
 int ref_synth_uniform_pairs(std::uint64_t v, std::uint64_t e, std::uint64_t seed, std::uint32_t* src,
                             std::uint32_t* dst) {
   std::mt19937_64 rng(seed);
   for (std::uint64_t i = 0; i < e; ++i) {
-    src[i] = static_cast<std::uint32_t>(rng() % v);
     dst[i] = static_cast<std::uint32_t>(rng() % v);
+    src[i] = static_cast<std::uint32_t>(rng() % v);
   }
   return 0;
+}
+
+// ---- io side (io/synthetic.hpp, io/batching.hpp, io/workload.hpp): golden generators for the
+// host-side mirror in paper_2306_08252_b200/io.py -------------------------------------------------
+
+// kind 0: synth_uniform (io/synthetic.hpp:16-27), 1: synth_power_law (:32-66); CSR out
+int ref_synth_csr(int kind, std::uint64_t v, std::uint64_t e, std::uint64_t seed, std::uint64_t* offsets,
+                  std::uint32_t* dsts) {
+  try {
+    const dyngraph::io::Csr csr = kind == 0 ? dyngraph::io::synth_uniform(v, e, seed) : dyngraph::io::synth_power_law(v, e, seed);
+    std::copy(csr.offsets.begin(), csr.offsets.end(), offsets);
+    std::copy(csr.destinations.begin(), csr.destinations.end(), dsts);
+    return 0;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
+// make_batches (io/batching.hpp:46-66) flattened: every batch's (src, dst) in CSR order, one after
+// the other; batch_sizes[i] = edges of batch i; returns the batch count (or -1)
+long long ref_make_batches_flat(std::uint64_t v, const std::uint64_t* offsets, const std::uint32_t* dsts, std::uint64_t e,
+                                std::uint64_t batch_size, int shuffled, std::uint64_t seed, std::uint32_t* src_out,
+                                std::uint32_t* dst_out, std::uint64_t* batch_sizes) {
+  try {
+    dyngraph::io::Csr csr;
+    csr.vertex_count = v;
+    csr.offsets.assign(offsets, offsets + v + 1);
+    csr.destinations.assign(dsts, dsts + e);
+    const auto batches = dyngraph::io::make_batches(csr, batch_size, dyngraph::BatchKind::Insert,
+                                                    shuffled ? dyngraph::io::EdgeOrder::Shuffled : dyngraph::io::EdgeOrder::Prefix, seed);
+    std::uint64_t k = 0;
+    for (std::size_t b = 0; b < batches.size(); ++b) {
+      batch_sizes[b] = batches[b].edge_count();
+      for (std::uint64_t u = 0; u < v; ++u)
+        for (std::uint64_t i = batches[b].offsets[u]; i < batches[b].offsets[u + 1]; ++i) {
+          src_out[k] = static_cast<std::uint32_t>(u);
+          dst_out[k] = batches[b].destinations[i];
+          ++k;
+        }
+    }
+    return static_cast<long long>(batches.size());
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// run_workload (io/workload.hpp:104-190) on a synthetic source with a fake clock (250 us per tick,
+// as the reference's io_test.cpp:51-57).  ops: 0 Insert, 1 Delete, 2 InsertThenDelete.
+// out[0..7] = edges_inserted, edges_deleted, queries_run, queries_hit, effective_block_size,
+//             rows, final active_edges, vertex_count; phases: comma-separated phase names
+int ref_run_workload_synth(int kind, std::uint64_t v, std::uint64_t e, std::uint64_t seed, std::uint64_t batch_size, int ops,
+                           int shuffled, std::uint32_t block_size, std::uint64_t query_sample, std::uint64_t arena_bytes,
+                           std::uint64_t* out, char* phases, std::uint64_t phases_cap) {
+  try {
+    dyngraph::io::WorkloadSpec spec;
+    spec.graph_name = "synth";
+    spec.source = kind == 0 ? dyngraph::io::WorkloadSpec::Source::SynthUniform : dyngraph::io::WorkloadSpec::Source::SynthPowerLaw;
+    spec.synth_vertices = v;
+    spec.synth_edges = e;
+    spec.seed = seed;
+    spec.batch_size = batch_size;
+    spec.ops = ops == 0 ? dyngraph::io::OpsMode::Insert : ops == 1 ? dyngraph::io::OpsMode::Delete : dyngraph::io::OpsMode::InsertThenDelete;
+    spec.order = shuffled ? dyngraph::io::EdgeOrder::Shuffled : dyngraph::io::EdgeOrder::Prefix;
+    spec.block_size = block_size;
+    spec.query_sample = query_sample;
+    spec.config.arena_bytes = arena_bytes;
+    std::uint64_t t = 0;
+    const dyngraph::io::RunReport r = dyngraph::io::run_workload(spec, [&t] { t += 250000; return t; });
+    out[0] = r.edges_inserted; out[1] = r.edges_deleted; out[2] = r.queries_run; out[3] = r.queries_hit;
+    out[4] = r.effective_block_size; out[5] = r.rows.size(); out[6] = r.final_stats.active_edges; out[7] = r.vertex_count;
+    std::string ph;
+    for (const auto& row : r.rows) { if (!ph.empty()) ph += ','; ph += row.phase; }
+    if (ph.size() + 1 > phases_cap) return 3;
+    std::memcpy(phases, ph.c_str(), ph.size() + 1);
+    return 0;
+  } catch (const dyngraph::DataError&) {
+    return 2;
+  } catch (const std::exception&) {
+    return 3;
+  }
 }
 
 }  // extern "C"

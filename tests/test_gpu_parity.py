@@ -368,6 +368,60 @@ def test_growing_pool_random_workloads_match_oracle():
     g.close()
 
 
+def test_run_workload_matches_reference_runs():
+    """run_workload over the GPU store (io/workload.hpp:104-190) against runs of the reference's own
+    run_workload (tests/golden/ref_io.npz): same phases in the same order, edges inserted / deleted,
+    auto block size, query hits of the reference's query mix, final live-edge count."""
+    from pathlib import Path
+    from paper_2306_08252_b200 import GraphConfig
+    from paper_2306_08252_b200 import io as dio
+    from tests.golden.make_golden import IO_RUNS
+    z = np.load(Path(__file__).resolve().parent / "golden" / "ref_io.npz")
+    for i, (kind, v, e, seed, batch, ops, shuffled, bs, qn, _arena) in enumerate(IO_RUNS):
+        spec = dio.WorkloadSpec(graph_name="synth", source=dio.Source.SynthUniform if kind == 0 else dio.Source.SynthPowerLaw,
+                                synth_vertices=v, synth_edges=e, seed=seed, batch_size=batch, ops=dio.OpsMode(ops),
+                                order=dio.EdgeOrder.Shuffled if shuffled else dio.EdgeOrder.Prefix, block_size=bs,
+                                query_sample=qn, config=GraphConfig(pool_blocks=1 << 15))
+        ticks = iter(range(250000, 1 << 40, 250000))
+        rep = dio.run_workload(spec, clock=lambda: next(ticks))   # the reference's fake clock (io_test.cpp:51-57)
+        want = z[f"run{i}_res"]
+        got = [rep.edges_inserted, rep.edges_deleted, rep.queries_run, rep.queries_hit, rep.effective_block_size,
+               len(rep.rows), rep.final_stats["active_edges"], rep.vertex_count]
+        assert got == [int(x) for x in want], (i, got, list(want))
+        assert ",".join(r.phase for r in rep.rows) == bytes(z[f"run{i}_phases"]).decode(), i
+        assert all(abs(r.ms - 0.25) < 1e-9 for r in rep.rows)
+        csv = dio.write_csv(rep)
+        lines = csv.splitlines()
+        assert lines[0] == "graph,batch_size,phase,ms,bytes_dict,bytes_sentinel,bytes_pool,bytes_total"
+        assert len(lines) == 1 + len(rep.rows) and lines[1].startswith(f"synth,{'bulk' if batch == 0 else batch},init,0.250,")
+        for r in rep.rows:   # io_test.cpp:255-272: the parts sum to the total
+            m = r.memory
+            assert m["total"] == m["dictionary_bytes"] + m["sentinel_bytes"] + m["pool_bytes"] + m["queue_bytes"]
+
+
+def test_run_workload_files_round_trip(tmp_path):
+    """io_test.cpp:213-242, :274-288: an empty edge list still reports init; insert-then-delete ends
+    empty; load -> slice -> insert reproduces the input's per-vertex multisets."""
+    from paper_2306_08252_b200 import DynamicGraph, GraphConfig
+    from paper_2306_08252_b200 import io as dio
+    (tmp_path / "empty.el").write_text("")
+    rep = dio.run_workload(dio.WorkloadSpec(graph_name="empty", source=dio.Source.EdgeList, input_path=str(tmp_path / "empty.el"),
+                                            config=GraphConfig(pool_blocks=64)))
+    assert rep.edges_inserted == 0 and rep.total_ms("init") > 0 and rep.final_stats["active_edges"] == 0
+    (tmp_path / "tri.mtx").write_text("%%MatrixMarket matrix coordinate real general\n3 3 3\n1 2 1.5\n2 3 2.5\n3 1 3.5\n")
+    rep = dio.run_workload(dio.WorkloadSpec(graph_name="triangle", input_path=str(tmp_path / "tri.mtx"), batch_size=2,
+                                            ops=dio.OpsMode.InsertThenDelete, config=GraphConfig(pool_blocks=64)))
+    assert (rep.edges_inserted, rep.edges_deleted, rep.final_stats["active_edges"]) == (3, 3, 0)
+    (tmp_path / "star.mtx").write_text("%%MatrixMarket matrix coordinate pattern symmetric\n5 5 4\n2 1\n3 1\n4 1\n5 1\n")
+    csr = dio.load_matrix_market(str(tmp_path / "star.mtx"), True)
+    g = DynamicGraph(GraphConfig(pool_blocks=64), csr.vertex_count, 2)
+    for b in dio.make_batches(csr, 3):
+        g.insert_batch(b)
+    off, dst = g.export_csr(sorted=True)
+    assert list(off) == [0, 4, 5, 6, 7, 8] and list(dst) == [1, 2, 3, 4, 0, 0, 0, 0]
+    g.close()
+
+
 def test_config1_uniform_2p16_1m():
     """BASELINE config 1: synth_uniform(65536, 1e6, 0xbeef), bulk init, 10 x 10K inserts then
     the same batches as deletes, 100K queries — full parity with the oracle."""
