@@ -709,6 +709,8 @@ void enqueue_plan_append(dg_graph* h, const BatchView& b, uint64_t runs_bound, u
   enqueue_append(h, b, a, runs_bound, n_edges, csr_path);
 }
 
+inline uint64_t big_bound(const dg_graph* h);
+
 struct Worklist {
   uint32_t* wl_off;
   uint32_t* wl_handle;
@@ -718,7 +720,7 @@ struct Worklist {
   uint2* long_items;
   uint32_t* big_list;  // chains longer than kLaneWalk blocks
   EnumLists lists(dg_graph* h) const {
-    return EnumLists{run_deg, wl_off, med_items, long_items, big_list, h->d_op()};
+    return EnumLists{run_deg, wl_off, med_items, long_items, big_list, (uint32_t)big_bound(h), h->d_op()};
   }
 };
 
@@ -757,7 +759,7 @@ void enqueue_walk(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t r
   GraphView g = view(h);
   // (inside a fork: the long-chain walk starts first, it is the critical path)
   DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_for(h, big_bound(h), 8), 256, 0, lane(h, 1)>>>(
-      g, b, w.wl_off, w.run_deg, w.big_list, w.wl_handle, w.wl_run, h->d_op()));
+      g, b, w.wl_off, w.run_deg, w.big_list, (uint32_t)big_bound(h), w.wl_handle, w.wl_run, h->d_op()));
   DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_for(h, runs_bound, 256), 256, 0, lane(h, 2)>>>(
       g, b, w.wl_off, w.run_deg, w.wl_handle, w.wl_run, h->d_op()));
 }

@@ -72,7 +72,7 @@ struct OpState {
   unsigned int med_cursor;        // dynamic work distribution of the medium / long match tiers
   unsigned int long_cursor;
   unsigned long long slots_tiny;  // part of `slots` inspected by the register-compare tier
-  unsigned int plan_ok;           // (unused, keeps the layout)
+  unsigned int n_huge;            // chains walked by a whole CTA (listed from the end of the big list)
   unsigned int committed;         // CSR insert: the append pass ran and published deg/tail/front (rollback needed on error)
   unsigned long long bad_index;   // CSR insert: smallest out-of-range destination index seen by the append pass (~0: none)
 };

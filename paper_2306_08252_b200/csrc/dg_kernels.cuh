@@ -1233,6 +1233,7 @@ csr_rollback_kernel(GraphView g, const unsigned long long* __restrict__ off, uin
 // work items of the long-chain match path)
 // ---------------------------------------------------------------------------
 constexpr uint32_t kLaneWalk = 16;       // chains up to this many blocks are walked by one lane
+constexpr uint32_t kHugeWalk = 1024;     // longer chains are walked by a whole CTA, 1024 links per round trip
 // Match tiers by the number of targets k the batch holds for a source:
 //   k <= kTinyTargets               thread-per-block register compare (match_tiny_kernel)
 //   kTinyTargets < k <= kMedTargets a warp per 32-block chunk, per-warp shared-memory table
@@ -1260,12 +1261,15 @@ struct EnumLists {
   uint32_t* wl_off;
   uint2* med_items;    // nullptr on paths without a batch (export, digest)
   uint2* long_items;
-  uint32_t* big_list;  // sources whose chain the whole warp walks (enumerate_big_kernel)
+  uint32_t* big_list;  // sources whose chain a whole warp walks (enumerate_big_kernel); chains longer than
+                       // kHugeWalk blocks are listed from the END of the same array and walked by a whole CTA
+  uint32_t big_cap;
   OpState* op;
   __device__ void write(uint32_t r, uint32_t d, uint32_t nblk, uint32_t k, unsigned long long excl_b) const {
     run_deg[r] = d;
     wl_off[r] = (uint32_t)excl_b;
-    if (nblk > kLaneWalk) big_list[atomicAdd(&op->n_big, 1ull)] = r;
+    if (nblk > kHugeWalk) big_list[big_cap - 1u - atomicAdd(&op->n_huge, 1u)] = r;
+    else if (nblk > kLaneWalk) big_list[atomicAdd(&op->n_big, 1ull)] = r;
     if (med_items != nullptr && nblk > 0) {
       if (k > kMedTargets) {
         const uint32_t n = (nblk + kLongChunk - 1) / kLongChunk;
@@ -1397,9 +1401,64 @@ enumerate_walk_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_
 // degrade to one block per latency.
 __global__ void __launch_bounds__(256)
 enumerate_big_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
-                     const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ big_list,
+                     const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ big_list, uint32_t big_cap,
                      uint32_t* __restrict__ wl_handle, uint32_t* __restrict__ wl_run, const OpState* op) {
   if (op->err) return;
+  // ---- chains of more than kHugeWalk blocks (the hubs: the critical path of the whole stage): one
+  // CTA per chain, every thread checks 4 links, i.e. 1024 blocks per memory round trip
+  {
+    __shared__ uint32_t s_fail[8];
+    __shared__ uint32_t s_next_h;
+    const uint32_t nhuge = op->n_huge;
+    const int lane = lane_id(), warp = threadIdx.x >> 5;
+    for (uint32_t i = blockIdx.x; i < nhuge; i += gridDim.x) {
+      const uint32_t r = big_list[big_cap - 1u - i];
+      const uint32_t base = wl_off[r];
+      const uint32_t nblk = blocks_for(g, run_deg[r]);
+      uint32_t h = g.head[batch_src(b, r)];
+      const uint32_t tag = run_tag(b, r);
+      uint32_t k = 0;
+      while (k < nblk) {
+        uint32_t nx[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {   // thread t owns links t + 256 q: coalesced
+          const unsigned long long hh = (unsigned long long)h + threadIdx.x + 256u * q;
+          nx[q] = (hh < g.ring_cap) ? g.next[hh] : kNull;
+        }
+        // first link (in chain order) that does not lead to the physically next block
+        // (per warp: the smallest failing index among ITS links; chain order interleaves warps per q)
+        uint32_t wfail = 1024u;
+#pragma unroll
+        for (int q = 3; q >= 0; --q) {
+          const unsigned long long hh = (unsigned long long)h + threadIdx.x + 256u * q;
+          const unsigned m = __ballot_sync(kFull, (unsigned long long)nx[q] != hh + 1);
+          if (m) wfail = 256u * q + 32u * warp + (uint32_t)__ffs(m) - 1u;
+        }
+        if (lane == 0) s_fail[warp] = wfail;
+        __syncthreads();
+        uint32_t first = 1024u;
+#pragma unroll
+        for (int w8 = 0; w8 < 8; ++w8) first = min(first, s_fail[w8]);
+        // blocks h .. h + len - 1 are consecutive in the chain (the first non-consecutive link still names a valid successor)
+        uint32_t len = min(first + 1u, 1024u);
+        len = min(len, nblk - k);
+        const uint32_t last = len - 1u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t o = threadIdx.x + 256u * q;
+          if (o < len) {
+            wl_handle[base + k + o] = h + o;
+            wl_run[base + k + o] = tag;
+          }
+          if (o == last) s_next_h = nx[q];
+        }
+        __syncthreads();
+        h = s_next_h;
+        k += len;
+        __syncthreads();
+      }
+    }
+  }
   const uint32_t nbig = (uint32_t)op->n_big;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
