@@ -80,6 +80,10 @@ struct GraphConfig {
   bool reclaim_on_delete = true;  // graph.hpp:26
   void* stream = nullptr;         // cudaStream_t; nullptr => library-owned stream
   std::uint64_t workspace_bytes = 0;  // per-op scratch reserved at construction
+  // GrowthPolicy (block_pool.hpp:18-29): pool_max_blocks plays the arena's role (0 => fixed pool)
+  std::uint64_t pool_max_blocks = 0;
+  float trigger_fraction = 0.8f;
+  float growth_fraction = 0.25f;
 };
 
 struct GraphStats {  // graph.hpp:54-70 (reported, not compared)
@@ -88,6 +92,7 @@ struct GraphStats {  // graph.hpp:54-70 (reported, not compared)
   std::uint64_t pool_blocks_created = 0, pool_blocks_in_use = 0, pool_queue_size = 0;
   std::uint64_t max_degree = 0;
   std::uint32_t block_size = 0;
+  std::uint32_t pool_growths = 0;   // graph.hpp:66 (growth rounds)
 };
 
 class DynamicGraph {
@@ -101,6 +106,9 @@ class DynamicGraph {
     c.pool_blocks = config.pool_blocks;
     c.stream = config.stream;
     c.workspace_bytes = config.workspace_bytes;
+    c.pool_max_blocks = config.pool_max_blocks;
+    c.trigger_fraction = config.trigger_fraction;
+    c.growth_fraction = config.growth_fraction;
     const int rc = dg_create(&c, initial_vertex_count, block_size, &h_);
     if (rc != DG_OK) raise(rc, dg_last_error(nullptr));
   }
@@ -191,7 +199,7 @@ class DynamicGraph {
     o.active_edges = s.active_edges; o.adjacency_blocks = s.adjacency_blocks; o.occupied_slots = s.occupied_slots;
     o.hole_slots = s.hole_slots; o.pool_blocks_created = s.pool_blocks_created;
     o.pool_blocks_in_use = s.pool_blocks_in_use; o.pool_queue_size = s.pool_queue_size;
-    o.max_degree = s.max_degree; o.block_size = s.block_size;
+    o.max_degree = s.max_degree; o.block_size = s.block_size; o.pool_growths = s.growth_count;
     return o;
   }
 

@@ -9,5 +9,7 @@ timeout 900 python bench.py --scale 24 --batch 10000000 --steps 5 --warmup 2 --n
 python scripts/show_bench.py gpurun_out/bench_c3.json | head -9
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-profile > gpurun_out/ncu_bench.log 2>&1; echo "ncu_list_rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"csr_append|csr_plan" -c 2 -o gpurun_out/prof_csr -f \
+  python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-profile > gpurun_out/ncu_csr.log 2>&1; echo "ncu_csr_rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"match_med|match_tiny|match_long" -s 3 -c 3 -o gpurun_out/prof_match -f \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-profile > gpurun_out/ncu_match.log 2>&1; echo "ncu_full_rc=$?"
