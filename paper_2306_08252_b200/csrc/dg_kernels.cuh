@@ -1253,7 +1253,9 @@ constexpr uint32_t kLongChunk = 256;     // blocks per CTA item of the long path
 
 // Enumeration plan: work-list segments are disjoint ranges too (alloc_kernel):
 //   word a = [63:32] touched sources (counting path only), [31:0] batch entries
-//   word b = blocks of the touched chains
+//   word b = [63:32] chains a whole warp walks (their big-list slots come out of the scan: one
+//            same-address atomic per such source cost more than the rest of the pass),
+//            [31:0] blocks of the touched chains
 // The match tiers' (run, chunk) items and the long-chain list are filled
 // through device counters (order is irrelevant: they only distribute work).
 struct EnumLists {
@@ -1268,8 +1270,8 @@ struct EnumLists {
   __device__ void write(uint32_t r, uint32_t d, uint32_t nblk, uint32_t k, unsigned long long excl_b) const {
     run_deg[r] = d;
     wl_off[r] = (uint32_t)excl_b;
-    if (nblk > kHugeWalk) big_list[big_cap - 1u - atomicAdd(&op->n_huge, 1u)] = r;
-    else if (nblk > kLaneWalk) big_list[atomicAdd(&op->n_big, 1ull)] = r;
+    if (nblk > kHugeWalk) big_list[big_cap - 1u - atomicAdd(&op->n_huge, 1u)] = r;   // (a few dozen per batch)
+    else if (nblk > kLaneWalk) big_list[(uint32_t)(excl_b >> 32)] = r;
     if (med_items != nullptr && nblk > 0) {
       if (k > kMedTargets) {
         const uint32_t n = (nblk + kLongChunk - 1) / kLongChunk;
@@ -1283,6 +1285,10 @@ struct EnumLists {
     }
   }
 };
+// word b of the enumeration plan for a chain of nblk blocks
+__device__ __forceinline__ unsigned long long enum_word_b(uint32_t nblk) {
+  return ((nblk > kLaneWalk && nblk <= kHugeWalk) ? (1ull << 32) : 0ull) | nblk;
+}
 // degree of a touched vertex as delete/query see it: dead or unknown sources have
 // none (graph.hpp:205, :229).  Predicated, independent loads (see alloc_kernel).
 __device__ __forceinline__ uint32_t live_degree(const GraphView& g, uint32_t v, bool wanted, int check_alive) {
@@ -1305,7 +1311,7 @@ struct EnumIn {
     const uint32_t r = (uint32_t)r64;
     const bool wanted = b.run_start == nullptr || run_len(b, r) != 0;  // empty runs: CSR batches
     x.d = live_degree(g, batch_src(b, r), wanted, check_alive);
-    return Sum2{0ull, blocks_for(g, x.d)};
+    return Sum2{0ull, enum_word_b(blocks_for(g, x.d))};
   }
 };
 struct EnumOut {
@@ -1331,7 +1337,7 @@ struct GroupEnumIn {
     const bool rep = rank[i] == 0;
     const uint32_t c = rep ? cnt[gi(s)] : 0u;
     x.d = live_degree(g, s, rep, check_alive);
-    return Sum2{c ? ((1ull << 32) | c) : 0ull, blocks_for(g, x.d)};
+    return Sum2{c ? ((1ull << 32) | c) : 0ull, enum_word_b(blocks_for(g, x.d))};
   }
 };
 struct GroupEnumOut {
@@ -1363,8 +1369,9 @@ struct EnumFin {
   int set_runs;
   __device__ void operator()(unsigned long long total_a, unsigned long long total_b) const {
     if (set_runs) op->n_runs = total_a >> 32;
-    op->wl_blocks = total_b;
-    if (total_b > wl_cap) {  // cannot happen: wl_cap >= blocks in use (host mirror)
+    op->wl_blocks = total_b & 0xFFFFFFFFull;
+    op->n_big = total_b >> 32;
+    if ((total_b & 0xFFFFFFFFull) > wl_cap) {  // cannot happen: wl_cap >= blocks in use (host mirror)
       op->err = 3;
       op->err_detail = kErrScratch;
     }
