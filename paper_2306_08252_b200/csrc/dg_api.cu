@@ -322,6 +322,29 @@ inline int grid_for(const dg_graph* h, uint64_t items, int per_block) {
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
 }
 
+// Grid of a grid-stride kernel: enough CTAs for the work, never more than are RESIDENT at once
+// (148 SMs x the kernel's occupancy): a partial second wave only adds a tail.
+template <class K>
+int resident_ctas_per_sm(K kernel, int block_threads, size_t dyn_smem) {
+  static std::map<const void*, int> cache;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block_threads, dyn_smem) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 1;
+  }
+  cache[key] = n;
+  return n;
+}
+template <class K>
+int grid_resident(const dg_graph* h, uint64_t items, int per_block, K kernel, int block_threads = 256, size_t dyn_smem = 0) {
+  const uint64_t want = (items + per_block - 1) / per_block;
+  const uint64_t cap = (uint64_t)h->sm_count * resident_ctas_per_sm(kernel, block_threads, dyn_smem);
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
+}
+
 // ---- fork / join of independent kernels ------------------------------------------
 // Between fork() and join() lane(h, i) names stream i of {op stream, aux 0, aux 1}.
 // With per-kernel profiling on, everything stays on the op stream so the event
@@ -758,9 +781,9 @@ inline size_t worklist_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n_bat
 void enqueue_walk(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound) {
   GraphView g = view(h);
   // (inside a fork: the long-chain walk starts first, it is the critical path)
-  DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_for(h, big_bound(h), 8), 256, 0, lane(h, 1)>>>(
+  DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_resident(h, big_bound(h), 8, enumerate_big_kernel), 256, 0, lane(h, 1)>>>(
       g, b, w.wl_off, w.run_deg, w.big_list, (uint32_t)big_bound(h), w.wl_handle, w.wl_run, h->d_op()));
-  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_for(h, runs_bound, 256), 256, 0, lane(h, 2)>>>(
+  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_resident(h, runs_bound, 256, enumerate_walk_kernel), 256, 0, lane(h, 2)>>>(
       g, b, w.wl_off, w.run_deg, w.wl_handle, w.wl_run, h->d_op()));
 }
 
@@ -799,7 +822,7 @@ void enqueue_match(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
             match_med_kernel<kIsDelete><<<med_grid, 256, med_smem, lane(h, 2)>>>(
                 g, b, w.wl_off, w.wl_handle, w.med_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
   DG_LAUNCH(h, kIsDelete ? "match_tiny_kernel<delete>" : "match_tiny_kernel<query>",
-            match_tiny_kernel<kIsDelete><<<grid_for(h, wl_bound, 256), 256, 0, lane(h, 0)>>>(
+            match_tiny_kernel<kIsDelete><<<grid_resident(h, wl_bound, 256, match_tiny_kernel<kIsDelete>), 256, 0, lane(h, 0)>>>(
                 g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
   join(h);
 }
@@ -970,10 +993,10 @@ int delete_matched(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
     if (attempt > 0) cudaMemsetAsync(hole_cnt, 0, 2 * (runs_bound + 1) * 4, h->stream);
     launch_alloc(h, "alloc_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{w.run_deg, run_matched},
                  MovesOut{mv_off}, MovesFin{h->d_op(), h->mv_cap});
-    DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_for(h, wl_bound, 256), 256, 0, h->stream>>>(
+    DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_resident(h, wl_bound, 256, delete_holes_kernel), 256, 0, h->stream>>>(
         g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, wl_mask, hole_cnt,
         h->mv_hole, h->d_op()));
-    DG_LAUNCH(h, "delete_moves_kernel", delete_moves_kernel<<<grid_for(h, wl_bound, 256), 256, 0, h->stream>>>(
+    DG_LAUNCH(h, "delete_moves_kernel", delete_moves_kernel<<<grid_resident(h, wl_bound, 256, delete_moves_kernel), 256, 0, h->stream>>>(
         g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, hole_cnt, surv_cnt,
         h->mv_hole, h->d_op()));
     const int rc = op_end(h);
