@@ -1,0 +1,82 @@
+#!/usr/bin/env python
+"""BASELINE config 1 (the reference's own CPU-runnable case): uniform random graph, 2^16 vertices /
+1M edges = synth_uniform(65536, 1000000, 0xbeef) (acceptance_test.cpp:241), bulk init, 10 batches
+of 10K inserts, the same batches as deletes, 100K edge queries — through run_workload-style phases
+on the GPU store and on the CPU reference (oracle/_ref, or the oracle port), same inputs, per-phase
+milliseconds side by side and the final canonical state compared.
+
+    python scripts/bench_c1.py > profiles/rNN_bench_c1.json
+"""
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def phases(g, is_gpu, base, B, ups, qs, qd):
+    out = {}
+    t = time.perf_counter(); g.insert_csr(base.offsets, base.destinations) if not is_gpu else g.bulk_init(base.offsets, base.destinations)
+    out["bulk_insert_ms"] = (time.perf_counter() - t) * 1e3
+    ins, dele = [], []
+    for s, d in ups:
+        t = time.perf_counter(); g.insert_pairs(s, d); ins.append((time.perf_counter() - t) * 1e3)
+    t = time.perf_counter(); ans1 = np.asarray(g.query_edges(qs, qd) if is_gpu else g.query(qs, qd), np.uint8)
+    out["query_ms"] = (time.perf_counter() - t) * 1e3
+    for s, d in ups:
+        t = time.perf_counter(); g.delete_pairs(s, d); dele.append((time.perf_counter() - t) * 1e3)
+    ans2 = np.asarray(g.query_edges(qs, qd) if is_gpu else g.query(qs, qd), np.uint8)
+    out["insert_ms_per_batch"] = float(np.median(ins)); out["delete_ms_per_batch"] = float(np.median(dele))
+    out["insert_medges_s"] = 10000 / out["insert_ms_per_batch"] / 1e3
+    out["delete_medges_s"] = 10000 / out["delete_ms_per_batch"] / 1e3
+    out["bulk_medges_s"] = 1000000 / out["bulk_insert_ms"] / 1e3
+    out["query_us_per_query"] = out["query_ms"] * 1e3 / qs.size
+    return out, ans1, ans2
+
+
+def main():
+    from paper_2306_08252_b200 import BatchKind, DynamicGraph, GraphConfig, compute_block_size, csr_from_pairs
+    from paper_2306_08252_b200 import io as dio
+    from tests.drivers import CpuGraph, load_oracle, load_ref
+    V, E = 65536, 1000000
+    s, d = dio.synth_uniform_pairs(V, E, 0xBEEF)
+    us, ud = dio.synth_uniform_pairs(V, 100000, 0xBEEF + 1)
+    base = csr_from_pairs(BatchKind.Insert, V, s, d)
+    B = compute_block_size(base)
+    ups = [(us[i * 10000:(i + 1) * 10000], ud[i * 10000:(i + 1) * 10000]) for i in range(10)]
+    rng = np.random.default_rng(0xBEEF)
+    pick = rng.integers(0, E, 50000)
+    qs = np.concatenate([s[pick], rng.integers(0, V, 50000).astype(np.uint32)])
+    qd = np.concatenate([d[pick], rng.integers(0, V, 50000).astype(np.uint32)])
+    # GPU: one warm-up graph (module load, workspace), then the measured one
+    for rep in range(2):
+        t = time.perf_counter()
+        g = DynamicGraph(GraphConfig(pool_blocks=1 << 18), V, B)
+        init_ms = (time.perf_counter() - t) * 1e3
+        gpu, a1, a2 = phases(g, True, base, B, ups, qs, qd)
+        gpu["init_ms"] = init_ms
+        state = (g.active_edges(), g.export_csr())
+        g.close()
+    ref = load_ref()
+    lib, prefix = (ref, "ref") if ref is not None else (load_oracle(), "orc")
+    t = time.perf_counter()
+    o = CpuGraph(lib, prefix, V, B, 512 << 20, 0.5, True, os.cpu_count() or 1)
+    init_ms = (time.perf_counter() - t) * 1e3
+    cpu, b1, b2 = phases(o, False, base, B, ups, qs, qd)
+    cpu["init_ms"] = init_ms
+    so = (o.active_edges(), o.export_csr())
+    same = (state[0] == so[0] and np.array_equal(state[1][0], so[1][0]) and np.array_equal(state[1][1], so[1][1])
+            and np.array_equal(a1, b1) and np.array_equal(a2, b2))
+    print(json.dumps({"workload": "config 1: synth_uniform(65536, 1000000, 0xbeef), auto block size %d, bulk init + 10 x 10K inserts + 100K queries "
+                                  "+ the same 10 batches as deletes; host batches through the synchronous public API" % B,
+                      "gpu": gpu, "cpu_reference": dict(cpu, kind="reference" if ref is not None else "port", cores=os.cpu_count()),
+                      "state_and_answers_identical": bool(same), "queries_hit": int(a1.sum())}))
+
+
+if __name__ == "__main__":
+    main()
