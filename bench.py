@@ -59,6 +59,9 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=1_000_000)
     ap.add_argument("--block-size", type=int, default=32,
                     help="edge-block size B; 32 = one 128-byte line (0 = the reference's compute_block_size rule)")
+    ap.add_argument("--pool-initial-fraction", type=float, default=0.0,
+                    help="start with this fraction of the pre-sized pool and let the growth policy (80 %% trigger / 25 %% "
+                         "rounds / on-demand, block_pool.hpp:162-189) commit the rest in place; 0 = pre-sized, no growth")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -325,6 +328,10 @@ def run_b200_arm(args):
             gen.coo_to_csr(src, dst, V, off, csr_dst)
             del src, dst
             pool_blocks = int((E_local // B + V) * 1.25) + (4 * b) // B + 4096
+            grow = {}
+            if args.pool_initial_fraction > 0:   # queue pressure: the pool grows while the graph is built
+                grow = {"pool_max_blocks": pool_blocks}
+                pool_blocks = max(1024, int(pool_blocks * args.pool_initial_fraction))
             ws_hint = 48 * V + 8 * (E_local // B) + (64 << 20)   # scratch of the bulk build, reserved at create
             bulk_ms = []
             g = None
@@ -333,7 +340,7 @@ def run_b200_arm(args):
                     g.close()
                 t0 = time.perf_counter()
                 g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream,
-                                             workspace_bytes=ws_hint), V, B)
+                                             workspace_bytes=ws_hint, **grow), V, B)
                 create_ms = (time.perf_counter() - t0) * 1e3
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 flush.zero_()
@@ -348,7 +355,7 @@ def run_b200_arm(args):
             if not args.no_profile:   # one more, untimed, build with per-kernel events
                 g.close()
                 g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream,
-                                             workspace_bytes=ws_hint), V, B)
+                                             workspace_bytes=ws_hint, **grow), V, B)
                 g.profile_enable(True)
                 g.bulk_init(off, csr_dst)
                 g.profile_enable(False)
@@ -543,7 +550,9 @@ def run_b200_arm(args):
                    "bulk_init_gbs": a_bulk / (min(m for _, m in bulk_ms) * 1e-3) / 1e9, "peak_gbs": hbm_peak},
         "op_report": {"insert": r_ins, "delete": r_del},
         "graph": {"active_edges": final_st["active_edges"], "blocks_in_use": final_st["pool_blocks_in_use"],
-                  "max_degree": final_st["max_degree"], "digest": f"{digest[0]:016x}"},
+                  "max_degree": final_st["max_degree"], "digest": f"{digest[0]:016x}",
+                  "pool_blocks_created": final_st["pool_blocks_created"], "growth_count": final_st["growth_count"],
+                  "memory": g.memory()},
         "wall_ms_per_step": wall_ms / K,
         "bulk_init_kernels_us": bulk_kernels, "clocks": clock_rec, "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
     }
