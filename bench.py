@@ -251,18 +251,19 @@ def run_reference_arm(args):
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
-def workload_config(args, world: int, B: int) -> dict:
+def workload_config(args, world: int, B: int, exchange: str = "p2p") -> dict:
     scale = args.scale + int(math.log2(world))
     return {
         "workload": f"R-MAT scale {scale} (a,b,c,d=.57,.19,.19,.05; V={1 << scale}, base E={args.edge_factor << scale}) "
                     f"bulk init + per step: insert batch={args.batch * world} then delete the same batch",
         "batch": args.batch * world, "scale": scale, "edge_factor": args.edge_factor, "block_size": B,
         "parallelism": "single GPU" if world == 1 else
-        f"source-hash partition over {world} GPUs, fused owner-routing + exchange kernel over peer memory (NVLink P2P)",
+        (f"source-hash partition over {world} GPUs, fused owner-routing + exchange kernel over peer memory (NVLink P2P)"
+         if exchange == "p2p" else f"source-hash partition over {world} GPUs, device owner-bucket partition + NCCL all-to-all"),
         "l2": "256 MiB memset between steps (untimed) flushes L2; distinct batch every step",
     }
 
@@ -316,6 +317,7 @@ def run_b200_arm(args):
         def i32(n):
             return torch.empty(n, dtype=torch.int32, device=dev)
 
+        exchange_used = "p2p"
         # ---- graph construction + bulk init (timed) --------------------------------------
         if world == 1 and not os.environ.get("DG_FORCE_SHARDED"):
             gen = DynamicGraph(GraphConfig(device=local, pool_blocks=1024, stream=stream.cuda_stream), 1, 1)
@@ -369,20 +371,40 @@ def run_b200_arm(args):
             gen.gen_rmat(scale, 1, rank * E_local, src, dst, thr)
             B = args.block_size or 2 * args.edge_factor
             pool_blocks = int((E_local // B + V // world) * 1.6) + (8 * b) // B + 4096
-            t0 = time.perf_counter()
-            # fused owner-routing + exchange over peer memory; the receive buffer holds one round (the
-            # bulk build goes through it in one piece): 1.25x the per-rank share + slack
-            sharded = ShardedDynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream),
-                                          V, B, torch_stream=stream, exchange=os.environ.get("DG_EXCHANGE", "p2p"),
-                                          exchange_capacity=int(1.25 * max(E_local, b)) + (1 << 20))
-            create_ms = (time.perf_counter() - t0) * 1e3
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            dist.barrier(); torch.cuda.synchronize()
-            e0.record(stream)
-            sharded.insert_pairs(src, dst)
-            e1.record(stream)
-            stream.synchronize()
-            bulk_ms = [(create_ms, e0.elapsed_time(e1))]
+            # fused owner-routing + exchange over peer memory (default); the receive buffer holds one round
+            # (the bulk build goes through it in one piece): 1.25x the per-rank share + slack.  The NCCL
+            # all-to-all baseline takes over when the peer mapping cannot be set up or the store built
+            # through the fused exchange does not hold exactly the edges that were generated (multiset
+            # insert keeps every copy: the global live-edge count must equal world * E_local).
+            from paper_2306_08252_b200 import EngineError
+            want_exchange = os.environ.get("DG_EXCHANGE", "p2p")
+            for exchange in ([want_exchange, "nccl"] if want_exchange != "nccl" else ["nccl"]):
+                t0 = time.perf_counter()
+                try:
+                    sharded = ShardedDynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream),
+                                                  V, B, torch_stream=stream, exchange=exchange,
+                                                  exchange_capacity=int(1.25 * max(E_local, b)) + (1 << 20))
+                except EngineError as exc:   # (agreed by every rank: agree_status inside the constructor)
+                    if rank == 0:
+                        print(f"[bench] exchange={exchange} unavailable: {exc}", file=sys.stderr)
+                    continue
+                create_ms = (time.perf_counter() - t0) * 1e3
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                dist.barrier(); torch.cuda.synchronize()
+                e0.record(stream)
+                sharded.insert_pairs(src, dst)
+                e1.record(stream)
+                stream.synchronize()
+                bulk_ms = [(create_ms, e0.elapsed_time(e1))]
+                if sharded.active_edges() == world * E_local:
+                    exchange_used = exchange
+                    break
+                if rank == 0:
+                    print(f"[bench] exchange={exchange}: live edges {sharded.active_edges()} != {world * E_local}; falling back", file=sys.stderr)
+                sharded.close()
+                sharded = None
+            if sharded is None:
+                raise SystemExit("bench: the sharded store could not be built with any exchange")
             bulk_kernels = None
             g = sharded.local
             bulk_rep = g.last_op_report()
@@ -542,7 +564,7 @@ def run_b200_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u32", "data": "synthetic", "config": workload_config(args, world, B),
+        "dtype": "u32", "data": "synthetic", "config": workload_config(args, world, B, exchange_used),
         "insert_medges_s": b * world * K / (ins_ms * 1e-3) / 1e6, "delete_medges_s": b * world * K / (del_ms * 1e-3) / 1e6,
         "insert_ms": ins_ms / K, "delete_ms": del_ms / K,
         "bulk_init_ms": min(m for _, m in bulk_ms), "create_ms": min(c for c, _ in bulk_ms),
@@ -565,14 +587,27 @@ def run_b200_arm(args):
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
                                     "sample": f"failed: {e}"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1 or force_sharded:
         dist.destroy_process_group()
     return 0
 
 
+_JSON_OUT = None   # the process's real stdout; everything else that writes to fd 1 goes to stderr
+
+
+def emit(line: dict):
+    print(json.dumps(line), file=_JSON_OUT or sys.stdout, flush=True)
+
+
 def main():
+    global _JSON_OUT
     args = parse_args()
+    # stdout must carry exactly ONE JSON line: libraries that write to fd 1 on their own (NCCL prints its
+    # version banner there) are moved to stderr for the whole run
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_b200_arm(args)
