@@ -239,12 +239,17 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    r = cpu_reference_run(args.scale, args.edge_factor, args.batch, args.warmup, args.steps, threads, args.block_size)
+    # the B200 arm's config at N GPUs is weak-scaled (scale + log2 N, batch * N); the CPU run is a BOUNDED
+    # sample of it (at most scale 24 / 4M-entry batches: ~2 minutes on 16 cores), described in `sample`
+    world = max(1, args.gpus)
+    ref_scale = min(args.scale + int(math.log2(world)), max(args.scale, 24))
+    ref_batch = min(args.batch * world, max(args.batch, 4_000_000))
+    r = cpu_reference_run(ref_scale, args.edge_factor, ref_batch, args.warmup, args.steps, threads, args.block_size)
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "config": workload_config(args, 1, r["block_size"]),
+        "data": "synthetic", "config": workload_config(args, world, r["block_size"]),
         "insert_medges_s": r["insert_medges_s"], "delete_medges_s": r["delete_medges_s"],
         "bulk_init_ms": r["init_ms"] + r["bulk_insert_ms"],
         "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
