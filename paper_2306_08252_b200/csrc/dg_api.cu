@@ -984,6 +984,7 @@ int delete_matched(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
   uint32_t* hole_cnt = zeroed + (runs_bound + 1);
   uint32_t* surv_cnt = zeroed + 2 * (runs_bound + 1);
   uint32_t* mv_off = ws_alloc<uint32_t>(h, runs_bound + 1);
+  uint32_t* free_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   uint32_t* wl_mask = ws_alloc<uint32_t>(h, (wl_bound + 1) * g.mw);
   cudaMemsetAsync(zeroed, 0, 3 * (runs_bound + 1) * 4, h->stream);
   enqueue_match<true>(h, b, w, n, run_matched, wl_mask, nullptr);
@@ -991,10 +992,10 @@ int delete_matched(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
   for (int attempt = 0; attempt < 2; ++attempt) {
     h->ws.off = ws_mark;
     if (attempt > 0) cudaMemsetAsync(hole_cnt, 0, 2 * (runs_bound + 1) * 4, h->stream);
-    launch_alloc(h, "alloc_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{w.run_deg, run_matched},
-                 MovesOut{mv_off}, MovesFin{h->d_op(), h->mv_cap});
+    launch_alloc(h, "alloc_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{g, w.run_deg, run_matched},
+                 MovesOut{mv_off, free_off}, MovesFin{g, h->d_op(), h->mv_cap});
     DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_resident(h, wl_bound, 256, delete_holes_kernel), 256, 0, h->stream>>>(
-        g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, wl_mask, hole_cnt,
+        g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, free_off, wl_mask, hole_cnt,
         h->mv_hole, h->d_op()));
     DG_LAUNCH(h, "delete_moves_kernel", delete_moves_kernel<<<grid_resident(h, wl_bound, 256, delete_moves_kernel), 256, 0, h->stream>>>(
         g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, hole_cnt, surv_cnt,
@@ -1010,7 +1011,7 @@ int delete_matched(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
 }
 inline size_t delete_matched_ws(const dg_graph* h, uint64_t runs_bound) {
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  return 4 * aligned((runs_bound + 1) * 4) + aligned((wl_bound + 1) * ((h->B + 31) / 32) * 4) + alloc_ws_bytes();
+  return 5 * aligned((runs_bound + 1) * 4) + aligned((wl_bound + 1) * ((h->B + 31) / 32) * 4) + alloc_ws_bytes();
 }
 
 }  // namespace

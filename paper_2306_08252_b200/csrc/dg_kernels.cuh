@@ -1987,125 +1987,111 @@ match_long_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
 struct NoAux {};
 struct MovesIn {
   using Aux = NoAux;
+  GraphView g;
   const uint32_t* run_deg;
   const uint32_t* run_matched;
+  // word a: blocks past the source's new tail (they go back to the ring: the plan hands every source
+  // its range of ring positions, so the push needs neither atomics nor barriers);  word b: moves
   __device__ Sum2 operator()(unsigned long long r, Aux&) const {
     const uint32_t m = run_matched[r];
-    const uint32_t nd = run_deg[r] - m;
-    return Sum2{0ull, min(m, nd)};
+    const uint32_t d = run_deg[r];
+    const uint32_t nd = d - m;
+    const uint32_t freed = (m != 0 && g.reclaim) ? blocks_for(g, d) - blocks_for(g, nd) : 0u;
+    return Sum2{freed, min(m, nd)};
   }
 };
 struct MovesOut {
   uint32_t* mv_off;
-  __device__ void operator()(unsigned long long r, unsigned long long, unsigned long long excl_b,
+  uint32_t* free_off;
+  __device__ void operator()(unsigned long long r, unsigned long long excl_a, unsigned long long excl_b,
                              Sum2, const NoAux&) const {
     mv_off[r] = (uint32_t)excl_b;
+    free_off[r] = (uint32_t)excl_a;
   }
 };
 struct MovesFin {
+  GraphView g;
   OpState* op;
   unsigned long long mv_cap;
-  __device__ void operator()(unsigned long long, unsigned long long total) const {
+  __device__ void operator()(unsigned long long total_a, unsigned long long total) const {
     op->aux0 = total;                      // scratch entries needed
     op->aux1 = total > mv_cap ? 1ull : 0ull;  // host grows the scratch and re-runs the tail
+    if (total <= mv_cap) {                 // reclaim (block_pool.hpp:192-209): one cursor bump for the whole batch
+      op->front_old = g.st->rear;          // (first ring position of the pushed handles)
+      g.st->rear += total_a;
+      op->pushed = total_a;
+    }
   }
 };
 
 // delete, step A — a thread per block of the touched chains, reading only the
 // match masks: lists the holes below the new degree (tickets from per-source
-// counters), returns blocks past the new tail to the ring rear
-// (block_pool.hpp:192-209, warp-aggregated) and, on a source's first block,
-// repairs degree / tail / head (detach_empty_tail, graph.hpp:398-414).
+// counters), returns blocks past the new tail to the ring rear at the positions
+// the plan reserved for their source (block_pool.hpp:192-209) and, on a
+// source's first block, repairs degree / tail / head (detach_empty_tail,
+// graph.hpp:398-414).  No barriers, no shared cursor.
 __global__ void __launch_bounds__(256)
 delete_holes_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                     const uint32_t* __restrict__ wl_handle, const uint32_t* __restrict__ wl_run,
                     const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ run_matched,
-                    const uint32_t* __restrict__ mv_off, const uint32_t* __restrict__ wl_mask,
+                    const uint32_t* __restrict__ mv_off, const uint32_t* __restrict__ free_off,
+                    const uint32_t* __restrict__ wl_mask,
                     uint32_t* __restrict__ hole_cnt, unsigned long long* __restrict__ hole_addr,
                     OpState* op) {
   if (op->err || op->aux1) return;
   __shared__ unsigned long long s_warp[8];
-  __shared__ uint32_t s_cnt[8];
-  __shared__ unsigned long long s_ring_base;
   const uint32_t W = (uint32_t)op->wl_blocks;
-  const uint32_t Wpad = (W + 255u) & ~255u;   // CTA-uniform trip count (barriers inside)
-  const int lane = lane_id();
-  const unsigned lt = (1u << lane) - 1u;
-  unsigned long long pushed = 0, matched = 0;
-  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < Wpad; w += gridDim.x * blockDim.x) {
-    bool do_free = false;
-    uint32_t h = 0;
-    if (w < W) {
-      const uint32_t r = wl_run[w] & kRunMask;
-      const uint32_t m = run_matched[r];
-      if (m != 0) {
-        h = wl_handle[w];
-        const uint32_t kb = w - wl_off[r];
-        const uint32_t d = run_deg[r];
-        const uint32_t nd = d - m;
-        const uint32_t new_nb = blocks_for(g, nd);
-        const uint32_t base = kb * g.B;
-        if (base < nd) {
-          const uint32_t lim = nd - base;  // slots [0, lim) of this block stay below the new degree
-          uint32_t nh = 0;
-          for (uint32_t i = 0; i < g.mw && 32 * i < lim; ++i) {
-            uint32_t bits = wl_mask[(unsigned long long)w * g.mw + i];
-            if (lim - 32 * i < 32) bits &= (1u << (lim - 32 * i)) - 1u;
-            nh += __popc(bits);
+  const unsigned long long rear_old = op->front_old;
+  unsigned long long matched = 0;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
+    const uint32_t r = wl_run[w] & kRunMask;
+    const uint32_t m = run_matched[r];
+    if (m == 0) continue;
+    const uint32_t h = wl_handle[w];
+    const uint32_t kb = w - wl_off[r];
+    const uint32_t d = run_deg[r];
+    const uint32_t nd = d - m;
+    const uint32_t new_nb = blocks_for(g, nd);
+    const uint32_t base = kb * g.B;
+    if (base < nd) {
+      const uint32_t lim = nd - base;  // slots [0, lim) of this block stay below the new degree
+      uint32_t nh = 0;
+      for (uint32_t i = 0; i < g.mw && 32 * i < lim; ++i) {
+        uint32_t bits = wl_mask[(unsigned long long)w * g.mw + i];
+        if (lim - 32 * i < 32) bits &= (1u << (lim - 32 * i)) - 1u;
+        nh += __popc(bits);
+      }
+      if (nh) {
+        uint32_t idx = mv_off[r] + atomicAdd(&hole_cnt[r], nh);
+        for (uint32_t i = 0; i < g.mw && 32 * i < lim; ++i) {
+          uint32_t bits = wl_mask[(unsigned long long)w * g.mw + i];
+          if (lim - 32 * i < 32) bits &= (1u << (lim - 32 * i)) - 1u;
+          while (bits) {
+            const uint32_t bit = __ffs(bits) - 1;
+            bits &= bits - 1;
+            hole_addr[idx++] = (unsigned long long)h * g.B + 32 * i + bit;
           }
-          if (nh) {
-            uint32_t idx = mv_off[r] + atomicAdd(&hole_cnt[r], nh);
-            for (uint32_t i = 0; i < g.mw && 32 * i < lim; ++i) {
-              uint32_t bits = wl_mask[(unsigned long long)w * g.mw + i];
-              if (lim - 32 * i < 32) bits &= (1u << (lim - 32 * i)) - 1u;
-              while (bits) {
-                const uint32_t bit = __ffs(bits) - 1;
-                bits &= bits - 1;
-                hole_addr[idx++] = (unsigned long long)h * g.B + 32 * i + bit;
-              }
-            }
-          }
-        }
-        do_free = kb >= new_nb && g.reclaim;
-        if (kb == 0) {
-          const uint32_t v = batch_src(b, r);
-          g.deg[v] = nd;
-          if (nd == 0) {
-            g.head[v] = kNull;
-            g.tail[v] = kNull;
-          } else {
-            const uint32_t t = wl_handle[wl_off[r] + new_nb - 1];
-            g.tail[v] = t;
-            g.next[t] = kNull;
-          }
-          matched += m;
         }
       }
     }
-    // blocks past the new tail go back to the ring rear: one cursor bump per CTA iteration
-    const unsigned fm = __ballot_sync(kFull, do_free);
-    const int wid = threadIdx.x >> 5;
-    if (lane == 0) s_cnt[wid] = __popc(fm);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t tot = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t c = s_cnt[i];
-        s_cnt[i] = tot;
-        tot += c;
+    if (kb >= new_nb && g.reclaim)   // past the new tail: back to the ring, at the source's reserved positions
+      g.ring[(rear_old + free_off[r] + (kb - new_nb)) % g.ring_cap] = h;
+    if (kb == 0) {
+      const uint32_t v = batch_src(b, r);
+      g.deg[v] = nd;
+      if (nd == 0) {
+        g.head[v] = kNull;
+        g.tail[v] = kNull;
+      } else {
+        const uint32_t t = wl_handle[wl_off[r] + new_nb - 1];
+        g.tail[v] = t;
+        g.next[t] = kNull;
       }
-      s_ring_base = tot ? atomicAdd(&g.st->rear, (unsigned long long)tot) : 0ull;
-      pushed += tot;
+      matched += m;
     }
-    __syncthreads();
-    if (do_free) g.ring[(s_ring_base + s_cnt[wid] + __popc(fm & lt)) % g.ring_cap] = h;
-    __syncthreads();
   }
-  const unsigned long long tp = block_reduce_sum(pushed, s_warp);
   const unsigned long long tm = block_reduce_sum(matched, s_warp);
   if (threadIdx.x == 0) {
-    if (tp) atomicAdd(&op->pushed, tp);
     if (tm) {
       atomicAdd(&op->matched, tm);
       atomicAdd(&g.st->active_edges, (unsigned long long)(-(long long)tm));  // graph.hpp:211-213
