@@ -371,6 +371,8 @@ int dg_ingest_stage_coo(dg_ingest* q, const uint32_t* src, const uint32_t* dst, 
 /* run the op on a staged slot (waits for its copy on the graph's stream); frees the slot */
 int dg_ingest_insert(dg_ingest* q, uint32_t slot);
 int dg_ingest_delete(dg_ingest* q, uint32_t slot);
+/* drop every staged batch (after a failed op: the reference loop would have stopped there) */
+int dg_ingest_reset(dg_ingest* q);
 
 #ifdef __cplusplus
 }

@@ -217,4 +217,53 @@ class DynamicGraph {
   dg_graph* h_ = nullptr;
 };
 
+// The batch loop of run_workload (io/workload.hpp:141-155) with the host->device copy of the next
+// batch overlapped with the running op (dg_ingest_*).  submit() applies batches in order exactly as
+// insert_pairs / delete_pairs would; a failing batch throws from the call that executes it.  The
+// host arrays must stay valid until their op ran.
+class BatchIngest {
+ public:
+  BatchIngest(DynamicGraph& g, std::uint64_t max_entries, std::uint32_t depth = 2) : g_(g), depth_(depth) {
+    if (dg_ingest_create(g.handle(), max_entries, depth, &q_) != DG_OK) throw EngineError(dg_last_error(g.handle()));
+  }
+  ~BatchIngest() { dg_ingest_destroy(q_); }
+  BatchIngest(const BatchIngest&) = delete;
+  BatchIngest& operator=(const BatchIngest&) = delete;
+
+  void submit(BatchKind kind, const VertexId* src, const VertexId* dst, std::uint64_t n) {
+    if (pending_.size() == depth_) run_oldest();
+    std::uint32_t slot = 0;
+    const int rc = dg_ingest_stage_coo(q_, src, dst, n, &slot);
+    if (rc != DG_OK) raise(rc);
+    pending_.emplace_back(kind, slot);
+    if (pending_.size() == depth_) run_oldest();
+  }
+  void flush() {
+    while (!pending_.empty()) run_oldest();
+  }
+
+ private:
+  void run_oldest() {
+    const auto [kind, slot] = pending_.front();
+    pending_.erase(pending_.begin());
+    const int rc = kind == BatchKind::Insert ? dg_ingest_insert(q_, slot) : dg_ingest_delete(q_, slot);
+    if (rc != DG_OK) {
+      pending_.clear();   // later staged batches are dropped, as the reference loop would have stopped here
+      const std::string msg = dg_last_error(g_.handle()) ? dg_last_error(g_.handle()) : "";
+      dg_ingest_reset(q_);
+      if (rc == DG_ERR_DATA) throw DataError(msg);
+      throw EngineError(msg);
+    }
+  }
+  [[noreturn]] void raise(int rc) const {
+    const char* msg = dg_last_error(g_.handle());
+    if (rc == DG_ERR_DATA) throw DataError(msg ? msg : "");
+    throw EngineError(msg ? msg : "");
+  }
+  DynamicGraph& g_;
+  dg_ingest* q_ = nullptr;
+  std::uint32_t depth_;
+  std::vector<std::pair<BatchKind, std::uint32_t>> pending_;
+};
+
 }  // namespace dyngraph_b200

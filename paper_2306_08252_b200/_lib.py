@@ -112,6 +112,7 @@ SIGNATURES = {
     "dg_ingest_stage_coo": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, u32p]),
     "dg_ingest_insert": (C.c_int, [C.c_void_p, C.c_uint32]),
     "dg_ingest_delete": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "dg_ingest_reset": (C.c_int, [C.c_void_p]),
 }
 
 _lib = None

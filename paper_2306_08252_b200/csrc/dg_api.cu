@@ -2076,6 +2076,15 @@ static int ingest_run(dg_ingest* q, uint32_t slot, bool is_insert) {
   q->state[slot] = 0;
   return rc;
 }
+int dg_ingest_reset(dg_ingest* q) {
+  if (!q) return DG_ERR_DATA;
+  dg_graph* h = q->h;
+  cudaSetDevice(h->device);
+  DG_CUDA(h, cudaStreamSynchronize(q->copy));
+  for (auto& st : q->state) st = 0;
+  q->next = 0;
+  return DG_OK;
+}
 int dg_ingest_insert(dg_ingest* q, uint32_t slot) { return ingest_run(q, slot, true); }
 int dg_ingest_delete(dg_ingest* q, uint32_t slot) { return ingest_run(q, slot, false); }
 

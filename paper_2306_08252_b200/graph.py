@@ -309,8 +309,7 @@ class BatchIngest:
         rc = fn(self._q, slot)
         if rc != 0:
             self._pending.clear()
-            self._lib.dg_ingest_destroy(self._q)   # drop whatever is still staged
-            self._open()
+            self._lib.dg_ingest_reset(self._q)   # drop whatever is still staged
             self._g._check(rc)
         return rc
 
