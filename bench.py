@@ -501,7 +501,7 @@ def run_b200_arm(args):
                 # copies cross step boundaries), every H2D copy and status read-back inside it; no L2
                 # flush in this pass — every step's inputs come from host memory and a step touches
                 # more graph data (> 230 MB) than the L2 holds.
-                q = g.ingest(b, depth=3)
+                q = g.ingest(b, depth=int(os.environ.get("DG_E2E_DEPTH", "3")))
                 for i in range(W):
                     hs, hd = host_batches[i]
                     q.submit("insert", hs, hd); q.submit("delete", hs, hd)

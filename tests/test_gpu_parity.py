@@ -193,6 +193,36 @@ def test_csr_native_block_path_hubs_fills_and_rollback():
     g.close()
 
 
+@pytest.mark.parametrize("V", [1, 31, 32, 33, 1000])
+def test_csr_native_block_path_degree_boundaries(V):
+    """B = 32 CSR insert at every boundary of the append pass: degrees around a block (31 / 32 / 33),
+    around the heavy threshold (127 / 128 / 129), around one staging round (1023 / 1024 / 1025) and
+    beyond (multi-item sources), vertex counts that do not fill a 32-vertex group, and repeated
+    inserts so every source resumes at an arbitrary tail offset (graph.hpp:344-349)."""
+    from paper_2306_08252_b200 import BatchKind, CsrBatch
+    rng = np.random.default_rng(V)
+    pattern = [0, 1, 31, 32, 33, 0, 127, 128, 129, 5, 1023, 1024, 1025, 0, 0, 2048, 4097, 7, 64, 96]
+    cfg = {"v0": V, "block_size": 32, "arena_bytes": 1 << 30}
+    g, o = _gpu(cfg, pool_blocks=1 << 16), _orc(cfg)
+    script = []
+    for rnd in range(4):
+        degs = np.array([pattern[(v + 3 * rnd) % len(pattern)] for v in range(V)], np.int64)
+        if V == 1000:
+            degs[rng.integers(0, V, 600)] = 0        # whole groups of zero-degree vertices
+        off = np.zeros(V + 1, np.uint64)
+        np.cumsum(degs, out=off[1:])
+        dst = rng.integers(0, V, int(off[-1])).astype(np.uint32)
+        script.append(("insert_csr", off, dst))
+        script.append(("check",))
+        if rnd == 1:   # delete a third of what was just inserted, as COO
+            src = np.repeat(np.arange(V, dtype=np.uint32), degs)
+            pick = rng.random(dst.size) < 0.33
+            script.append(("delete", src[pick], dst[pick]))
+            script.append(("check",))
+    assert_same(run_script(g, script), run_script(o, script), f"csr boundaries V={V}")
+    g.close()
+
+
 def test_csr_native_block_path_unaligned_device_pointers():
     """The TMA staging aligns the source range down to 16 bytes and copies the ragged tail through
     the lanes: device batches starting at every 4-byte phase must give the same graph."""
