@@ -716,3 +716,86 @@ def test_sharded_store_world_size_1_on_gpu(exchange):
     p.join(timeout=300)
     assert p.exitcode == 0
     assert q.get(timeout=5) == "ok"
+
+
+def _sharded_world2_one_gpu(rank, port, q):
+    """One of two ranks that share cuda:0: gloo carries the collectives (NCCL refuses two ranks on
+    one device), CUDA IPC maps the OTHER process's receive buffers, so the fused owner-routing +
+    exchange kernel really stores into and bumps cursors in a peer's memory."""
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2306_08252_b200 import GraphConfig
+        from paper_2306_08252_b200.sharded import ShardedDynamicGraph
+        rng = np.random.default_rng(17)   # same stream on both ranks: every rank feeds ITS half of each batch
+        V = 5000
+        sg = ShardedDynamicGraph(GraphConfig(pool_blocks=1 << 15), V, 32, exchange="p2p", exchange_capacity=1 << 17)
+        orc = CpuGraph(load_oracle(), "orc", V, 32, 1 << 28)
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
+        log = []
+        for it in range(7):
+            s = (rng.zipf(1.35, 40000) % V).astype(np.uint32)
+            d = rng.integers(0, V, 40000).astype(np.uint32)
+            if it % 3 == 2:
+                s[:15000], d[:15000] = log[-1][0][:15000], log[-1][1][:15000]
+                sg.delete_pairs(dev(s[rank::2]), dev(d[rank::2])); orc.delete_pairs(s, d)
+            else:
+                sg.insert_pairs(dev(s[rank::2]), dev(d[rank::2])); orc.insert_pairs(s, d)
+            log.append((s, d))
+            assert sg.active_edges() == orc.active_edges(), (it, sg.active_edges(), orc.active_edges())
+        qs = np.concatenate([log[0][0][:4000], rng.integers(0, V + 5, 2000).astype(np.uint32)])
+        qd = np.concatenate([log[0][1][:4000], rng.integers(0, V + 5, 2000).astype(np.uint32)])
+        ans = sg.query_edges(dev(qs[rank::2]), dev(qd[rank::2])).cpu().numpy()
+        assert np.array_equal(ans, orc.query(qs[rank::2], qd[rank::2]))
+        # this rank's shard: local id l holds vertex perm_inv(l * world + rank)
+        off, dst = sg.local.export_csr(sorted=True)
+        ooff, odst = orc.export_csr(sorted=True)
+        seen = 0
+        for lid in range(len(off) - 1):
+            v = sg._lib.dg_owner_perm_inv(lid * 2 + rank, sg.bits)
+            got = dst[int(off[lid]):int(off[lid + 1])]
+            want = odst[int(ooff[v]):int(ooff[v + 1])] if v < V else np.zeros(0, np.uint32)
+            assert np.array_equal(got, want), (lid, v)
+            seen += len(got)
+        assert 0 < seen < orc.active_edges()          # both ranks own a real share
+        d_s, n_s = sg.digest()
+        off2, dst2 = orc.export_csr(sorted=False)
+        srcs = np.repeat(np.arange(V, dtype=np.uint32), np.diff(off2.astype(np.int64)))
+        assert (d_s, n_s) == (_np_digest(srcs, dst2), len(dst2))
+        # a bad source on ONE rank rejects the batch on both (status agreement), nothing changes
+        bad_s = np.array([V + 7 if rank == 1 else 3], np.uint32)
+        try:
+            sg.insert_pairs(dev(bad_s), dev(np.array([0], np.uint32)))
+            q.put(f"rank {rank}: no error raised")
+            return
+        except Exception as e:
+            assert "DataError" in type(e).__name__, type(e)
+        assert sg.active_edges() == orc.active_edges()
+        sg.close()
+        q.put("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_store_world_size_2_peer_memory_on_one_gpu():
+    """The fused owner-routing + exchange kernel against a REAL peer: two processes on the one GPU,
+    each mapping the other's receive buffers through CUDA IPC (the same mechanism that maps NVLink
+    peers on an 8-GPU box), gloo for the collectives.  Full parity with the oracle on both shards."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_sharded_world2_one_gpu, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=300)
+    assert [p.exitcode for p in ps] == [0, 0]
+    assert sorted(q.get(timeout=5) for _ in range(2)) == ["ok", "ok"]
