@@ -289,13 +289,22 @@ def run_b200_arm(args):
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("bench.py --gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
+    # DG_BENCH_ONE_DEVICE=1: functional check of the N > 1 flow where only one GPU exists — every rank
+    # uses cuda:0 and gloo carries the collectives (NCCL refuses two ranks on one device); the peers'
+    # buffers are still mapped through CUDA IPC.  Timings of such a run mean nothing.
+    one_device = bool(os.environ.get("DG_BENCH_ONE_DEVICE"))
+    if one_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     force_sharded = bool(os.environ.get("DG_FORCE_SHARDED"))   # exercise the multi-GPU path on one GPU
     if world > 1 or force_sharded:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        if one_device:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
     from paper_2306_08252_b200 import DynamicGraph, GraphConfig, rmat
     from paper_2306_08252_b200._lib import load
