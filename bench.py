@@ -568,6 +568,7 @@ def run_b200_arm(args):
         clock_rec = clocks.stop()   # sampled over the timed, split, e2e and per-kernel passes
         final_st = g.stats()
         digest = g.digest()
+        global_edges = sharded.active_edges() if sharded is not None else final_st["active_edges"]   # (collective)
 
     value = 2 * b * world * K / (total_ms * 1e-3) / 1e6
     r_ins, r_del = reps[-1]
@@ -585,7 +586,8 @@ def run_b200_arm(args):
         "op_hbm": {"insert_gbs": a_ins / (ins_ms / K * 1e-3) / 1e9, "delete_gbs": a_del / (del_ms / K * 1e-3) / 1e9,
                    "bulk_init_gbs": a_bulk / (min(m for _, m in bulk_ms) * 1e-3) / 1e9, "peak_gbs": hbm_peak},
         "op_report": {"insert": r_ins, "delete": r_del},
-        "graph": {"active_edges": final_st["active_edges"], "blocks_in_use": final_st["pool_blocks_in_use"],
+        "graph": {"active_edges": global_edges, "rank0_active_edges": final_st["active_edges"],
+                  "blocks_in_use": final_st["pool_blocks_in_use"],
                   "max_degree": final_st["max_degree"], "digest": f"{digest[0]:016x}",
                   "pool_blocks_created": final_st["pool_blocks_created"], "growth_count": final_st["growth_count"],
                   "memory": g.memory()},
