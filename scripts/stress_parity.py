@@ -21,12 +21,56 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seeds", type=int, default=200)
     ap.add_argument("--first", type=int, default=5000)
+    ap.add_argument("--hubs", action="store_true",
+                    help="hub-heavy scripts instead of the verify mix: few vertices, zipf sources, 50K-400K-entry batches "
+                         "(chains of thousands of blocks, table tiers with several 4096-target slices, heavy CSR items)")
     a = ap.parse_args()
     from paper_2306_08252_b200 import BatchKind, DynamicGraph, GraphConfig, csr_from_pairs
     from tests.drivers import CpuGraph, GpuGraph, assert_same, load_oracle, run_script
     from tests.workloads import make_workload
     orc = load_oracle()
     fails, t0 = 0, time.time()
+    if a.hubs:
+        for seed in range(a.first, a.first + a.seeds):
+            rng = np.random.default_rng(seed)
+            V = int(rng.choice([50, 700, 5000, 40000]))
+            B = int(rng.choice([32, 32, 32, 8, 33]))
+            zipf = float(rng.choice([1.1, 1.3, 1.8]))
+            script, log = [], []
+            for it in range(int(rng.integers(4, 9))):
+                n = int(rng.choice([50000, 150000, 400000]))
+                s = (rng.zipf(zipf, n) % V).astype(np.uint32)
+                d = rng.integers(0, V, n).astype(np.uint32)
+                kind = "insert" if it < 2 or rng.random() < 0.55 else "delete"
+                if kind == "delete":
+                    ps, pd = log[int(rng.integers(0, len(log)))]
+                    k = min(n, len(ps)) * 7 // 10
+                    s[:k], d[:k] = ps[:k], pd[:k]
+                else:
+                    log.append((s, d))
+                if rng.integers(0, 3) == 0:
+                    b = csr_from_pairs(BatchKind.Insert if kind == "insert" else BatchKind.Delete, V, s, d)
+                    script.append((kind + "_csr", b.offsets, b.destinations))
+                else:
+                    script.append((kind, s, d))
+                script.append(("check",))
+            qs, qd = log[0][0][:20000].copy(), log[0][1][:20000].copy()
+            qd[::3] = rng.integers(0, V, len(qd[::3])).astype(np.uint32)
+            script.append(("query", qs, qd))
+            grow = bool(rng.integers(0, 2))
+            g = GpuGraph.__new__(GpuGraph)
+            g.g = DynamicGraph(GraphConfig(pool_blocks=(256 if grow else 1 << 19), pool_max_blocks=(1 << 20 if grow else 0),
+                                           group=str(rng.choice(["auto", "radix", "count"]))), V, B)
+            o = CpuGraph(orc, "orc", V, B, 4 << 30, 0.5, True, 1)
+            try:
+                assert_same(run_script(g, script), run_script(o, script), f"hub seed {seed}")
+            except AssertionError as e:
+                fails += 1
+                print(f"FAIL hub seed={seed} V={V} B={B} zipf={zipf} grow={grow}: {str(e)[:200]}", flush=True)
+            finally:
+                g.close(); o.close()
+        print(f"stress_parity --hubs: {a.seeds} seeds, {fails} failures, {time.time() - t0:.0f} s")
+        return 1 if fails else 0
     for seed in range(a.first, a.first + a.seeds):
         rng = np.random.default_rng(seed ^ 0xABCDEF)
         cfg, script = make_workload(seed, max_vertices=6000, max_edges=int(rng.choice([3000, 30000, 150000])),
