@@ -800,31 +800,39 @@ Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound,
   return w;
 }
 
-// match over an enumerated worklist: three tiers by the number of targets per source
-template <bool kIsDelete>
-void enqueue_match(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t n_batch,
-                   uint32_t* run_matched, uint32_t* wl_mask, uint8_t* hit) {
+// match over an enumerated worklist: three tiers by the number of targets per source.  kNative: B = 32
+// (block size, mask words and the 16-byte staging are compile-time constants); otherwise the same kernels
+// with 4-byte staging copies and ceil(B / 32) passes per block.
+template <bool kIsDelete, bool kNative>
+void enqueue_match_impl(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t n_batch,
+                        uint32_t* run_matched, uint32_t* wl_mask, uint8_t* hit) {
   GraphView g = view(h);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   const size_t med_smem = kIsDelete ? kMedSmemDelete : kMedSmemQuery;
   const size_t long_smem = kIsDelete ? kLongSmemDelete : kLongSmemQuery;
   // opt in to > 48 KB of dynamic shared memory (per device: cheap enough to repeat)
-  cudaFuncSetAttribute(match_med_kernel<kIsDelete>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)med_smem);
-  cudaFuncSetAttribute(match_long_kernel<kIsDelete>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_smem);
+  cudaFuncSetAttribute(match_med_kernel<kIsDelete, kNative>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)med_smem);
+  cudaFuncSetAttribute(match_long_kernel<kIsDelete, kNative>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_smem);
   // the tiers touch disjoint blocks: side by side, heaviest items first
   fork(h);
   const int long_grid = (int)std::min<uint64_t>(long_items_bound(h, n_batch), (uint64_t)h->sm_count * 3);
   DG_LAUNCH(h, kIsDelete ? "match_long_kernel<delete>" : "match_long_kernel<query>",
-            match_long_kernel<kIsDelete><<<long_grid, kLongThreads, long_smem, lane(h, 1)>>>(
+            match_long_kernel<kIsDelete, kNative><<<long_grid, kLongThreads, long_smem, lane(h, 1)>>>(
                 g, b, w.wl_off, w.wl_handle, w.long_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
   const int med_grid = (int)std::min<uint64_t>(grid_for(h, med_items_bound(h, n_batch), 8), (uint64_t)h->sm_count * 4);
   DG_LAUNCH(h, kIsDelete ? "match_med_kernel<delete>" : "match_med_kernel<query>",
-            match_med_kernel<kIsDelete><<<med_grid, 256, med_smem, lane(h, 2)>>>(
+            match_med_kernel<kIsDelete, kNative><<<med_grid, 256, med_smem, lane(h, 2)>>>(
                 g, b, w.wl_off, w.wl_handle, w.med_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
   DG_LAUNCH(h, kIsDelete ? "match_tiny_kernel<delete>" : "match_tiny_kernel<query>",
-            match_tiny_kernel<kIsDelete><<<grid_resident(h, wl_bound, 256, match_tiny_kernel<kIsDelete>), 256, 0, lane(h, 0)>>>(
+            match_tiny_kernel<kIsDelete, kNative><<<grid_resident(h, wl_bound, 256, match_tiny_kernel<kIsDelete, kNative>), 256, 0, lane(h, 0)>>>(
                 g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
   join(h);
+}
+template <bool kIsDelete>
+void enqueue_match(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t n_batch,
+                   uint32_t* run_matched, uint32_t* wl_mask, uint8_t* hit) {
+  if (h->B == 32) enqueue_match_impl<kIsDelete, true>(h, b, w, n_batch, run_matched, wl_mask, hit);
+  else enqueue_match_impl<kIsDelete, false>(h, b, w, n_batch, run_matched, wl_mask, hit);
 }
 
 // ---- grouping a COO batch by source --------------------------------------------------------------

@@ -118,6 +118,22 @@ __device__ __forceinline__ uint4 block_chunk(uint32_t (*stg)[32], int u, int c) 
 __device__ __forceinline__ uint32_t block_slot(uint32_t (*stg)[32], int u, uint32_t s) {
   return stg[u][((((s >> 2) + u) & 7) << 2) | (s & 3)];
 }
+// Any block size: pass p stages words [32p, min(32p + 32, B)) of up to 32 blocks into the same
+// swizzled rows, one 4-byte cp.async per lane and block (blocks of B != 32 words are not 16-byte
+// aligned), so the lane-per-block compare below runs unchanged on 32-word rows; a block of B > 32
+// slots takes ceil(B / 32) passes and one 32-bit mask word per pass.
+__device__ __forceinline__ void stage_rows32(const GraphView& g, uint32_t (*dst)[32], uint32_t hd_lane,
+                                             unsigned want, uint32_t p) {
+  const int lane = lane_id();
+  const uint32_t nwords = min(32u, g.B - 32u * p);
+#pragma unroll 4
+  for (int u = 0; u < 32; ++u) {
+    const uint32_t hu = __shfl_sync(kFull, hd_lane, u);
+    if (((want >> u) & 1u) && (uint32_t)lane < nwords)
+      cp_async4(&dst[u][(((((uint32_t)lane >> 2) + u) & 7) << 2) | ((uint32_t)lane & 3)],
+                g.slab + (unsigned long long)hu * g.B + 32u * p + lane);
+  }
+}
 // second, independent hash for the membership filters
 __device__ __forceinline__ uint32_t filter_hash(uint32_t x, int bits) { return (x * 0x85EBCA6Bu) >> (32 - bits); }
 
@@ -1542,8 +1558,9 @@ enumerate_big_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_o
 //   first compare.  Compare phase: per block, the <= 8 targets are broadcast
 //   reads from the strip; __ballot_sync builds the match mask, lane u keeps
 //   block u's mask so masks and counters leave coalesced.
-//   Other block sizes: one thread per block, scalar loop.
-template <bool kIsDelete>
+//   Other block sizes: the same with 4-byte staging copies and ceil(B / 32) passes of 32 slots
+//   (stage_rows32), one mask word per pass.
+template <bool kIsDelete, bool kNative>
 __global__ void __launch_bounds__(256)
 match_tiny_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                   const uint32_t* __restrict__ wl_handle, const uint32_t* __restrict__ wl_run,
@@ -1554,9 +1571,11 @@ match_tiny_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
   __shared__ __align__(16) uint32_t s_slots[8][32][32];  // [warp][block][slot]
   const uint32_t W = (uint32_t)op->wl_blocks;
   unsigned long long slots = 0;
-  if (g.B == 32) {
+  {
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const int lane = lane_id();
+    const uint32_t B = kNative ? 32u : g.B;     // (compile-time constants on the native path)
+    const uint32_t mw = kNative ? 1u : g.mw;
     uint32_t(*stg)[32] = s_slots[threadIdx.x >> 5];
     for (uint32_t w0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; w0 < W; w0 += nwarps * 32u) {
       // ---- metadata: lane = block
@@ -1569,104 +1588,67 @@ match_tiny_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
       const bool tiny = !(tag & kTierBit);
       const unsigned tmask32 = __ballot_sync(kFull, tiny);
       if (tmask32 == 0) continue;
-      // ---- stage: every tiny block of the group in flight at once
-      stage_blocks32(g, stg, h, tmask32);
-      uint32_t r = 0, rs = 0, k = 0, cnt = 0;
+      // ---- stage (first 32 words): every tiny block of the group in flight at once
+      if (kNative) stage_blocks32(g, stg, h, tmask32); else stage_rows32(g, stg, h, tmask32, 0);
+      uint32_t r = 0, rs = 0, k = 0, cb = 0;
       uint32_t tg[kTinyTargets];
       if (tiny) {
         r = tag;
         rs = b.run_start[r];
         k = b.run_end[r] - rs;
-        cnt = min(32u, run_deg[r] - (w - wl_off[r]) * 32u);
+        cb = min(B, run_deg[r] - (w - wl_off[r]) * B);   // live slots of this block
       }
 #pragma unroll
       for (int j = 0; j < (int)kTinyTargets; ++j) tg[j] = ((uint32_t)j < k) ? batch_value(b, rs + j) : kTomb;
-      slots += cnt;
-      cp_async_wait_all();
-      __syncwarp();
-      // ---- compare: lane = block.  Pass 1 tests every slot against a 64-bit filter of the lane's
-      // targets (6 instructions per slot); pass 2 compares only the few candidates exactly.
-      if (tiny) {
-        unsigned long long filt = 0;
+      slots += cb;
+      unsigned long long filt = 0;
 #pragma unroll
-        for (int j = 0; j < (int)kTinyTargets; ++j)
-          if ((uint32_t)j < k) filt |= 1ull << filter_hash(tg[j], 6);
-        uint32_t cand = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 v = block_chunk(stg, lane, c);
-          cand |= (uint32_t)((filt >> filter_hash(v.x, 6)) & 1ull) << (4 * c);
-          cand |= (uint32_t)((filt >> filter_hash(v.y, 6)) & 1ull) << (4 * c + 1);
-          cand |= (uint32_t)((filt >> filter_hash(v.z, 6)) & 1ull) << (4 * c + 2);
-          cand |= (uint32_t)((filt >> filter_hash(v.w, 6)) & 1ull) << (4 * c + 3);
-        }
-        cand &= cnt == 32 ? 0xFFFFFFFFu : ((1u << cnt) - 1u);  // slots past deg hold stale values
-        uint32_t mask = 0;
-        while (cand) {
-          const uint32_t bit = __ffs(cand) - 1;
-          cand &= cand - 1;
-          const uint32_t e = block_slot(stg, lane, bit);
-#pragma unroll
-          for (int j = 0; j < (int)kTinyTargets; ++j) {
-            if ((uint32_t)j < k && e == tg[j]) {
-              mask |= 1u << bit;
-              if (!kIsDelete) hit[rs + j] = 1;
-            }
-          }
-        }
-        if (kIsDelete) {
-          wl_mask[w] = mask;
-          if (mask) atomicAdd(&run_matched[r], (uint32_t)__popc(mask));
-          while (mask) {
-            const uint32_t bit = __ffs(mask) - 1;
-            mask &= mask - 1;
-            g.slab[(unsigned long long)h * 32u + bit] = kTomb;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  } else {
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
-      const uint32_t tag = wl_run[w];
-      const uint32_t h = wl_handle[w];
-      if (tag & kTierBit) continue;  // the table tiers' work
-      const uint32_t r = tag;
-      const uint32_t rs = b.run_start[r];
-      const uint32_t k = b.run_end[r] - rs;
-      const uint32_t d = run_deg[r];
-      const uint32_t kb = w - wl_off[r];
-      const uint32_t cnt = min(g.B, d - kb * g.B);
-      slots += cnt;
-      uint32_t* blk = g.slab + (unsigned long long)h * g.B;
-      uint32_t tg[kTinyTargets];
-#pragma unroll
-      for (int j = 0; j < (int)kTinyTargets; ++j) tg[j] = ((uint32_t)j < k) ? batch_value(b, rs + j) : kTomb;
+      for (int j = 0; j < (int)kTinyTargets; ++j)
+        if ((uint32_t)j < k) filt |= 1ull << filter_hash(tg[j], 6);
       uint32_t matched = 0;
-      for (uint32_t s0 = 0; s0 < cnt; s0 += 32) {
-        uint32_t mask = 0;
-        const uint32_t ns = min(32u, cnt - s0);
-        for (uint32_t s = 0; s < ns; ++s) {
-          const uint32_t e = blk[s0 + s];
-          bool found = false;
+#pragma unroll 1
+      for (uint32_t p = 0; p < mw; ++p) {   // one pass per 32 slots of the block (B = 32: one)
+        if (p > 0) stage_rows32(g, stg, h, tmask32, p);
+        cp_async_wait_all();
+        __syncwarp();
+        // ---- compare: lane = block.  Pass 1 tests every slot against a 64-bit filter of the lane's
+        // targets (6 instructions per slot); pass 2 compares only the few candidates exactly.
+        if (tiny) {
+          const uint32_t cnt = cb > 32u * p ? min(32u, cb - 32u * p) : 0u;
+          uint32_t cand = 0;
 #pragma unroll
-          for (int j = 0; j < (int)kTinyTargets; ++j) {
-            if ((uint32_t)j < k && tg[j] == e) {
-              found = true;
-              if (!kIsDelete) hit[rs + j] = 1;
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = block_chunk(stg, lane, c);
+            cand |= (uint32_t)((filt >> filter_hash(v.x, 6)) & 1ull) << (4 * c);
+            cand |= (uint32_t)((filt >> filter_hash(v.y, 6)) & 1ull) << (4 * c + 1);
+            cand |= (uint32_t)((filt >> filter_hash(v.z, 6)) & 1ull) << (4 * c + 2);
+            cand |= (uint32_t)((filt >> filter_hash(v.w, 6)) & 1ull) << (4 * c + 3);
+          }
+          cand &= cnt == 32 ? 0xFFFFFFFFu : ((1u << cnt) - 1u);  // slots past deg (and past B) hold stale values
+          uint32_t mask = 0;
+          while (cand) {
+            const uint32_t bit = __ffs(cand) - 1;
+            cand &= cand - 1;
+            const uint32_t e = block_slot(stg, lane, bit);
+#pragma unroll
+            for (int j = 0; j < (int)kTinyTargets; ++j) {
+              if ((uint32_t)j < k && e == tg[j]) {
+                mask |= 1u << bit;
+                if (!kIsDelete) hit[rs + j] = 1;
+              }
             }
           }
-          if (found) mask |= 1u << s;
-        }
-        if (kIsDelete) {
-          wl_mask[(unsigned long long)w * g.mw + (s0 >> 5)] = mask;
-          matched += __popc(mask);
-          while (mask) {
-            const uint32_t bit = __ffs(mask) - 1;
-            mask &= mask - 1;
-            blk[s0 + bit] = kTomb;
+          if (kIsDelete) {
+            wl_mask[(unsigned long long)w * mw + p] = mask;
+            matched += (uint32_t)__popc(mask);
+            while (mask) {
+              const uint32_t bit = __ffs(mask) - 1;
+              mask &= mask - 1;
+              g.slab[(unsigned long long)h * B + 32u * p + bit] = kTomb;
+            }
           }
         }
+        __syncwarp();   // the rows are restaged by the next pass / group
       }
       if (kIsDelete && matched) atomicAdd(&run_matched[r], matched);
     }
@@ -1706,13 +1688,12 @@ __device__ __forceinline__ int table_find(const uint32_t* tab, uint32_t tmask, i
 // holds the handle of block u in lane u.  first: this is the first (or only)
 // table slice for these blocks, so the mask words are stored rather than OR-ed.
 // Returns the number of matches (valid in every lane).
-//   B = 32 (one line per block): ALL blocks of the group are staged in the warp's
-//   shared-memory strip `stg` with asynchronous copies (up to 32 x 128 bytes in
-//   flight per warp), then a rolled loop probes one slot per lane and collects a
-//   __ballot_sync mask per block; lane u keeps block u's mask so the masks leave
-//   coalesced.
-//   Other block sizes: scalar-per-block loop, 8 blocks at a time.
-template <bool kIsDelete>
+//   ALL blocks of the group are staged in the warp's shared-memory strip `stg` with
+//   asynchronous copies (B = 32: one 128-byte line per block, 16-byte copies; other
+//   block sizes: 32 words per pass, 4-byte copies, ceil(B / 32) passes), then each
+//   lane filters and probes the 32 staged slots of ITS block; lane u keeps block
+//   u's mask word so the masks leave coalesced.
+template <bool kIsDelete, bool kNative>
 __device__ __forceinline__ uint32_t table_scan(const GraphView& g, const uint32_t* tab, uint8_t* flag,
                                                uint32_t tmask, int hshift, const uint32_t* bm, int bm_bits,
                                                uint32_t (*stg)[32],
@@ -1721,19 +1702,25 @@ __device__ __forceinline__ uint32_t table_scan(const GraphView& g, const uint32_
                                                uint32_t* __restrict__ wl_mask, bool first,
                                                unsigned long long& slots) {
   const int lane = lane_id();
+  const uint32_t B = kNative ? 32u : g.B;     // (compile-time constants on the native path)
+  const uint32_t mw = kNative ? 1u : g.mw;
+  const unsigned want = ng >= 32 ? 0xFFFFFFFFu : ((1u << ng) - 1u);
+  // live slots of the lane's block: every block but possibly the chain's last one is full
+  const uint32_t rem = d - kb_first * B;              // slots from the group's first block to the chain end
+  const uint32_t cb = ((uint32_t)lane < ng && rem > B * lane) ? min(B, rem - B * lane) : 0u;
   uint32_t matched = 0;
-  if (g.B == 32) {
-    // slots of the group: every block but possibly the chain's last one is full
-    const uint32_t rem = d - kb_first * 32u;            // slots from the group's first block to the chain end
-    const uint32_t gslots = min(rem, ng * 32u);
-    stage_blocks32(g, stg, hd_lane, ng >= 32 ? 0xFFFFFFFFu : ((1u << ng) - 1u));
+#pragma unroll 1
+  for (uint32_t p = 0; p < mw; ++p) {   // one pass per 32 slots of the blocks (B = 32: one)
+    // ALL blocks of the group are staged in the warp's shared-memory strip with asynchronous copies
+    // (up to 32 x 128 bytes in flight per warp)
+    if (kNative) stage_blocks32(g, stg, hd_lane, want); else stage_rows32(g, stg, hd_lane, want, p);
     cp_async_wait_all();
     __syncwarp();
     // lane = block.  Pass 1 tests the lane's 32 slots against the bitmap filter of the targets;
     // pass 2 probes the table only for the candidates.
     uint32_t mask = 0;
     if ((uint32_t)lane < ng) {
-      const uint32_t cnt = min(32u, gslots - 32u * lane);
+      const uint32_t cnt = cb > 32u * p ? min(32u, cb - 32u * p) : 0u;
       uint32_t cand = 0;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -1763,57 +1750,27 @@ __device__ __forceinline__ uint32_t table_scan(const GraphView& g, const uint32_
         }
       }
       if (kIsDelete) {
-        if (first) wl_mask[w_first + lane] = mask;
-        else if (mask) wl_mask[w_first + lane] |= mask;  // the same warp owns these blocks in every slice
+        uint32_t* mword = &wl_mask[(unsigned long long)(w_first + lane) * mw + p];
+        if (first) *mword = mask;
+        else if (mask) *mword |= mask;  // the same warp owns these blocks in every slice
         uint32_t m2 = mask;
         while (m2) {
           const uint32_t bit = __ffs(m2) - 1;
           m2 &= m2 - 1;
-          g.slab[(unsigned long long)hd_lane * 32u + bit] = kTomb;
+          g.slab[(unsigned long long)hd_lane * B + 32u * p + bit] = kTomb;
         }
       }
     }
-    matched = __popc(mask);
-#pragma unroll
-    for (int dlt = 16; dlt > 0; dlt >>= 1) matched += __shfl_xor_sync(kFull, matched, dlt);
-    if (first && lane == 0) slots += gslots;
-    __syncwarp();  // the staging strip is reused by the caller's next group
-    return matched;
+    matched += __popc(mask);
+    __syncwarp();  // the staging strip is reused by the next pass / the caller's next group
   }
-  for (uint32_t u0 = 0; u0 < ng; u0 += 8) {
-    uint32_t e[8], cn[8];
-    uint32_t* blk[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t hd = __shfl_sync(kFull, hd_lane, (u0 + u) & 31);
-      blk[u] = g.slab + (unsigned long long)hd * g.B;
-      cn[u] = (u0 + u < ng) ? min(g.B, d - (kb_first + u0 + u) * g.B) : 0u;
-      e[u] = ((uint32_t)lane < cn[u]) ? blk[u][lane] : kTomb;
-    }
+  for (int dlt = 16; dlt > 0; dlt >>= 1) matched += __shfl_xor_sync(kFull, matched, dlt);
+  if (first) {
+    uint32_t gs = cb;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (cn[u] == 0) continue;  // warp-uniform
-      for (uint32_t s0 = 0; s0 < cn[u]; s0 += 32) {
-        const uint32_t s = s0 + lane;
-        const uint32_t ev = (s0 == 0) ? e[u] : ((s < cn[u]) ? blk[u][s] : kTomb);
-        bool found = false;
-        if (ev != kTomb) {  // padding lanes and entries tombstoned by an earlier slice
-          const int pos = table_find(tab, tmask, hshift, ev);
-          found = pos >= 0;
-          if (!kIsDelete && found) flag[pos] = 1;
-        }
-        if (kIsDelete) {
-          const unsigned m = __ballot_sync(kFull, found);
-          if (found) blk[u][s] = kTomb;
-          if (lane == 0) {
-            uint32_t* mword = &wl_mask[(unsigned long long)(w_first + u0 + u) * g.mw + (s0 >> 5)];
-            *mword = first ? m : (*mword | m);
-          }
-          matched += __popc(m);
-        }
-      }
-      if (first && lane == 0) slots += cn[u];
-    }
+    for (int dlt = 16; dlt > 0; dlt >>= 1) gs += __shfl_xor_sync(kFull, gs, dlt);
+    if (lane == 0) slots += gs;
   }
   return matched;
 }
@@ -1826,7 +1783,7 @@ constexpr uint32_t kMedTable = 512;   // >= 4 x kMedTargets: short probe sequenc
 constexpr int kMedFilterBits = 12;     // 4096-bit membership filter per warp: <= 3% false positives
 constexpr size_t kMedSmemDelete = 8 * (kMedTable * 4 + 32 * 32 * 4 + (1u << kMedFilterBits) / 8);
 constexpr size_t kMedSmemQuery = kMedSmemDelete + 8 * kMedTable;
-template <bool kIsDelete>
+template <bool kIsDelete, bool kNative>
 __global__ void __launch_bounds__(256, 4)
 match_med_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                  const uint32_t* __restrict__ wl_handle, const uint2* __restrict__ items,
@@ -1872,7 +1829,7 @@ match_med_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
     for (uint32_t i = lane; i < k; i += 32)
       table_insert(tab, tmask, hshift, bm, kMedFilterBits, batch_value(b, rs + i));
     __syncwarp();
-    const uint32_t matched = table_scan<kIsDelete>(g, tab, flag, tmask, hshift, bm, kMedFilterBits, stg, hd_all, nb,
+    const uint32_t matched = table_scan<kIsDelete, kNative>(g, tab, flag, tmask, hshift, bm, kMedFilterBits, stg, hd_all, nb,
                                                    d, kb0, wbase + kb0, wl_mask, true, slots);
     if (kIsDelete) {
       if (lane == 0 && matched) atomicAdd(&run_matched[r], matched);
@@ -1901,7 +1858,7 @@ constexpr int kLongFilterBits = 16;    // 64K-bit membership filter per CTA: <= 
 constexpr size_t kLongSmemDelete = (kLongThreads / 32) * 32 * 32 * 4 + kTableSize * 4 + (1u << kLongFilterBits) / 8;
 constexpr size_t kLongSmemQuery = kLongSmemDelete + kTableSize;
 
-template <bool kIsDelete>
+template <bool kIsDelete, bool kNative>
 __global__ void __launch_bounds__(kLongThreads)
 match_long_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                   const uint32_t* __restrict__ wl_handle, const uint2* __restrict__ items,
@@ -1953,7 +1910,7 @@ match_long_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
         const uint32_t kbg = kb0 + 32 * gi;
         const uint32_t ng = min(32u, kb1 - kbg);
         const uint32_t hd_lane = ((uint32_t)lane < ng) ? wl_handle[wbase + kbg + lane] : 0u;
-        const uint32_t mm = table_scan<kIsDelete>(g, s_table, s_flag, tmask, hshift, s_bm, kLongFilterBits, stg,
+        const uint32_t mm = table_scan<kIsDelete, kNative>(g, s_table, s_flag, tmask, hshift, s_bm, kLongFilterBits, stg,
                                                   hd_lane, ng, d, kbg, wbase + kbg, wl_mask, t0 == 0, slots);
         if (lane == 0) matched += mm;
       }
