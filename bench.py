@@ -45,7 +45,7 @@ if str(ROOT) not in sys.path:
 
 METRIC = "batch edge insert+delete throughput (batch=1M, R-MAT s22)"
 UNIT = "Medges/s"
-STATUS_BYTES = 224  # sizeof(DeviceState) + sizeof(OpState): the per-op D2H status read (csrc/dg_api.cu op_end)
+STATUS_BYTES = 248  # sizeof(DeviceState) + sizeof(OpState): the per-op D2H status read (csrc/dg_api.cu op_end)
 
 
 def parse_args():
@@ -139,10 +139,14 @@ def kernel_bytes(name: str, rep: dict, B: int) -> float | None:
     b, T = rep["batch_entries"], rep["touched_sources"]
     W, S, M = rep["blocks_scanned"], rep["slots_scanned"], rep["moved"]
     SL, ST = rep.get("slots_scanned_long", 0), rep.get("slots_scanned_tiny", 0)
+    SF = rep.get("slots_scanned_fused", 0)
+    if name.startswith("fused_delete"):
+        # slab slots of the warp-owned sources + their next links + targets + per-source state (read + repaired)
+        return 4 * SF + 4 * (SF // B) + 8 * b + 32 * T
     if name.startswith("match_long"):
         return 4 * SL + 8 * (SL // B) + 8 * b            # slab slots of the tier + handles + masks + targets
     if name.startswith("match_med"):
-        SM = S - SL - ST
+        SM = S - SL - ST - SF
         return 4 * SM + 8 * (SM // B) + 8 * b
     if name.startswith("match_tiny"):
         return 4 * ST + 12 * W + 8 * b + 4 * T           # slab slots + every block's (tag, handle) + mask + targets

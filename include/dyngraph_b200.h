@@ -133,6 +133,7 @@ typedef struct dg_op_report {
   uint64_t kernel_launches; /* kernels enqueued by the op */
   uint64_t slots_scanned_long; /* part of slots_scanned handled by the CTA-table tier (k > 128 targets) */
   uint64_t slots_scanned_tiny; /* part handled by the register-compare tier (k <= 8 targets) */
+  uint64_t slots_scanned_fused; /* part handled by fused_delete_kernel (sources a single warp owns) */
 } dg_op_report;
 
 /* ---- lifecycle ------------------------------------------------------- */

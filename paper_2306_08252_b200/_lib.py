@@ -53,7 +53,7 @@ class DgMemory(C.Structure):
 class DgOpReport(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "batch_entries", "touched_sources", "blocks_popped", "blocks_pushed", "slots_scanned",
-        "blocks_scanned", "matched", "moved", "kernel_launches", "slots_scanned_long", "slots_scanned_tiny")]
+        "blocks_scanned", "matched", "moved", "kernel_launches", "slots_scanned_long", "slots_scanned_tiny", "slots_scanned_fused")]
 
 
 # every symbol include/dyngraph_b200.h declares: name -> (restype, argtypes)

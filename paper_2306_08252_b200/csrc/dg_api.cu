@@ -21,7 +21,7 @@
 #include <vector>
 
 #include "../../include/dyngraph_b200.h"
-#include "dg_kernels.cuh"
+#include "dg_fused.cuh"
 
 using namespace dg;
 
@@ -168,7 +168,7 @@ struct dg_graph {
   // independent kernels of one op (chain walks, the match tiers) run side by side on two
   // auxiliary streams between a fork and a join on the op's stream
   cudaStream_t aux[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr}, ev_main = nullptr;
   bool forked = false;
   // alloc_kernel cursors carved from a buffer an earlier memset of the op already zeroed
   unsigned long long* pre_zero = nullptr;
@@ -416,7 +416,8 @@ int op_end(dg_graph* h) {
   h->report.blocks_popped = op.total_need;
   h->report.blocks_pushed = op.pushed;
   h->report.slots_scanned = op.slots;
-  h->report.blocks_scanned = op.wl_blocks;
+  h->report.blocks_scanned = op.wl_blocks + op.fused_blocks;
+  h->report.slots_scanned_fused = op.slots_fused;
   h->report.matched = op.matched;
   h->report.moved = op.moves;
   h->report.kernel_launches = h->launches;
@@ -445,7 +446,8 @@ void launch_scan(dg_graph* h, const char* name, uint64_t n_bound, const unsigned
 // unordered range allocation over [0, *n_ptr): see alloc_kernel
 template <class In, class Out, class Fin>
 void launch_alloc(dg_graph* h, const char* name, uint64_t n_bound, const unsigned long long* n_ptr,
-                  In in, Out out, Fin fin) {
+                  In in, Out out, Fin fin, cudaStream_t stream = nullptr) {
+  if (stream == nullptr) stream = h->stream;
   unsigned long long* scratch;
   if (h->pre_zero_left > 0) {
     scratch = h->pre_zero;
@@ -453,16 +455,16 @@ void launch_alloc(dg_graph* h, const char* name, uint64_t n_bound, const unsigne
     --h->pre_zero_left;
   } else {
     scratch = ws_alloc<unsigned long long>(h, kAllocScratchWords);
-    cudaMemsetAsync(scratch, 0, kAllocScratchWords * sizeof(unsigned long long), h->stream);
+    cudaMemsetAsync(scratch, 0, kAllocScratchWords * sizeof(unsigned long long), stream);
   }
   if (n_bound > (2u << 20)) {
     constexpr int kTile = kAllocThreads * kAllocItemsLarge;
     const unsigned tiles = (unsigned)((n_bound + kTile - 1) / kTile);
-    DG_LAUNCH(h, name, alloc_kernel<kAllocItemsLarge><<<tiles, kAllocThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
+    DG_LAUNCH(h, name, alloc_kernel<kAllocItemsLarge><<<tiles, kAllocThreads, 0, stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
   } else {
     constexpr int kTile = kAllocThreads * kAllocItemsSmall;
     const unsigned tiles = (unsigned)std::max<uint64_t>(1, (n_bound + kTile - 1) / kTile);
-    DG_LAUNCH(h, name, alloc_kernel<kAllocItemsSmall><<<tiles, kAllocThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
+    DG_LAUNCH(h, name, alloc_kernel<kAllocItemsSmall><<<tiles, kAllocThreads, 0, stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
   }
 }
 inline size_t alloc_ws_bytes() { return aligned(kAllocScratchWords * sizeof(unsigned long long)); }
@@ -742,8 +744,10 @@ struct Worklist {
   uint2* med_items;    // (run, chunk) items of the medium / long match tiers (nullptr without a batch)
   uint2* long_items;
   uint32_t* big_list;  // chains longer than kLaneWalk blocks
+  uint32_t* run_head;  // fused delete only: head block of the warp-owned sources (else nullptr)
+  uint32_t* fmed_list; // fused delete only: runs of the medium class
   EnumLists lists(dg_graph* h) const {
-    return EnumLists{run_deg, wl_off, med_items, long_items, big_list, (uint32_t)big_bound(h), h->d_op()};
+    return EnumLists{run_deg, wl_off, med_items, long_items, big_list, (uint32_t)big_bound(h), h->d_op(), run_head, fmed_list};
   }
 };
 
@@ -756,9 +760,17 @@ inline uint64_t long_items_bound(const dg_graph* h, uint64_t n) {
 }
 inline uint64_t big_bound(const dg_graph* h) { return h->blocks_in_use() / (kLaneWalk + 1) + 16; }
 
+// sources of the fused medium class: more than kFusedSmallBlocks blocks or more than kFusedSmallTargets targets
+inline uint64_t fused_med_bound(const dg_graph* h, uint64_t runs_bound, uint64_t n_batch) {
+  return std::min<uint64_t>(runs_bound, h->blocks_in_use() / (kFusedSmallBlocks + 1) + n_batch / (kFusedSmallTargets + 1) + 1) + 1;
+}
 // n_batch: entries of the batch the runs index into; has_batch false: export, digest
-Worklist alloc_worklist(dg_graph* h, uint64_t runs_bound, uint64_t n_batch, bool has_batch) {
+Worklist alloc_worklist(dg_graph* h, uint64_t runs_bound, uint64_t n_batch, bool has_batch, bool fuse = false) {
   Worklist w{};
+  if (fuse) {
+    w.run_head = ws_alloc<uint32_t>(h, runs_bound + 1);
+    w.fmed_list = ws_alloc<uint32_t>(h, fused_med_bound(h, runs_bound, n_batch));
+  }
   const uint64_t wl_cap = h->blocks_in_use();
   w.wl_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   w.run_deg = ws_alloc<uint32_t>(h, runs_bound + 1);
@@ -772,28 +784,33 @@ Worklist alloc_worklist(dg_graph* h, uint64_t runs_bound, uint64_t n_batch, bool
   return w;
 }
 inline size_t worklist_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n_batch) {
-  return 2 * aligned((runs_bound + 1) * 4) + 2 * aligned((h->blocks_in_use() + 1) * 4) +
+  return 3 * aligned((runs_bound + 1) * 4) + aligned(fused_med_bound(h, runs_bound, n_batch) * 4) + aligned(kTallyStripes * kTalWords * 8) +
+         2 * aligned((h->blocks_in_use() + 1) * 4) +
          aligned(med_items_bound(h, n_batch) * 8) + aligned(long_items_bound(h, n_batch) * 8) +
          aligned(big_bound(h) * 4) + alloc_ws_bytes();
 }
 
 // chain walk over a planned worklist
-void enqueue_walk(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound) {
+void enqueue_walk(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound, cudaStream_t s_big, cudaStream_t s_small) {
   GraphView g = view(h);
-  // (inside a fork: the long-chain walk starts first, it is the critical path)
-  DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_resident(h, big_bound(h), 8, enumerate_big_kernel), 256, 0, lane(h, 1)>>>(
+  // (the long-chain walk starts first, it is the critical path)
+  DG_LAUNCH(h, "enumerate_big_kernel", enumerate_big_kernel<<<grid_resident(h, big_bound(h), 8, enumerate_big_kernel), 256, 0, s_big>>>(
       g, b, w.wl_off, w.run_deg, w.big_list, (uint32_t)big_bound(h), w.wl_handle, w.wl_run, h->d_op()));
-  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_resident(h, runs_bound, 256, enumerate_walk_kernel), 256, 0, lane(h, 2)>>>(
+  DG_LAUNCH(h, "enumerate_walk_kernel", enumerate_walk_kernel<<<grid_resident(h, runs_bound, 256, enumerate_walk_kernel), 256, 0, s_small>>>(
       g, b, w.wl_off, w.run_deg, w.wl_handle, w.wl_run, h->d_op()));
+}
+void enqueue_walk(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound) {   // inside a fork
+  enqueue_walk(h, b, w, runs_bound, lane(h, 1), lane(h, 2));
 }
 
 // enumeration over an already grouped batch (radix path, CSR batches) or over every vertex (export)
 Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n_batch,
-                           int check_alive) {
+                           int check_alive, bool fuse = false, bool walk = true) {
   GraphView g = view(h);
-  Worklist w = alloc_worklist(h, runs_bound, n_batch, b.run_start != nullptr);
-  launch_alloc(h, "alloc_kernel<enum>", runs_bound, d_n_runs(h), EnumIn{g, b, check_alive}, EnumOut{b, w.lists(h)},
+  Worklist w = alloc_worklist(h, runs_bound, n_batch, b.run_start != nullptr, fuse);
+  launch_alloc(h, "alloc_kernel<enum>", runs_bound, d_n_runs(h), EnumIn{g, b, check_alive, fuse}, EnumOut{g, b, w.lists(h)},
                EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/0});
+  if (!walk) return w;
   fork(h);
   enqueue_walk(h, b, w, runs_bound);
   join(h);
@@ -805,7 +822,8 @@ Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound,
 // with 4-byte staging copies and ceil(B / 32) passes per block.
 template <bool kIsDelete, bool kNative>
 void enqueue_match_impl(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t n_batch,
-                        uint32_t* run_matched, uint32_t* wl_mask, uint8_t* hit) {
+                        uint32_t* run_matched, uint32_t* wl_mask, uint8_t* hit, cudaStream_t s_long, cudaStream_t s_med,
+                        cudaStream_t s_tiny) {
   GraphView g = view(h);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   const size_t med_smem = kIsDelete ? kMedSmemDelete : kMedSmemQuery;
@@ -814,25 +832,25 @@ void enqueue_match_impl(dg_graph* h, const BatchView& b, const Worklist& w, uint
   cudaFuncSetAttribute(match_med_kernel<kIsDelete, kNative>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)med_smem);
   cudaFuncSetAttribute(match_long_kernel<kIsDelete, kNative>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_smem);
   // the tiers touch disjoint blocks: side by side, heaviest items first
-  fork(h);
   const int long_grid = (int)std::min<uint64_t>(long_items_bound(h, n_batch), (uint64_t)h->sm_count * 3);
   DG_LAUNCH(h, kIsDelete ? "match_long_kernel<delete>" : "match_long_kernel<query>",
-            match_long_kernel<kIsDelete, kNative><<<long_grid, kLongThreads, long_smem, lane(h, 1)>>>(
+            match_long_kernel<kIsDelete, kNative><<<long_grid, kLongThreads, long_smem, s_long>>>(
                 g, b, w.wl_off, w.wl_handle, w.long_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
   const int med_grid = (int)std::min<uint64_t>(grid_for(h, med_items_bound(h, n_batch), 8), (uint64_t)h->sm_count * 4);
   DG_LAUNCH(h, kIsDelete ? "match_med_kernel<delete>" : "match_med_kernel<query>",
-            match_med_kernel<kIsDelete, kNative><<<med_grid, 256, med_smem, lane(h, 2)>>>(
+            match_med_kernel<kIsDelete, kNative><<<med_grid, 256, med_smem, s_med>>>(
                 g, b, w.wl_off, w.wl_handle, w.med_items, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
   DG_LAUNCH(h, kIsDelete ? "match_tiny_kernel<delete>" : "match_tiny_kernel<query>",
-            match_tiny_kernel<kIsDelete, kNative><<<grid_resident(h, wl_bound, 256, match_tiny_kernel<kIsDelete, kNative>), 256, 0, lane(h, 0)>>>(
+            match_tiny_kernel<kIsDelete, kNative><<<grid_resident(h, wl_bound, 256, match_tiny_kernel<kIsDelete, kNative>), 256, 0, s_tiny>>>(
                 g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, wl_mask, hit, h->d_op()));
-  join(h);
 }
 template <bool kIsDelete>
 void enqueue_match(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t n_batch,
                    uint32_t* run_matched, uint32_t* wl_mask, uint8_t* hit) {
-  if (h->B == 32) enqueue_match_impl<kIsDelete, true>(h, b, w, n_batch, run_matched, wl_mask, hit);
-  else enqueue_match_impl<kIsDelete, false>(h, b, w, n_batch, run_matched, wl_mask, hit);
+  fork(h);
+  if (h->B == 32) enqueue_match_impl<kIsDelete, true>(h, b, w, n_batch, run_matched, wl_mask, hit, lane(h, 1), lane(h, 2), lane(h, 0));
+  else enqueue_match_impl<kIsDelete, false>(h, b, w, n_batch, run_matched, wl_mask, hit, lane(h, 1), lane(h, 2), lane(h, 0));
+  join(h);
 }
 
 // ---- grouping a COO batch by source --------------------------------------------------------------
@@ -956,7 +974,7 @@ int require_pool(dg_graph* h) {
   return DG_OK;
 }
 
-// group + enumerate a COO batch for delete / query (either strategy)
+// group + enumerate a COO batch for a query (either strategy)
 template <int kMode>
 Grouped group_and_enumerate(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n,
                             bool with_index, uint64_t max_src, Worklist* w_out) {
@@ -964,7 +982,7 @@ Grouped group_and_enumerate(dg_graph* h, const uint32_t* d_src, const uint32_t* 
   if (use_counting(h, n)) {
     Grouped gr = group_count<kMode>(h, d_src, d_dst, n, with_index);
     Worklist w = alloc_worklist(h, gr.runs_bound, n, true);
-    launch_alloc(h, "alloc_kernel<group+enum>", n, d_n_input(h), GroupEnumIn{g, gr.gi, d_src, gr.rank, gr.cnt, 1},
+    launch_alloc(h, "alloc_kernel<group+enum>", n, d_n_input(h), GroupEnumIn{g, gr.gi, d_src, gr.rank, gr.cnt, 1, false},
                  GroupEnumOut{g, gr.gi, d_src, gr.cnt, gr.run_src, gr.run_start, gr.run_end, w.lists(h)},
                  EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/1});
     fork(h);   // the scatter and the two chain walks are independent
@@ -983,8 +1001,17 @@ inline size_t group_enumerate_ws(const dg_graph* h, uint64_t n, bool with_index,
          worklist_ws(h, n, n);  // either strategy's run bound
 }
 
-// delete over a grouped + enumerated batch
-int delete_matched(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound, uint64_t n) {
+// ---- delete over a grouped batch -----------------------------------------------------------------
+// Warp-owned sources (fused_class: short chains, few targets — B = 32 only) are finished by ONE kernel on
+// the op stream; the hubs keep the multi-kernel path (walk -> match tiers -> compaction plan -> holes ->
+// moves) on the two high-priority side streams, beside it.  Enqueue order on entry: the enumeration plan
+// (alloc_kernel<...enum>, which also classifies the sources) is already on the op stream.
+//   scatter(): the counting group-by's scatter (needed by both the fused kernel and the hub match).
+inline cudaStream_t side(const dg_graph* h, int i) { return h->profiling ? h->stream : h->aux[i]; }
+
+template <class Scatter>
+int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound, uint64_t n, bool fuse,
+               Scatter&& scatter) {
   GraphView g = view(h);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   uint32_t* zeroed = ws_alloc<uint32_t>(h, 3 * (runs_bound + 1));  // one memset for the three counters
@@ -995,19 +1022,60 @@ int delete_matched(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t 
   uint32_t* free_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   uint32_t* wl_mask = ws_alloc<uint32_t>(h, (wl_bound + 1) * g.mw);
   cudaMemsetAsync(zeroed, 0, 3 * (runs_bound + 1) * 4, h->stream);
-  enqueue_match<true>(h, b, w, n, run_matched, wl_mask, nullptr);
+  unsigned long long* tally = nullptr;
+  if (fuse) {
+    tally = ws_alloc<unsigned long long>(h, kTallyStripes * kTalWords);
+    cudaMemsetAsync(tally, 0, kTallyStripes * kTalWords * sizeof(unsigned long long), h->stream);
+  }
+  const bool par = !h->profiling;
+  cudaStream_t s0 = side(h, 0), s1 = side(h, 1);
+  if (par) {
+    cudaEventRecord(h->ev_fork, h->stream);
+    cudaStreamWaitEvent(s0, h->ev_fork, 0);
+    cudaStreamWaitEvent(s1, h->ev_fork, 0);
+  }
+  enqueue_walk(h, b, w, runs_bound, s0, s1);   // hub chains only
+  scatter();
+  if (par) cudaEventRecord(h->ev_main, h->stream);
+  if (fuse) {
+    // one-warp CTAs: the medium sources first (heaviest), strided over a bounded grid, then 32 runs per warp
+    const uint32_t g_med = (uint32_t)std::clamp<uint64_t>((fused_med_bound(h, runs_bound, n) + 7) / 8, 1, 32768);
+    const unsigned grid = g_med + (unsigned)((runs_bound + 31) / 32);
+    DG_LAUNCH(h, "fused_delete_kernel", fused_delete_kernel<<<grid, 32, 0, h->stream>>>(
+        g, b, w.wl_off, w.run_deg, w.run_head, w.fmed_list, g_med, tally, h->d_op()));
+    DG_LAUNCH(h, "fused_tally_kernel", fused_tally_kernel<<<1, 32, 0, h->stream>>>(g, tally, h->d_op()));
+  }
+  if (par) {   // the hub match needs both walks and the scatter
+    cudaEventRecord(h->ev_join[0], s0);
+    cudaEventRecord(h->ev_join[1], s1);
+    cudaStreamWaitEvent(s0, h->ev_join[1], 0);
+    cudaStreamWaitEvent(s0, h->ev_main, 0);
+    cudaStreamWaitEvent(s1, h->ev_join[0], 0);
+    cudaStreamWaitEvent(s1, h->ev_main, 0);
+  }
+  if (h->B == 32) enqueue_match_impl<true, true>(h, b, w, n, run_matched, wl_mask, nullptr, s0, s1, s1);
+  else enqueue_match_impl<true, false>(h, b, w, n, run_matched, wl_mask, nullptr, s0, s1, s1);
+  if (par) {
+    cudaEventRecord(h->ev_join[1], s1);
+    cudaStreamWaitEvent(s0, h->ev_join[1], 0);
+  }
   const size_t ws_mark = h->ws.off;
   for (int attempt = 0; attempt < 2; ++attempt) {
     h->ws.off = ws_mark;
-    if (attempt > 0) cudaMemsetAsync(hole_cnt, 0, 2 * (runs_bound + 1) * 4, h->stream);
+    cudaStream_t st = attempt == 0 ? s0 : h->stream;
+    if (attempt > 0) cudaMemsetAsync(hole_cnt, 0, 2 * (runs_bound + 1) * 4, st);
     launch_alloc(h, "alloc_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{g, w.run_deg, run_matched},
-                 MovesOut{mv_off, free_off}, MovesFin{g, h->d_op(), h->mv_cap});
-    DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_resident(h, wl_bound, 256, delete_holes_kernel), 256, 0, h->stream>>>(
+                 MovesOut{mv_off, free_off}, MovesFin{g, h->d_op(), h->mv_cap}, st);
+    DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_resident(h, wl_bound, 256, delete_holes_kernel), 256, 0, st>>>(
         g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, free_off, wl_mask, hole_cnt,
         h->mv_hole, h->d_op()));
-    DG_LAUNCH(h, "delete_moves_kernel", delete_moves_kernel<<<grid_resident(h, wl_bound, 256, delete_moves_kernel), 256, 0, h->stream>>>(
+    DG_LAUNCH(h, "delete_moves_kernel", delete_moves_kernel<<<grid_resident(h, wl_bound, 256, delete_moves_kernel), 256, 0, st>>>(
         g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, hole_cnt, surv_cnt,
         h->mv_hole, h->d_op()));
+    if (par && attempt == 0) {
+      cudaEventRecord(h->ev_join[0], s0);
+      cudaStreamWaitEvent(h->stream, h->ev_join[0], 0);
+    }
     const int rc = op_end(h);
     if (rc != DG_OK) return rc;
     if (h->h_blk->op.aux1 == 0) return DG_OK;
@@ -1021,6 +1089,24 @@ inline size_t delete_matched_ws(const dg_graph* h, uint64_t runs_bound) {
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   return 5 * aligned((runs_bound + 1) * 4) + aligned((wl_bound + 1) * ((h->B + 31) / 32) * 4) + alloc_ws_bytes();
 }
+
+// delete of a COO batch: group (either strategy) + enumeration plan with classification, then delete_run
+int delete_coo_run(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, uint64_t max_src) {
+  GraphView g = view(h);
+  const bool fuse = h->B == 32;
+  if (use_counting(h, n)) {
+    Grouped gr = group_count<kPackDelete>(h, d_src, d_dst, n, false);
+    Worklist w = alloc_worklist(h, gr.runs_bound, n, true, fuse);
+    launch_alloc(h, "alloc_kernel<group+enum>", n, d_n_input(h), GroupEnumIn{g, gr.gi, d_src, gr.rank, gr.cnt, 1, fuse},
+                 GroupEnumOut{g, gr.gi, d_src, gr.cnt, gr.run_src, gr.run_start, gr.run_end, w.lists(h)},
+                 EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/1});
+    return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, [&] { group_scatter<kPackDelete>(h, gr, d_src, d_dst, n); });
+  }
+  Grouped gr = group_radix<kPackDelete>(h, d_src, d_dst, n, false, max_src);
+  Worklist w = enqueue_enumerate(h, gr.b, gr.runs_bound, n, /*check_alive=*/1, fuse, /*walk=*/false);
+  return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, [] {});
+}
+
 
 }  // namespace
 
@@ -1102,12 +1188,16 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
     if (rc != DG_OK) return bail(rc, h->last_error);
   }
   if (ensure_mv_scratch(h, 1 << 16) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
+  // side streams run the (few, latency-critical) hub kernels of an op beside its bulk kernel: highest priority
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   for (int i = 0; i < 2; ++i) {
-    if (cudaStreamCreateWithFlags(&h->aux[i], cudaStreamNonBlocking) != cudaSuccess ||
+    if (cudaStreamCreateWithPriority(&h->aux[i], cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
       return bail(DG_ERR_CUDA, "dg_create: auxiliary stream");
   }
-  if (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+  if (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_main, cudaEventDisableTiming) != cudaSuccess)
     return bail(DG_ERR_CUDA, "dg_create: auxiliary stream");
   if (cfg.workspace_bytes && ws_reserve(h, cfg.workspace_bytes) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
   e = cudaStreamSynchronize(h->stream);
@@ -1141,6 +1231,7 @@ void dg_destroy(dg_graph* h) {
     if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_main) cudaEventDestroy(h->ev_main);
   for (auto& sp : h->prof_open) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
   for (auto e : h->prof_pool) cudaEventDestroy(e);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -1337,9 +1428,7 @@ int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
     group_radix<kPackDelete>(h, d_src, d_dst, n, false, h->size - 1);
     return op_end(h);
   }
-  Worklist w;
-  Grouped gr = group_and_enumerate<kPackDelete>(h, d_src, d_dst, n, false, h->size - 1, &w);
-  return delete_matched(h, gr.b, w, gr.runs_bound, n);
+  return delete_coo_run(h, d_src, d_dst, n, h->size - 1);
 }
 
 int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
@@ -1374,8 +1463,9 @@ int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets
   if (n == 0 || V == 0 || h->B == 0) return op_end(h);
   // a CSR batch is already grouped: run r is vertex r (empty runs are skipped by the enumeration)
   BatchView b{nullptr, d_dst, nullptr, run_start, run_start + 1};
-  Worklist w = enqueue_enumerate(h, b, V, n, /*check_alive=*/1);
-  return delete_matched(h, b, w, V, n);
+  const bool fuse = h->B == 32;
+  Worklist w = enqueue_enumerate(h, b, V, n, /*check_alive=*/1, fuse, /*walk=*/false);
+  return delete_run(h, b, w, V, n, fuse, [] {});
 }
 
 // ---- query ---------------------------------------------------------------------

@@ -75,6 +75,10 @@ struct OpState {
   unsigned int n_huge;            // chains walked by a whole CTA (listed from the end of the big list)
   unsigned int committed;         // CSR insert: the append pass ran and published deg/tail/front (rollback needed on error)
   unsigned long long bad_index;   // CSR insert: smallest out-of-range destination index seen by the append pass (~0: none)
+  unsigned long long fused_blocks;  // blocks of the warp-owned sources (fused_delete_kernel); wl_blocks counts the rest
+  unsigned long long slots_fused;   // part of `slots` inspected by fused_delete_kernel
+  unsigned int n_fmed;              // sources of the fused medium class listed by the enumeration plan
+  unsigned int pad0;
 };
 
 __device__ __forceinline__ void set_error(OpState* op, uint32_t code, uint32_t detail,

@@ -1267,6 +1267,26 @@ __device__ __forceinline__ uint32_t run_tag(const BatchView& b, uint32_t r) {
 }
 constexpr uint32_t kLongChunk = 256;     // blocks per CTA item of the long path
 
+// ---- sources a single warp owns for the whole delete (dg_fused.cuh) ----
+// class of a touched source, stored in wl_off[r] (real work-list offsets are < 2^31)
+constexpr uint32_t kClsNone = 0xFFFFFFFFu;    // nothing stored (dead / unknown source, empty chain)
+constexpr uint32_t kClsSmall = 0xFFFFFFFEu;
+constexpr uint32_t kClsMed = 0xFFFFFFFDu;
+constexpr uint32_t kClsMin = 0xFFFFFFF0u;     // wl_off values >= this are classes, not offsets
+constexpr uint32_t kFusedSmallBlocks = 16;
+constexpr uint32_t kFusedSmallTargets = kTinyTargets;   // 8
+constexpr uint32_t kFusedMedBlocks = 256;
+constexpr uint32_t kFusedMedTargets = kMedTargets;      // 128
+constexpr uint32_t kFusedListBlocks = 256;    // blocks a warp keeps (handle + mask) at a time
+
+__host__ __device__ inline uint32_t fused_class(uint32_t k, uint32_t nblk) {
+  if (nblk == 0 || k == 0) return kClsNone;
+  if (k <= kFusedSmallTargets && nblk <= kFusedSmallBlocks) return kClsSmall;
+  if (k <= kFusedMedTargets && nblk <= kFusedMedBlocks) return kClsMed;
+  return 0u;   // hub: multi-kernel path
+}
+
+
 // Enumeration plan: work-list segments are disjoint ranges too (alloc_kernel):
 //   word a = [63:32] touched sources (counting path only), [31:0] batch entries
 //   word b = [63:32] chains a whole warp walks (their big-list slots come out of the scan: one
@@ -1283,8 +1303,19 @@ struct EnumLists {
                        // kHugeWalk blocks are listed from the END of the same array and walked by a whole CTA
   uint32_t big_cap;
   OpState* op;
-  __device__ void write(uint32_t r, uint32_t d, uint32_t nblk, uint32_t k, unsigned long long excl_b) const {
+  uint32_t* run_head;  // fused delete: head block of every warp-owned source (nullptr: no fusion)
+  uint32_t* fmed_list; // fused delete: runs of the medium class (a warp per source), filled through op->n_fmed
+  __device__ void write(uint32_t r, uint32_t d, uint32_t nblk, uint32_t k, uint32_t head, unsigned long long excl_b) const {
     run_deg[r] = d;
+    if (run_head != nullptr) {   // warp-owned sources take no work-list segment: wl_off carries their class
+      const uint32_t cls = fused_class(k, nblk);
+      if (cls != 0u) {
+        wl_off[r] = cls;
+        run_head[r] = head;
+        if (cls == kClsMed) fmed_list[atomicAdd(&op->n_fmed, 1u)] = r;
+        return;
+      }
+    }
     wl_off[r] = (uint32_t)excl_b;
     if (nblk > kHugeWalk) big_list[big_cap - 1u - atomicAdd(&op->n_huge, 1u)] = r;   // (a few dozen per batch)
     else if (nblk > kLaneWalk) big_list[(uint32_t)(excl_b >> 32)] = r;
@@ -1305,6 +1336,10 @@ struct EnumLists {
 __device__ __forceinline__ unsigned long long enum_word_b(uint32_t nblk) {
   return ((nblk > kLaneWalk && nblk <= kHugeWalk) ? (1ull << 32) : 0ull) | nblk;
 }
+// fuse: sources a warp owns (fused_class != 0) stay out of the work list
+__device__ __forceinline__ unsigned long long enum_word_b(uint32_t nblk, uint32_t k, bool fuse) {
+  return (fuse && fused_class(k, nblk) != 0u) ? 0ull : enum_word_b(nblk);
+}
 // degree of a touched vertex as delete/query see it: dead or unknown sources have
 // none (graph.hpp:205, :229).  Predicated, independent loads (see alloc_kernel).
 __device__ __forceinline__ uint32_t live_degree(const GraphView& g, uint32_t v, bool wanted, int check_alive) {
@@ -1314,7 +1349,7 @@ __device__ __forceinline__ uint32_t live_degree(const GraphView& g, uint32_t v, 
   return ((aw >> (v & 31)) & 1u) ? d : 0u;
 }
 struct EnumAux {
-  uint32_t d;
+  uint32_t d, head;
 };
 
 // over already-grouped runs (radix path, CSR batches, export: runs = vertices)
@@ -1323,20 +1358,25 @@ struct EnumIn {
   GraphView g;
   BatchView b;
   int check_alive;
+  bool fuse;
   __device__ Sum2 operator()(unsigned long long r64, Aux& x) const {
     const uint32_t r = (uint32_t)r64;
-    const bool wanted = b.run_start == nullptr || run_len(b, r) != 0;  // empty runs: CSR batches
-    x.d = live_degree(g, batch_src(b, r), wanted, check_alive);
-    return Sum2{0ull, enum_word_b(blocks_for(g, x.d))};
+    const uint32_t k = b.run_start != nullptr ? run_len(b, r) : 0u;
+    const bool wanted = b.run_start == nullptr || k != 0;  // empty runs: CSR batches
+    const uint32_t v = batch_src(b, r);
+    x.d = live_degree(g, v, wanted, check_alive);
+    x.head = (fuse && wanted && v < g.size) ? g.head[v] : kNull;
+    return Sum2{0ull, enum_word_b(blocks_for(g, x.d), k, fuse)};
   }
 };
 struct EnumOut {
+  GraphView g;
   BatchView b;
   EnumLists lists;
   __device__ void operator()(unsigned long long r, unsigned long long, unsigned long long excl_b,
                              Sum2 v, const EnumAux& x) const {
     const uint32_t k = b.run_start != nullptr ? run_len(b, (uint32_t)r) : 0u;
-    lists.write((uint32_t)r, x.d, (uint32_t)v.b, k, excl_b);
+    lists.write((uint32_t)r, x.d, blocks_for(g, x.d), k, x.head, excl_b);
   }
 };
 // fused with the counting group-by: one pass over the batch entries (see GroupPlanIn)
@@ -1348,12 +1388,14 @@ struct GroupEnumIn {
   const uint32_t* rank;
   const uint32_t* cnt;
   int check_alive;
+  bool fuse;
   __device__ Sum2 operator()(unsigned long long i, Aux& x) const {
     const uint32_t s = min(src[i], g.size);  // query batches: unknown sources share one slot
     const bool rep = rank[i] == 0;
     const uint32_t c = rep ? cnt[gi(s)] : 0u;
     x.d = live_degree(g, s, rep, check_alive);
-    return Sum2{c ? ((1ull << 32) | c) : 0ull, enum_word_b(blocks_for(g, x.d))};
+    x.head = (fuse && rep && s < g.size) ? g.head[s] : kNull;
+    return Sum2{c ? ((1ull << 32) | c) : 0ull, enum_word_b(blocks_for(g, x.d), c, fuse)};
   }
 };
 struct GroupEnumOut {
@@ -1376,7 +1418,7 @@ struct GroupEnumOut {
     run_start[r] = es;
     run_end[r] = es + c;
     cnt[gi(v)] = es;
-    lists.write(r, x.d, (uint32_t)val.b, c, excl_b);
+    lists.write(r, x.d, blocks_for(g, x.d), c, x.head, excl_b);
   }
 };
 struct EnumFin {
@@ -1406,7 +1448,7 @@ enumerate_walk_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < T; r += gridDim.x * blockDim.x) {
     const uint32_t base = wl_off[r];
     const uint32_t nblk = blocks_for(g, run_deg[r]);
-    if (nblk == 0 || nblk > kLaneWalk) continue;
+    if (nblk == 0 || nblk > kLaneWalk || base >= kClsMin) continue;   // (class words: warp-owned sources)
     uint32_t h = g.head[batch_src(b, r)];
     const uint32_t tag = run_tag(b, r);
     for (uint32_t k = 0; k < nblk; ++k) {
@@ -1974,9 +2016,9 @@ struct MovesFin {
     op->aux0 = total;                      // scratch entries needed
     op->aux1 = total > mv_cap ? 1ull : 0ull;  // host grows the scratch and re-runs the tail
     if (total <= mv_cap) {                 // reclaim (block_pool.hpp:192-209): one cursor bump for the whole batch
-      op->front_old = g.st->rear;          // (first ring position of the pushed handles)
-      g.st->rear += total_a;
-      op->pushed = total_a;
+      // (atomics: the warp-owned sources push to the same ring from fused_delete_kernel, side by side)
+      op->front_old = atomicAdd(&g.st->rear, total_a);   // first ring position of the pushed handles
+      atomicAdd(&op->pushed, total_a);
     }
   }
 };
