@@ -23,20 +23,18 @@
 
 namespace dg {
 
-// per-warp shared memory (a CTA is ONE warp: the hardware CTA scheduler is the load balancer, no warp ever
-// waits at a CTA barrier for a heavier neighbour)
-struct __align__(16) FusedWarp {
-  uint32_t stg[32][32];            // staged blocks (swizzled rows); medium compaction: prefix arrays
-  uint32_t hnd[kFusedListBlocks];  // handles of the blocks in hand
-  uint32_t msk[kFusedListBlocks];  // their match masks
-  uint32_t tab[kMedTable];         // medium: target table; small: targets [32][8] + filters
-  uint32_t bm[(1u << kMedFilterBits) / 32];
-  uint16_t own[kFusedListBlocks];  // small: [4:0] owner lane, [10:5] live slots - 1
-};
+// Per-warp shared memory (a CTA is ONE warp: the hardware CTA scheduler is the load balancer, no warp ever
+// waits at a CTA barrier for a heavier neighbour).  One byte array, carved per role:
+//   small : stg 4096 | hnd 128 x 4 | msk 128 x 4 | own 128 x 2 | targets 32 x 8 x 4 | filters 32 x 8      = 6656 B
+//   medium: stg 4096 (compaction: prefix arrays) | hnd 256 x 4 | msk 256 x 4 | table 256 x 4 | filter 512 = 7680 B
+constexpr uint32_t kFusedSmallList = 128;   // blocks a warp holds at a time in the small role
+constexpr uint32_t kFusedTable = 256;       // >= 2 x kFusedMedTargets
+constexpr size_t kFusedSmemBytes = 7680;
 // tallies are striped over kTallyStripes x 8 words (one stripe per CTA, round-robin) and folded into
 // OpState / DeviceState by fused_tally_kernel: tens of thousands of one-warp CTAs never share a counter line
 constexpr uint32_t kTallyStripes = 64;
 enum Tally : int { kTalMatched = 0, kTalSlots, kTalBlocks, kTalMoves, kTalPushed, kTalWords = 8 };
+static_assert(kFusedMedBlocks <= kFusedListBlocks && kFusedTable >= 2 * kFusedMedTargets, "medium role layout");
 
 __device__ __forceinline__ uint32_t low_bits(uint32_t n) { return n >= 32u ? 0xFFFFFFFFu : ((1u << n) - 1u); }
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
@@ -63,6 +61,7 @@ __device__ __forceinline__ uint32_t warp_push_freed(const GraphView& g, const ui
   unsigned long long base = 0;
   if (lane_id() == 0) base = atomicAdd(&g.st->rear, (unsigned long long)total) % g.ring_cap;
   unsigned long long p = __shfl_sync(kFull, base, 0) + (incl - cnt);   // < 2 * ring_cap
+#pragma unroll 1
   for (uint32_t j = 0; j < cnt; ++j, ++p) {
     if (p >= g.ring_cap) p -= g.ring_cap;
     g.ring[p] = hnd[first + j];
@@ -70,42 +69,52 @@ __device__ __forceinline__ uint32_t warp_push_freed(const GraphView& g, const ui
   return total;
 }
 
-__device__ __forceinline__ void tally_flush(unsigned long long* tally, unsigned long long matched, unsigned long long slots,
-                                            unsigned long long blocks, unsigned long long moves, unsigned long long pushed) {
-  // every lane holds its own partial sums; one atomic per counter and warp, on the CTA's stripe
-  unsigned long long v[5] = {matched, slots, blocks, moves, pushed};
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) v[i] += __shfl_xor_sync(kFull, v[i], d);
-  }
+__device__ __forceinline__ uint32_t redux_add(uint32_t v) {
+  uint32_t r;
+  asm volatile("redux.sync.add.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
+// per-lane 32-bit partial sums -> one REDUX per counter, one atomic per counter and warp on the CTA's stripe
+__device__ __noinline__ void tally_flush(unsigned long long* tally, uint32_t matched, uint32_t slots, uint32_t blocks,
+                                         uint32_t moves, uint32_t pushed) {
+  const uint32_t v[5] = {redux_add(matched), redux_add(slots), redux_add(blocks), redux_add(moves), redux_add(pushed)};
   if (lane_id() == 0) {
     unsigned long long* t = tally + (size_t)(blockIdx.x % kTallyStripes) * kTalWords;
 #pragma unroll
     for (int i = 0; i < 5; ++i)
-      if (v[i]) atomicAdd(&t[i], v[i]);
+      if (v[i]) atomicAdd(&t[i], (unsigned long long)v[i]);
   }
 }
 
 // grid: [0, g_med) medium role — CTA c takes med_list[c], med_list[c + g_med], ... (heaviest work first);
 //       [g_med, g_med + ceil(T / 32)) small role — 32 consecutive runs per warp, lane = run.
-__global__ void __launch_bounds__(32, 24)
+__global__ void __launch_bounds__(32, 28)
 fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_cls, const uint32_t* __restrict__ run_deg,
                     const uint32_t* __restrict__ run_head, const uint32_t* __restrict__ med_list, uint32_t g_med,
                     unsigned long long* tally, OpState* op) {
-  if (op->err) return;
-  __shared__ FusedWarp sw;
+  __shared__ __align__(16) unsigned char smem[kFusedSmemBytes];
   const int lane = lane_id();
-  uint32_t(*stg)[32] = sw.stg;
-  unsigned long long t_matched = 0, t_slots = 0, t_blocks = 0, t_moves = 0, t_pushed = 0;
+  uint32_t(*stg)[32] = reinterpret_cast<uint32_t(*)[32]>(smem);
+  // the op words share one line: requested together, tested after the role's own first loads are in flight
+  const uint32_t op_err = op->err;
+  uint32_t t_matched = 0, t_slots = 0, t_blocks = 0, t_moves = 0, t_pushed = 0;
 
   if (blockIdx.x >= g_med) {
     // =========================== small sources: lane = source ===========================
+    struct SmallSmem {
+      uint32_t stg[32][32];
+      uint32_t hnd[kFusedSmallList], msk[kFusedSmallList];
+      uint16_t own[kFusedSmallList];   // [4:0] owner lane, [10:5] live slots - 1
+      uint32_t tg[32 * 8];
+      unsigned long long filt[32];
+    };
+    static_assert(sizeof(SmallSmem) <= kFusedSmemBytes, "small role layout");
+    SmallSmem& sw = *reinterpret_cast<SmallSmem*>(smem);
     const uint32_t T = (uint32_t)op->n_runs;
     const uint32_t r = (blockIdx.x - g_med) * 32u + lane;
-    if (r - lane >= T) return;
-    uint32_t* s_tg = sw.tab;   // targets [32][8], then 64-bit filters [32]
-    unsigned long long* s_filt = reinterpret_cast<unsigned long long*>(sw.tab + 256);
+    if (op_err || r - lane >= T) return;
+    uint32_t* s_tg = sw.tg;
+    unsigned long long* s_filt = sw.filt;
     uint32_t cls = kClsNone, v = 0, es = 0, k = 0, d = 0, h0 = kNull;
     if (r < T) {
       cls = run_cls[r];
@@ -126,10 +135,11 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
       for (uint32_t q = 0; q < 4; ++q)
         if (q < nb && (unsigned long long)h0 + q < g.ring_cap) prefetch_l2(g.slab + ((unsigned long long)h0 + q) * 32u);
     }
+#pragma unroll 1
     while (pending) {
       const bool mine_p = (pending >> lane) & 1u;
       const uint32_t incl = warp_incl_scan(mine_p ? nb : 0u);
-      const bool mine = mine_p && incl <= kFusedListBlocks;   // a prefix of the pending lanes
+      const bool mine = mine_p && incl <= kFusedSmallList;   // a prefix of the pending lanes
       const unsigned bmask = __ballot_sync(kFull, mine);
       pending &= ~bmask;
       const uint32_t off = incl - nb;
@@ -141,6 +151,7 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
         for (int j = 0; j < (int)kFusedSmallTargets; ++j) tg[j] = ((uint32_t)j < k) ? batch_value(b, es + j) : kTomb;
         // ---- chain walk: up to four physically consecutive blocks per round trip
         uint32_t h = h0, j = 0;
+#pragma unroll 1
         while (j < nb) {
           uint32_t nx[4];
 #pragma unroll
@@ -176,6 +187,7 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
       }
       __syncwarp();
       // ---- match: 32 blocks per round, lane = block
+#pragma unroll 1
       for (uint32_t base = 0; base < N; base += 32) {
         const uint32_t bi = base + lane;
         const bool valid = bi < N;
@@ -202,6 +214,7 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
           if (cand) {
             const uint4 ta = *reinterpret_cast<const uint4*>(&s_tg[o * 8]);
             const uint4 tb = *reinterpret_cast<const uint4*>(&s_tg[o * 8 + 4]);
+#pragma unroll 1
             while (cand) {
               const uint32_t bit = __ffs(cand) - 1;
               cand &= cand - 1;
@@ -218,16 +231,20 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
       uint32_t nfree = 0, new_nb = nb;
       if (mine) {
         uint32_t m = 0;
+#pragma unroll 1
         for (uint32_t j = 0; j < nb; ++j) m += __popc(sw.msk[off + j]);
         if (m) {
           const uint32_t nd = d - m;
           new_nb = (nd + 31u) >> 5;
           uint32_t ps = nd;   // next candidate survivor position (>= nd)
+#pragma unroll 1
           for (uint32_t kb = 0; kb * 32u < nd; ++kb) {
             uint32_t bits = sw.msk[off + kb] & low_bits(nd - kb * 32u);
+#pragma unroll 1
             while (bits) {
               const uint32_t bit = __ffs(bits) - 1;
               bits &= bits - 1;
+#pragma unroll 1
               while ((sw.msk[off + (ps >> 5)] >> (ps & 31u)) & 1u) ++ps;
               const uint32_t val = g.slab[(unsigned long long)sw.hnd[off + (ps >> 5)] * 32u + (ps & 31u)];
               g.slab[(unsigned long long)sw.hnd[off + kb] * 32u + bit] = val;
@@ -259,7 +276,17 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
   }
 
   // =========================== medium sources: the warp = one source ===========================
+  struct MedSmem {
+    uint32_t stg[32][32];
+    uint32_t hnd[kFusedListBlocks], msk[kFusedListBlocks];
+    uint32_t tab[kFusedTable];
+    uint32_t bm[(1u << kMedFilterBits) / 32];
+  };
+  static_assert(sizeof(MedSmem) <= kFusedSmemBytes, "medium role layout");
+  MedSmem& sw = *reinterpret_cast<MedSmem*>(smem);
   const uint32_t n_med = op->n_fmed;
+  if (op_err) return;
+#pragma unroll 1
   for (uint32_t qi = blockIdx.x; qi < n_med; qi += g_med) {
     const uint32_t r = med_list[qi];
     const uint32_t mv = batch_src(b, r);
@@ -284,15 +311,21 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
       const unsigned long long hh = (unsigned long long)h0 + 32u * q + lane;
       if (32u * q + lane < mnb && hh < g.ring_cap) prefetch_l2(g.slab + hh * 32u);
     }
-    // ---- table + filter of the targets
-    constexpr int hshift = 32 - 9;
-    constexpr uint32_t tmask = kMedTable - 1;
-    for (uint32_t i = lane; i < kMedTable; i += 32) sw.tab[i] = kTomb;
-    for (uint32_t i = lane; i < (1u << kMedFilterBits) / 32; i += 32) sw.bm[i] = 0;
-    __syncwarp();
+    // ---- table (2^tb >= 2 k entries, at least 32: sized to the source) + 4096-bit membership filter of the targets
+    const int tb = max(5, 32 - __clz(2u * mk - 1u));
+    const uint32_t tmask = (1u << tb) - 1u;
+    const int hshift = 32 - tb;
+    constexpr int fb = kMedFilterBits;
+#pragma unroll 1
+    for (uint32_t i = lane; i <= tmask; i += 32) sw.tab[i] = kTomb;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (32u * q + lane < mk) table_insert(sw.tab, tmask, hshift, sw.bm, kMedFilterBits, tg[q]);
+    for (uint32_t i = 0; i < (1u << fb) / 32; i += 32) sw.bm[i + lane] = 0;
+    __syncwarp();
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t t = q == 0 ? tg[0] : q == 1 ? tg[1] : q == 2 ? tg[2] : tg[3];
+      if (32u * q + lane < mk) table_insert(sw.tab, tmask, hshift, sw.bm, fb, t);
+    }
     // ---- handles: the confirmed consecutive prefix, then a dependent walk for whatever is left
     uint32_t conf = 0;   // blocks h0 .. h0 + conf - 1 are the first conf blocks of the chain
     uint32_t h = h0;
@@ -312,6 +345,7 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
         }
       }
     }
+#pragma unroll 1
     while (conf < mnb) {   // (recycled chains) one round trip per physically consecutive run
       const unsigned long long hh = (unsigned long long)h + lane;
       const uint32_t nxw = hh < g.ring_cap ? g.next[hh] : kNull;
@@ -325,6 +359,7 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
     __syncwarp();
     // ---- match, 32 blocks per round
     uint32_t matched = 0;
+#pragma unroll 1
     for (uint32_t kb = 0; kb < mnb; kb += 32) {
       const uint32_t cnt = min(32u, mnb - kb);
       const uint32_t hd = ((uint32_t)lane < cnt) ? sw.hnd[kb + lane] : 0u;
@@ -342,17 +377,19 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
           const uint32_t evs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const uint32_t hb = filter_hash(evs[i], kMedFilterBits);
+            const uint32_t hb = filter_hash(evs[i], fb);
             cand |= ((sw.bm[hb >> 5] >> (hb & 31)) & 1u) << (4 * c + i);
           }
         }
         cand &= low_bits(cb);
+#pragma unroll 1
         while (cand) {
           const uint32_t bit = __ffs(cand) - 1;
           cand &= cand - 1;
           const uint32_t ev = block_slot(stg, lane, bit);
           uint32_t pos = (ev * 0x9E3779B1u) >> hshift;
           uint32_t t = sw.tab[pos];
+#pragma unroll 1
           while (t != ev && t != kTomb) {
             pos = (pos + 1) & tmask;
             t = sw.tab[pos];
@@ -364,19 +401,36 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
       matched += __popc(mask);
       __syncwarp();   // the strip is restaged by the next round
     }
-    matched = warp_sum(matched);
+    matched = redux_add(matched);
     if (lane == 0) {
       t_slots += md;
       t_blocks += mnb;
     }
     uint32_t new_nb = mnb, nfree = 0;
+    uint32_t moves = 0;
     if (matched) {
-      // ---- warp-parallel compaction: hole j (below the new degree) takes survivor j (above it)
+      // matches at or above the new degree leave no hole: moves = matches below it (often none: the
+      // newest entries of a source sit at the end of its chain)
+      const uint32_t nd = md - matched;
+      uint32_t m_hi = 0;
+#pragma unroll 1
+      for (uint32_t bi = (nd >> 5) + lane; bi < mnb; bi += 32) {
+        const uint32_t lo = bi * 32u;
+        m_hi += __popc(sw.msk[bi] & ~low_bits(nd > lo ? nd - lo : 0u));
+      }
+      moves = matched - redux_add(m_hi);
+    }
+    if (matched) {
       const uint32_t nd = md - matched;
       new_nb = (nd + 31u) >> 5;
+    }
+    if (moves) {
+      // ---- warp-parallel compaction: hole j (below the new degree) takes survivor j (above it)
+      const uint32_t nd = md - matched;
       uint16_t* hpre = reinterpret_cast<uint16_t*>(&stg[0][0]);   // exclusive hole / survivor counts per block
       uint16_t* spre = hpre + kFusedListBlocks;
       uint32_t carry_h = 0, carry_s = 0;
+#pragma unroll 1
       for (uint32_t c0 = 0; c0 < mnb; c0 += 32) {
         const uint32_t bi = c0 + lane;
         uint32_t hc = 0, sc = 0;
@@ -397,12 +451,13 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
         carry_s += __shfl_sync(kFull, si, 31);
       }
       __syncwarp();
-      const uint32_t moves = carry_h;   // == carry_s
-      const uint32_t sb0 = nd >> 5;     // first block that can hold a survivor
+      const uint32_t sb0 = nd >> 5;     // first block that can hold a survivor (carry_h == carry_s == moves)
+#pragma unroll 1
       for (uint32_t j = lane; j < moves; j += 32) {
         // largest block index with prefix <= j: the block that holds entry j (an empty block shares its
         // prefix with its successor, so it is never the largest)
         uint32_t lo = 0, hi = new_nb;   // holes live in blocks [0, new_nb)
+#pragma unroll 1
         while (hi - lo > 1) {
           const uint32_t mid = (lo + hi) >> 1;
           if (hpre[mid] <= j) lo = mid; else hi = mid;
@@ -413,6 +468,7 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
         const uint32_t hslot = __fns(hbits, 0, (int)(j - hpre[hb]) + 1);
         lo = sb0;
         hi = mnb;
+#pragma unroll 1
         while (hi - lo > 1) {
           const uint32_t mid = (lo + hi) >> 1;
           if (spre[mid] <= j) lo = mid; else hi = mid;
@@ -424,6 +480,9 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
         const uint32_t val = g.slab[(unsigned long long)sw.hnd[sb] * 32u + sslot];
         g.slab[(unsigned long long)sw.hnd[hb] * 32u + hslot] = val;
       }
+    }
+    if (matched) {
+      const uint32_t nd = md - matched;
       if (lane == 0) {
         g.deg[mv] = nd;
         if (nd == 0) {

@@ -1709,6 +1709,7 @@ __device__ __forceinline__ void table_insert(uint32_t* tab, uint32_t tmask, int 
   const uint32_t hb = filter_hash(x, bm_bits);
   atomicOr(&bm[hb >> 5], 1u << (hb & 31));
   uint32_t pos = (x * 0x9E3779B1u) >> hshift;
+#pragma unroll 1
   while (true) {
     const uint32_t old = atomicCAS(&tab[pos], kTomb, x);
     if (old == kTomb || old == x) break;
