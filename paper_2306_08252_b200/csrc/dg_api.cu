@@ -170,9 +170,16 @@ struct dg_graph {
   cudaStream_t aux[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr}, ev_main = nullptr;
   bool forked = false;
-  // alloc_kernel cursors carved from a buffer an earlier memset of the op already zeroed
-  unsigned long long* pre_zero = nullptr;
-  int pre_zero_left = 0;
+  // Persistent scratch that every op hands back ZEROED (no memset between ops): the per-vertex counters
+  // of the counting group-by (their users reset the words they touched), the alloc_kernel cursors (the
+  // last tile resets them) and the striped tallies of fused_delete_kernel (fused_tally_kernel resets them).
+  // After a failed or non-self-cleaning op the `*_clean` flags are false and the next user clears the buffer.
+  uint32_t* cnt_buf = nullptr;
+  uint64_t cnt_cap = 0;          // words
+  bool cnt_clean = false;
+  unsigned long long* zscratch = nullptr;   // [0, 8 x 4) alloc cursors, then kTallyStripes x kTalWords tallies
+  bool zscratch_clean = false;
+  int zslot = 0;
 
   std::string last_error;
   uint64_t last_shortfall = 0;  // blocks the last rejected insert was short of (0: it was not a pool underflow)
@@ -366,6 +373,36 @@ void join(dg_graph* h) {
   h->forked = false;
 }
 
+constexpr size_t kZAllocSlots = 8;
+constexpr size_t kZScratchWords = kZAllocSlots * kAllocScratchWords + (size_t)kTallyStripes * kTalWords;
+inline unsigned long long* tally_buf(const dg_graph* h) { return h->zscratch + kZAllocSlots * kAllocScratchWords; }
+
+// the counting group-by's counter array: persistent, zero between ops (see dg_graph::cnt_buf)
+inline uint64_t cnt_words_for(const dg_graph* h) { return std::bit_ceil(std::max<uint64_t>(h->size, 1)) + 4; }
+// (re)allocates for the current vertex count: call before the op's workspace is laid out
+int ensure_cnt(dg_graph* h) {
+  const uint64_t words = cnt_words_for(h);
+  if (words > h->cnt_cap) {
+    DG_CUDA(h, cudaStreamSynchronize(h->stream));
+    if (h->cnt_buf) cudaFree(h->cnt_buf);
+    h->cnt_buf = nullptr;
+    h->cnt_cap = 0;
+    if (cudaMalloc(&h->cnt_buf, words * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(h, DG_ERR_ENGINE, "group-by counters: device allocation failed");
+    }
+    h->cnt_cap = words;
+    h->cnt_clean = false;
+  }
+  return DG_OK;
+}
+// hands out the counters, all zero; `self_cleaning`: the op resets every word it touches (its success keeps the flag)
+uint32_t* acquire_cnt(dg_graph* h, bool self_cleaning) {
+  if (!h->cnt_clean) cudaMemsetAsync(h->cnt_buf, 0, h->cnt_cap * 4, h->stream);
+  h->cnt_clean = self_cleaning;   // (op_end clears the flag when the op is rejected)
+  return h->cnt_buf;
+}
+
 // ---- op bracket -----------------------------------------------------------
 int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
   OpState& op = h->h_blk->op;
@@ -378,7 +415,11 @@ int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
   op.n_aux = h->size + 1;
   DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
   h->launches = 0;
-  h->pre_zero_left = 0;
+  h->zslot = 0;
+  if (!h->zscratch_clean) {
+    DG_CUDA(h, cudaMemsetAsync(h->zscratch, 0, kZScratchWords * sizeof(unsigned long long), h->stream));
+    h->zscratch_clean = true;
+  }
   h->report = dg_op_report{};
   h->report.batch_entries = n_input;
   return DG_OK;
@@ -424,6 +465,8 @@ int op_end(dg_graph* h) {
   h->report.slots_scanned_long = op.slots_long;
   h->report.slots_scanned_tiny = op.slots_tiny;
   if (op.err != 0) {
+    h->zscratch_clean = false;   // kernels of a rejected op return early: cursors / tallies may be left behind
+    h->cnt_clean = false;
     h->report.blocks_popped = 0;
     if (op.err_detail == kErrPoolUnderflow) h->last_shortfall = op.err_index;
     return fail(h, (int)op.err,
@@ -448,15 +491,8 @@ template <class In, class Out, class Fin>
 void launch_alloc(dg_graph* h, const char* name, uint64_t n_bound, const unsigned long long* n_ptr,
                   In in, Out out, Fin fin, cudaStream_t stream = nullptr) {
   if (stream == nullptr) stream = h->stream;
-  unsigned long long* scratch;
-  if (h->pre_zero_left > 0) {
-    scratch = h->pre_zero;
-    h->pre_zero += kAllocScratchWords;
-    --h->pre_zero_left;
-  } else {
-    scratch = ws_alloc<unsigned long long>(h, kAllocScratchWords);
-    cudaMemsetAsync(scratch, 0, kAllocScratchWords * sizeof(unsigned long long), stream);
-  }
+  // cursors: a slot of the persistent zeroed scratch (the kernel's last tile hands it back zeroed)
+  unsigned long long* scratch = h->zscratch + (size_t)(h->zslot++ % kZAllocSlots) * kAllocScratchWords;
   if (n_bound > (2u << 20)) {
     constexpr int kTile = kAllocThreads * kAllocItemsLarge;
     const unsigned tiles = (unsigned)((n_bound + kTile - 1) / kTile);
@@ -745,9 +781,12 @@ struct Worklist {
   uint2* long_items;
   uint32_t* big_list;  // chains longer than kLaneWalk blocks
   uint32_t* run_head;  // fused delete only: head block of the warp-owned sources (else nullptr)
-  uint32_t* fmed_list; // fused delete only: runs of the medium class
+  uint4* fmed_rec;     // fused delete only: sources of the medium class (two words each)
+  uint32_t* zero3;     // delete only: run_matched / hole_cnt / surv_cnt, zeroed per run by the enumeration plan
+  uint32_t zstride;
   EnumLists lists(dg_graph* h) const {
-    return EnumLists{run_deg, wl_off, med_items, long_items, big_list, (uint32_t)big_bound(h), h->d_op(), run_head, fmed_list};
+    return EnumLists{run_deg, wl_off, med_items, long_items, big_list, (uint32_t)big_bound(h), h->d_op(), run_head, fmed_rec,
+                     zero3, zstride};
   }
 };
 
@@ -765,11 +804,16 @@ inline uint64_t fused_med_bound(const dg_graph* h, uint64_t runs_bound, uint64_t
   return std::min<uint64_t>(runs_bound, h->blocks_in_use() / (kFusedSmallBlocks + 1) + n_batch / (kFusedSmallTargets + 1) + 1) + 1;
 }
 // n_batch: entries of the batch the runs index into; has_batch false: export, digest
-Worklist alloc_worklist(dg_graph* h, uint64_t runs_bound, uint64_t n_batch, bool has_batch, bool fuse = false) {
+Worklist alloc_worklist(dg_graph* h, uint64_t runs_bound, uint64_t n_batch, bool has_batch, bool fuse = false,
+                        bool for_delete = false) {
   Worklist w{};
+  if (for_delete) {
+    w.zero3 = ws_alloc<uint32_t>(h, 3 * (runs_bound + 1));
+    w.zstride = (uint32_t)(runs_bound + 1);
+  }
   if (fuse) {
     w.run_head = ws_alloc<uint32_t>(h, runs_bound + 1);
-    w.fmed_list = ws_alloc<uint32_t>(h, fused_med_bound(h, runs_bound, n_batch));
+    w.fmed_rec = ws_alloc<uint4>(h, 2 * fused_med_bound(h, runs_bound, n_batch));
   }
   const uint64_t wl_cap = h->blocks_in_use();
   w.wl_off = ws_alloc<uint32_t>(h, runs_bound + 1);
@@ -784,7 +828,7 @@ Worklist alloc_worklist(dg_graph* h, uint64_t runs_bound, uint64_t n_batch, bool
   return w;
 }
 inline size_t worklist_ws(const dg_graph* h, uint64_t runs_bound, uint64_t n_batch) {
-  return 3 * aligned((runs_bound + 1) * 4) + aligned(fused_med_bound(h, runs_bound, n_batch) * 4) + aligned(kTallyStripes * kTalWords * 8) +
+  return 3 * aligned((runs_bound + 1) * 4) + aligned(fused_med_bound(h, runs_bound, n_batch) * 32) +
          2 * aligned((h->blocks_in_use() + 1) * 4) +
          aligned(med_items_bound(h, n_batch) * 8) + aligned(long_items_bound(h, n_batch) * 8) +
          aligned(big_bound(h) * 4) + alloc_ws_bytes();
@@ -805,9 +849,9 @@ void enqueue_walk(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t r
 
 // enumeration over an already grouped batch (radix path, CSR batches) or over every vertex (export)
 Worklist enqueue_enumerate(dg_graph* h, const BatchView& b, uint64_t runs_bound, uint64_t n_batch,
-                           int check_alive, bool fuse = false, bool walk = true) {
+                           int check_alive, bool fuse = false, bool walk = true, bool for_delete = false) {
   GraphView g = view(h);
-  Worklist w = alloc_worklist(h, runs_bound, n_batch, b.run_start != nullptr, fuse);
+  Worklist w = alloc_worklist(h, runs_bound, n_batch, b.run_start != nullptr, fuse, for_delete);
   launch_alloc(h, "alloc_kernel<enum>", runs_bound, d_n_runs(h), EnumIn{g, b, check_alive, fuse}, EnumOut{g, b, w.lists(h)},
                EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/0});
   if (!walk) return w;
@@ -903,9 +947,8 @@ Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, u
   const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
   out.gi = GroupIndex{(uint32_t)(cap - 1), (uint32_t)h->size};
   out.cnt_words = cap + 1;
-  // the counters and the op's alloc_kernel cursors are zeroed by ONE memset
-  const uint64_t cnt_words = (cap + 3) & ~1ull;  // even: the 64-bit cursors follow
-  out.cnt = ws_alloc<uint32_t>(h, cnt_words + 2 * 2 * kAllocScratchWords);
+  // fused delete (B = 32) resets every counter it touched; query / other block sizes leave them behind
+  out.cnt = acquire_cnt(h, kMode == kPackDelete && h->B == 32);
   out.rank = ws_alloc<uint32_t>(h, n);
   out.gdst = ws_alloc<uint32_t>(h, n);
   if (with_index) out.index = ws_alloc<uint32_t>(h, n);
@@ -913,9 +956,6 @@ Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, u
   out.run_start = ws_alloc<uint32_t>(h, out.runs_bound + 1);
   out.run_end = ws_alloc<uint32_t>(h, out.runs_bound + 1);
   out.run_src = ws_alloc<uint32_t>(h, out.runs_bound + 1);
-  cudaMemsetAsync(out.cnt, 0, (cnt_words + 2 * 2 * kAllocScratchWords) * 4, h->stream);
-  h->pre_zero = reinterpret_cast<unsigned long long*>(out.cnt + cnt_words);
-  h->pre_zero_left = 2;
   DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
       g, out.gi, d_src, d_dst, (uint32_t)n, out.cnt, out.rank, h->d_op()));
   out.b = BatchView{nullptr, out.gdst, out.run_src, out.run_start, out.run_end};
@@ -1011,22 +1051,16 @@ inline cudaStream_t side(const dg_graph* h, int i) { return h->profiling ? h->st
 
 template <class Scatter>
 int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound, uint64_t n, bool fuse,
-               Scatter&& scatter) {
+               GroupIndex gi, uint32_t* cnt, Scatter&& scatter) {
   GraphView g = view(h);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  uint32_t* zeroed = ws_alloc<uint32_t>(h, 3 * (runs_bound + 1));  // one memset for the three counters
-  uint32_t* run_matched = zeroed;
-  uint32_t* hole_cnt = zeroed + (runs_bound + 1);
-  uint32_t* surv_cnt = zeroed + 2 * (runs_bound + 1);
+  uint32_t* run_matched = w.zero3;   // (zeroed per run by the enumeration plan)
+  uint32_t* hole_cnt = w.zero3 + (runs_bound + 1);
+  uint32_t* surv_cnt = w.zero3 + 2 * (runs_bound + 1);
   uint32_t* mv_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   uint32_t* free_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   uint32_t* wl_mask = ws_alloc<uint32_t>(h, (wl_bound + 1) * g.mw);
-  cudaMemsetAsync(zeroed, 0, 3 * (runs_bound + 1) * 4, h->stream);
-  unsigned long long* tally = nullptr;
-  if (fuse) {
-    tally = ws_alloc<unsigned long long>(h, kTallyStripes * kTalWords);
-    cudaMemsetAsync(tally, 0, kTallyStripes * kTalWords * sizeof(unsigned long long), h->stream);
-  }
+  unsigned long long* tally = tally_buf(h);   // persistent, zero between ops
   const bool par = !h->profiling;
   cudaStream_t s0 = side(h, 0), s1 = side(h, 1);
   if (par) {
@@ -1042,7 +1076,7 @@ int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs
     const uint32_t g_med = (uint32_t)std::clamp<uint64_t>((fused_med_bound(h, runs_bound, n) + 7) / 8, 1, 32768);
     const unsigned grid = g_med + (unsigned)((runs_bound + 31) / 32);
     DG_LAUNCH(h, "fused_delete_kernel", fused_delete_kernel<<<grid, 32, 0, h->stream>>>(
-        g, b, w.wl_off, w.run_deg, w.run_head, w.fmed_list, g_med, tally, h->d_op()));
+        g, b, w.wl_off, w.run_deg, w.run_head, w.fmed_rec, g_med, (uint32_t)runs_bound, gi, cnt, tally, h->d_op()));
     DG_LAUNCH(h, "fused_tally_kernel", fused_tally_kernel<<<1, 32, 0, h->stream>>>(g, tally, h->d_op()));
   }
   if (par) {   // the hub match needs both walks and the scatter
@@ -1096,15 +1130,16 @@ int delete_coo_run(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, ui
   const bool fuse = h->B == 32;
   if (use_counting(h, n)) {
     Grouped gr = group_count<kPackDelete>(h, d_src, d_dst, n, false);
-    Worklist w = alloc_worklist(h, gr.runs_bound, n, true, fuse);
+    Worklist w = alloc_worklist(h, gr.runs_bound, n, true, fuse, /*for_delete=*/true);
     launch_alloc(h, "alloc_kernel<group+enum>", n, d_n_input(h), GroupEnumIn{g, gr.gi, d_src, gr.rank, gr.cnt, 1, fuse},
                  GroupEnumOut{g, gr.gi, d_src, gr.cnt, gr.run_src, gr.run_start, gr.run_end, w.lists(h)},
                  EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/1});
-    return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, [&] { group_scatter<kPackDelete>(h, gr, d_src, d_dst, n); });
+    return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, gr.gi, fuse ? gr.cnt : nullptr,
+                      [&] { group_scatter<kPackDelete>(h, gr, d_src, d_dst, n); });
   }
   Grouped gr = group_radix<kPackDelete>(h, d_src, d_dst, n, false, max_src);
-  Worklist w = enqueue_enumerate(h, gr.b, gr.runs_bound, n, /*check_alive=*/1, fuse, /*walk=*/false);
-  return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, [] {});
+  Worklist w = enqueue_enumerate(h, gr.b, gr.runs_bound, n, /*check_alive=*/1, fuse, /*walk=*/false, /*for_delete=*/true);
+  return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, GroupIndex{}, nullptr, [] {});
 }
 
 
@@ -1188,6 +1223,10 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
     if (rc != DG_OK) return bail(rc, h->last_error);
   }
   if (ensure_mv_scratch(h, 1 << 16) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
+  if (cudaMalloc(&h->zscratch, kZScratchWords * sizeof(unsigned long long)) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(DG_ERR_ENGINE, "dg_create: device allocation failed");
+  }
   // side streams run the (few, latency-critical) hub kernels of an op beside its bulk kernel: highest priority
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
@@ -1226,6 +1265,8 @@ void dg_destroy(dg_graph* h) {
   if (h->h_blk) cudaFreeHost(h->h_blk);
   cudaFree(h->ws.base);
   cudaFree(h->mv_hole);
+  cudaFree(h->cnt_buf);
+  cudaFree(h->zscratch);
   for (int i = 0; i < 2; ++i) {
     if (h->aux[i]) { cudaStreamSynchronize(h->aux[i]); cudaStreamDestroy(h->aux[i]); }
     if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
@@ -1250,6 +1291,7 @@ static int insert_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
   const bool counting = use_counting(h, n);
+  if (counting && ensure_cnt(h) != DG_OK) return DG_ERR_ENGINE;
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
   if (counting) {
@@ -1271,18 +1313,14 @@ static int insert_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst
     GraphView g = view(h);
     const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
     GroupIndex gi{(uint32_t)(cap - 1), (uint32_t)h->size};
-    const uint64_t cnt_words = (cap + 3) & ~1ull;  // even: the 64-bit cursors follow
-    uint32_t* cnt = ws_alloc<uint32_t>(h, cnt_words + 2 * kAllocScratchWords);
+    uint32_t* cnt = acquire_cnt(h, /*self_cleaning=*/true);   // the plan pass hands every touched counter back zeroed
     uint32_t* rank = ws_alloc<uint32_t>(h, n);
     uint4* info = ws_alloc<uint4>(h, cap + 2);
-    cudaMemsetAsync(cnt, 0, (cnt_words + 2 * kAllocScratchWords) * 4, h->stream);  // counters + the alloc cursors
-    h->pre_zero = reinterpret_cast<unsigned long long*>(cnt + cnt_words);
-    h->pre_zero_left = 1;
     const unsigned grid = (unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems));
     DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kPackInsert><<<grid, 256, 0, h->stream>>>(
         g, gi, d_src, d_dst, (uint32_t)n, cnt, rank, h->d_op()));
     launch_alloc(h, "alloc_kernel<group+plan>", n, d_n_input(h), GroupPlanIn{g, gi, d_src, rank, cnt},
-                 GroupPlanOut{gi, d_src, info}, PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/1});
+                 GroupPlanOut{gi, d_src, info, cnt}, PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/1});
     DG_LAUNCH(h, "append_entries_kernel", append_entries_kernel<<<grid, 256, 0, h->stream>>>(
         g, gi, d_src, d_dst, rank, (uint32_t)n, info, h->d_op()));
     return op_end(h);
@@ -1414,6 +1452,7 @@ int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
   const bool no_pool = h->B == 0;  // no pool yet => no edges: only validation can have an effect
+  if (!no_pool && use_counting(h, n) && ensure_cnt(h) != DG_OK) return DG_ERR_ENGINE;
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
   if (no_pool) sz.total += group_ws_bytes(h, n, false, h->size - 1);
@@ -1464,8 +1503,8 @@ int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets
   // a CSR batch is already grouped: run r is vertex r (empty runs are skipped by the enumeration)
   BatchView b{nullptr, d_dst, nullptr, run_start, run_start + 1};
   const bool fuse = h->B == 32;
-  Worklist w = enqueue_enumerate(h, b, V, n, /*check_alive=*/1, fuse, /*walk=*/false);
-  return delete_run(h, b, w, V, n, fuse, [] {});
+  Worklist w = enqueue_enumerate(h, b, V, n, /*check_alive=*/1, fuse, /*walk=*/false, /*for_delete=*/true);
+  return delete_run(h, b, w, V, n, fuse, GroupIndex{}, nullptr, [] {});
 }
 
 // ---- query ---------------------------------------------------------------------
@@ -1481,6 +1520,7 @@ int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64
     else DG_CUDA(h, cudaMemsetAsync(out, 0, n, h->stream));
     return DG_OK;
   }
+  if (use_counting(h, n) && ensure_cnt(h) != DG_OK) return DG_ERR_ENGINE;
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); sz.add<uint8_t>(n); }
   sz.total += group_enumerate_ws(h, n, true, h->size);  // ids are clamped to size (unknown source)

@@ -228,7 +228,7 @@ scan_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* sc
 //   In(i)                         -> Sum2 (PURE loads; see scan_kernel)
 //   Out(i, excl.a, excl.b, value) -> per element
 //   Fin(total.a, total.b)         -> once, by the last tile to finish
-// scratch: [0] cursor a, [1] cursor b, [2] finished tiles; zeroed before launch.
+// scratch: [0] cursor a, [1] cursor b, [2] finished tiles; zero at launch, zeroed again by the last tile.
 struct Sum2 {
   unsigned long long a, b;
 };
@@ -315,7 +315,11 @@ alloc_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* s
     const unsigned long long done = atomicAdd(&scratch[2], 1ull);
     if (done == num_tiles - 1) {
       __threadfence();
-      fin(ld_volatile_u64(&scratch[0]), ld_volatile_u64(&scratch[1]));
+      const unsigned long long ta = ld_volatile_u64(&scratch[0]), tb = ld_volatile_u64(&scratch[1]);
+      scratch[0] = 0ull;   // the cursors are handed back zeroed: the host keeps them in a persistent
+      scratch[1] = 0ull;   // buffer and never clears them between ops
+      scratch[2] = 0ull;
+      fin(ta, tb);
     }
   }
 }

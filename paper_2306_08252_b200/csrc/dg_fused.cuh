@@ -90,8 +90,8 @@ __device__ __noinline__ void tally_flush(unsigned long long* tally, uint32_t mat
 //       [g_med, g_med + ceil(T / 32)) small role — 32 consecutive runs per warp, lane = run.
 __global__ void __launch_bounds__(32, 28)
 fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_cls, const uint32_t* __restrict__ run_deg,
-                    const uint32_t* __restrict__ run_head, const uint32_t* __restrict__ med_list, uint32_t g_med,
-                    unsigned long long* tally, OpState* op) {
+                    const uint32_t* __restrict__ run_head, const uint4* __restrict__ med_rec, uint32_t g_med,
+                    uint32_t runs_bound, GroupIndex gi, uint32_t* __restrict__ cnt, unsigned long long* tally, OpState* op) {
   __shared__ __align__(16) unsigned char smem[kFusedSmemBytes];
   const int lane = lane_id();
   uint32_t(*stg)[32] = reinterpret_cast<uint32_t(*)[32]>(smem);
@@ -110,20 +110,23 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
     };
     static_assert(sizeof(SmallSmem) <= kFusedSmemBytes, "small role layout");
     SmallSmem& sw = *reinterpret_cast<SmallSmem*>(smem);
-    const uint32_t T = (uint32_t)op->n_runs;
+    // every first load is issued before anything is waited for (the run arrays cover the whole grid: entries
+    // past the run count hold garbage and are discarded once the count has arrived)
     const uint32_t r = (blockIdx.x - g_med) * 32u + lane;
+    const uint32_t rr = min(r, runs_bound - 1u);
+    uint32_t cls = run_cls[rr];
+    const uint32_t es = b.run_start[rr];
+    const uint32_t k = b.run_end[rr] - es;
+    const uint32_t d = run_deg[rr];
+    const uint32_t h0 = run_head[rr];
+    const uint32_t v = batch_src(b, rr);
+    const uint32_t T = (uint32_t)op->n_runs;
     if (op_err || r - lane >= T) return;
+    if (r >= T) cls = kClsNone;
+    // the counting group-by's per-source word goes back to zero (it is never cleared between ops)
+    if (cnt != nullptr && r < T) cnt[gi(v)] = 0u;
     uint32_t* s_tg = sw.tg;
     unsigned long long* s_filt = sw.filt;
-    uint32_t cls = kClsNone, v = 0, es = 0, k = 0, d = 0, h0 = kNull;
-    if (r < T) {
-      cls = run_cls[r];
-      es = b.run_start[r];
-      k = b.run_end[r] - es;
-      d = run_deg[r];
-      h0 = run_head[r];
-      v = batch_src(b, r);
-    }
     const bool small = cls == kClsSmall;
     const uint32_t nb = small ? (d + 31u) >> 5 : 0u;
     unsigned pending = __ballot_sync(kFull, small);
@@ -284,16 +287,17 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
   };
   static_assert(sizeof(MedSmem) <= kFusedSmemBytes, "medium role layout");
   MedSmem& sw = *reinterpret_cast<MedSmem*>(smem);
+  uint4 rec0 = med_rec[2u * blockIdx.x], rec1 = med_rec[2u * blockIdx.x + 1u];   // (garbage past the count: unused)
   const uint32_t n_med = op->n_fmed;
   if (op_err) return;
 #pragma unroll 1
   for (uint32_t qi = blockIdx.x; qi < n_med; qi += g_med) {
-    const uint32_t r = med_list[qi];
-    const uint32_t mv = batch_src(b, r);
-    const uint32_t mes = b.run_start[r];
-    const uint32_t mk = b.run_end[r] - mes;
-    const uint32_t md = run_deg[r];
-    const uint32_t h0 = run_head[r];
+    if (qi != blockIdx.x) {
+      rec0 = med_rec[2u * qi];
+      rec1 = med_rec[2u * qi + 1u];
+    }
+    const uint32_t mv = rec0.y, mes = rec0.z, mk = rec0.w;
+    const uint32_t md = rec1.x, h0 = rec1.y;
     const uint32_t mnb = (md + 31u) >> 5;
     // ---- one round trip: the targets, every link of the chain under the guess that it is physically
     // consecutive (bulk-built and ring-popped chains are), and the first blocks on their way to L2
@@ -511,12 +515,15 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
 }
 
 // folds the striped tallies into the op words and the live-edge count (graph.hpp:211-213)
-__global__ void fused_tally_kernel(GraphView g, const unsigned long long* __restrict__ tally, OpState* op) {
+__global__ void fused_tally_kernel(GraphView g, unsigned long long* __restrict__ tally, OpState* op) {
   if (op->err) return;
   unsigned long long v = 0;
   const int w = threadIdx.x;   // one thread per tally word
   if (w < 5)
-    for (uint32_t s = 0; s < kTallyStripes; ++s) v += tally[(size_t)s * kTalWords + w];
+    for (uint32_t s = 0; s < kTallyStripes; ++s) {
+      v += tally[(size_t)s * kTalWords + w];
+      tally[(size_t)s * kTalWords + w] = 0ull;   // handed back zeroed (persistent buffer)
+    }
   if (v == 0) return;
   if (w == kTalMatched) {
     atomicAdd(&op->matched, v);

@@ -515,11 +515,14 @@ struct GroupPlanOut {
   GroupIndex gi;
   const uint32_t* src;
   uint4* info;
+  uint32_t* cnt;   // the source's counter is handed back zeroed (the counter array is never cleared between ops)
   __device__ void operator()(unsigned long long i, unsigned long long, unsigned long long excl_b,
                              Sum2 val, const PlanAux& x) const {
     const uint32_t c = (uint32_t)val.a;
     if (c == 0) return;
-    info[gi(src[i])] = make_uint4(x.d, x.tail, (uint32_t)excl_b, c);
+    const uint32_t slot = gi(src[i]);
+    info[slot] = make_uint4(x.d, x.tail, (uint32_t)excl_b, c);
+    cnt[slot] = 0u;
   }
 };
 struct PlanFin {
@@ -1304,15 +1307,28 @@ struct EnumLists {
   uint32_t big_cap;
   OpState* op;
   uint32_t* run_head;  // fused delete: head block of every warp-owned source (nullptr: no fusion)
-  uint32_t* fmed_list; // fused delete: runs of the medium class (a warp per source), filled through op->n_fmed
-  __device__ void write(uint32_t r, uint32_t d, uint32_t nblk, uint32_t k, uint32_t head, unsigned long long excl_b) const {
+  uint4* fmed_rec;     // fused delete: sources of the medium class (a warp per source), two 16-byte words each
+                       // {run, vertex, first target, targets} {degree, head, -, -}, filled through op->n_fmed
+  uint32_t* zero3;     // delete: run_matched / hole_cnt / surv_cnt of the run start at zero (no memset)
+  uint32_t zstride;
+  __device__ void write(uint32_t r, uint32_t d, uint32_t nblk, uint32_t k, uint32_t head, uint32_t v, uint32_t es,
+                        unsigned long long excl_b) const {
     run_deg[r] = d;
+    if (zero3 != nullptr) {
+      zero3[r] = 0u;
+      zero3[r + zstride] = 0u;
+      zero3[r + 2u * zstride] = 0u;
+    }
     if (run_head != nullptr) {   // warp-owned sources take no work-list segment: wl_off carries their class
       const uint32_t cls = fused_class(k, nblk);
       if (cls != 0u) {
         wl_off[r] = cls;
         run_head[r] = head;
-        if (cls == kClsMed) fmed_list[atomicAdd(&op->n_fmed, 1u)] = r;
+        if (cls == kClsMed) {
+          const uint32_t slot = atomicAdd(&op->n_fmed, 1u);
+          fmed_rec[2u * slot] = make_uint4(r, v, es, k);
+          fmed_rec[2u * slot + 1u] = make_uint4(d, head, 0u, 0u);
+        }
         return;
       }
     }
@@ -1376,7 +1392,8 @@ struct EnumOut {
   __device__ void operator()(unsigned long long r, unsigned long long, unsigned long long excl_b,
                              Sum2 v, const EnumAux& x) const {
     const uint32_t k = b.run_start != nullptr ? run_len(b, (uint32_t)r) : 0u;
-    lists.write((uint32_t)r, x.d, blocks_for(g, x.d), k, x.head, excl_b);
+    lists.write((uint32_t)r, x.d, blocks_for(g, x.d), k, x.head, batch_src(b, (uint32_t)r),
+                b.run_start != nullptr ? b.run_start[r] : 0u, excl_b);
   }
 };
 // fused with the counting group-by: one pass over the batch entries (see GroupPlanIn)
@@ -1418,7 +1435,7 @@ struct GroupEnumOut {
     run_start[r] = es;
     run_end[r] = es + c;
     cnt[gi(v)] = es;
-    lists.write(r, x.d, blocks_for(g, x.d), c, x.head, excl_b);
+    lists.write(r, x.d, blocks_for(g, x.d), c, x.head, v, es, excl_b);
   }
 };
 struct EnumFin {
