@@ -558,14 +558,16 @@ void sort_keys(dg_graph* h, unsigned long long** keys, unsigned long long** keys
   if (!hist_done)
     DG_LAUNCH(h, "sort_hist_kernel", sort_hist_kernel<<<grid_for(h, n, 256 * 8), 256, 0, h->stream>>>(*keys, n, plan, sc.hist, h->d_op()));
   const unsigned tiles = (unsigned)sort_tiles(n);
+  cudaFuncSetAttribute(sort_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemKeysVals);
+  cudaFuncSetAttribute(sort_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemKeys);
   for (int p = 0; p < plan.passes; ++p) {
     if (vals && *vals) {
-      DG_LAUNCH(h, "sort_pass_kernel<true>", sort_pass_kernel<true><<<tiles, kSortThreads, 0, h->stream>>>(
+      DG_LAUNCH(h, "sort_pass_kernel<true>", sort_pass_kernel<true><<<tiles, kSortThreads, kSortSmemKeysVals, h->stream>>>(
           *keys, *keys_alt, *vals, *vals_alt, n, plan.shift[p], plan.bits[p], sc.hist + p * kRadix,
           sc.status + (size_t)p * sc.per_pass, h->d_op()));
       std::swap(*vals, *vals_alt);
     } else {
-      DG_LAUNCH(h, "sort_pass_kernel<false>", sort_pass_kernel<false><<<tiles, kSortThreads, 0, h->stream>>>(
+      DG_LAUNCH(h, "sort_pass_kernel<false>", sort_pass_kernel<false><<<tiles, kSortThreads, kSortSmemKeys, h->stream>>>(
           *keys, *keys_alt, nullptr, nullptr, n, plan.shift[p], plan.bits[p], sc.hist + p * kRadix,
           sc.status + (size_t)p * sc.per_pass, h->d_op()));
     }
