@@ -65,7 +65,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=2, help="batches in the cpu_baseline sample")
+    ap.add_argument("--cpu-steps", type=int, default=0,
+                    help="batches in the cpu_baseline sample; 0 = all warm-up + timed batches, which also makes the "
+                         "final states comparable (the `parity` block)")
     return ap.parse_args()
 
 
@@ -177,7 +179,7 @@ def kernel_bytes(name: str, rep: dict, B: int) -> float | None:
 # CPU baseline (reference arm and the cpu_baseline leg)
 # --------------------------------------------------------------------------------------
 def cpu_reference_run(scale: int, edge_factor: int, batch: int, warmup: int, steps: int, threads: int,
-                      block_size: int = 32):
+                      block_size: int = 32, want_state: bool = False):
     """Times the reference's CPU implementation of the step on this host.
 
     Uses oracle/_ref/libdyngraph_ref.so (the unmodified reference headers behind
@@ -226,9 +228,15 @@ def cpu_reference_run(scale: int, edge_factor: int, batch: int, warmup: int, ste
         if i >= warmup:
             t_ins += ti
             t_del += td
+    state = None
+    if want_state:   # observables oracle_compare checks (oracle.hpp:98-163), in their scale-independent form
+        dg, ne = g.digest()
+        state = {"active_edges": g.active_edges(), "digest": dg, "entries": ne, "degrees": g.degrees(),
+                 "alive_vertices": g.alive_vertices(), "logical_size": g.logical_size()}
     g.close()
     total = t_ins + t_del
     return {
+        "state": state,
         "kind": kind, "cores": threads, "block_size": B,
         "value": 2 * batch * steps / total / 1e6, "unit": UNIT,
         "insert_medges_s": batch * steps / t_ins / 1e6, "delete_medges_s": batch * steps / t_del / 1e6,
@@ -572,6 +580,7 @@ def run_b200_arm(args):
         clock_rec = clocks.stop()   # sampled over the timed, split, e2e and per-kernel passes
         final_st = g.stats()
         digest = g.digest()
+        gpu_degrees = g.degrees() if sharded is None else None
         global_edges = sharded.active_edges() if sharded is not None else final_st["active_edges"]   # (collective)
 
     value = 2 * b * world * K / (total_ms * 1e-3) / 1e6
@@ -598,11 +607,31 @@ def run_b200_arm(args):
         "wall_ms_per_step": wall_ms / K,
         "bulk_init_kernels_us": bulk_kernels, "clocks": clock_rec, "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
     }
+    parity_failed = False
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference_run(args.scale, args.edge_factor, args.batch, 1, args.cpu_steps, os.cpu_count() or 1, B)
+            # The reference applies the SAME batches (all W + K of them, once each: repeating a step on the GPU
+            # does not change the outcome — a delete removes every copy of its pairs, base copies included) to
+            # the SAME base graph; both stores must then hold the same multiset: live-edge count, per-vertex
+            # degrees and the digest over (source, destination) copies.  Untimed on the GPU side.
+            full = args.cpu_steps == 0
+            r = cpu_reference_run(args.scale, args.edge_factor, args.batch, 0 if full else 1, (K + W) if full else args.cpu_steps,
+                                  os.cpu_count() or 1, B, want_state=full)
             line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample",
                                                      "insert_medges_s", "delete_medges_s", "bulk_insert_ms", "init_ms")}
+            if full and r["state"] is not None and gpu_degrees is not None:
+                st_ref = r["state"]
+                deg_equal = bool(np.array_equal(np.asarray(gpu_degrees, dtype=np.uint64), np.asarray(st_ref["degrees"], dtype=np.uint64)))
+                ok = (deg_equal and st_ref["active_edges"] == final_st["active_edges"] and st_ref["digest"] == digest[0]
+                      and st_ref["entries"] == digest[1] and st_ref["alive_vertices"] == final_st["alive_vertices"]
+                      and st_ref["logical_size"] == final_st["logical_size"])
+                line["parity"] = {"ok": ok, "against": r["kind"], "batches_applied": K + W,
+                                  "active_edges": [final_st["active_edges"], st_ref["active_edges"]],
+                                  "digest": [f"{digest[0]:016x}", f"{st_ref['digest']:016x}"],
+                                  "entries": [digest[1], st_ref["entries"]], "degrees_equal": deg_equal,
+                                  "what": "GPU store after every pass of this run vs the reference after the same base graph + "
+                                          "the same batches: live edges, per-vertex degrees, digest of all (src, dst) copies"}
+                parity_failed = not ok
         except Exception as e:  # the baseline is reported, never required for the CUDA number
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
                                     "sample": f"failed: {e}"}
@@ -610,6 +639,9 @@ def run_b200_arm(args):
         emit(line)
     if world > 1 or force_sharded:
         dist.destroy_process_group()
+    if parity_failed:
+        print("bench.py: PARITY FAILURE against the reference (see the `parity` block)", file=sys.stderr)
+        return 3
     return 0
 
 

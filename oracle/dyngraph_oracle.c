@@ -538,6 +538,35 @@ int orc_degrees(void* p, uint64_t* out) {
   return ORC_OK;
 }
 
+/* Order-independent digest of the stored multiset: sum over live entries of mix64(v << 32 | dst)
+ * (the device twin is digest_kernel; same coverage as orc_export_csr: active_destinations of every
+ * v < logical_size, graph.hpp:116-129). */
+static uint64_t orc_mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+int orc_digest(void* p, uint64_t* digest, uint64_t* entries) {
+  Oracle* g = (Oracle*)p;
+  uint64_t acc = 0, cnt = 0;
+  for (uint64_t v = 0; v < g->size; ++v) {
+    const Sentinel* s = &g->sent[v];
+    for (uint32_t k = 0; k < s->block_count; ++k) {
+      const uint32_t h = s->blocks[k];
+      for (uint32_t i = 0; i < g->occupied[h]; ++i) {
+        const uint64_t slot = (uint64_t)h * g->B + i;
+        if (g->tomb[slot]) continue;
+        acc += orc_mix64((v << 32) | g->dst[slot]);
+        cnt++;
+      }
+    }
+  }
+  if (digest) *digest = acc;
+  if (entries) *entries = cnt;
+  return ORC_OK;
+}
+
 /* active_destinations (graph.hpp:116-129) for every vertex, optionally sorted */
 int orc_export_csr(void* p, uint64_t* offsets, uint32_t* dsts, uint64_t cap, int sorted) {
   Oracle* g = (Oracle*)p;

@@ -168,6 +168,29 @@ int ref_degrees(void* p, std::uint64_t* out) {
   return 0;
 }
 
+// Order-independent digest of the stored multiset (sum over live entries of mix64(v << 32 | dst)): the
+// device twin is digest_kernel.  Walks active_destinations (graph.hpp:116-129) of every v < logical_size.
+static std::uint64_t shim_mix64(std::uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+int ref_digest(void* p, std::uint64_t* digest, std::uint64_t* entries) {
+  auto* r = static_cast<Ref*>(p);
+  std::uint64_t acc = 0, cnt = 0;
+  const std::uint64_t n = r->g->logical_size();
+  for (std::uint64_t v = 0; v < n; ++v) {
+    for (std::uint32_t d : r->g->active_destinations(static_cast<dyngraph::VertexId>(v))) {
+      acc += shim_mix64((v << 32) | d);
+      ++cnt;
+    }
+  }
+  if (digest) *digest = acc;
+  if (entries) *entries = cnt;
+  return 0;
+}
+
 int ref_export_csr(void* p, std::uint64_t* offsets, std::uint32_t* dsts, std::uint64_t cap, int sorted) {
   auto* r = static_cast<Ref*>(p);
   std::uint64_t w = 0;

@@ -55,6 +55,7 @@ def _bind(lib, prefix: str):
         "blocks_in_use": (C.c_uint64, [_vp]),
         "degrees": (C.c_int, [_vp, _vp]),
         "export_csr": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int]),
+        "digest": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, f"{prefix}_{name}")
@@ -165,6 +166,12 @@ class CpuGraph:
         out = np.zeros(self.logical_size(), np.uint64)
         self._f("degrees")(self.h, _p(out))
         return out
+
+    def digest(self):
+        """(sum over live entries of mix64(v << 32 | dst), live entries) -- the twin of DynamicGraph.digest()"""
+        d, n = C.c_uint64(), C.c_uint64()
+        assert self._f("digest")(self.h, C.byref(d), C.byref(n)) == 0
+        return int(d.value), int(n.value)
 
     def export_csr(self, sorted=True):
         n = self.logical_size()

@@ -544,6 +544,70 @@ def test_rmat_device_generator_and_round_trip(scale, batch):
     g.close()
 
 
+@pytest.mark.parametrize("scale,batch,steps", [(22, 1_000_000, 2), (24, 10_000_000, 1)], ids=["C2_s22_1M", "C3_s24_10M"])
+def test_headline_scale_parity_vs_reference(scale, batch, steps):
+    """BASELINE configs 2 and 3 at their stated sizes: R-MAT base graph bulk-built on both sides, the same
+    update batches inserted then deleted; after every op the CUDA store and the reference (the unmodified
+    headers, oracle/_ref — the oracle port where they were not compiled) must agree on the live-edge count,
+    every vertex's degree and the digest over all (source, destination) copies (oracle.hpp:98-163
+    observables in their scale-independent form)."""
+    import psutil
+    import torch
+    from paper_2306_08252_b200 import DynamicGraph, GraphConfig, rmat
+    V, E = 1 << scale, 16 << scale
+    need_host = 48 * E + (6 << 30)   # reference arena (8-byte entries + headers at half fill) + the edge lists
+    if psutil.virtual_memory().available < need_host:
+        pytest.skip(f"needs {need_host >> 30} GiB of host memory")
+    free_dev, _ = torch.cuda.mem_get_info()
+    if free_dev < 40 * E + (4 << 30):
+        pytest.skip("not enough device memory")
+    orc, ref = load_oracle(), load_ref()
+    lib, pfx = (ref, "ref") if ref is not None else (orc, "orc")
+    thr = rmat.thresholds()
+
+    def host_rmat(seed, first, n):
+        s, d = np.empty(n, np.uint32), np.empty(n, np.uint32)
+        orc.orc_gen_rmat(scale, seed, first, n, thr[0], thr[1], thr[2], C.c_void_p(s.ctypes.data), C.c_void_p(d.ctypes.data))
+        return s, d
+
+    B = 32
+    g = DynamicGraph(GraphConfig(pool_blocks=int((E // B + V) * 1.25) + 4 * batch // B + 4096), V, B)
+    src = torch.empty(E, dtype=torch.int32, device="cuda")
+    dst = torch.empty(E, dtype=torch.int32, device="cuda")
+    g.gen_rmat(scale, 1, 0, src, dst, thr)
+    off = torch.empty(V + 1, dtype=torch.int64, device="cuda")
+    cdst = torch.empty(E, dtype=torch.int32, device="cuda")
+    g.coo_to_csr(src, dst, V, off, cdst)
+    del src, dst
+    g.bulk_init(off, cdst)
+    del off, cdst
+    cpu = CpuGraph(lib, pfx, V, B, max(8 << 30, 48 * E), 0.5, True, __import__("os").cpu_count() or 1)
+    hs, hd = host_rmat(1, 0, E)
+    assert cpu.insert_pairs(hs, hd) == 0, cpu.last_error()
+    del hs, hd
+
+    def same(what):
+        assert g.active_edges() == cpu.active_edges(), what
+        assert g.digest() == cpu.digest(), what
+        assert np.array_equal(g.degrees(), cpu.degrees()), what
+
+    same("bulk init")
+    for i in range(steps):
+        bs, bd = host_rmat(2, i * batch, batch)
+        ds, dd = torch.from_numpy(bs.view(np.int32)).cuda(), torch.from_numpy(bd.view(np.int32)).cuda()
+        torch.cuda.synchronize()   # (the graph runs on its own stream)
+        g.insert_pairs(ds, dd)
+        assert cpu.insert_pairs(bs, bd) == 0
+        same(f"insert {i}")
+        assert g.query_edges(bs[:50000], bd[:50000]).all()
+        g.delete_pairs(ds, dd)
+        assert cpu.delete_pairs(bs, bd) == 0
+        same(f"delete {i}")
+        assert not g.query_edges(bs[:50000], bd[:50000]).any()
+    g.close()
+    cpu.close()
+
+
 def test_cpp_dropin_against_reference_class():
     """oracle/dropin_check.cpp: one templated workload through dyngraph::DynamicGraph (the unmodified
     reference, compiled into the binary in the build container) and through the C++ mirror
