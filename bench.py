@@ -145,13 +145,15 @@ def kernel_bytes(name: str, rep: dict, B: int) -> float | None:
     if name.startswith("fused_delete"):
         # slab slots of the warp-owned sources + their next links + targets + per-source state (read + repaired)
         return 4 * SF + 4 * (SF // B) + 8 * b + 32 * T
+    # the hub tiers: slab slots of the tier + handles + masks (their share of the 8b target bytes is not reported
+    # per tier and is left out rather than charged three times)
     if name.startswith("match_long"):
-        return 4 * SL + 8 * (SL // B) + 8 * b            # slab slots of the tier + handles + masks + targets
+        return 4 * SL + 8 * (SL // B)
     if name.startswith("match_med"):
         SM = S - SL - ST - SF
-        return 4 * SM + 8 * (SM // B) + 8 * b
+        return 4 * SM + 8 * (SM // B)
     if name.startswith("match_tiny"):
-        return 4 * ST + 12 * W + 8 * b + 4 * T           # slab slots + every block's (tag, handle) + mask + targets
+        return 4 * ST + 12 * (ST // B)
     if name.startswith("delete_holes_kernel"):
         return 12 * W + 8 * M + 32 * T                   # worklist + masks, hole records, per-source repair
     if name.startswith("delete_moves_kernel"):
@@ -567,9 +569,12 @@ def run_b200_arm(args):
                 avg_ms = ms / n
                 ach = bytes_launch / (avg_ms * 1e-3) / 1e9
                 traffic = None
-                try:   # dram__bytes_read+write per launch of this kernel from the committed ncu --set full capture
+                try:   # dram__bytes_read+write per launch of this kernel from the committed ncu --set full capture —
+                    # only when that capture was taken on THIS workload (scale, batch, block size)
                     tfile = sorted((ROOT / "profiles").glob("*traffic.json"))[-1]
-                    traffic = json.loads(tfile.read_text()).get(name.split("<")[0])
+                    tj = json.loads(tfile.read_text())
+                    if tj.get("workload") == {"scale": scale, "batch": b, "block_size": B, "n_gpus": world}:
+                        traffic = tj.get(name.split("<")[0])
                 except Exception:
                     pass
                 roofline = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",

@@ -209,6 +209,14 @@ int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64
 int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
                   uint64_t n_dst_capacity, int sorted, int mem);
 
+/*
+ * active_destinations(v) (graph.hpp:116-129) for ONE vertex: its live destinations in traversal order, at
+ * most `capacity` of them, into `out` (host or device per `mem`); *n_out receives the vertex's degree.
+ * An unknown vertex yields 0 entries (graph.hpp:118).  DG_ERR_DATA (with *n_out set) when capacity < degree:
+ * call again with a larger buffer — dg_degrees / a first call with capacity 0 give the size.
+ */
+int dg_active_destinations(dg_graph* h, uint32_t v, uint32_t* out, uint64_t capacity, uint64_t* n_out, int mem);
+
 /* sentinel_of(v).active_edge_count for every v < logical_size (graph.hpp:108). */
 int dg_degrees(dg_graph* h, uint64_t* out, int mem);
 

@@ -15,6 +15,7 @@
 // arena(), dictionary(), pool(), sentinel_of(), adjacency_blocks(), plan_batch().
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -169,11 +170,18 @@ class DynamicGraph {
 
   // graph.hpp:116-129 (traversal order; sorted = canonical order of oracle_compare)
   std::vector<VertexId> active_destinations(VertexId v, bool sorted = false) const {
-    std::vector<std::uint64_t> off;
-    std::vector<VertexId> dst;
-    export_csr(off, dst, sorted);
     if (v >= logical_size()) return {};
-    return std::vector<VertexId>(dst.begin() + off[v], dst.begin() + off[v + 1]);
+    std::vector<VertexId> out(64);
+    std::uint64_t n = 0;
+    int rc = dg_active_destinations(h_, v, out.data(), out.size(), &n, DG_MEM_HOST);
+    if (rc == DG_ERR_DATA && n > out.size()) {   // the degree came back: once more with room for it
+      out.resize(n);
+      rc = dg_active_destinations(h_, v, out.data(), out.size(), &n, DG_MEM_HOST);
+    }
+    check(rc);
+    out.resize(n);
+    if (sorted) std::sort(out.begin(), out.end());
+    return out;
   }
   // every vertex's active_destinations as one CSR
   void export_csr(std::vector<std::uint64_t>& offsets, std::vector<VertexId>& destinations, bool sorted) const {

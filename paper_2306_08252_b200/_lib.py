@@ -70,6 +70,7 @@ SIGNATURES = {
     "dg_bulk_init_csr": (C.c_int, [_H, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_int]),
     "dg_query_edges": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int]),
     "dg_export_csr": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int]),
+    "dg_active_destinations": (C.c_int, [_H, C.c_uint32, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_int]),
     "dg_degrees": (C.c_int, [_H, C.c_void_p, C.c_int]),
     "dg_digest": (C.c_int, [_H, u64p, u64p]),
     "dg_insert_vertices": (C.c_int, [_H, C.c_uint64]),

@@ -15,7 +15,7 @@ PKG_DIR = Path(__file__).resolve().parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libdyngraph_b200.so"
 SOURCES = [CSRC / "dg_api.cu"]
-HEADERS = [CSRC / "dg_device.cuh", CSRC / "dg_kernels.cuh", PKG_DIR.parent / "include" / "dyngraph_b200.h"]
+HEADERS = [CSRC / "dg_device.cuh", CSRC / "dg_kernels.cuh", CSRC / "dg_fused.cuh", PKG_DIR.parent / "include" / "dyngraph_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

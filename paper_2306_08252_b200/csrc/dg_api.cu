@@ -15,6 +15,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <tuple>
 #include <new>
 #include <string>
 #include <unordered_set>
@@ -151,6 +153,9 @@ struct dg_graph {
   uint64_t nb_max = 0;          // most blocks the pool may hold; <= NB: fixed pool
   double trigger = 0.8, growth = 0.25;
   uint64_t consumed = 0;        // cumulative pops (block_pool.hpp consumed())
+  uint64_t total_capacity = 0;  // handles ever made available: created + every re-push of a reclaimed one (block_pool.hpp:42-44)
+  bool ws_overflow = false;     // a scratch request did not fit the reserved workspace: the op is rejected
+  cudaError_t launch_error = cudaSuccess;   // first kernel launch error of the op (checked at the launch site)
   uint32_t growth_count = 0;
   uint64_t ring_identity = 0;   // ring[p] == p for queue positions below this
   bool pool_vm = false;         // slab / next live in VmRanges
@@ -253,11 +258,18 @@ void prof_collect(dg_graph* h) {
   h->prof_open.clear();
   cudaGetLastError();
 }
-#define DG_LAUNCH(h, name, ...)   \
-  do {                            \
-    ProfScope ps__((h), (name));  \
-    __VA_ARGS__;                  \
-    (h)->launches += 1;           \
+#define DG_LAUNCH(h, name, ...)                                                   \
+  do {                                                                            \
+    if (!(h)->ws_overflow) {                                                      \
+      ProfScope ps__((h), (name));                                                \
+      __VA_ARGS__;                                                                \
+      const cudaError_t le__ = cudaPeekAtLastError();                             \
+      if (le__ != cudaSuccess && (h)->launch_error == cudaSuccess) {              \
+        (h)->launch_error = le__;                                                 \
+        std::fprintf(stderr, "dyngraph_b200: launch of %s failed: %s\n", (name), cudaGetErrorString(le__)); \
+      }                                                                           \
+      (h)->launches += 1;                                                         \
+    }                                                                             \
   } while (0)
 
 GraphView view(const dg_graph* h) {
@@ -310,9 +322,19 @@ T* ws_alloc(dg_graph* h, size_t count) {
   const size_t bytes = aligned(count * sizeof(T));
   T* p = reinterpret_cast<T*>(h->ws.base + h->ws.off);
   h->ws.off += bytes;
-  if (h->ws.off > h->ws.cap) {  // sizing bug: fail loudly rather than corrupt memory
-    std::fprintf(stderr, "dyngraph_b200: workspace overflow (%zu > %zu)\n", h->ws.off, h->ws.cap);
-    std::abort();
+  if (h->ws.off > h->ws.cap) {
+    // Sizing bug.  Never hand out memory past the reservation: the request aliases the start of the workspace,
+    // the op is poisoned on the device (every kernel of an op starts with `if (op->err) return`), launches are
+    // skipped from here on and op_end reports an engine error.
+    if (!h->ws_overflow) {
+      std::fprintf(stderr, "dyngraph_b200: workspace overflow (%zu > %zu): rejecting the op\n", h->ws.off, h->ws.cap);
+      cudaMemsetAsync(&h->d_op()->err, 0x03, sizeof(uint32_t), h->stream);
+      for (int i = 0; i < 2; ++i)
+        if (h->aux[i]) cudaMemsetAsync(&h->d_op()->err, 0x03, sizeof(uint32_t), h->aux[i]);
+    }
+    h->ws_overflow = true;
+    h->ws.off = bytes;
+    return reinterpret_cast<T*>(h->ws.base);
   }
   return p;
 }
@@ -333,8 +355,12 @@ inline int grid_for(const dg_graph* h, uint64_t items, int per_block) {
 // (148 SMs x the kernel's occupancy): a partial second wave only adds a tail.
 template <class K>
 int resident_ctas_per_sm(K kernel, int block_threads, size_t dyn_smem) {
-  static std::map<const void*, int> cache;
-  const void* key = reinterpret_cast<const void*>(kernel);
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), block_threads, dyn_smem, dev);
+  std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int n = 0;
@@ -448,6 +474,17 @@ int op_end(dg_graph* h) {
   DG_CUDA(h, cudaStreamSynchronize(h->stream));
   DG_CUDA(h, cudaGetLastError());
   if (h->profiling) prof_collect(h);
+  if (h->launch_error != cudaSuccess) {
+    const cudaError_t e = h->launch_error;
+    h->launch_error = cudaSuccess;
+    h->zscratch_clean = h->cnt_clean = false;
+    return fail(h, DG_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+  }
+  if (h->ws_overflow) {   // (the op was poisoned on the device before anything mutated: see ws_alloc)
+    h->ws_overflow = false;
+    h->zscratch_clean = h->cnt_clean = false;
+    return fail(h, DG_ERR_ENGINE, "internal: per-op workspace was sized too small; the batch was not applied");
+  }
   const DeviceState& st = h->h_blk->st;
   const OpState& op = h->h_blk->op;
   h->front = st.front;
@@ -456,6 +493,7 @@ int op_end(dg_graph* h) {
   h->report.touched_sources = op.n_runs;
   h->report.blocks_popped = op.total_need;
   h->report.blocks_pushed = op.pushed;
+  if (op.err == 0) h->total_capacity += op.pushed;   // every re-push counts (block_pool.hpp:56-61)
   h->report.slots_scanned = op.slots;
   h->report.blocks_scanned = op.wl_blocks + op.fused_blocks;
   h->report.slots_scanned_fused = op.slots_fused;
@@ -622,6 +660,7 @@ int create_pool(dg_graph* h, uint32_t B) {
   h->ring_identity = nb;
   h->B = B;
   h->NB = nb;
+  h->total_capacity = nb;
   DG_LAUNCH(h, "ring_fill_kernel", ring_fill_kernel<<<grid_for(h, nb, 256 * 4), 256, 0, h->stream>>>(h->ring, nb));
   DG_CUDA(h, cudaMemsetAsync(h->next, 0xFF, nb * sizeof(uint32_t), h->stream));
   h->h_blk->st.front = 0;
@@ -639,7 +678,7 @@ int create_pool(dg_graph* h, uint32_t B) {
 // what the budget still allows.  Returns false when the pool cannot grow any further.
 bool try_grow(dg_graph* h) {
   if (!h->pool_vm || h->NB >= h->nb_max) return false;
-  uint64_t want = (uint64_t)((double)h->NB * h->growth);
+  uint64_t want = (uint64_t)((double)h->total_capacity * h->growth);   // block_pool.hpp:253-254
   if (want == 0) want = 1;
   const uint64_t grant = std::min<uint64_t>(want, h->nb_max - h->NB);
   const uint64_t nb_new = h->NB + grant;
@@ -663,6 +702,7 @@ bool try_grow(dg_graph* h) {
   cudaFree(h->ring);
   h->ring = ring_new;
   h->NB = nb_new;
+  h->total_capacity += grant;
   ++h->growth_count;
   return cudaGetLastError() == cudaSuccess;
 }
@@ -670,8 +710,8 @@ bool try_grow(dg_graph* h) {
 // commit_front's growth rule (block_pool.hpp:162-172): after a batch popped `popped` blocks, grow
 // once if cumulative consumption reached trigger_fraction of the capacity.
 void after_pop(dg_graph* h, uint64_t popped) {
-  h->consumed += popped;
-  if (h->pool_vm && h->NB > 0 && (double)h->consumed / (double)h->NB >= h->trigger) try_grow(h);
+  h->consumed += popped;   // occupancy() = consumed / total_capacity (block_pool.hpp:168-172)
+  if (h->pool_vm && h->total_capacity > 0 && (double)h->consumed / (double)h->total_capacity >= h->trigger) try_grow(h);
 }
 
 // ensure_available (block_pool.hpp:177-189) for a batch that was rejected for `shortfall` missing
@@ -1390,11 +1430,7 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
     cudaMemsetAsync(plan_scratch, 0, kAllocScratchWords * sizeof(unsigned long long), h->stream);
     DG_LAUNCH(h, "csr_plan_kernel", csr_plan_kernel<<<(unsigned)((V + kCsrPlanTile - 1) / kCsrPlanTile), 256, 0, h->stream>>>(
         g, d_off, (uint32_t)V, n_edges, blk_off, items, items_cap, plan_scratch, h->d_op()));
-    static int csr_ctas_per_sm = 0;
-    if (csr_ctas_per_sm == 0) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&csr_ctas_per_sm, csr_append_kernel, kCsrWarps * 32, 0);
-      csr_ctas_per_sm = std::max(1, csr_ctas_per_sm);
-    }
+    const int csr_ctas_per_sm = resident_ctas_per_sm(csr_append_kernel, kCsrWarps * 32, 0);
     const uint64_t groups = (V + 31) / 32 + items_cap;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((groups + kCsrWarps - 1) / kCsrWarps, (uint64_t)h->sm_count * csr_ctas_per_sm));
     DG_LAUNCH(h, "csr_append_kernel", csr_append_kernel<<<grid, kCsrWarps * 32, 0, h->stream>>>(
@@ -1614,6 +1650,26 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
   return op_end(h);
 }
 
+int dg_active_destinations(dg_graph* h, uint32_t v, uint32_t* out, uint64_t capacity, uint64_t* n_out, int mem) {
+  if (!h || !n_out || (capacity && !out)) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  *n_out = 0;
+  if (v >= h->size || h->B == 0) return DG_OK;   // graph.hpp:118: unknown vertex -> empty
+  int rc = ws_reserve(h, mem == DG_MEM_HOST ? aligned(capacity * 4) : 0);
+  if (rc != DG_OK) return rc;
+  uint32_t* d_out = (mem == DG_MEM_HOST && capacity) ? ws_alloc<uint32_t>(h, capacity) : out;
+  if ((rc = op_begin(h, 1, 0)) != DG_OK) return rc;
+  DG_LAUNCH(h, "adjacency_copy_kernel", adjacency_copy_kernel<<<1, 256, 0, h->stream>>>(view(h), v, d_out, capacity, h->d_op()));
+  if ((rc = op_end(h)) != DG_OK) return rc;
+  const uint64_t d = h->h_blk->op.aux0;
+  *n_out = d;
+  if (d > capacity)
+    return fail(h, DG_ERR_DATA, "active_destinations: capacity " + std::to_string(capacity) + " < degree " + std::to_string(d));
+  if (mem == DG_MEM_HOST && d) DG_CUDA(h, cudaMemcpy(out, d_out, d * 4, cudaMemcpyDeviceToHost));
+  return DG_OK;
+}
+
 int dg_degrees(dg_graph* h, uint64_t* out, int mem) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
@@ -1714,22 +1770,30 @@ int dg_delete_vertices(dg_graph* h, const uint32_t* ids, uint64_t n, uint32_t* s
       ++ns;
       continue;
     }
-    h->alive_host[v >> 6] &= ~(1ull << (v & 63));
+    h->alive_host[v >> 6] &= ~(1ull << (v & 63));   // (in-call duplicates must see it; restored if the op fails)
     winners.push_back(v);
   }
+  auto restore_mirror = [&] {
+    for (uint32_t v : winners) h->alive_host[v >> 6] |= 1ull << (v & 63);
+  };
   if (n_skipped) *n_skipped = ns;
   if (winners.empty()) return DG_OK;
-  h->alive_count -= winners.size();
   int rc = ws_reserve(h, aligned(winners.size() * 4));
-  if (rc != DG_OK) return rc;
+  if (rc != DG_OK) { restore_mirror(); return rc; }
   uint32_t* d_ids = ws_alloc<uint32_t>(h, winners.size());
-  DG_CUDA(h, cudaMemcpyAsync(d_ids, winners.data(), winners.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  if ((rc = op_begin(h, winners.size(), 0)) != DG_OK) return rc;
+  if (cudaMemcpyAsync(d_ids, winners.data(), winners.size() * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) {
+    restore_mirror();
+    return fail(h, DG_ERR_CUDA, "delete_vertices: copy of the ids failed");
+  }
+  if ((rc = op_begin(h, winners.size(), 0)) != DG_OK) { restore_mirror(); return rc; }
   GraphView g = view(h);
   if (h->B == 0) g.reclaim = 0;
   DG_LAUNCH(h, "retire_vertices_kernel", retire_vertices_kernel<<<grid_for(h, winners.size(), 8), 256, 0, h->stream>>>(
       g, d_ids, (uint32_t)winners.size(), h->d_op()));
-  return op_end(h);
+  rc = op_end(h);
+  if (rc != DG_OK) { restore_mirror(); return rc; }   // nothing retired on the device: the mirror follows it
+  h->alive_count -= winners.size();
+  return DG_OK;
 }
 
 // ---- observables -----------------------------------------------------------------------

@@ -2272,6 +2272,46 @@ export_copy_kernel(GraphView g, const uint32_t* __restrict__ wl_off,
   }
 }
 
+// active_destinations(v) (graph.hpp:116-129) for ONE vertex: one CTA.  Warp 0 walks the chain, confirming up to
+// 32 physically consecutive blocks per round trip; the whole CTA then copies that run (chains are compact: the
+// live entries are exactly positions [0, degree) in chain order).  op->aux0 = the vertex's degree; at most `cap`
+// entries are written.
+__global__ void __launch_bounds__(256)
+adjacency_copy_kernel(GraphView g, uint32_t v, uint32_t* __restrict__ out, unsigned long long cap, OpState* op) {
+  __shared__ uint32_t s_h, s_len;
+  const uint32_t d = v < g.size ? g.deg[v] : 0u;
+  if (threadIdx.x == 0) op->aux0 = d;
+  if (d == 0) return;
+  const uint32_t nblk = blocks_for(g, d);
+  const unsigned long long lim = cap < d ? cap : (unsigned long long)d;
+  uint32_t h = g.head[v];
+  uint32_t kb = 0;
+  while (kb < nblk) {
+    if (threadIdx.x < 32) {
+      const unsigned long long hh = (unsigned long long)h + threadIdx.x;
+      const uint32_t nx = hh < g.ring_cap ? g.next[hh] : kNull;
+      const unsigned okm = __ballot_sync(kFull, (unsigned long long)nx == hh + 1);
+      uint32_t len = (okm == kFull) ? 32u : (uint32_t)__ffs(~okm);
+      len = min(len, nblk - kb);
+      const uint32_t nh = __shfl_sync(kFull, nx, len - 1);
+      if (threadIdx.x == 0) {
+        s_len = len;
+        s_h = nh;
+      }
+    }
+    __syncthreads();
+    const uint32_t len = s_len;
+    const unsigned long long first = (unsigned long long)kb * g.B;
+    const unsigned long long count = (unsigned long long)len * g.B;
+    for (unsigned long long i = threadIdx.x; i < count; i += blockDim.x)
+      if (first + i < lim) out[first + i] = g.slab[(unsigned long long)h * g.B + i];
+    const uint32_t nh = s_h;
+    __syncthreads();
+    h = nh;
+    kb += len;
+  }
+}
+
 __global__ void keys_low_kernel(const unsigned long long* __restrict__ keys, unsigned long long n,
                                 uint32_t* __restrict__ out) {
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;

@@ -187,10 +187,17 @@ class DynamicGraph:
         return offsets, dsts
 
     def active_destinations(self, v: int) -> np.ndarray:
-        if v >= self.logical_size():
+        """Live destinations of ONE vertex in traversal order (graph.hpp:116-129): dg_active_destinations."""
+        if v < 0 or v >= self.logical_size():
             return np.zeros(0, dtype=np.uint32)
-        off, dst = self.export_csr(sorted=False)
-        return dst[int(off[v]):int(off[v + 1])]
+        n = C.c_uint64()
+        out = np.zeros(64, dtype=np.uint32)
+        rc = self._lib.dg_active_destinations(self._h, v, C.c_void_p(out.ctypes.data), out.size, C.byref(n), _lib.DG_MEM_HOST)
+        if rc == _lib.DG_ERR_DATA and n.value > out.size:   # the degree came back: once more with room for it
+            out = np.zeros(int(n.value), dtype=np.uint32)
+            rc = self._lib.dg_active_destinations(self._h, v, C.c_void_p(out.ctypes.data), out.size, C.byref(n), _lib.DG_MEM_HOST)
+        self._check(rc)
+        return out[:int(n.value)]
 
     def degrees(self) -> np.ndarray:
         out = np.zeros(self.logical_size(), dtype=np.uint64)

@@ -608,6 +608,27 @@ def test_headline_scale_parity_vs_reference(scale, batch, steps):
     cpu.close()
 
 
+def test_active_destinations_single_vertex_over_the_abi():
+    """dg_active_destinations (graph.hpp:116-129): one vertex's live destinations without exporting the
+    graph — short chains, a hub of thousands of blocks (capacity retry), dead and unknown vertices."""
+    rng = np.random.default_rng(11)
+    V, B = 20000, 32
+    src = np.concatenate([rng.integers(0, V, 200000), np.full(150000, 3)]).astype(np.uint32)
+    dst = rng.integers(0, V, len(src)).astype(np.uint32)
+    g, o = GpuGraph(V, B, pool_blocks=1 << 15), CpuGraph(load_oracle(), "orc", V, B, 1 << 30)
+    for x in (g, o):
+        assert x.insert_pairs(src, dst) == 0
+        assert x.delete_pairs(src[::7], dst[::7]) == 0
+        x.delete_vertices(np.array([7], np.uint32))
+    off, ds = o.export_csr(sorted=True)
+    for v in (0, 1, 3, 7, 150, V - 1):
+        got = np.sort(g.g.active_destinations(v))
+        assert np.array_equal(got, ds[int(off[v]):int(off[v + 1])]), v
+    assert len(g.g.active_destinations(3)) == int(o.degrees()[3]) > 64
+    assert len(g.g.active_destinations(V + 5)) == 0 and len(g.g.active_destinations(7)) == 0
+    g.close()
+
+
 def test_cpp_dropin_against_reference_class():
     """oracle/dropin_check.cpp: one templated workload through dyngraph::DynamicGraph (the unmodified
     reference, compiled into the binary in the build container) and through the C++ mirror
