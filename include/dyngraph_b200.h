@@ -180,6 +180,14 @@ int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
                         int mem);
 
 /*
+ * Validation + plan of a COO batch WITHOUT applying it: the status dg_insert_batch_coo / dg_delete_batch_coo
+ * would return (validate_batch csr.hpp:49-73, dead-source rule graph.hpp:320-328, ensure_available
+ * block_pool.hpp:177-189).  The source-partitioned store calls it on every rank and agrees on the outcome
+ * before any rank mutates (NCCL exchange; the peer-memory exchange agrees on the device instead).
+ */
+int dg_check_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, int is_insert, int mem);
+
+/*
  * Bulk init = the reference's ctor followed by the first insert_batch of the
  * whole graph (io/workload.hpp:113-139).  Requires an empty graph whose
  * logical size is n_offsets - 1; identical to dg_insert_batch_csr otherwise.
@@ -328,14 +336,20 @@ int dg_route_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t
  * partition -> count exchange -> NCCL all-to-all, ONE kernel computes every
  * pair's owner and stores it straight into the owner's receive buffer
  * (peer-mapped through CUDA IPC), reserving slots with a warp-aggregated
- * system-scope atomicAdd on the owner's cursor.  A collective barrier (any
- * all-reduce, e.g. the status agreement) then publishes the round.
+ * system-scope atomicAdd on the owner's cursor.  The round protocol runs ON
+ * THE DEVICE — no host collective per batch: arrival and status counters live
+ * in the peer-mapped buffers (system-scope atomics + a one-warp waiting
+ * kernel), two buffer sets alternate between rounds.
  *
- * Round protocol, every rank:  dg_exchange_reset -> barrier -> dg_exchange_push_coo
- * -> dg_synchronize -> barrier -> dg_exchange_received -> local batch op on the
- * received DEVICE arrays.  Queries additionally carry (origin rank, origin index)
- * and return their answers with dg_exchange_push_answers into the origin's
- * answer buffer -> barrier -> dg_exchange_answers.
+ * One round = one batch op; every rank calls the same sequence:
+ *     dg_exchange_push_coo      validate + push + "my push has landed" to every rank
+ *     dg_exchange_received      wait for every rank's arrival; what this rank received
+ *     the local batch op on the received DEVICE arrays (with dg_exchange_attach the op posts its
+ *       validation / plan status to every rank and mutates only on an all-clear: a batch is applied
+ *       on every rank or on none, graph.hpp:168-171), or dg_exchange_agree when nothing was received
+ *     [queries: dg_exchange_push_answers ; dg_exchange_answers]
+ *     dg_exchange_end_round
+ * A rank that fails to take part makes its peers give up after ~4 s with DG_ERR_ENGINE.
  */
 typedef struct dg_exchange dg_exchange;
 #define DG_IPC_HANDLE_BYTES 64
@@ -346,19 +360,32 @@ void dg_exchange_destroy(dg_exchange* x);
 /* IPC handle of this rank's buffers (64 bytes) — all-gather it, then hand every peer's to set_peer */
 int dg_exchange_ipc_handle(dg_exchange* x, void* handle_out);
 int dg_exchange_set_peer(dg_exchange* x, uint32_t peer_rank, const void* handle);
-int dg_exchange_reset(dg_exchange* x);
-/* validates src < vertex_count (DG_ERR_DATA, nothing pushed), else pushes (local src id, global dst,
- * origin index) of every pair to its owner.  src/dst: DEVICE arrays. */
+/* on != 0: insert / delete COO ops of x's graph agree their status with the peers before mutating */
+int dg_exchange_attach(dg_exchange* x, int on);
+/* validates src < vertex_count, pushes (local src id, global dst, origin index) of every pair to its owner and
+ * signals this rank's arrival (carrying its status) to every rank.  src/dst: DEVICE arrays.  A local
+ * DG_ERR_* is returned here; the other ranks learn it in dg_exchange_received. */
 int dg_exchange_push_coo(dg_exchange* x, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t bits,
                          uint64_t vertex_count);
-/* after the barrier: what this rank received (DEVICE arrays owned by the exchange) */
+/* waits until every rank has arrived; what this rank received (DEVICE arrays owned by the exchange).
+ * DG_ERR_DATA / DG_ERR_ENGINE on EVERY rank when any rank's push was rejected (nothing to apply). */
 int dg_exchange_received(dg_exchange* x, uint64_t* n, uint32_t** src_local, uint32_t** dst,
                          uint32_t** origin_index, uint32_t** origin_rank);
+/* the agreement step for a rank that runs no local op this round; *agreed = max status over the ranks */
+int dg_exchange_agree(dg_exchange* x, int local_status, int* agreed);
 /* answers[i] (DEVICE, one per received entry) go to answer slot origin_index[i] of rank origin_rank[i] */
 int dg_exchange_push_answers(dg_exchange* x, const uint8_t* answers, uint64_t n);
-/* after the barrier: the first n answers this rank got back (indexed by the position in its own
- * query batch), copied to `out` (host or device per `mem`) */
+/* waits for every rank's answers; the first n (indexed by the position in this rank's own query batch)
+ * are copied to `out` (host or device per `mem`) */
 int dg_exchange_answers(dg_exchange* x, uint8_t* out, uint64_t n, int mem);
+/* the round is over: its buffer set is handed back, the next round uses the other one */
+int dg_exchange_end_round(dg_exchange* x);
+
+/*
+ * dg_digest of a shard expressed over GLOBAL source ids (local id l of rank r is vertex
+ * perm_inv(l * world + r)): the sum over the ranks equals the single-GPU digest of the same multiset.
+ */
+int dg_digest_global(dg_graph* h, uint32_t rank, uint32_t world, uint32_t bits, uint64_t* out_digest, uint64_t* out_entries);
 
 /* ---- host -> device batch ingest (nothing in the reference) ----------
  *

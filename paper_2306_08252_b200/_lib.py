@@ -102,7 +102,11 @@ SIGNATURES = {
     "dg_exchange_destroy": (None, [C.c_void_p]),
     "dg_exchange_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dg_exchange_set_peer": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
-    "dg_exchange_reset": (C.c_int, [C.c_void_p]),
+    "dg_exchange_attach": (C.c_int, [C.c_void_p, C.c_int]),
+    "dg_exchange_agree": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int)]),
+    "dg_exchange_end_round": (C.c_int, [C.c_void_p]),
+    "dg_check_batch_coo": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int]),
+    "dg_digest_global": (C.c_int, [_H, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u64p]),
     "dg_exchange_push_coo": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64]),
     "dg_exchange_received": (C.c_int, [C.c_void_p, u64p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                        C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),

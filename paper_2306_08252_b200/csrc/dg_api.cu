@@ -186,6 +186,7 @@ struct dg_graph {
   bool zscratch_clean = false;
   int zslot = 0;
 
+  struct dg_exchange* agree_x = nullptr;   // sharded store: ops agree their status with the peers before mutating
   std::string last_error;
   uint64_t last_shortfall = 0;  // blocks the last rejected insert was short of (0: it was not a pool underflow)
   dg_op_report report{};
@@ -204,6 +205,18 @@ struct dg_graph {
   uint64_t dst_limit() const { return dst_limit_override ? dst_limit_override : size; }
   uint64_t blocks_in_use() const { return NB - (rear - front); }
   bool alive_h(uint64_t v) const { return v < size && ((alive_host[v >> 6] >> (v & 63)) & 1ull); }
+};
+
+struct dg_exchange {
+  dg_graph* h = nullptr;
+  uint32_t rank = 0, world = 1;
+  uint64_t capacity = 0;
+  char* base = nullptr;          // this rank's buffers (one cudaMalloc: IPC-exportable)
+  size_t bytes = 0;
+  void* peer_base[kMaxPeers] = {};  // opened IPC mappings (nullptr for self / not set)
+  PeerBuffers pb{};
+  uint64_t epoch = 0;            // rounds completed; the current round uses buffer set epoch & 1
+  int set() const { return (int)(epoch & 1); }
 };
 
 namespace {
@@ -345,6 +358,14 @@ struct WsSizer {
   void add(size_t count) { total += aligned(count * sizeof(T)); }
 };
 
+// the op's validation / plan status is agreed with the peers before anything mutates (see exchange_agree_kernel)
+void enqueue_agree(dg_graph* h, bool commit_insert) {
+  dg_exchange* x = h->agree_x;
+  if (x == nullptr) return;
+  DG_LAUNCH(h, "exchange_agree_kernel", exchange_agree_kernel<<<1, 32, 0, h->stream>>>(x->pb, x->set(), h->d_op(), h->d_state(),
+                                                                                      commit_insert ? 1 : 0));
+}
+
 inline int grid_for(const dg_graph* h, uint64_t items, int per_block) {
   const uint64_t want = (items + per_block - 1) / per_block;
   const uint64_t cap = (uint64_t)h->sm_count * 8;
@@ -464,6 +485,7 @@ const char* detail_text(uint32_t d) {
     case kErrOffsetsEnd: return "destinations length does not match offsets";
     case kErrPoolUnderflow: return "batch needs more blocks than the pool can still provide";
     case kErrScratch: return "internal scratch exhausted";
+    case kErrPeer: return "rejected on another rank of the sharded store (nothing was applied on any rank)";
     default: return "unknown";
   }
 }
@@ -731,7 +753,11 @@ template <class F>
 int insert_with_growth(dg_graph* h, F&& run) {
   int rc = run();
   if (!h) return rc;
-  if (rc == DG_ERR_ENGINE && h->last_shortfall != 0 && grow_for_shortfall(h, h->last_shortfall)) rc = run();
+  if (rc == DG_ERR_ENGINE && h->last_shortfall != 0 && grow_for_shortfall(h, h->last_shortfall)) {
+    // sharded store: every rank rejected the batch together (device-side agreement) — the pool has grown,
+    // the caller repeats the batch on every rank; a lone retry here would wait for peers that never come
+    if (h->agree_x == nullptr) rc = run();
+  }
   if (rc == DG_OK) after_pop(h, h->report.blocks_popped);
   return rc;
 }
@@ -807,8 +833,10 @@ void enqueue_plan_append(dg_graph* h, const BatchView& b, uint64_t runs_bound, u
                          bool csr_path) {
   GraphView g = view(h);
   PlanArrays a = alloc_plan_arrays(h, runs_bound, n_edges);
+  const bool agree = !csr_path && h->agree_x != nullptr;   // sharded store: the commit waits for every rank's all-clear
   launch_alloc(h, "alloc_kernel<plan>", runs_bound, d_n_runs(h), PlanIn{g, b}, PlanOut{a},
-               PlanFin{g, h->d_op(), n_edges, /*set_runs=*/0, csr_path ? 0 : 1});
+               PlanFin{g, h->d_op(), n_edges, /*set_runs=*/0, (csr_path || agree) ? 0 : 1});
+  if (agree) enqueue_agree(h, /*commit_insert=*/true);
   enqueue_append(h, b, a, runs_bound, n_edges, csr_path);
 }
 
@@ -967,9 +995,9 @@ struct Grouped {
   uint32_t *run_src = nullptr, *run_start = nullptr, *run_end = nullptr;
 };
 
-inline size_t group_ws_bytes(const dg_graph* h, uint64_t n, bool with_index, uint64_t max_src) {
+inline size_t group_ws_bytes(const dg_graph* h, uint64_t n, bool with_index, uint64_t max_src, bool force_radix = false) {
   size_t t = 0;
-  if (use_counting(h, n)) {
+  if (!force_radix && use_counting(h, n)) {
     t += aligned((std::bit_ceil(std::max<uint64_t>(h->size, 1)) + 4 + 4 * kAllocScratchWords) * 4) + 2 * aligned(n * 4) + (with_index ? aligned(n * 4) : 0);
     t += 3 * aligned((std::min<uint64_t>(n, h->size + 1) + 1) * 4);
   } else {
@@ -1176,11 +1204,13 @@ int delete_coo_run(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, ui
     launch_alloc(h, "alloc_kernel<group+enum>", n, d_n_input(h), GroupEnumIn{g, gr.gi, d_src, gr.rank, gr.cnt, 1, fuse},
                  GroupEnumOut{g, gr.gi, d_src, gr.cnt, gr.run_src, gr.run_start, gr.run_end, w.lists(h)},
                  EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/1});
+    enqueue_agree(h, false);
     return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, gr.gi, fuse ? gr.cnt : nullptr,
                       [&] { group_scatter<kPackDelete>(h, gr, d_src, d_dst, n); });
   }
   Grouped gr = group_radix<kPackDelete>(h, d_src, d_dst, n, false, max_src);
   Worklist w = enqueue_enumerate(h, gr.b, gr.runs_bound, n, /*check_alive=*/1, fuse, /*walk=*/false, /*for_delete=*/true);
+  enqueue_agree(h, false);
   return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, GroupIndex{}, nullptr, [] {});
 }
 
@@ -1323,8 +1353,10 @@ void dg_destroy(dg_graph* h) {
 }
 
 // ---- insert -------------------------------------------------------------------
+// check_only: validation + plan (every reason the reference would reject the batch for: csr.hpp:49-73,
+// graph.hpp:320-328, ensure_available block_pool.hpp:177-189) without any mutation
 static int insert_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
-                           int mem) {
+                           int mem, bool check_only = false) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
   h->last_shortfall = 0;
@@ -1362,12 +1394,24 @@ static int insert_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst
     DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kPackInsert><<<grid, 256, 0, h->stream>>>(
         g, gi, d_src, d_dst, (uint32_t)n, cnt, rank, h->d_op()));
     launch_alloc(h, "alloc_kernel<group+plan>", n, d_n_input(h), GroupPlanIn{g, gi, d_src, rank, cnt},
-                 GroupPlanOut{gi, d_src, info, cnt}, PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/1});
+                 GroupPlanOut{gi, d_src, info, cnt},
+                 PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/(h->agree_x || check_only) ? 0 : 1});
+    if (check_only) return op_end(h);
+    enqueue_agree(h, /*commit_insert=*/true);
     DG_LAUNCH(h, "append_entries_kernel", append_entries_kernel<<<grid, 256, 0, h->stream>>>(
         g, gi, d_src, d_dst, rank, (uint32_t)n, info, h->d_op()));
     return op_end(h);
   }
   Grouped gr = group_radix<kPackInsert>(h, d_src, d_dst, n, false, h->size - 1);
+  if (check_only) {
+    if (h->B != 0) {   // (deferred pool: the first batch sizes it, nothing to run out of)
+      GraphView g = view(h);
+      PlanArrays a = alloc_plan_arrays(h, gr.runs_bound, n);
+      launch_alloc(h, "alloc_kernel<plan>", gr.runs_bound, d_n_runs(h), PlanIn{g, gr.b}, PlanOut{a},
+                   PlanFin{g, h->d_op(), n, /*set_runs=*/0, /*commit_globals=*/0});
+    }
+    return op_end(h);
+  }
   if (h->B == 0) {
     // deferred pool: compute_block_size (csr.hpp:77-88) from this first batch
     if ((rc = op_end(h)) != DG_OK) return rc;
@@ -1481,19 +1525,18 @@ int dg_bulk_init_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
 }
 
 // ---- delete -------------------------------------------------------------------
-int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n,
-                        int mem) {
+static int delete_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, int mem, bool check_only) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
   cudaSetDevice(h->device);
   if (n == 0) return DG_OK;
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
-  const bool no_pool = h->B == 0;  // no pool yet => no edges: only validation can have an effect
+  const bool no_pool = h->B == 0 || check_only;  // no pool yet => no edges: only validation can have an effect
   if (!no_pool && use_counting(h, n) && ensure_cnt(h) != DG_OK) return DG_ERR_ENGINE;
   WsSizer sz;
   if (mem == DG_MEM_HOST) { sz.add<uint32_t>(n); sz.add<uint32_t>(n); }
-  if (no_pool) sz.total += group_ws_bytes(h, n, false, h->size - 1);
+  if (no_pool) sz.total += group_ws_bytes(h, n, false, h->size - 1, /*force_radix=*/true);
   else sz.total += group_enumerate_ws(h, n, false, h->size - 1) + delete_matched_ws(h, n);
   int rc = ws_reserve(h, sz.total);
   if (rc != DG_OK) return rc;
@@ -1506,6 +1549,18 @@ int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
     return op_end(h);
   }
   return delete_coo_run(h, d_src, d_dst, n, h->size - 1);
+}
+int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, int mem) {
+  return delete_coo_impl(h, src, dst, n, mem, false);
+}
+
+int dg_check_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, int is_insert, int mem) {
+  if (!h) return DG_ERR_DATA;
+  if (!is_insert) return delete_coo_impl(h, src, dst, n, mem, true);
+  const int rc = insert_coo_impl(h, src, dst, n, mem, true);
+  // (a pool underflow the growth budget covers is not a rejection: the real insert grows the pool first)
+  if (rc == DG_ERR_ENGINE && h->last_shortfall != 0 && h->pool_vm && h->nb_max - h->NB >= h->last_shortfall) return DG_OK;
+  return rc;
 }
 
 int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
@@ -2019,42 +2074,43 @@ int dg_route_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t
 }
 
 // ---- fused routing + exchange over peer memory ------------------------------------------------
-struct dg_exchange {
-  dg_graph* h = nullptr;
-  uint32_t rank = 0, world = 1;
-  uint64_t capacity = 0;
-  char* base = nullptr;          // this rank's buffers (one cudaMalloc: IPC-exportable)
-  size_t bytes = 0;
-  void* peer_base[kMaxPeers] = {};  // opened IPC mappings (nullptr for self / not set)
-  PeerBuffers pb{};
-};
-
 namespace {
 struct ExchangeLayout {
-  size_t cursor, src, dst, idx, from, ans, total;
+  size_t words, src[2], dst[2], idx[2], from[2], ans[2], total;
 };
 ExchangeLayout exchange_layout(uint64_t cap) {
   ExchangeLayout l{};
   size_t off = 0;
-  l.cursor = off; off += 256;
-  l.src = off; off += aligned(cap * 4);
-  l.dst = off; off += aligned(cap * 4);
-  l.idx = off; off += aligned(cap * 4);
-  l.from = off; off += aligned(cap * 4);
-  l.ans = off; off += aligned(cap);
+  l.words = off; off += 256;
+  for (int s = 0; s < 2; ++s) {
+    l.src[s] = off; off += aligned(cap * 4);
+    l.dst[s] = off; off += aligned(cap * 4);
+    l.idx[s] = off; off += aligned(cap * 4);
+    l.from[s] = off; off += aligned(cap * 4);
+    l.ans[s] = off; off += aligned(cap);
+  }
   l.total = off;
   return l;
 }
+static_assert(sizeof(RoundWords) <= 256, "round words fit their slot");
 void exchange_bind(dg_exchange* x, uint32_t peer, char* base) {
   const ExchangeLayout l = exchange_layout(x->capacity);
-  x->pb.cursor[peer] = reinterpret_cast<unsigned long long*>(base + l.cursor);
-  x->pb.src[peer] = reinterpret_cast<uint32_t*>(base + l.src);
-  x->pb.dst[peer] = reinterpret_cast<uint32_t*>(base + l.dst);
-  x->pb.idx[peer] = reinterpret_cast<uint32_t*>(base + l.idx);
-  x->pb.from[peer] = reinterpret_cast<uint32_t*>(base + l.from);
-  x->pb.ans[peer] = reinterpret_cast<uint8_t*>(base + l.ans);
+  x->pb.words[peer] = reinterpret_cast<RoundWords*>(base + l.words);
+  for (int s = 0; s < 2; ++s) {
+    x->pb.src[peer][s] = reinterpret_cast<uint32_t*>(base + l.src[s]);
+    x->pb.dst[peer][s] = reinterpret_cast<uint32_t*>(base + l.dst[s]);
+    x->pb.idx[peer][s] = reinterpret_cast<uint32_t*>(base + l.idx[s]);
+    x->pb.from[peer][s] = reinterpret_cast<uint32_t*>(base + l.from[s]);
+    x->pb.ans[peer][s] = reinterpret_cast<uint8_t*>(base + l.ans[s]);
+  }
+}
+int exchange_ready(dg_exchange* x) {
+  for (uint32_t p = 0; p < x->world; ++p)
+    if (x->pb.words[p] == nullptr) return fail(x->h, DG_ERR_ENGINE, "exchange: peer " + std::to_string(p) + " not set");
+  return DG_OK;
 }
 }  // namespace
+
 
 int dg_exchange_create(dg_graph* h, uint32_t rank, uint32_t world, uint64_t capacity, dg_exchange** out) {
   if (!h || !out) return DG_ERR_DATA;
@@ -2090,6 +2146,7 @@ void dg_exchange_destroy(dg_exchange* x) {
   if (!x) return;
   cudaSetDevice(x->h->device);
   cudaStreamSynchronize(x->h->stream);
+  if (x->h->agree_x == x) x->h->agree_x = nullptr;
   for (int p = 0; p < kMaxPeers; ++p)
     if (x->peer_base[p]) cudaIpcCloseMemHandle(x->peer_base[p]);
   cudaFree(x->base);
@@ -2121,11 +2178,9 @@ int dg_exchange_set_peer(dg_exchange* x, uint32_t peer_rank, const void* handle)
   return DG_OK;
 }
 
-int dg_exchange_reset(dg_exchange* x) {
+int dg_exchange_attach(dg_exchange* x, int on) {
   if (!x) return DG_ERR_DATA;
-  cudaSetDevice(x->h->device);
-  DG_CUDA(x->h, cudaMemsetAsync(x->base, 0, 256, x->h->stream));
-  DG_CUDA(x->h, cudaStreamSynchronize(x->h->stream));
+  x->h->agree_x = on ? x : nullptr;
   return DG_OK;
 }
 
@@ -2135,57 +2190,134 @@ int dg_exchange_push_coo(dg_exchange* x, const uint32_t* src, const uint32_t* ds
   dg_graph* h = x->h;
   h->last_error.clear();
   cudaSetDevice(h->device);
-  if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
-  if (n > x->capacity)  // origin indices address the origin's answer buffer
-    return fail(h, DG_ERR_ENGINE, "exchange: batch larger than the exchange capacity");
-  if (bits > 32 || vertex_count > (bits >= 32 ? (1ull << 32) : (1ull << bits)))
-    return fail(h, DG_ERR_DATA, "exchange: vertex_count exceeds 2^bits");
-  for (uint32_t p = 0; p < x->world; ++p)
-    if (x->pb.cursor[p] == nullptr) return fail(h, DG_ERR_ENGINE, "exchange: peer " + std::to_string(p) + " not set");
-  if (n == 0) return DG_OK;
   int rc;
+  if ((rc = exchange_ready(x)) != DG_OK) return rc;
+  // host-side rejections still ARRIVE (with their status), so that no peer waits for this rank
+  int early = DG_OK;
+  if (n >= (1ull << 31)) early = fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  else if (n > x->capacity) early = fail(h, DG_ERR_ENGINE, "exchange: batch larger than the exchange capacity");   // origin indices address the answer buffer
+  else if (bits > 32 || vertex_count > (bits >= 32 ? (1ull << 32) : (1ull << bits)))
+    early = fail(h, DG_ERR_DATA, "exchange: vertex_count exceeds 2^bits");
+  const std::string early_msg = h->last_error;
   if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
-  DG_LAUNCH(h, "exchange_validate_kernel", exchange_validate_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      src, (uint32_t)n, (uint32_t)std::min<uint64_t>(vertex_count, 0xFFFFFFFFull), h->d_op()));
-  DG_LAUNCH(h, "exchange_push_kernel", exchange_push_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      x->pb, src, dst, (uint32_t)n, bits, h->d_op()));
-  return op_end(h);
+  if (early != DG_OK) {
+    cudaMemsetAsync(&h->d_op()->err, early == DG_ERR_DATA ? 0x02 : 0x03, 1, h->stream);   // (low byte: the status code)
+  } else if (n > 0) {
+    DG_LAUNCH(h, "exchange_validate_kernel", exchange_validate_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+        src, (uint32_t)n, (uint32_t)std::min<uint64_t>(vertex_count, 0xFFFFFFFFull), h->d_op()));
+    DG_LAUNCH(h, "exchange_push_kernel", exchange_push_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+        x->pb, x->set(), src, dst, (uint32_t)n, bits, h->d_op()));
+  }
+  DG_LAUNCH(h, "exchange_signal_kernel", exchange_signal_kernel<<<1, 32, 0, h->stream>>>(x->pb, x->set(), 0, h->d_op()));
+  rc = op_end(h);
+  if (early != DG_OK) {
+    h->last_error = early_msg;
+    return early;
+  }
+  return rc;
 }
 
 int dg_exchange_received(dg_exchange* x, uint64_t* n, uint32_t** src_local, uint32_t** dst,
                          uint32_t** origin_index, uint32_t** origin_rank) {
   if (!x || !n) return DG_ERR_DATA;
-  cudaSetDevice(x->h->device);
-  unsigned long long c = 0;
-  DG_CUDA(x->h, cudaMemcpy(&c, x->base, sizeof(c), cudaMemcpyDeviceToHost));
-  if (c > x->capacity) return fail(x->h, DG_ERR_ENGINE, "exchange: receive buffer overflow");
+  dg_graph* h = x->h;
+  cudaSetDevice(h->device);
+  *n = 0;
+  int rc;
+  if ((rc = op_begin(h, 0, 0)) != DG_OK) return rc;
+  DG_LAUNCH(h, "exchange_wait_kernel", exchange_wait_kernel<<<1, 32, 0, h->stream>>>(x->pb, x->set(), 0, h->d_op()));
+  if ((rc = op_end(h)) != DG_OK) return rc;
+  const uint64_t agreed = h->h_blk->op.aux0, c = h->h_blk->op.aux1;
+  const int s = x->set();
+  if (src_local) *src_local = x->pb.src[x->rank][s];
+  if (dst) *dst = x->pb.dst[x->rank][s];
+  if (origin_index) *origin_index = x->pb.idx[x->rank][s];
+  if (origin_rank) *origin_rank = x->pb.from[x->rank][s];
+  if (agreed != 0)
+    return fail(h, (int)agreed, agreed == DG_ERR_DATA ? "sharded batch: a rank rejected the batch while routing (source id out of range)"
+                                                       : "sharded batch: a rank failed while routing (receive buffer full, or a peer never arrived)");
+  if (c > x->capacity) return fail(h, DG_ERR_ENGINE, "exchange: receive buffer overflow");
   *n = c;
-  if (src_local) *src_local = x->pb.src[x->rank];
-  if (dst) *dst = x->pb.dst[x->rank];
-  if (origin_index) *origin_index = x->pb.idx[x->rank];
-  if (origin_rank) *origin_rank = x->pb.from[x->rank];
   return DG_OK;
+}
+
+int dg_exchange_agree(dg_exchange* x, int local_status, int* agreed) {
+  if (!x) return DG_ERR_DATA;
+  dg_graph* h = x->h;
+  cudaSetDevice(h->device);
+  int rc;
+  if ((rc = exchange_ready(x)) != DG_OK) return rc;
+  if ((rc = op_begin(h, 0, 0)) != DG_OK) return rc;
+  if (local_status != 0) cudaMemsetAsync(&h->d_op()->err, local_status == DG_ERR_DATA ? 0x02 : 0x03, 1, h->stream);
+  DG_LAUNCH(h, "exchange_agree_kernel", exchange_agree_kernel<<<1, 32, 0, h->stream>>>(x->pb, x->set(), h->d_op(), h->d_state(), 0));
+  rc = op_end(h);
+  const int a = (int)h->h_blk->op.aux0;
+  if (agreed) *agreed = a;
+  if (rc != DG_OK && local_status == 0 && a != 0)
+    return fail(h, a, "sharded batch: rejected on another rank");
+  return a != 0 ? a : DG_OK;
 }
 
 int dg_exchange_push_answers(dg_exchange* x, const uint8_t* answers, uint64_t n) {
   if (!x) return DG_ERR_DATA;
   dg_graph* h = x->h;
   cudaSetDevice(h->device);
-  if (n == 0) return DG_OK;
-  DG_LAUNCH(h, "exchange_answers_kernel", exchange_answers_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
-      x->pb, answers, x->pb.idx[x->rank], x->pb.from[x->rank], (uint32_t)n));
-  DG_CUDA(h, cudaStreamSynchronize(h->stream));
+  const int s = x->set();
+  if (n > 0) {
+    DG_LAUNCH(h, "exchange_answers_kernel", exchange_answers_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(
+        x->pb, s, answers, x->pb.idx[x->rank][s], x->pb.from[x->rank][s], (uint32_t)n));
+  }
+  DG_LAUNCH(h, "exchange_signal_kernel", exchange_signal_kernel<<<1, 32, 0, h->stream>>>(x->pb, s, 2, h->d_op()));
+  DG_CUDA(h, cudaGetLastError());
   return DG_OK;
 }
 
 int dg_exchange_answers(dg_exchange* x, uint8_t* out, uint64_t n, int mem) {
   if (!x || (!out && n)) return DG_ERR_DATA;
-  if (n > x->capacity) return fail(x->h, DG_ERR_DATA, "exchange: more answers than the buffer holds");
-  cudaSetDevice(x->h->device);
-  if (n == 0) return DG_OK;
-  DG_CUDA(x->h, cudaMemcpyAsync(out, x->pb.ans[x->rank], n,
-                                mem == DG_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, x->h->stream));
-  DG_CUDA(x->h, cudaStreamSynchronize(x->h->stream));
+  dg_graph* h = x->h;
+  if (n > x->capacity) return fail(h, DG_ERR_DATA, "exchange: more answers than the buffer holds");
+  cudaSetDevice(h->device);
+  int rc;
+  if ((rc = op_begin(h, 0, 0)) != DG_OK) return rc;
+  DG_LAUNCH(h, "exchange_wait_kernel", exchange_wait_kernel<<<1, 32, 0, h->stream>>>(x->pb, x->set(), 2, h->d_op()));
+  if (n)
+    DG_CUDA(h, cudaMemcpyAsync(out, x->pb.ans[x->rank][x->set()], n,
+                               mem == DG_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
+  if ((rc = op_end(h)) != DG_OK) return rc;
+  if (h->h_blk->op.aux0 != 0) return fail(h, DG_ERR_ENGINE, "sharded query: a peer's answers never arrived");
+  return DG_OK;
+}
+
+int dg_exchange_end_round(dg_exchange* x) {
+  if (!x) return DG_ERR_DATA;
+  dg_graph* h = x->h;
+  cudaSetDevice(h->device);
+  // this round's set is consumed: its cursor goes back to zero (in stream order, after the local op that read it)
+  DG_CUDA(h, cudaMemsetAsync(&x->pb.words[x->rank]->cursor[x->set()], 0, sizeof(unsigned long long), h->stream));
+  x->epoch += 1;
+  return DG_OK;
+}
+
+int dg_digest_global(dg_graph* h, uint32_t rank, uint32_t world, uint32_t bits, uint64_t* out_digest, uint64_t* out_entries) {
+  if (!h || world == 0 || rank >= world) return DG_ERR_DATA;
+  h->last_error.clear();
+  cudaSetDevice(h->device);
+  const uint64_t V = h->size;
+  if (out_digest) *out_digest = 0;
+  if (out_entries) *out_entries = 0;
+  if (V == 0 || h->B == 0) return DG_OK;
+  int rc = ws_reserve(h, worklist_ws(h, V, 0));
+  if (rc != DG_OK) return rc;
+  if ((rc = op_begin(h, V, V)) != DG_OK) return rc;
+  GraphView g = view(h);
+  BatchView b{nullptr, nullptr, nullptr, nullptr, nullptr};
+  Worklist w = enqueue_enumerate(h, b, V, 0, 0);
+  const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
+  DG_LAUNCH(h, "digest_global_kernel", digest_global_kernel<<<grid_for(h, wl_bound, 8), 256, 0, h->stream>>>(
+      g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, rank, world, bits, h->d_op()));
+  if ((rc = op_end(h)) != DG_OK) return rc;
+  if (out_digest) *out_digest = h->h_blk->op.aux0;
+  if (out_entries) *out_entries = h->h_blk->op.aux1;
   return DG_OK;
 }
 

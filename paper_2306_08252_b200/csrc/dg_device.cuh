@@ -35,6 +35,7 @@ enum ErrDetail : uint32_t {
   kErrOffsetsEnd = 6,     // csr.hpp:62-66
   kErrPoolUnderflow = 7,  // block_pool.hpp:177-189
   kErrScratch = 8,        // internal: compaction scratch too small, host retries
+  kErrPeer = 9,           // sharded store: the batch was rejected on another rank (or a peer never arrived)
 };
 
 // Persistent device-resident scalars of one graph (the queue cursors use the

@@ -2501,16 +2501,58 @@ __global__ void route_gather_kernel(const unsigned long long* __restrict__ keys,
 // the lanes store their records straight into the owner's buffers.
 // ---------------------------------------------------------------------------
 constexpr int kMaxPeers = 16;
+// Round words of one rank (first 256 bytes of its exchange allocation).  Two buffer sets alternate between
+// rounds: a peer can run at most one round ahead (it cannot finish round e before this rank has ARRIVED in
+// round e, which in stream order follows this rank's consumption of round e - 1), so set e & 1 is free again
+// when round e + 2 starts.  Counters are only ever ADDED to by peers and reset by their owner.
+//   cursor      entries pushed into the set (system-scope atomicAdd by the pushing warps)
+//   arrive      [7:0] ranks whose push has landed, [15:8] of them with a data error, [23:16] with an engine error
+//   agree       the same encoding, for the validation / plan status of the local op (batch atomicity across
+//               ranks, graph.hpp:168-171: nobody mutates unless every rank validated)
+//   ans_arrive  ranks whose query answers have landed
+struct RoundWords {
+  unsigned long long cursor[2];
+  unsigned int arrive[2];
+  unsigned int agree[2];
+  unsigned int ans_arrive[2];
+};
 struct PeerBuffers {
-  unsigned long long* cursor[kMaxPeers];
-  uint32_t* src[kMaxPeers];
-  uint32_t* dst[kMaxPeers];
-  uint32_t* idx[kMaxPeers];
-  uint32_t* from[kMaxPeers];
-  uint8_t* ans[kMaxPeers];
+  RoundWords* words[kMaxPeers];
+  uint32_t* src[kMaxPeers][2];
+  uint32_t* dst[kMaxPeers][2];
+  uint32_t* idx[kMaxPeers][2];
+  uint32_t* from[kMaxPeers][2];
+  uint8_t* ans[kMaxPeers][2];
   unsigned long long capacity;
   uint32_t world, rank;
 };
+__device__ __forceinline__ unsigned int status_bits(uint32_t err) {
+  return 1u | (err == 2u ? 1u << 8 : 0u) | (err >= 3u ? 1u << 16 : 0u);
+}
+__device__ __forceinline__ uint32_t status_agreed(unsigned int v) {
+  return ((v >> 16) & 0xFFu) ? 3u : (((v >> 8) & 0xFFu) ? 2u : 0u);
+}
+__device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// spins until every rank has added to *word (or ~4 s have passed); returns the counter, resets it
+__device__ __forceinline__ unsigned int wait_all_ranks(unsigned int* word, uint32_t world, bool* timed_out) {
+  const long long t0 = clock64();
+  unsigned int v = ld_acquire_sys_u32(word);
+  *timed_out = false;
+  while ((v & 0xFFu) < world) {
+    if (clock64() - t0 > 8000000000ll) {
+      *timed_out = true;
+      break;
+    }
+    __nanosleep(200);
+    v = ld_acquire_sys_u32(word);
+  }
+  *word = 0u;
+  return v;
+}
 
 __global__ void __launch_bounds__(256)
 exchange_validate_kernel(const uint32_t* __restrict__ src, uint32_t n, uint32_t vertex_count, OpState* op) {
@@ -2519,7 +2561,7 @@ exchange_validate_kernel(const uint32_t* __restrict__ src, uint32_t n, uint32_t 
 }
 
 __global__ void __launch_bounds__(256)
-exchange_push_kernel(PeerBuffers pb, const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+exchange_push_kernel(PeerBuffers pb, int set, const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
                      uint32_t n, uint32_t bits, OpState* op) {
   if (op->err) return;  // a rejected batch pushes nothing
   const int lane = lane_id();
@@ -2537,15 +2579,15 @@ exchange_push_kernel(PeerBuffers pb, const uint32_t* __restrict__ src, const uin
     const unsigned peers = __match_any_sync(kFull, owner);
     const int leader = __ffs(peers) - 1;
     unsigned long long base = 0;
-    if (valid && lane == leader) base = atomicAdd_system(pb.cursor[owner], (unsigned long long)__popc(peers));
+    if (valid && lane == leader) base = atomicAdd_system(&pb.words[owner]->cursor[set], (unsigned long long)__popc(peers));
     base = __shfl_sync(kFull, base, leader);
     if (valid) {
       const unsigned long long pos = base + __popc(peers & lt);
       if (pos < pb.capacity) {
-        pb.src[owner][pos] = local;
-        pb.dst[owner][pos] = d;
-        pb.idx[owner][pos] = i;
-        pb.from[owner][pos] = pb.rank;
+        pb.src[owner][set][pos] = local;
+        pb.dst[owner][set][pos] = d;
+        pb.idx[owner][set][pos] = i;
+        pb.from[owner][set][pos] = pb.rank;
       } else {
         set_error(op, 3, kErrScratch, i);  // receive buffer of `owner` is full
       }
@@ -2553,11 +2595,95 @@ exchange_push_kernel(PeerBuffers pb, const uint32_t* __restrict__ src, const uin
   }
 }
 
+// After the push (or the answers) of this rank: tell every rank that it has landed.  The fence makes the
+// stores of the preceding kernel visible system-wide before the counters move (fences are cumulative).
+// which: 0 arrive (carries this rank's routing status), 2 ans_arrive
+__global__ void exchange_signal_kernel(PeerBuffers pb, int set, int which, const OpState* op) {
+  __threadfence_system();
+  const uint32_t p = threadIdx.x;
+  if (p < pb.world) {
+    unsigned int* w = which == 0 ? &pb.words[p]->arrive[set] : &pb.words[p]->ans_arrive[set];
+    atomicAdd_system(w, which == 0 ? status_bits(op->err) : 1u);
+  }
+}
+
+// Waits until every rank has arrived in this rank's set.  which 0: op->aux0 = agreed routing status,
+// op->aux1 = entries received; which 2: answers.
+__global__ void exchange_wait_kernel(PeerBuffers pb, int set, int which, OpState* op) {
+  if (threadIdx.x != 0) return;
+  RoundWords* own = pb.words[pb.rank];
+  bool timed_out;
+  const unsigned int v = wait_all_ranks(which == 0 ? &own->arrive[set] : &own->ans_arrive[set], pb.world, &timed_out);
+  __threadfence_system();
+  if (which == 0) {
+    op->aux0 = timed_out ? 3u : status_agreed(v);
+    op->aux1 = own->cursor[set];
+  } else {
+    op->aux0 = timed_out ? 3u : 0u;
+  }
+}
+
+// Batch atomicity across ranks: posts this rank's validation / plan status to every rank, waits for all of
+// them, and only an all-clear lets the op's mutating kernels run (they start with `if (op->err) return`).
+// An insert's queue front / live-edge count are committed here instead of in the plan's last tile.
+__global__ void exchange_agree_kernel(PeerBuffers pb, int set, OpState* op, DeviceState* st, int commit_insert) {
+  const uint32_t p = threadIdx.x;
+  const uint32_t mine = op->err;
+  __threadfence_system();
+  if (p < pb.world) atomicAdd_system(&pb.words[p]->agree[set], status_bits(mine));
+  if (p != 0) return;
+  bool timed_out;
+  const unsigned int v = wait_all_ranks(&pb.words[pb.rank]->agree[set], pb.world, &timed_out);
+  const uint32_t agreed = timed_out ? 3u : status_agreed(v);
+  op->aux0 = agreed;
+  if (agreed != 0 && mine == 0) {
+    op->err_detail = kErrPeer;
+    op->err_index = 0;
+    __threadfence();
+    op->err = agreed;
+  }
+  if (agreed == 0 && commit_insert) {
+    st->front += op->total_need;          // commit_front (block_pool.hpp:162-166)
+    st->active_edges += op->n_edges;      // graph.hpp:186
+  }
+}
+
 __global__ void __launch_bounds__(256)
-exchange_answers_kernel(PeerBuffers pb, const uint8_t* __restrict__ answers, const uint32_t* __restrict__ idx,
+exchange_answers_kernel(PeerBuffers pb, int set, const uint8_t* __restrict__ answers, const uint32_t* __restrict__ idx,
                         const uint32_t* __restrict__ from, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    pb.ans[from[i]][idx[i]] = answers[i];
+    pb.ans[from[i]][set][idx[i]] = answers[i];
+}
+
+// dg_digest over GLOBAL source ids for a shard of the source-partitioned store: local id l of rank r is
+// vertex perm_inv(l * world + r), so the sum over ranks equals the single-GPU digest of the same multiset.
+__global__ void __launch_bounds__(256)
+digest_global_kernel(GraphView g, const uint32_t* __restrict__ wl_off, const uint32_t* __restrict__ wl_handle,
+                     const uint32_t* __restrict__ wl_run, const uint32_t* __restrict__ run_deg, uint32_t rank, uint32_t world,
+                     uint32_t bits, OpState* op) {
+  __shared__ unsigned long long s_warp[8];
+  const uint32_t W = (uint32_t)op->wl_blocks;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  unsigned long long acc = 0, cntacc = 0;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < W; w += nwarps) {
+    const uint32_t v = wl_run[w] & kRunMask;
+    const unsigned long long gv = owner_perm_inv(v * world + rank, bits);
+    const uint32_t h = wl_handle[w];
+    const uint32_t k = w - wl_off[v];
+    const uint32_t cnt = min(g.B, run_deg[v] - k * g.B);
+    const uint32_t* blk = g.slab + (unsigned long long)h * g.B;
+    for (uint32_t s = lane; s < cnt; s += 32) {
+      acc += mix64((gv << 32) | blk[s]);
+      ++cntacc;
+    }
+  }
+  const unsigned long long ta = block_reduce_sum(acc, s_warp);
+  const unsigned long long tc = block_reduce_sum(cntacc, s_warp);
+  if (threadIdx.x == 0) {
+    atomicAdd(&op->aux0, ta);
+    atomicAdd(&op->aux1, tc);
+  }
 }
 
 }  // namespace dg

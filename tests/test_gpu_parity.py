@@ -742,7 +742,8 @@ def _sharded_world1(port, q, exchange):
         from paper_2306_08252_b200.sharded import ShardedDynamicGraph
         rng = np.random.default_rng(9)
         V = 3000
-        sg = ShardedDynamicGraph(GraphConfig(pool_blocks=1 << 15), V, 8, exchange=exchange, exchange_capacity=1 << 16)
+        sg = ShardedDynamicGraph(GraphConfig(pool_blocks=1 << 15), V, 8, exchange=exchange, exchange_capacity=1 << 16,
+                                 reserve_vertices=V + 64)
         orc = CpuGraph(load_oracle(), "orc", V, 8, 1 << 28)
         dev = lambda a: torch.from_numpy(a.view(np.int32)).cuda()
         log = []
@@ -779,9 +780,55 @@ def _sharded_world1(port, q, exchange):
             return
         except Exception as e:
             assert "DataError" in type(e).__name__, type(e)
+        _sharded_vertex_ops_and_atomicity(sg, orc, V, 0, 1, dev, rng)
         q.put("ok")
     finally:
         dist.destroy_process_group()
+
+
+def _sharded_vertex_ops_and_atomicity(sg, orc, V, rank, world, dev, rng):
+    """Shared tail of the sharded tests: a destination out of range inside one rank's share rejects the batch on
+    EVERY rank and leaves every shard untouched (graph.hpp:168-171 across ranks); degrees over global ids;
+    vertex delete / insert routed to the owners with the reference's skipped list."""
+    before = (sg.active_edges(), sg.digest())
+    s = rng.integers(0, V, 4000).astype(np.uint32)
+    d = rng.integers(0, V, 4000).astype(np.uint32)
+    d[1234] = V + 99                                   # lands on whichever rank owns s[1234]
+    try:
+        sg.insert_pairs(dev(s[rank::world]), dev(d[rank::world]))
+        raise AssertionError("no error raised for an out-of-range destination")
+    except Exception as e:
+        assert "DataError" in type(e).__name__, (type(e), e)
+    assert (sg.active_edges(), sg.digest()) == before   # nothing was applied on ANY rank
+    assert np.array_equal(sg.degrees().cpu().numpy().astype(np.uint64), orc.degrees())
+    # vertex delete: same list on every rank; skipped = unknown / dead / repeated ids in encounter order
+    ids = np.array([5, 17, 5, V + 3, 200, 17], np.uint32)
+    _, want = orc.delete_vertices(ids)
+    got = sg.delete_vertices(ids)
+    assert np.array_equal(np.asarray(got, np.uint32), np.asarray(want, np.uint32)), (got, want)
+    assert sg.active_edges() == orc.active_edges() and sg.alive_vertices() == orc.alive_vertices()
+    assert np.array_equal(sg.degrees().cpu().numpy().astype(np.uint64), orc.degrees())
+    # an insert naming a retired source is rejected everywhere
+    try:
+        sg.insert_pairs(dev(np.array([5, 9], np.uint32)[rank::world]), dev(np.array([1, 2], np.uint32)[rank::world]))
+        raise AssertionError("no error raised for a retired source")
+    except Exception as e:
+        assert "DataError" in type(e).__name__, (type(e), e)
+    assert sg.active_edges() == orc.active_edges()
+    # vertex insert: replicated metadata, the new ids are usable at once (room left by reserve_vertices)
+    sg.insert_vertices(40)
+    assert orc.insert_vertices(40) == 0
+    assert sg.logical_size() == orc.logical_size() == V + 40
+    s2 = rng.integers(0, V + 40, 3000).astype(np.uint32)
+    s2 = s2[(s2 != 5) & (s2 != 17) & (s2 != 200)]
+    d2 = rng.integers(0, V + 40, len(s2)).astype(np.uint32)
+    sg.insert_pairs(dev(s2[rank::world]), dev(d2[rank::world]))
+    assert orc.insert_pairs(s2, d2) == 0
+    assert sg.active_edges() == orc.active_edges()
+    assert np.array_equal(sg.degrees().cpu().numpy().astype(np.uint64), orc.degrees())
+    off2, dst2 = orc.export_csr(sorted=False)
+    srcs = np.repeat(np.arange(V + 40, dtype=np.uint32), np.diff(off2.astype(np.int64)))
+    assert sg.digest() == (_np_digest(srcs, dst2), len(dst2))
 
 
 @pytest.mark.parametrize("exchange", ["p2p", "nccl"])
@@ -818,7 +865,8 @@ def _sharded_world2_one_gpu(rank, port, q):
         from paper_2306_08252_b200.sharded import ShardedDynamicGraph
         rng = np.random.default_rng(17)   # same stream on both ranks: every rank feeds ITS half of each batch
         V = 5000
-        sg = ShardedDynamicGraph(GraphConfig(pool_blocks=1 << 15), V, 32, exchange="p2p", exchange_capacity=1 << 17)
+        sg = ShardedDynamicGraph(GraphConfig(pool_blocks=1 << 15), V, 32, exchange="p2p", exchange_capacity=1 << 17,
+                                 reserve_vertices=V + 64)
         orc = CpuGraph(load_oracle(), "orc", V, 32, 1 << 28)
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
         log = []
@@ -860,6 +908,7 @@ def _sharded_world2_one_gpu(rank, port, q):
         except Exception as e:
             assert "DataError" in type(e).__name__, type(e)
         assert sg.active_edges() == orc.active_edges()
+        _sharded_vertex_ops_and_atomicity(sg, orc, V, rank, 2, dev, rng)
         sg.close()
         q.put("ok")
     finally:

@@ -101,6 +101,24 @@ def _worker(rank, world, port, V, B, seed, q):
         q.put(("query", rank, qs, qd, out))
         # status agreement: one failing rank fails everyone
         assert agree_status(2 if rank == 1 else 0, torch.device("cpu")) == 2
+        # batch atomicity ACROSS ranks (graph.hpp:168-171): check on every rank -> agree -> apply.  One bad
+        # destination inside the share of whichever rank owns its source: the other rank's share is valid, yet
+        # neither rank may apply anything.
+        before = (store.active_edges(), store.degrees().copy())
+        bs = np.arange(40, dtype=np.uint32) + 7
+        bd = np.full(40, 3, dtype=np.uint32)
+        if rank == 0:
+            bd[11] = V + 5
+        ls_, d_, _, counts = _route_np(bs, bd, bits, world)
+        (rs, rd), _ = exchange_buckets([torch.from_numpy(ls_.astype(np.int64)), torch.from_numpy(d_.astype(np.int64))],
+                                       counts.tolist())
+        check = 2 if (rd.numpy() >= V).any() else 0           # the CPU stand-in of dg_check_batch_coo
+        agreed = agree_status(check, torch.device("cpu"))
+        assert agreed == 2
+        if agreed == 0:
+            store.insert_pairs(rs.numpy().astype(np.uint32), rd.numpy().astype(np.uint32))
+        assert store.active_edges() == before[0] and np.array_equal(store.degrees(), before[1])
+        q.put(("atomic", rank, int(check)))
         # export this rank's shard in GLOBAL ids
         off, dst = store.export_csr(sorted=True)
         lib = _lib.load()
@@ -125,7 +143,7 @@ def test_two_rank_routed_store_equals_single_store(seed):
     for p in procs:
         p.start()
     msgs = []
-    expected = world * (6 + 1 + 1)
+    expected = world * (6 + 1 + 1 + 1)
     while len(msgs) < expected:
         msgs.append(q.get(timeout=120))
     for p in procs:
@@ -152,3 +170,5 @@ def test_two_rank_routed_store_equals_single_store(seed):
         assert np.array_equal(want, got), v
     for _, _, qs, qd, out in [m for m in msgs if m[0] == "query"]:
         assert np.array_equal(single.query(qs, qd), out)
+    # the bad destination reached exactly ONE rank's share; both ranks held back (asserted in the workers)
+    assert sorted(m[2] for m in msgs if m[0] == "atomic") == [0, 2]
