@@ -229,9 +229,12 @@ scan_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* sc
 //   In(i)                         -> Sum2 (PURE loads; see scan_kernel)
 //   Out(i, excl.a, excl.b, value) -> per element
 //   Fin(total.a, total.b)         -> once, by the last tile to finish
-// scratch: [0] cursor a, [1] cursor b, [2] finished tiles; zero at launch, zeroed again by the last tile.
+// scratch: [0] cursor a, [1] cursor b, [2] finished tiles, [3] cursor c; zero at launch, zeroed again by the last tile
+// (cursor c is read by nobody here: the op reads it from its own counter, see EnumFin).
 struct Sum2 {
   unsigned long long a, b;
+  unsigned int c = 0;        // a third, 32-bit quantity (its cursor is scratch[3]); most users leave it at 0
+  unsigned int c_excl = 0;   // Out only: the element's exclusive prefix of c (handed over inside the value)
 };
 constexpr size_t kAllocScratchWords = 4;
 constexpr int kAllocThreads = 256;
@@ -254,7 +257,7 @@ alloc_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* s
   const unsigned long long num_tiles = (n + kAllocTile - 1) / kAllocTile;
   const unsigned int tile = blockIdx.x;
   if (tile >= num_tiles) {
-    if (n == 0 && tile == 0 && threadIdx.x == 0) fin(0ull, 0ull);
+    if (n == 0 && tile == 0 && threadIdx.x == 0) fin(0ull, 0ull, 0u);
     return;
   }
   const unsigned long long base = (unsigned long long)tile * kAllocTile +
@@ -269,15 +272,18 @@ alloc_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* s
     if (i >= n) v[j] = Sum2{0ull, 0ull};
     thread_sum.a += v[j].a;
     thread_sum.b += v[j].b;
+    thread_sum.c += v[j].c;
   }
   Sum2 incl = thread_sum;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const unsigned long long ta = __shfl_up_sync(kFull, incl.a, d);
     const unsigned long long tb = __shfl_up_sync(kFull, incl.b, d);
+    const unsigned int tc = __shfl_up_sync(kFull, incl.c, d);
     if (lane_id() >= d) {
       incl.a += ta;
       incl.b += tb;
+      incl.c += tc;
     }
   }
   const int warp = threadIdx.x >> 5;
@@ -290,24 +296,30 @@ alloc_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* s
     if (w < warp) {
       warp_excl.a += sw.a;
       warp_excl.b += sw.b;
+      warp_excl.c += sw.c;
     }
     tile_sum.a += sw.a;
     tile_sum.b += sw.b;
+    tile_sum.c += sw.c;
   }
   if (threadIdx.x == 0) {
     Sum2 bs{0ull, 0ull};
     if (tile_sum.a) bs.a = atomicAdd(&scratch[0], tile_sum.a);
     if (tile_sum.b) bs.b = atomicAdd(&scratch[1], tile_sum.b);
+    if (tile_sum.c) bs.c = (unsigned int)atomicAdd(&scratch[3], (unsigned long long)tile_sum.c);
     s_base = bs;
   }
   __syncthreads();
-  Sum2 run{s_base.a + warp_excl.a + (incl.a - thread_sum.a), s_base.b + warp_excl.b + (incl.b - thread_sum.b)};
+  Sum2 run{s_base.a + warp_excl.a + (incl.a - thread_sum.a), s_base.b + warp_excl.b + (incl.b - thread_sum.b),
+           s_base.c + warp_excl.c + (incl.c - thread_sum.c)};
 #pragma unroll
   for (int j = 0; j < kAllocItems; ++j) {
     const unsigned long long i = base + j;
+    v[j].c_excl = run.c;
     if (i < n) out(i, run.a, run.b, v[j], aux[j]);
     run.a += v[j].a;
     run.b += v[j].b;
+    run.c += v[j].c;
   }
   // (off the tile's critical path) the last tile to get here sees every tile's
   // contribution to the cursors: thread 0's cursor atomics precede its fence
@@ -317,10 +329,12 @@ alloc_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* s
     if (done == num_tiles - 1) {
       __threadfence();
       const unsigned long long ta = ld_volatile_u64(&scratch[0]), tb = ld_volatile_u64(&scratch[1]);
+      const unsigned long long tc = ld_volatile_u64(&scratch[3]);
       scratch[0] = 0ull;   // the cursors are handed back zeroed: the host keeps them in a persistent
       scratch[1] = 0ull;   // buffer and never clears them between ops
       scratch[2] = 0ull;
-      fin(ta, tb);
+      scratch[3] = 0ull;
+      fin(ta, tb, (unsigned int)tc);
     }
   }
 }

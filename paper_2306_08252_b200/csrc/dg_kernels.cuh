@@ -531,7 +531,7 @@ struct PlanFin {
   unsigned long long n_edges;
   int set_runs;        // counting path: the pass also counted the runs
   int commit_globals;  // COO path: validation is complete, commit here; CSR path: commit_insert_kernel
-  __device__ void operator()(unsigned long long total_a, unsigned long long total_b) const {
+  __device__ void operator()(unsigned long long total_a, unsigned long long total_b, unsigned int) const {
     const unsigned long long need = total_b & 0xFFFFFFFFull;
     const unsigned long long units = total_b >> 32;
     if (set_runs) op->n_runs = total_a >> 32;
@@ -1312,7 +1312,7 @@ struct EnumLists {
   uint32_t* zero3;     // delete: run_matched / hole_cnt / surv_cnt of the run start at zero (no memset)
   uint32_t zstride;
   __device__ void write(uint32_t r, uint32_t d, uint32_t nblk, uint32_t k, uint32_t head, uint32_t v, uint32_t es,
-                        unsigned long long excl_b) const {
+                        unsigned long long excl_b, uint32_t med_slot) const {
     run_deg[r] = d;
     if (zero3 != nullptr) {
       zero3[r] = 0u;
@@ -1324,10 +1324,9 @@ struct EnumLists {
       if (cls != 0u) {
         wl_off[r] = cls;
         run_head[r] = head;
-        if (cls == kClsMed) {
-          const uint32_t slot = atomicAdd(&op->n_fmed, 1u);
-          fmed_rec[2u * slot] = make_uint4(r, v, es, k);
-          fmed_rec[2u * slot + 1u] = make_uint4(d, head, 0u, 0u);
+        if (cls == kClsMed) {   // (the slot came out of the scan: no same-address atomic per listed source)
+          fmed_rec[2u * med_slot] = make_uint4(r, v, es, k);
+          fmed_rec[2u * med_slot + 1u] = make_uint4(d, head, 0u, 0u);
         }
         return;
       }
@@ -1382,7 +1381,8 @@ struct EnumIn {
     const uint32_t v = batch_src(b, r);
     x.d = live_degree(g, v, wanted, check_alive);
     x.head = (fuse && wanted && v < g.size) ? g.head[v] : kNull;
-    return Sum2{0ull, enum_word_b(blocks_for(g, x.d), k, fuse)};
+    const uint32_t nblk = blocks_for(g, x.d);
+    return Sum2{0ull, enum_word_b(nblk, k, fuse), (fuse && fused_class(k, nblk) == kClsMed) ? 1u : 0u};
   }
 };
 struct EnumOut {
@@ -1393,7 +1393,7 @@ struct EnumOut {
                              Sum2 v, const EnumAux& x) const {
     const uint32_t k = b.run_start != nullptr ? run_len(b, (uint32_t)r) : 0u;
     lists.write((uint32_t)r, x.d, blocks_for(g, x.d), k, x.head, batch_src(b, (uint32_t)r),
-                b.run_start != nullptr ? b.run_start[r] : 0u, excl_b);
+                b.run_start != nullptr ? b.run_start[r] : 0u, excl_b, v.c_excl);
   }
 };
 // fused with the counting group-by: one pass over the batch entries (see GroupPlanIn)
@@ -1412,7 +1412,8 @@ struct GroupEnumIn {
     const uint32_t c = rep ? cnt[gi(s)] : 0u;
     x.d = live_degree(g, s, rep, check_alive);
     x.head = (fuse && rep && s < g.size) ? g.head[s] : kNull;
-    return Sum2{c ? ((1ull << 32) | c) : 0ull, enum_word_b(blocks_for(g, x.d), c, fuse)};
+    const uint32_t nblk = blocks_for(g, x.d);
+    return Sum2{c ? ((1ull << 32) | c) : 0ull, enum_word_b(nblk, c, fuse), (fuse && fused_class(c, nblk) == kClsMed) ? 1u : 0u};
   }
 };
 struct GroupEnumOut {
@@ -1435,14 +1436,15 @@ struct GroupEnumOut {
     run_start[r] = es;
     run_end[r] = es + c;
     cnt[gi(v)] = es;
-    lists.write(r, x.d, blocks_for(g, x.d), c, x.head, v, es, excl_b);
+    lists.write(r, x.d, blocks_for(g, x.d), c, x.head, v, es, excl_b, val.c_excl);
   }
 };
 struct EnumFin {
   OpState* op;
   unsigned long long wl_cap;
   int set_runs;
-  __device__ void operator()(unsigned long long total_a, unsigned long long total_b) const {
+  __device__ void operator()(unsigned long long total_a, unsigned long long total_b, unsigned int total_c) const {
+    op->n_fmed = total_c;   // sources of the fused medium class (their record slots came out of the scan)
     if (set_runs) op->n_runs = total_a >> 32;
     op->wl_blocks = total_b & 0xFFFFFFFFull;
     op->n_big = total_b >> 32;
@@ -2030,7 +2032,7 @@ struct MovesFin {
   GraphView g;
   OpState* op;
   unsigned long long mv_cap;
-  __device__ void operator()(unsigned long long total_a, unsigned long long total) const {
+  __device__ void operator()(unsigned long long total_a, unsigned long long total, unsigned int) const {
     op->aux0 = total;                      // scratch entries needed
     op->aux1 = total > mv_cap ? 1ull : 0ull;  // host grows the scratch and re-runs the tail
     if (total <= mv_cap) {                 // reclaim (block_pool.hpp:192-209): one cursor bump for the whole batch
