@@ -199,6 +199,11 @@ struct dg_graph {
   std::vector<cudaEvent_t> prof_pool;
   std::map<std::string, std::pair<double, uint64_t>> prof_acc;  // name -> (ms, launches)
   std::string prof_text;
+  // optional timeline of the last op (DG_TIMELINE=1): events at named points of the op's streams, without
+  // serialising them — where the op's time goes when kernels run side by side
+  bool timeline = false;
+  struct TlMark { const char* name; cudaEvent_t ev; };
+  std::vector<TlMark> tl_marks;
 
   DeviceState* d_state() const { return &d_blk->st; }
   OpState* d_op() const { return &d_blk->op; }
@@ -269,6 +274,27 @@ void prof_collect(dg_graph* h) {
     h->prof_pool.push_back(sp.b);
   }
   h->prof_open.clear();
+  cudaGetLastError();
+}
+void tl_mark(dg_graph* h, const char* name, cudaStream_t s) {
+  if (!h->timeline) return;
+  cudaEvent_t e = prof_event(h);
+  cudaEventRecord(e, s);
+  h->tl_marks.push_back({name, e});
+}
+void tl_report(dg_graph* h) {   // after the op's final synchronise
+  if (!h->timeline || h->tl_marks.empty()) return;
+  std::string line = "[timeline us]";
+  for (size_t i = 1; i < h->tl_marks.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->tl_marks[0].ev, h->tl_marks[i].ev);
+    char buf[96];
+    std::snprintf(buf, sizeof buf, " %s=%.1f", h->tl_marks[i].name, ms * 1e3);
+    line += buf;
+  }
+  std::fprintf(stderr, "%s\n", line.c_str());
+  for (auto& m : h->tl_marks) h->prof_pool.push_back(m.ev);
+  h->tl_marks.clear();
   cudaGetLastError();
 }
 #define DG_LAUNCH(h, name, ...)                                                   \
@@ -460,6 +486,7 @@ int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
   op.aux1 = 0;
   op.n_input = n_input;  // device-resident copy of the input length for scans
   op.n_aux = h->size + 1;
+  tl_mark(h, "begin", h->stream);
   DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
   h->launches = 0;
   h->zslot = 0;
@@ -492,10 +519,12 @@ const char* detail_text(uint32_t d) {
 
 // read back {DeviceState, OpState}; translate a device-side error
 int op_end(dg_graph* h) {
+  tl_mark(h, "end", h->stream);
   DG_CUDA(h, cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(DevBlock), cudaMemcpyDeviceToHost, h->stream));
   DG_CUDA(h, cudaStreamSynchronize(h->stream));
   DG_CUDA(h, cudaGetLastError());
   if (h->profiling) prof_collect(h);
+  tl_report(h);
   if (h->launch_error != cudaSuccess) {
     const cudaError_t e = h->launch_error;
     h->launch_error = cudaSuccess;
@@ -1028,19 +1057,23 @@ Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, u
   out.run_src = ws_alloc<uint32_t>(h, out.runs_bound + 1);
   DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
       g, out.gi, d_src, d_dst, (uint32_t)n, out.cnt, out.rank, h->d_op()));
+  tl_mark(h, "K1", h->stream);
   out.b = BatchView{nullptr, out.gdst, out.run_src, out.run_start, out.run_end};
   return out;
 }
 // counting path, step 3 (after the op's alloc pass turned cnt into group starts)
+inline unsigned scatter_grid(uint64_t n) { return (unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)); }
 template <int kMode>
-void group_scatter(dg_graph* h, const Grouped& gr, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n) {
+void group_scatter(dg_graph* h, const Grouped& gr, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n,
+                   cudaStream_t stream = nullptr) {
   GraphView g = view(h);
-  const unsigned grid = (unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems));
+  if (stream == nullptr) stream = h->stream;
+  const unsigned grid = scatter_grid(n);
   if (gr.index) {
-    DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, true><<<grid, 256, 0, h->stream>>>(
+    DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, true><<<grid, 256, 0, stream>>>(
         g, gr.gi, d_src, d_dst, (uint32_t)n, gr.cnt, gr.rank, gr.gdst, gr.index, h->d_op()));
   } else {
-    DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, false><<<grid, 256, 0, h->stream>>>(
+    DG_LAUNCH(h, "group_scatter_kernel", group_scatter_kernel<kMode, false><<<grid, 256, 0, stream>>>(
         g, gr.gi, d_src, d_dst, (uint32_t)n, gr.cnt, gr.rank, gr.gdst, nullptr, h->d_op()));
   }
 }
@@ -1119,9 +1152,11 @@ inline size_t group_enumerate_ws(const dg_graph* h, uint64_t n, bool with_index,
 //   scatter(): the counting group-by's scatter (needed by both the fused kernel and the hub match).
 inline cudaStream_t side(const dg_graph* h, int i) { return h->profiling ? h->stream : h->aux[i]; }
 
+//   scatter(stream): the counting group-by's scatter; scatter_ctas: its grid (0: the batch is already grouped).
+//   The fused kernel is launched beside it and waits for its CTAs on the device (wait_scatter).
 template <class Scatter>
 int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs_bound, uint64_t n, bool fuse,
-               GroupIndex gi, uint32_t* cnt, Scatter&& scatter) {
+               GroupIndex gi, uint32_t* cnt, uint32_t scatter_ctas, Scatter&& scatter) {
   GraphView g = view(h);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   uint32_t* run_matched = w.zero3;   // (zeroed per run by the enumeration plan)
@@ -1138,16 +1173,25 @@ int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs
     cudaStreamWaitEvent(s0, h->ev_fork, 0);
     cudaStreamWaitEvent(s1, h->ev_fork, 0);
   }
+  tl_mark(h, "K2", h->stream);
   enqueue_walk(h, b, w, runs_bound, s0, s1);   // hub chains only
-  scatter();
+  tl_mark(h, "walk_big", s0);
+  tl_mark(h, "walk_small", s1);
+  // (Launching the fused kernel BESIDE the scatter, with a device-side wait for the scatter's CTAs right before
+  // the first target load, was measured: the kernel ended 4 us earlier, the scatter itself took up to 50 us
+  // longer under the spinning warps.  Stream order it is.)
+  scatter(h->stream);
+  tl_mark(h, "scatter", h->stream);
   if (par) cudaEventRecord(h->ev_main, h->stream);
   if (fuse) {
     // one-warp CTAs: the medium sources first (heaviest), strided over a bounded grid, then 32 runs per warp
     const uint32_t g_med = (uint32_t)std::clamp<uint64_t>((fused_med_bound(h, runs_bound, n) + 7) / 8, 1, 32768);
     const unsigned grid = g_med + (unsigned)((runs_bound + 31) / 32);
     DG_LAUNCH(h, "fused_delete_kernel", fused_delete_kernel<<<grid, 32, 0, h->stream>>>(
-        g, b, w.wl_off, w.run_deg, w.run_head, w.fmed_rec, g_med, (uint32_t)runs_bound, gi, cnt, tally, h->d_op()));
-    DG_LAUNCH(h, "fused_tally_kernel", fused_tally_kernel<<<1, 32, 0, h->stream>>>(g, tally, h->d_op()));
+        g, b, w.wl_off, w.run_deg, w.run_head, w.fmed_rec, g_med, (uint32_t)runs_bound, gi, cnt, scatter_ctas, tally, h->d_op()));
+    tl_mark(h, "fused", h->stream);
+    DG_LAUNCH(h, "fused_tally_kernel", fused_tally_kernel<<<1, 5 * 32, 0, h->stream>>>(g, tally, h->d_op()));
+    tl_mark(h, "tally", h->stream);
   }
   if (par) {   // the hub match needs both walks and the scatter
     cudaEventRecord(h->ev_join[0], s0);
@@ -1159,6 +1203,8 @@ int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs
   }
   if (h->B == 32) enqueue_match_impl<true, true>(h, b, w, n, run_matched, wl_mask, nullptr, s0, s1, s1);
   else enqueue_match_impl<true, false>(h, b, w, n, run_matched, wl_mask, nullptr, s0, s1, s1);
+  tl_mark(h, "match_long", s0);
+  tl_mark(h, "match_med_tiny", s1);
   if (par) {
     cudaEventRecord(h->ev_join[1], s1);
     cudaStreamWaitEvent(s0, h->ev_join[1], 0);
@@ -1176,6 +1222,7 @@ int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs
     DG_LAUNCH(h, "delete_moves_kernel", delete_moves_kernel<<<grid_resident(h, wl_bound, 256, delete_moves_kernel), 256, 0, st>>>(
         g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, hole_cnt, surv_cnt,
         h->mv_hole, h->d_op()));
+    tl_mark(h, "hub_tail", st);
     if (par && attempt == 0) {
       cudaEventRecord(h->ev_join[0], s0);
       cudaStreamWaitEvent(h->stream, h->ev_join[0], 0);
@@ -1205,13 +1252,13 @@ int delete_coo_run(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, ui
                  GroupEnumOut{g, gr.gi, d_src, gr.cnt, gr.run_src, gr.run_start, gr.run_end, w.lists(h)},
                  EnumFin{h->d_op(), h->blocks_in_use(), /*set_runs=*/1});
     enqueue_agree(h, false);
-    return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, gr.gi, fuse ? gr.cnt : nullptr,
-                      [&] { group_scatter<kPackDelete>(h, gr, d_src, d_dst, n); });
+    return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, gr.gi, fuse ? gr.cnt : nullptr, /*scatter_ctas=*/0,
+                      [&](cudaStream_t st) { group_scatter<kPackDelete>(h, gr, d_src, d_dst, n, st); });
   }
   Grouped gr = group_radix<kPackDelete>(h, d_src, d_dst, n, false, max_src);
   Worklist w = enqueue_enumerate(h, gr.b, gr.runs_bound, n, /*check_alive=*/1, fuse, /*walk=*/false, /*for_delete=*/true);
   enqueue_agree(h, false);
-  return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, GroupIndex{}, nullptr, [] {});
+  return delete_run(h, gr.b, w, gr.runs_bound, n, fuse, GroupIndex{}, nullptr, 0, [](cudaStream_t) {});
 }
 
 
@@ -1241,6 +1288,7 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
   h->cfg = cfg;
   h->device = cfg.device;
   h->reclaim = (cfg.flags & DG_FLAG_NO_RECLAIM) ? 0 : 1;
+  h->timeline = std::getenv("DG_TIMELINE") != nullptr;
   h->group_mode = (cfg.flags & DG_FLAG_GROUP_RADIX) ? 1 : ((cfg.flags & DG_FLAG_GROUP_COUNT) ? 2 : 0);
   if (cfg.trigger_fraction > 0.f) h->trigger = cfg.trigger_fraction;
   if (cfg.growth_fraction > 0.f) h->growth = cfg.growth_fraction;
@@ -1396,6 +1444,7 @@ static int insert_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst
     launch_alloc(h, "alloc_kernel<group+plan>", n, d_n_input(h), GroupPlanIn{g, gi, d_src, rank, cnt},
                  GroupPlanOut{gi, d_src, info, cnt},
                  PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/(h->agree_x || check_only) ? 0 : 1});
+    tl_mark(h, "plan", h->stream);
     if (check_only) return op_end(h);
     enqueue_agree(h, /*commit_insert=*/true);
     DG_LAUNCH(h, "append_entries_kernel", append_entries_kernel<<<grid, 256, 0, h->stream>>>(
@@ -1597,7 +1646,7 @@ int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets
   BatchView b{nullptr, d_dst, nullptr, run_start, run_start + 1};
   const bool fuse = h->B == 32;
   Worklist w = enqueue_enumerate(h, b, V, n, /*check_alive=*/1, fuse, /*walk=*/false, /*for_delete=*/true);
-  return delete_run(h, b, w, V, n, fuse, GroupIndex{}, nullptr, [] {});
+  return delete_run(h, b, w, V, n, fuse, GroupIndex{}, nullptr, 0, [](cudaStream_t) {});
 }
 
 // ---- query ---------------------------------------------------------------------

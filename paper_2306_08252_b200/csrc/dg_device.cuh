@@ -79,7 +79,7 @@ struct OpState {
   unsigned long long fused_blocks;  // blocks of the warp-owned sources (fused_delete_kernel); wl_blocks counts the rest
   unsigned long long slots_fused;   // part of `slots` inspected by fused_delete_kernel
   unsigned int n_fmed;              // sources of the fused medium class listed by the enumeration plan
-  unsigned int pad0;
+  unsigned int scatter_ctas;        // CTAs of group_scatter_kernel that have finished (fused_delete_kernel starts beside it)
 };
 
 __device__ __forceinline__ void set_error(OpState* op, uint32_t code, uint32_t detail,

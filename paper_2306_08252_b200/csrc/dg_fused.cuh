@@ -51,6 +51,20 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
   return v;
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// The kernel is launched BESIDE the counting group-by's scatter: everything that does not need the grouped
+// targets (run records, chain links, the blocks on their way to L2) is issued first, then the warp waits
+// until every scatter CTA has finished.  expected == 0: the batch was grouped before the launch.
+__device__ __forceinline__ void wait_scatter(const OpState* op, uint32_t expected) {
+  if (expected == 0) return;
+  if (lane_id() == 0) {
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&op->scatter_ctas) : "memory");
+      if (v < expected) __nanosleep(64);
+    } while (v < expected);
+  }
+  __syncwarp();
+}
 
 // Pushes `cnt` handles hnd[first .. first + cnt) of every lane to the ring rear: ONE atomicAdd per
 // warp (reclaim, block_pool.hpp:192-209).  All lanes must call.
@@ -91,7 +105,8 @@ __device__ __noinline__ void tally_flush(unsigned long long* tally, uint32_t mat
 __global__ void __launch_bounds__(32, 28)
 fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_cls, const uint32_t* __restrict__ run_deg,
                     const uint32_t* __restrict__ run_head, const uint4* __restrict__ med_rec, uint32_t g_med,
-                    uint32_t runs_bound, GroupIndex gi, uint32_t* __restrict__ cnt, unsigned long long* tally, OpState* op) {
+                    uint32_t runs_bound, GroupIndex gi, uint32_t* __restrict__ cnt, uint32_t scatter_expected,
+                    unsigned long long* tally, OpState* op) {
   __shared__ __align__(16) unsigned char smem[kFusedSmemBytes];
   const int lane = lane_id();
   uint32_t(*stg)[32] = reinterpret_cast<uint32_t(*)[32]>(smem);
@@ -138,6 +153,7 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
       for (uint32_t q = 0; q < 4; ++q)
         if (q < nb && (unsigned long long)h0 + q < g.ring_cap) prefetch_l2(g.slab + ((unsigned long long)h0 + q) * 32u);
     }
+    wait_scatter(op, scatter_expected);
 #pragma unroll 1
     while (pending) {
       const bool mine_p = (pending >> lane) & 1u;
@@ -301,9 +317,6 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
     const uint32_t mnb = (md + 31u) >> 5;
     // ---- one round trip: the targets, every link of the chain under the guess that it is physically
     // consecutive (bulk-built and ring-popped chains are), and the first blocks on their way to L2
-    uint32_t tg[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) tg[q] = (32u * q + lane < mk) ? batch_value(b, mes + 32u * q + lane) : kTomb;
     uint32_t nx[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -315,6 +328,10 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
       const unsigned long long hh = (unsigned long long)h0 + 32u * q + lane;
       if (32u * q + lane < mnb && hh < g.ring_cap) prefetch_l2(g.slab + hh * 32u);
     }
+    wait_scatter(op, scatter_expected);
+    uint32_t tg[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tg[q] = (32u * q + lane < mk) ? batch_value(b, mes + 32u * q + lane) : kTomb;
     // ---- table (2^tb >= 2 k entries, at least 32: sized to the source) + 4096-bit membership filter of the targets
     const int tb = max(5, 32 - __clz(2u * mk - 1u));
     const uint32_t tmask = (1u << tb) - 1u;
@@ -514,17 +531,21 @@ fused_delete_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ run_c
   tally_flush(tally, t_matched, t_slots, t_blocks, t_moves, t_pushed);
 }
 
-// folds the striped tallies into the op words and the live-edge count (graph.hpp:211-213)
+// folds the striped tallies into the op words and the live-edge count (graph.hpp:211-213); one warp per
+// counter, two stripes per lane, every word handed back zeroed (the buffer is persistent)
 __global__ void fused_tally_kernel(GraphView g, unsigned long long* __restrict__ tally, OpState* op) {
   if (op->err) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;   // blockDim = 5 warps
   unsigned long long v = 0;
-  const int w = threadIdx.x;   // one thread per tally word
-  if (w < 5)
-    for (uint32_t s = 0; s < kTallyStripes; ++s) {
-      v += tally[(size_t)s * kTalWords + w];
-      tally[(size_t)s * kTalWords + w] = 0ull;   // handed back zeroed (persistent buffer)
-    }
-  if (v == 0) return;
+#pragma unroll
+  for (uint32_t s = lane; s < kTallyStripes; s += 32) {
+    unsigned long long* p = &tally[(size_t)s * kTalWords + w];
+    v += *p;
+    *p = 0ull;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+  if (lane != 0 || v == 0) return;
   if (w == kTalMatched) {
     atomicAdd(&op->matched, v);
     atomicAdd(&g.st->active_edges, (unsigned long long)(-(long long)v));

@@ -318,6 +318,12 @@ group_scatter_kernel(GraphView g, GroupIndex gi, const uint32_t* __restrict__ sr
       if (kWithIndex) out_index[pos[q]] = base + q * 256;
     }
   }
+  // consumers that started beside this kernel (fused_delete_kernel) wait for the count of finished CTAs
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&op->scatter_ctas, 1u);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1268,7 +1274,7 @@ __device__ __forceinline__ uint32_t run_tag(const BatchView& b, uint32_t r) {
   if (b.run_start == nullptr) return r;
   return (run_len(b, r) > kTinyTargets) ? (r | kTierBit) : r;
 }
-constexpr uint32_t kLongChunk = 256;     // blocks per CTA item of the long path
+constexpr uint32_t kLongChunk = 1024;    // blocks per CTA item of the long path (the table is built once per item: 256 measured 39 us for the tier at C2)
 
 // ---- sources a single warp owns for the whole delete (dg_fused.cuh) ----
 // class of a touched source, stored in wl_off[r] (real work-list offsets are < 2^31)
