@@ -4,14 +4,19 @@
     python bench.py --gpus N --steps K --warmup W            # the CUDA path (this repo)
     python bench.py --impl reference --gpus N --steps K ...  # the reference's CPU path
 
-One STEP = one pass of the hot path over one batch: `dg_insert_batch_coo` of a
-1M-pair R-MAT batch followed by `dg_delete_batch_coo` of the same batch, on a
-graph bulk-built from the 16*2^22-edge R-MAT base (so a step processes 2*batch
-edge updates and the graph keeps its size from step to step).  Every step uses
-a distinct batch.  Printed: ONE JSON line (rank 0).
+One STEP = one pass of the hot path over one batch: the insert of a 1M-pair
+R-MAT batch followed by the delete of the same batch, on a graph bulk-built from
+the 16*2^22-edge R-MAT base (so a step processes 2*batch edge updates and the
+graph keeps its size from step to step).  Every step uses a distinct batch.
+Printed: ONE JSON line (rank 0).
 
   value      whole-job Medges/s with the batch already resident in HBM
-             (CUDA events on the graph's stream, sum over the K steps, max over ranks)
+             (CUDA events on the graph's stream, sum over the K steps, max over ranks);
+             the two ops of a step are SUBMITTED (`dg_submit_insert_coo`,
+             `dg_submit_delete_coo`: validated and applied on the device in stream order,
+             no host wait between them) and flushed inside the step's bracket;
+             `sync_calls` is the same pass through `dg_insert_batch_coo` /
+             `dg_delete_batch_coo` (one host wait per op)
   e2e        the same steps through the public API with HOST (pinned) batches:
              the H2D copy of the pairs and the D2H read of the op status are inside
              the timed region
@@ -456,20 +461,26 @@ def run_b200_arm(args):
                 host_batches.append((hs.numpy().view(np.uint32), hd.numpy().view(np.uint32)))
         target = sharded if sharded is not None else g
 
-        def step(i, host=False, reports=False):
+        def step(i, host=False, reports=False, submit=False):
             s, d = (host_batches if host else batches)[i]
             if host and sharded is not None:   # the sharded API takes device tensors: the H2D copy is explicit
                 s = torch.from_numpy(s.view(np.int32)).to(dev, non_blocking=True)
                 d = torch.from_numpy(d.view(np.int32)).to(dev, non_blocking=True)
+            if submit:   # dg_submit_*_coo: both ops enqueued without a host wait; the caller flushes
+                g.submit_insert_pairs(s, d)
+                g.submit_delete_pairs(s, d)
+                return None, None
             target.insert_pairs(s, d)
             r_ins = g.last_op_report() if reports else None   # (kept out of the timed passes: host work between ops)
             target.delete_pairs(s, d)
             return r_ins, (g.last_op_report() if reports else None)
 
-        def timed_pass(host: bool):
+        def timed_pass(host: bool, submit: bool = False):
             """W warm-up + K timed steps; returns (sum of per-step device ms, per-step list, reports)."""
             for i in range(W):
-                step(i, host)
+                step(i, host, submit=submit)
+            if submit:
+                g.flush()
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
@@ -479,8 +490,10 @@ def run_b200_arm(args):
                 flush.zero_()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                reps.append(step(i, host))
+                reps.append(step(i, host, submit=submit))
                 e1.record(stream)
+                if submit:
+                    assert g.flush() == 2   # both status read-backs are inside the bracket; raises if an op failed
                 e1.synchronize()
                 per.append(e0.elapsed_time(e1))
             if world > 1:
@@ -506,7 +519,15 @@ def run_b200_arm(args):
 
         clocks = ClockSampler(local)
         clocks.start()
-        total_ms, per_step, _, wall_ms = timed_pass(host=False)
+        # headline: the two ops of a step SUBMITTED back to back (no host round trip between insert and delete);
+        # the same step through the synchronous calls is reported beside it
+        sync_total_ms, _, _, sync_wall_ms = timed_pass(host=False)
+        if sharded is None:
+            total_ms, per_step, _, wall_ms = timed_pass(host=False, submit=True)
+            value_api = "dg_submit_insert_coo + dg_submit_delete_coo per step, dg_flush per step (device-resident batches)"
+        else:
+            total_ms, per_step, wall_ms = sync_total_ms, None, sync_wall_ms
+            value_api = "ShardedDynamicGraph.insert_pairs / delete_pairs (synchronous per op)"
         reps = [step(i, reports=True) for i in range(W, W + K)]   # same batches again, untimed: op reports
         launches = sum(r[0]["kernel_launches"] + r[1]["kernel_launches"] for r in reps)
         ins_ms, del_ms = split_pass()
@@ -609,7 +630,10 @@ def run_b200_arm(args):
                   "max_degree": final_st["max_degree"], "digest": f"{digest[0]:016x}",
                   "pool_blocks_created": final_st["pool_blocks_created"], "growth_count": final_st["growth_count"],
                   "memory": g.memory()},
-        "wall_ms_per_step": wall_ms / K,
+        "wall_ms_per_step": wall_ms / K, "value_api": value_api,
+        "sync_calls": {"value": 2 * b * world * K / (sync_total_ms * 1e-3) / 1e6, "ms_per_step": sync_total_ms / K,
+                       "wall_ms_per_step": sync_wall_ms / K,
+                       "api": "dg_insert_batch_coo + dg_delete_batch_coo (one host wait per op)"},
         "bulk_init_kernels_us": bulk_kernels, "clocks": clock_rec, "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
     }
     parity_failed = False

@@ -409,6 +409,36 @@ int dg_ingest_insert(dg_ingest* q, uint32_t slot);
 int dg_ingest_delete(dg_ingest* q, uint32_t slot);
 /* drop every staged batch (after a failed op: the reference loop would have stopped there) */
 int dg_ingest_reset(dg_ingest* q);
+/* the same ops SUBMITTED (see below): no host wait, the slot is handed back by an event on the graph's stream;
+ * the host arrays must stay valid until a later dg_flush returned (or depth + 8 more batches were submitted) */
+int dg_ingest_submit_insert(dg_ingest* q, uint32_t slot, uint64_t* ticket);
+int dg_ingest_submit_delete(dg_ingest* q, uint32_t slot, uint64_t* ticket);
+
+/* ---- submitted updates: insert_batch / delete_batch without a host round trip per batch -------
+ *
+ * The reference's callers apply batches in a loop (io/workload.hpp:141-155): each call validates, mutates
+ * and returns or throws before the next one starts (graph.hpp:167-188, :195-222).  The synchronous entry
+ * points above keep that shape and pay one host wait per batch, during which the GPU idles.
+ * dg_submit_insert_coo / dg_submit_delete_coo enqueue the same op on the graph's stream and return at once;
+ * dg_flush waits for everything submitted and returns the FIRST failure (DG_OK when every op applied).
+ * The reference's contract is kept on the device: an op submitted behind one that failed does not run (every
+ * kernel of it returns at its first line) — a failed batch is reported before anything after it mutates
+ * (graph.hpp:168-171).  After a failure dg_flush sets *n_applied to the number of submitted ops that were
+ * applied since the previous dg_flush: exactly the ops before the failed one; the caller may fix the batch and
+ * submit again from there.  Until the failure has been returned (by dg_flush, or by the next synchronous call
+ * of any kind, which returns it INSTEAD of running) further submits are refused with the same status.
+ * `src` / `dst` are DEVICE arrays that must stay valid until the op has been flushed.  *ticket (optional)
+ * receives the op's sequence number, 0 when the call ran the op synchronously: when the host cannot bound
+ * what it would otherwise decide between two ops (pool underflow -> growth, block_pool.hpp:177-189; the growth
+ * trigger, :162-172; sharded stores; a graph without a pool yet) the call waits for what is in flight and runs
+ * the op the synchronous way — outcomes never differ, only the overlap is lost.  Every other entry point first
+ * waits for the submitted ops, so mixing is safe.  At most 7 submitted ops are in flight; one more submit waits
+ * for the oldest.
+ */
+int dg_submit_insert_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, uint64_t* ticket);
+int dg_submit_delete_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, uint64_t* ticket);
+int dg_flush(dg_graph* h, uint64_t* n_applied);
+uint64_t dg_pending_ops(const dg_graph* h);
 
 #ifdef __cplusplus
 }

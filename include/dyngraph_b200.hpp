@@ -145,6 +145,24 @@ class DynamicGraph {
     check(dg_delete_batch_coo(h_, src, dst, n, mem));
   }
 
+  // the same two operators SUBMITTED: device arrays, no host wait per batch (dg_submit_*_coo); flush() waits for
+  // all of them, throws the first failure and returns how many were applied (ops behind a failed one are not)
+  std::uint64_t submit_insert_pairs(const VertexId* src_dev, const VertexId* dst_dev, std::uint64_t n) {
+    std::uint64_t ticket = 0;
+    check(dg_submit_insert_coo(h_, src_dev, dst_dev, n, &ticket));
+    return ticket;
+  }
+  std::uint64_t submit_delete_pairs(const VertexId* src_dev, const VertexId* dst_dev, std::uint64_t n) {
+    std::uint64_t ticket = 0;
+    check(dg_submit_delete_coo(h_, src_dev, dst_dev, n, &ticket));
+    return ticket;
+  }
+  std::uint64_t flush() {
+    std::uint64_t applied = 0;
+    check(dg_flush(h_, &applied));
+    return applied;
+  }
+
   // graph.hpp:228-241
   bool query_edge(VertexId source, VertexId destination) const {
     std::uint8_t out = 0;
@@ -231,7 +249,10 @@ class DynamicGraph {
 // host arrays must stay valid until their op ran.
 class BatchIngest {
  public:
-  BatchIngest(DynamicGraph& g, std::uint64_t max_entries, std::uint32_t depth = 2) : g_(g), depth_(depth) {
+  // synchronous: one host wait per op (dg_ingest_insert / _delete); otherwise ops are SUBMITTED
+  // (dg_ingest_submit_*): copies, ops and the host loop overlap, failures surface at a later submit() or flush()
+  BatchIngest(DynamicGraph& g, std::uint64_t max_entries, std::uint32_t depth = 2, bool synchronous = false)
+      : g_(g), depth_(depth), sync_(synchronous) {
     if (dg_ingest_create(g.handle(), max_entries, depth, &q_) != DG_OK) throw EngineError(dg_last_error(g.handle()));
   }
   ~BatchIngest() { dg_ingest_destroy(q_); }
@@ -239,18 +260,41 @@ class BatchIngest {
   BatchIngest& operator=(const BatchIngest&) = delete;
 
   void submit(BatchKind kind, const VertexId* src, const VertexId* dst, std::uint64_t n) {
-    if (pending_.size() == depth_) run_oldest();
+    if (sync_ && pending_.size() == depth_) run_oldest();
     std::uint32_t slot = 0;
-    const int rc = dg_ingest_stage_coo(q_, src, dst, n, &slot);
+    int rc = dg_ingest_stage_coo(q_, src, dst, n, &slot);
     if (rc != DG_OK) raise(rc);
-    pending_.emplace_back(kind, slot);
-    if (pending_.size() == depth_) run_oldest();
+    if (sync_) {
+      pending_.emplace_back(kind, slot);
+      if (pending_.size() == depth_) run_oldest();
+      return;
+    }
+    rc = kind == BatchKind::Insert ? dg_ingest_submit_insert(q_, slot, nullptr) : dg_ingest_submit_delete(q_, slot, nullptr);
+    if (rc != DG_OK) {
+      const std::string msg = dg_last_error(g_.handle()) ? dg_last_error(g_.handle()) : "";
+      dg_ingest_reset(q_);
+      collect();
+      if (rc == DG_ERR_DATA) throw DataError(msg);
+      throw EngineError(msg);
+    }
   }
+  // waits for everything submitted; throws the first failure; applied() counts the batches that went in
   void flush() {
     while (!pending_.empty()) run_oldest();
+    if (!sync_) {
+      const int rc = collect();
+      if (rc != DG_OK) raise(rc);
+    }
   }
+  std::uint64_t applied() const { return applied_; }
 
  private:
+  int collect() {
+    std::uint64_t n = 0;
+    const int rc = dg_flush(g_.handle(), &n);
+    applied_ += n;
+    return rc;
+  }
   void run_oldest() {
     const auto [kind, slot] = pending_.front();
     pending_.erase(pending_.begin());
@@ -262,6 +306,7 @@ class BatchIngest {
       if (rc == DG_ERR_DATA) throw DataError(msg);
       throw EngineError(msg);
     }
+    ++applied_;
   }
   [[noreturn]] void raise(int rc) const {
     const char* msg = dg_last_error(g_.handle());
@@ -271,6 +316,8 @@ class BatchIngest {
   DynamicGraph& g_;
   dg_ingest* q_ = nullptr;
   std::uint32_t depth_;
+  bool sync_;
+  std::uint64_t applied_ = 0;
   std::vector<std::pair<BatchKind, std::uint32_t>> pending_;
 };
 

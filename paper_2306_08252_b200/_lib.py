@@ -118,6 +118,12 @@ SIGNATURES = {
     "dg_ingest_insert": (C.c_int, [C.c_void_p, C.c_uint32]),
     "dg_ingest_delete": (C.c_int, [C.c_void_p, C.c_uint32]),
     "dg_ingest_reset": (C.c_int, [C.c_void_p]),
+    "dg_ingest_submit_insert": (C.c_int, [C.c_void_p, C.c_uint32, u64p]),
+    "dg_ingest_submit_delete": (C.c_int, [C.c_void_p, C.c_uint32, u64p]),
+    "dg_submit_insert_coo": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
+    "dg_submit_delete_coo": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
+    "dg_flush": (C.c_int, [_H, u64p]),
+    "dg_pending_ops": (C.c_uint64, [_H]),
 }
 
 _lib = None

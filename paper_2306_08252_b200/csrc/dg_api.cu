@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -162,8 +163,32 @@ struct dg_graph {
   VmRange vm_slab, vm_next;
 
   DevBlock* d_blk = nullptr;  // device
-  DevBlock* h_blk = nullptr;  // pinned host mirror
-  uint64_t front = 0, rear = 0, active_edges = 0;
+  DevBlock* h_blk = nullptr;  // pinned host mirror of the CURRENT op: one slot of h_ring
+  DevBlock* h_ring = nullptr; // pinned status slots: every op reads back into its own, so submitted ops need no host wait
+  uint32_t h_ring_next = 0;
+  uint64_t front = 0, rear = 0, active_edges = 0;   // as of the last RETIRED op
+
+  // Submitted (asynchronous) ops, oldest first: enqueued on the stream, status not yet looked at.
+  struct Pending {
+    uint64_t ticket;
+    bool is_insert;
+    uint64_t pop_bound;   // most blocks the op can pop (inserts)
+    DevBlock* slot;       // where its {DeviceState, OpState} lands
+    cudaEvent_t done;     // recorded behind the read-back
+    uint64_t launches;
+    uint64_t n;
+  };
+  std::deque<Pending> pending;
+  std::vector<cudaEvent_t> done_pool;
+  bool submitting = false;        // the op being enqueued ends without a host wait (op_end)
+  bool submit_is_insert = false;
+  uint64_t submit_pop_bound = 0;
+  uint64_t next_ticket = 1;
+  uint64_t pending_pop_bound = 0; // sum over `pending`
+  uint64_t submitted_applied = 0; // submitted ops retired successfully since the last dg_flush
+  int deferred_rc = 0;            // first failure among retired submitted ops, not yet returned to the caller
+  uint64_t deferred_ticket = 0;
+  std::string deferred_error;
 
   Workspace ws;
   // compaction scratch (grown on demand, survives workspace resets)
@@ -208,7 +233,8 @@ struct dg_graph {
   DeviceState* d_state() const { return &d_blk->st; }
   OpState* d_op() const { return &d_blk->op; }
   uint64_t dst_limit() const { return dst_limit_override ? dst_limit_override : size; }
-  uint64_t blocks_in_use() const { return NB - (rear - front); }
+  // (an upper bound while submitted inserts are in flight: sizes work lists, never read as a count)
+  uint64_t blocks_in_use() const { return std::min<uint64_t>(NB, NB - (rear - front) + pending_pop_bound); }
   bool alive_h(uint64_t v) const { return v < size && ((alive_host[v >> 6] >> (v & 63)) & 1ull); }
 };
 
@@ -477,7 +503,16 @@ uint32_t* acquire_cnt(dg_graph* h, bool self_cleaning) {
 }
 
 // ---- op bracket -----------------------------------------------------------
+constexpr uint32_t kStatusSlots = 8;   // pinned {DeviceState, OpState} slots: at most kStatusSlots - 1 submitted ops in flight
+int retire_oldest(dg_graph* h, bool wait);
+
 int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
+  // a slot of the pinned status ring nobody is still waiting on
+  while (h->pending.size() >= kStatusSlots - 1) {
+    const int rc = retire_oldest(h, /*wait=*/true);
+    if (rc != DG_OK) return rc;
+  }
+  h->h_blk = &h->h_ring[h->h_ring_next++ % kStatusSlots];
   OpState& op = h->h_blk->op;
   std::memset(&op, 0, sizeof(op));
   op.err_index = ~0ull;
@@ -487,8 +522,14 @@ int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
   op.n_input = n_input;  // device-resident copy of the input length for scans
   op.n_aux = h->size + 1;
   tl_mark(h, "begin", h->stream);
-  DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
-  h->launches = 0;
+  if (h->submitting) {
+    // the op words are installed by a kernel that first looks at what the previous submitted op left behind
+    op_arm_kernel<<<1, 1, 0, h->stream>>>(op, h->d_state(), h->d_op(), h->pending.empty() ? 0 : 1);
+    DG_CUDA(h, cudaPeekAtLastError());
+  } else {
+    DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
+  }
+  h->launches = h->submitting ? 1 : 0;   // (op_arm_kernel)
   h->zslot = 0;
   if (!h->zscratch_clean) {
     DG_CUDA(h, cudaMemsetAsync(h->zscratch, 0, kZScratchWords * sizeof(unsigned long long), h->stream));
@@ -517,10 +558,60 @@ const char* detail_text(uint32_t d) {
   }
 }
 
-// read back {DeviceState, OpState}; translate a device-side error
+// the host-side conclusion of an op from its status slot: mirrors, report, device-side error
+int op_conclude(dg_graph* h, const DevBlock& blk, uint64_t n_input, uint64_t launches) {
+  const DeviceState& st = blk.st;
+  const OpState& op = blk.op;
+  h->report = dg_op_report{};
+  h->report.batch_entries = n_input;
+  h->report.touched_sources = op.n_runs;
+  h->report.blocks_popped = op.total_need;
+  h->report.blocks_pushed = op.pushed;
+  h->report.slots_scanned = op.slots;
+  h->report.blocks_scanned = op.wl_blocks + op.fused_blocks;
+  h->report.slots_scanned_fused = op.slots_fused;
+  h->report.matched = op.matched;
+  h->report.moved = op.moves;
+  h->report.kernel_launches = launches;
+  h->report.slots_scanned_long = op.slots_long;
+  h->report.slots_scanned_tiny = op.slots_tiny;
+  h->front = st.front;
+  h->rear = st.rear;
+  h->active_edges = st.active_edges;
+  if (op.err != 0) {
+    h->zscratch_clean = false;   // kernels of a rejected op return early: cursors / tallies may be left behind
+    h->cnt_clean = false;
+    h->report.blocks_popped = 0;
+    if (op.err_detail == kErrPoolUnderflow) h->last_shortfall = op.err_index;
+    if (op.err_detail == kErrSkipped)
+      return fail(h, (int)op.err, "not applied: an op submitted before this one failed");
+    return fail(h, (int)op.err,
+                std::string(op.err == DG_ERR_DATA ? "csr batch: " : "block pool: ") +
+                    detail_text(op.err_detail) + " (index " + std::to_string(op.err_index) + ")");
+  }
+  h->total_capacity += op.pushed;   // every re-push counts (block_pool.hpp:56-61)
+  return DG_OK;
+}
+
+// read back {DeviceState, OpState}; translate a device-side error.  A submitted op only enqueues the read-back
+// (into its own pinned slot) and an event: its status is looked at when it is retired.
 int op_end(dg_graph* h) {
   tl_mark(h, "end", h->stream);
   DG_CUDA(h, cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(DevBlock), cudaMemcpyDeviceToHost, h->stream));
+  if (h->submitting && h->launch_error == cudaSuccess && !h->ws_overflow) {
+    cudaEvent_t ev = nullptr;
+    if (!h->done_pool.empty()) {
+      ev = h->done_pool.back();
+      h->done_pool.pop_back();
+    } else {
+      DG_CUDA(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    DG_CUDA(h, cudaEventRecord(ev, h->stream));
+    h->pending.push_back(dg_graph::Pending{h->next_ticket++, h->submit_is_insert, h->submit_pop_bound, h->h_blk, ev,
+                                           h->launches, h->report.batch_entries});
+    h->pending_pop_bound += h->submit_pop_bound;
+    return DG_OK;
+  }
   DG_CUDA(h, cudaStreamSynchronize(h->stream));
   DG_CUDA(h, cudaGetLastError());
   if (h->profiling) prof_collect(h);
@@ -536,33 +627,74 @@ int op_end(dg_graph* h) {
     h->zscratch_clean = h->cnt_clean = false;
     return fail(h, DG_ERR_ENGINE, "internal: per-op workspace was sized too small; the batch was not applied");
   }
-  const DeviceState& st = h->h_blk->st;
-  const OpState& op = h->h_blk->op;
-  h->front = st.front;
-  h->rear = st.rear;
-  h->active_edges = st.active_edges;
-  h->report.touched_sources = op.n_runs;
-  h->report.blocks_popped = op.total_need;
-  h->report.blocks_pushed = op.pushed;
-  if (op.err == 0) h->total_capacity += op.pushed;   // every re-push counts (block_pool.hpp:56-61)
-  h->report.slots_scanned = op.slots;
-  h->report.blocks_scanned = op.wl_blocks + op.fused_blocks;
-  h->report.slots_scanned_fused = op.slots_fused;
-  h->report.matched = op.matched;
-  h->report.moved = op.moves;
-  h->report.kernel_launches = h->launches;
-  h->report.slots_scanned_long = op.slots_long;
-  h->report.slots_scanned_tiny = op.slots_tiny;
-  if (op.err != 0) {
-    h->zscratch_clean = false;   // kernels of a rejected op return early: cursors / tallies may be left behind
-    h->cnt_clean = false;
-    h->report.blocks_popped = 0;
-    if (op.err_detail == kErrPoolUnderflow) h->last_shortfall = op.err_index;
-    return fail(h, (int)op.err,
-                std::string(op.err == DG_ERR_DATA ? "csr batch: " : "block pool: ") +
-                    detail_text(op.err_detail) + " (index " + std::to_string(op.err_index) + ")");
+  return op_conclude(h, *h->h_blk, h->report.batch_entries, h->launches);
+}
+
+// ---- submitted ops: retire / drain ---------------------------------------------------------------
+// Looks at the oldest submitted op (waiting for it when `wait`): folds its outcome into the host mirrors, or
+// records the pipeline's first failure (returned once, by dg_flush or by the next synchronous call).
+// Returns DG_OK when an op was retired or nothing is ready; DG_ERR_CUDA on a runtime error.
+int retire_oldest(dg_graph* h, bool wait) {
+  if (h->pending.empty()) return DG_OK;
+  dg_graph::Pending p = h->pending.front();
+  if (wait) {
+    DG_CUDA(h, cudaEventSynchronize(p.done));
+  } else {
+    const cudaError_t q = cudaEventQuery(p.done);
+    if (q == cudaErrorNotReady) return DG_OK;
+    DG_CUDA(h, q);
+  }
+  h->pending.pop_front();
+  h->pending_pop_bound -= p.pop_bound;
+  h->done_pool.push_back(p.done);
+  if (h->deferred_rc != DG_OK) return DG_OK;   // (queued behind the failure: skipped on the device, nothing to fold in)
+  const std::string keep = h->last_error;
+  const int rc = op_conclude(h, *p.slot, p.n, p.launches);
+  if (rc == DG_OK) {
+    ++h->submitted_applied;
+    if (p.is_insert) h->consumed += h->report.blocks_popped;   // (submit made sure this stays below the growth trigger)
+    h->last_error = keep;
+  } else {
+    h->deferred_rc = rc;
+    h->deferred_ticket = p.ticket;
+    h->deferred_error = "submitted op #" + std::to_string(p.ticket) + " failed: " + h->last_error +
+                        "; ops submitted after it were not applied";
+    h->last_error = keep;
   }
   return DG_OK;
+}
+// waits for every submitted op
+int drain(dg_graph* h) {
+  while (!h->pending.empty()) {
+    const int rc = retire_oldest(h, /*wait=*/true);
+    if (rc != DG_OK) return rc;
+  }
+  return DG_OK;
+}
+// returns (once) the failure of a submitted op
+int take_deferred(dg_graph* h) {
+  if (h->deferred_rc == DG_OK) return DG_OK;
+  const int rc = h->deferred_rc;
+  h->last_error = h->deferred_error;
+  h->deferred_rc = DG_OK;
+  h->deferred_error.clear();
+  return rc;
+}
+// Every synchronous entry point starts here: nothing submitted is left in flight, and an unreported failure of
+// a submitted op is returned INSTEAD of running the call (the caller learns about it before anything else mutates).
+int enter(dg_graph* h) {
+  cudaSetDevice(h->device);
+  if (h->pending.empty() && h->deferred_rc == DG_OK) return DG_OK;
+  const int rc = drain(h);
+  if (rc != DG_OK) return rc;
+  return take_deferred(h);
+}
+// accessors that cannot return a status: drained state, the failure (if any) stays for the next status call
+void enter_quiet(const dg_graph* ch) {
+  dg_graph* h = const_cast<dg_graph*>(ch);
+  if (h->pending.empty()) return;
+  cudaSetDevice(h->device);
+  drain(h);
 }
 
 // ---- scan / sort launchers -------------------------------------------------
@@ -717,7 +849,7 @@ int create_pool(dg_graph* h, uint32_t B) {
   h->h_blk->st.front = 0;
   h->h_blk->st.rear = nb;
   h->h_blk->st.active_edges = h->active_edges;
-  h->h_blk->st.pad = 0;
+  h->h_blk->st.poison = 0;
   DG_CUDA(h, cudaMemcpyAsync(h->d_state(), &h->h_blk->st, sizeof(DeviceState), cudaMemcpyHostToDevice, h->stream));
   DG_CUDA(h, cudaStreamSynchronize(h->stream));
   h->front = 0;
@@ -794,14 +926,15 @@ int insert_with_growth(dg_graph* h, F&& run) {
 int ensure_mv_scratch(dg_graph* h, uint64_t entries) {
   if (entries <= h->mv_cap) return DG_OK;
   DG_CUDA(h, cudaStreamSynchronize(h->stream));
-  if (h->mv_hole) cudaFree(h->mv_hole);
-  h->mv_hole = nullptr;
-  h->mv_cap = 0;
+  // (the old scratch is only given up once the new one exists: a failed allocation leaves the graph usable)
   const uint64_t want = entries + entries / 4 + 1024;
-  if (cudaMalloc(&h->mv_hole, want * sizeof(unsigned long long)) != cudaSuccess) {
+  unsigned long long* fresh = nullptr;
+  if (cudaMalloc(&fresh, want * sizeof(unsigned long long)) != cudaSuccess) {
     cudaGetLastError();
     return fail(h, DG_ERR_ENGINE, "compaction scratch: device allocation failed");
   }
+  if (h->mv_hole) cudaFree(h->mv_hole);
+  h->mv_hole = fresh;
   h->mv_cap = want;
   return DG_OK;
 }
@@ -1229,6 +1362,7 @@ int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs
     }
     const int rc = op_end(h);
     if (rc != DG_OK) return rc;
+    if (h->submitting) return DG_OK;   // (submit_coo sized the scratch for the worst case: no retry to decide on)
     if (h->h_blk->op.aux1 == 0) return DG_OK;
     // compaction scratch was too small: nothing past the tombstones was touched; grow and redo
     const int rc2 = ensure_mv_scratch(h, h->h_blk->op.aux0);
@@ -1323,11 +1457,12 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
       cudaMalloc(&h->deg, h->capacity * 4) != cudaSuccess ||
       cudaMalloc(&h->alive, words * 4) != cudaSuccess ||
       cudaMalloc(&h->d_blk, sizeof(DevBlock)) != cudaSuccess ||
-      cudaMallocHost(&h->h_blk, sizeof(DevBlock)) != cudaSuccess) {
+      cudaMallocHost(&h->h_ring, kStatusSlots * sizeof(DevBlock)) != cudaSuccess) {
     cudaGetLastError();
     return bail(DG_ERR_ENGINE, "vertex dictionary: device allocation failed");
   }
-  std::memset(h->h_blk, 0, sizeof(DevBlock));
+  std::memset(h->h_ring, 0, kStatusSlots * sizeof(DevBlock));
+  h->h_blk = &h->h_ring[0];
   cudaMemsetAsync(h->d_blk, 0, sizeof(DevBlock), h->stream);
   cudaMemsetAsync(h->head, 0xFF, h->capacity * 4, h->stream);
   cudaMemsetAsync(h->tail, 0xFF, h->capacity * 4, h->stream);
@@ -1368,6 +1503,7 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
 void dg_destroy(dg_graph* h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  if (h->h_ring) drain(h);
   if (h->stream) cudaStreamSynchronize(h->stream);
   cudaFree(h->head);
   cudaFree(h->tail);
@@ -1382,7 +1518,9 @@ void dg_destroy(dg_graph* h) {
   }
   cudaFree(h->ring);
   cudaFree(h->d_blk);
-  if (h->h_blk) cudaFreeHost(h->h_blk);
+  if (h->h_ring) cudaFreeHost(h->h_ring);
+  for (auto& pd : h->pending) cudaEventDestroy(pd.done);
+  for (auto e : h->done_pool) cudaEventDestroy(e);
   cudaFree(h->ws.base);
   cudaFree(h->mv_hole);
   cudaFree(h->cnt_buf);
@@ -1408,7 +1546,8 @@ static int insert_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
   h->last_shortfall = 0;
-  cudaSetDevice(h->device);
+  if (h->submitting) cudaSetDevice(h->device);
+  else if (const int erc = enter(h)) return erc;
   if (n == 0) return DG_OK;  // EmptyBatchChangesNothing
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
@@ -1487,7 +1626,7 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
   h->last_shortfall = 0;
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   if (n_offsets != h->size + 1)  // csr.hpp:50-53
     return fail(h, DG_ERR_DATA, "csr batch: offsets length " + std::to_string(n_offsets) +
                                     " does not match vertex count " + std::to_string(h->size) + " + 1");
@@ -1577,7 +1716,8 @@ int dg_bulk_init_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
 static int delete_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, int mem, bool check_only) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (h->submitting) cudaSetDevice(h->device);
+  else if (const int erc = enter(h)) return erc;
   if (n == 0) return DG_OK;
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (h->size == 0) return fail(h, DG_ERR_DATA, "csr batch: source id out of range (graph has no vertices)");
@@ -1603,6 +1743,89 @@ int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
   return delete_coo_impl(h, src, dst, n, mem, false);
 }
 
+// ---- submitted (asynchronous) COO updates ----------------------------------------------------------
+// The op is enqueued and the call returns without waiting for it: its status lands in a pinned slot and is
+// looked at by a later submit / dg_flush / any synchronous call.  Everything the host decides BETWEEN ops in
+// the synchronous path is decided here from bounds, before the enqueue; when a bound does not hold the call
+// simply runs the op the synchronous way (after waiting for what is in flight), so the outcome never differs:
+//   - ensure_available (block_pool.hpp:177-189): the free handles known to the host minus what the inserts
+//     in flight can pop at most must cover this insert (an insert pops at most one block per entry);
+//   - commit_front's growth rule (block_pool.hpp:162-172): cumulative consumption, counted with the same
+//     bounds, must stay below the trigger — the pool never has to grow behind a submitted op;
+//   - compaction scratch of the hub path of a delete: moves <= live edges / 2, allocated up front.
+static int submit_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, bool is_insert, uint64_t* ticket) {
+  if (!h) return DG_ERR_DATA;
+  if (ticket) *ticket = 0;
+  cudaSetDevice(h->device);
+  if (h->deferred_rc != DG_OK) {   // an earlier submitted op failed: report it before anything else is queued
+    const int rc = drain(h);
+    return rc != DG_OK ? rc : take_deferred(h);
+  }
+  while (!h->pending.empty()) {    // fold in whatever has finished: keeps the bounds tight
+    const size_t before = h->pending.size();
+    const int rc = retire_oldest(h, /*wait=*/false);
+    if (rc != DG_OK) return rc;
+    if (h->pending.size() == before) break;
+  }
+  if (h->deferred_rc != DG_OK) {
+    const int rc = drain(h);
+    return rc != DG_OK ? rc : take_deferred(h);
+  }
+  bool async_ok = h->B != 0 && h->slab != nullptr && !h->profiling && !h->timeline && h->agree_x == nullptr && n > 0;
+  if (async_ok && is_insert) {
+    const uint64_t free_known = h->rear - h->front;
+    if (free_known < h->pending_pop_bound + n) async_ok = false;
+    if (h->pool_vm && h->total_capacity > 0 &&
+        (double)(h->consumed + h->pending_pop_bound + n) / (double)h->total_capacity >= h->trigger)
+      async_ok = false;
+  }
+  if (async_ok && !is_insert) {
+    uint64_t live_bound = h->active_edges;
+    for (const auto& pd : h->pending)
+      if (pd.is_insert) live_bound += pd.n;
+    if (ensure_mv_scratch(h, live_bound / 2 + 1) != DG_OK) async_ok = false;
+  }
+  if (!async_ok) {
+    int rc = drain(h);
+    if (rc != DG_OK) return rc;
+    if ((rc = take_deferred(h)) != DG_OK) return rc;
+    rc = is_insert ? dg_insert_batch_coo(h, src, dst, n, DG_MEM_DEVICE) : dg_delete_batch_coo(h, src, dst, n, DG_MEM_DEVICE);
+    if (rc == DG_OK) ++h->submitted_applied;
+    return rc;
+  }
+  h->submitting = true;
+  h->submit_is_insert = is_insert;
+  h->submit_pop_bound = is_insert ? n : 0;
+  const size_t before = h->pending.size();
+  const uint64_t t = h->next_ticket;
+  const int rc = is_insert ? insert_coo_impl(h, src, dst, n, DG_MEM_DEVICE) : delete_coo_impl(h, src, dst, n, DG_MEM_DEVICE, false);
+  h->submitting = false;
+  if (rc != DG_OK) return rc;            // rejected on the host before anything was enqueued
+  if (h->pending.size() == before) {     // (the op ended synchronously after all: launch error path, workspace overflow)
+    ++h->submitted_applied;
+    return DG_OK;
+  }
+  if (ticket) *ticket = t;
+  return DG_OK;
+}
+
+int dg_submit_insert_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, uint64_t* ticket) {
+  return submit_coo(h, src, dst, n, true, ticket);
+}
+int dg_submit_delete_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, uint64_t* ticket) {
+  return submit_coo(h, src, dst, n, false, ticket);
+}
+int dg_flush(dg_graph* h, uint64_t* n_applied) {
+  if (!h) return DG_ERR_DATA;
+  cudaSetDevice(h->device);
+  int rc = drain(h);
+  if (n_applied) *n_applied = h->submitted_applied;
+  h->submitted_applied = 0;
+  if (rc != DG_OK) return rc;
+  return take_deferred(h);
+}
+uint64_t dg_pending_ops(const dg_graph* h) { return h ? h->pending.size() : 0; }
+
 int dg_check_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, int is_insert, int mem) {
   if (!h) return DG_ERR_DATA;
   if (!is_insert) return delete_coo_impl(h, src, dst, n, mem, true);
@@ -1616,7 +1839,7 @@ int dg_delete_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets
                         const uint32_t* destinations, uint64_t n_edges, int mem) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   if (n_offsets != h->size + 1)
     return fail(h, DG_ERR_DATA, "csr batch: offsets length " + std::to_string(n_offsets) +
                                     " does not match vertex count " + std::to_string(h->size) + " + 1");
@@ -1654,7 +1877,7 @@ int dg_query_edges(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64
                    uint8_t* out, int mem) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   if (n == 0) return DG_OK;
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (h->B == 0 || h->size == 0) {  // no edges stored: every answer is false
@@ -1690,7 +1913,7 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
                   uint64_t n_dst_capacity, int sorted, int mem) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   const uint64_t V = h->size;
   // phase 1: degrees -> offsets
   WsSizer sz1;
@@ -1757,7 +1980,7 @@ int dg_export_csr(dg_graph* h, uint64_t* offsets, uint32_t* destinations,
 int dg_active_destinations(dg_graph* h, uint32_t v, uint32_t* out, uint64_t capacity, uint64_t* n_out, int mem) {
   if (!h || !n_out || (capacity && !out)) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   *n_out = 0;
   if (v >= h->size || h->B == 0) return DG_OK;   // graph.hpp:118: unknown vertex -> empty
   int rc = ws_reserve(h, mem == DG_MEM_HOST ? aligned(capacity * 4) : 0);
@@ -1777,7 +2000,7 @@ int dg_active_destinations(dg_graph* h, uint32_t v, uint32_t* out, uint64_t capa
 int dg_degrees(dg_graph* h, uint64_t* out, int mem) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   const uint64_t V = h->size;
   if (V == 0) return DG_OK;
   int rc = ws_reserve(h, aligned(V * 8));
@@ -1794,7 +2017,7 @@ int dg_degrees(dg_graph* h, uint64_t* out, int mem) {
 int dg_digest(dg_graph* h, uint64_t* out_digest, uint64_t* out_entries) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   const uint64_t V = h->size;
   if (out_digest) *out_digest = 0;
   if (out_entries) *out_entries = 0;
@@ -1818,7 +2041,7 @@ int dg_digest(dg_graph* h, uint64_t* out_digest, uint64_t* out_entries) {
 int dg_insert_vertices(dg_graph* h, uint64_t count) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   if (count == 0) return DG_OK;  // InsertVertices.ZeroIsANoop
   const uint64_t new_size = h->size + count;
   if (new_size >= 0xFFFFFFFFull || new_size < h->size)
@@ -1862,7 +2085,7 @@ int dg_delete_vertices(dg_graph* h, const uint32_t* ids, uint64_t n, uint32_t* s
                        uint64_t* n_skipped) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   uint64_t ns = 0;
   std::vector<uint32_t> winners;
   winners.reserve(n);
@@ -1905,13 +2128,17 @@ uint32_t dg_block_size(const dg_graph* h) { return h ? h->B : 0; }
 uint64_t dg_logical_size(const dg_graph* h) { return h ? h->size : 0; }
 uint64_t dg_vertex_capacity(const dg_graph* h) { return h ? h->capacity : 0; }
 uint64_t dg_alive_vertices(const dg_graph* h) { return h ? h->alive_count : 0; }
-uint64_t dg_active_edges(const dg_graph* h) { return h ? h->active_edges : 0; }
+uint64_t dg_active_edges(const dg_graph* h) {
+  if (!h) return 0;
+  enter_quiet(h);
+  return h->active_edges;
+}
 int dg_vertex_alive(const dg_graph* h, uint32_t v) { return h && h->alive_h(v) ? 1 : 0; }
 
 int dg_stats_get(dg_graph* h, dg_stats* out) {
   if (!h || !out) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   std::memset(out, 0, sizeof(*out));
   int rc;
   if (h->size > 0 && h->B > 0) {
@@ -1939,6 +2166,7 @@ int dg_stats_get(dg_graph* h, dg_stats* out) {
 
 int dg_memory_get(const dg_graph* h, dg_memory* out) {
   if (!h || !out) return DG_ERR_DATA;
+  enter_quiet(h);
   out->dictionary_bytes = h->capacity * 4 + (h->capacity + 31) / 32 * 4;
   out->sentinel_bytes = h->capacity * 8;
   out->pool_bytes = h->NB ? h->blocks_in_use() * ((uint64_t)h->B * 4 + 4) : 0;
@@ -1950,13 +2178,14 @@ int dg_memory_get(const dg_graph* h, dg_memory* out) {
 
 int dg_last_op_report(const dg_graph* h, dg_op_report* out) {
   if (!h || !out) return DG_ERR_DATA;
+  enter_quiet(h);
   *out = h->report;
   return DG_OK;
 }
 
 int dg_profile_enable(dg_graph* h, int on) {
   if (!h) return DG_ERR_DATA;
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   cudaStreamSynchronize(h->stream);
   prof_collect(h);
   h->profiling = on != 0;
@@ -1980,7 +2209,7 @@ void* dg_stream(const dg_graph* h) { return h ? (void*)h->stream : nullptr; }
 
 int dg_synchronize(dg_graph* h) {
   if (!h) return DG_ERR_DATA;
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   DG_CUDA(h, cudaStreamSynchronize(h->stream));
   return DG_OK;
 }
@@ -1990,7 +2219,7 @@ int dg_compute_block_size_coo(dg_graph* h, const uint32_t* src, uint64_t n, int 
                               uint32_t* out_block_size) {
   if (!h || !out_block_size) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   if (n == 0) return fail(h, DG_ERR_DATA, "compute_block_size: first batch contains no edges");
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   SortPlan plan = make_sort_plan(0, 32);
@@ -2030,7 +2259,7 @@ int dg_gen_rmat(dg_graph* h, uint32_t scale, uint64_t seed, uint64_t first_index
                 uint32_t* dst_dev) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   if (scale == 0 || scale > 32) return fail(h, DG_ERR_DATA, "rmat: scale must be in [1, 32]");
   if (n == 0) return DG_OK;
   DG_LAUNCH(h, "rmat_kernel", rmat_kernel<<<grid_for(h, n, 256 * 4), 256, 0, h->stream>>>(scale, seed, first_index, n, thr_a,
@@ -2043,7 +2272,7 @@ int dg_coo_to_csr(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_
                   uint64_t vertex_count, uint64_t* offsets_dev, uint32_t* destinations_dev) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   if (n >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
   if (vertex_count == 0 || vertex_count >= 0xFFFFFFFFull)
     return fail(h, DG_ERR_DATA, "coo_to_csr: bad vertex count");
@@ -2090,7 +2319,7 @@ int dg_route_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t
                  uint32_t* out_index, uint64_t* counts_host) {
   if (!h) return DG_ERR_DATA;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   if (world == 0 || world > 65536) return fail(h, DG_ERR_DATA, "route: world must be in [1, 65536]");
   if (bits > 32 || vertex_count > (bits >= 32 ? (1ull << 32) : (1ull << bits)))
     return fail(h, DG_ERR_DATA, "route: vertex_count exceeds 2^bits");
@@ -2165,7 +2394,7 @@ int dg_exchange_create(dg_graph* h, uint32_t rank, uint32_t world, uint64_t capa
   if (!h || !out) return DG_ERR_DATA;
   *out = nullptr;
   h->last_error.clear();
-  cudaSetDevice(h->device);
+  if (const int erc = enter(h)) return erc;
   if (world == 0 || world > (uint32_t)kMaxPeers || rank >= world)
     return fail(h, DG_ERR_DATA, "exchange: world must be in [1, 16] and rank < world");
   if (capacity == 0 || capacity >= (1ull << 31)) return fail(h, DG_ERR_DATA, "exchange: bad capacity");
@@ -2419,6 +2648,7 @@ int dg_ingest_create(dg_graph* h, uint64_t max_entries, uint32_t depth, dg_inges
 void dg_ingest_destroy(dg_ingest* q) {
   if (!q) return;
   cudaSetDevice(q->h->device);
+  drain(q->h);   // submitted ops may still read the slots
   if (q->copy) { cudaStreamSynchronize(q->copy); cudaStreamDestroy(q->copy); }
   for (auto p : q->src) cudaFree(p);
   for (auto p : q->dst) cudaFree(p);
@@ -2472,5 +2702,19 @@ int dg_ingest_reset(dg_ingest* q) {
 }
 int dg_ingest_insert(dg_ingest* q, uint32_t slot) { return ingest_run(q, slot, true); }
 int dg_ingest_delete(dg_ingest* q, uint32_t slot) { return ingest_run(q, slot, false); }
+// the same without the host wait: the op is submitted (dg_submit_*_coo), the slot is handed back by an event
+static int ingest_submit(dg_ingest* q, uint32_t slot, bool is_insert, uint64_t* ticket) {
+  if (!q || slot >= q->depth) return DG_ERR_DATA;
+  dg_graph* h = q->h;
+  cudaSetDevice(h->device);
+  if (q->state[slot] != 1) return fail(h, DG_ERR_DATA, "ingest: slot holds no staged batch");
+  DG_CUDA(h, cudaStreamWaitEvent(h->stream, q->filled[slot], 0));
+  const int rc = submit_coo(h, q->src[slot], q->dst[slot], q->n[slot], is_insert, ticket);
+  cudaEventRecord(q->freed[slot], h->stream);
+  q->state[slot] = 0;
+  return rc;
+}
+int dg_ingest_submit_insert(dg_ingest* q, uint32_t slot, uint64_t* ticket) { return ingest_submit(q, slot, true, ticket); }
+int dg_ingest_submit_delete(dg_ingest* q, uint32_t slot, uint64_t* ticket) { return ingest_submit(q, slot, false, ticket); }
 
 }  // extern "C"

@@ -36,6 +36,7 @@ enum ErrDetail : uint32_t {
   kErrPoolUnderflow = 7,  // block_pool.hpp:177-189
   kErrScratch = 8,        // internal: compaction scratch too small, host retries
   kErrPeer = 9,           // sharded store: the batch was rejected on another rank (or a peer never arrived)
+  kErrSkipped = 10,       // submitted behind an op that failed: not applied (the failed op reports first, graph.hpp:168-171)
 };
 
 // Persistent device-resident scalars of one graph (the queue cursors use the
@@ -44,7 +45,7 @@ struct DeviceState {
   unsigned long long front;         // next queue position to serve
   unsigned long long rear;          // one past the last pushed handle
   unsigned long long active_edges;  // graph.hpp:100
-  unsigned long long pad;
+  unsigned long long poison;        // != 0: a submitted op failed and has not been reported yet — ops queued behind it do not run
 };
 
 // Transient per-op words; zeroed by the host before every op.

@@ -138,6 +138,26 @@ __device__ __forceinline__ void stage_rows32(const GraphView& g, uint32_t (*dst)
 __device__ __forceinline__ uint32_t filter_hash(uint32_t x, int bits) { return (x * 0x85EBCA6Bu) >> (32 - bits); }
 
 // ---------------------------------------------------------------------------
+// submitted (asynchronous) ops: arming the op words on the device
+// ---------------------------------------------------------------------------
+// A submitted op does not wait for the host between ops, so "a failed batch reports before the next
+// one mutates" (graph.hpp:168-171) is kept on the device: the op words of the NEXT op are installed by
+// this one-thread kernel (they travel as the kernel argument — no host buffer to keep alive), which
+// first looks at the words the previous op left behind.  chain != 0: the previous op of the stream was
+// submitted too and has not been reported — if it failed (or an earlier one did: the poison word),
+// this op starts out rejected and every kernel of it returns at its first line.
+__global__ void op_arm_kernel(OpState fresh, DeviceState* st, OpState* op, int chain) {
+  if (chain && (st->poison != 0 || op->err != 0)) {
+    st->poison = 1;
+    fresh.err = 3u;   // DG_ERR_ENGINE
+    fresh.err_detail = kErrSkipped;
+  } else {
+    st->poison = 0;
+  }
+  *op = fresh;
+}
+
+// ---------------------------------------------------------------------------
 // init
 // ---------------------------------------------------------------------------
 // block_pool.hpp:242-247 pushes one handle per block; here one coalesced store.
@@ -244,6 +264,7 @@ group_count_kernel(GraphView g, GroupIndex gi, const uint32_t* __restrict__ src,
                    const uint32_t* __restrict__ dst, uint32_t n, uint32_t* __restrict__ cnt,
                    uint32_t* __restrict__ rank, OpState* op) {
   const uint32_t base = blockIdx.x * (256 * kGroupItems) + threadIdx.x;
+  const uint32_t op_err = op->err;   // (an op submitted behind a failed one starts out rejected; tested after the first loads are in flight)
   uint32_t s[kGroupItems], d[kGroupItems];
   bool ok[kGroupItems];
 #pragma unroll
@@ -253,6 +274,7 @@ group_count_kernel(GraphView g, GroupIndex gi, const uint32_t* __restrict__ src,
     s[q] = ok[q] ? src[i] : 0u;
     d[q] = ok[q] ? dst[i] : 0u;
   }
+  if (op_err) return;
   uint32_t aw[kGroupItems];
   if (kMode == kPackInsert) {
 #pragma unroll

@@ -147,6 +147,35 @@ class DynamicGraph:
         s, d = self._pair_args(src, dst)
         self._check(self._lib.dg_delete_batch_coo(self._h, s.ptr, d.ptr, s.n, s.mem))
 
+    # -- submitted updates (dg_submit_*_coo / dg_flush: no host wait per batch) -----------------
+    def submit_insert_pairs(self, src, dst) -> int:
+        """insert_pairs without waiting for the op: DEVICE arrays that stay alive until flush().  Returns the
+        op's ticket (0: the call had to run it synchronously).  A failure surfaces at flush() or at the next
+        call of any kind; ops submitted behind a failed one are not applied (graph.hpp:168-171)."""
+        return self._submit(self._lib.dg_submit_insert_coo, src, dst)
+
+    def submit_delete_pairs(self, src, dst) -> int:
+        return self._submit(self._lib.dg_submit_delete_coo, src, dst)
+
+    def _submit(self, fn, src, dst) -> int:
+        s, d = self._pair_args(src, dst)
+        if s.mem != _lib.DG_MEM_DEVICE:
+            raise DataError("submit: device arrays only (host batches go through ingest())")
+        t = C.c_uint64()
+        self._check(fn(self._h, s.ptr, d.ptr, s.n, C.byref(t)))
+        return int(t.value)
+
+    def flush(self) -> int:
+        """Waits for every submitted op; raises the first failure; returns how many were applied."""
+        n = C.c_uint64()
+        rc = self._lib.dg_flush(self._h, C.byref(n))
+        self._last_flush_applied = int(n.value)
+        self._check(rc)
+        return int(n.value)
+
+    def pending_ops(self) -> int:
+        return int(self._lib.dg_pending_ops(self._h))
+
     @staticmethod
     def _pair_args(src, dst):
         s, d = _Arg(src, np.uint32), _Arg(dst, np.uint32)
@@ -222,10 +251,10 @@ class DynamicGraph:
         return [int(x) for x in skipped[: ns.value]]
 
     # -- pipelined host batches ------------------------------------------------------------------
-    def ingest(self, max_entries: int, depth: int = 2) -> "BatchIngest":
+    def ingest(self, max_entries: int, depth: int = 2, synchronous: bool = False) -> "BatchIngest":
         """Ingest queue for a stream of HOST batches: the copy of the next batch overlaps the
         current op (the loop of io/workload.hpp:141-155, with the PCIe copy taken off its path)."""
-        return BatchIngest(self, max_entries, depth)
+        return BatchIngest(self, max_entries, depth, synchronous)
 
     # -- reports -----------------------------------------------------------------------------
     def stats(self) -> dict:
@@ -280,19 +309,25 @@ class DynamicGraph:
 
 class BatchIngest:
     """`submit("insert" | "delete", src, dst)` applies host batches in order, exactly like calling
-    insert_pairs / delete_pairs one after the other, but keeps up to `depth - 1` later batches in
-    flight to the device while an op runs.  A failing batch raises from the submit / flush call that
-    executes it; later staged batches are dropped (the reference loop would have stopped there too).
-    Host arrays must stay alive until their op ran (pinned memory makes the copy asynchronous)."""
+    insert_pairs / delete_pairs one after the other, without a host wait per batch: the copy of a batch goes
+    to one of `depth` device slots on its own stream and the op is SUBMITTED behind it (dg_ingest_submit_*),
+    so copies, ops and the host loop overlap.  A failing batch raises from a later submit or from flush();
+    batches submitted behind it are not applied (the reference loop would have stopped there too) and
+    `applied` tells how many were.  Host arrays are kept alive here until their op has certainly run
+    (pinned memory makes the copy asynchronous).  `synchronous=True` keeps the round-1 behaviour: one host
+    wait per op, `depth - 1` copies in flight behind the running op."""
 
-    def __init__(self, graph: DynamicGraph, max_entries: int, depth: int = 2):
+    def __init__(self, graph: DynamicGraph, max_entries: int, depth: int = 2, synchronous: bool = False):
         self._g = graph
         self._lib = graph._lib
         self._max_entries = max_entries
         self._depth = depth
+        self._sync = synchronous
         self._q = None
         self._open()
-        self._pending = []   # (kind, slot, keep-alive arrays)
+        self._pending = []   # synchronous mode: (kind, slot, keep-alive arrays)
+        self._keep = []      # submitted mode: host arrays of the last depth + 8 batches
+        self.applied = 0
 
     def _open(self):
         q = C.c_void_p()
@@ -318,6 +353,7 @@ class BatchIngest:
             self._pending.clear()
             self._lib.dg_ingest_reset(self._q)   # drop whatever is still staged
             self._g._check(rc)
+        self.applied += 1
         return rc
 
     def submit(self, kind: str, src, dst):
@@ -327,15 +363,37 @@ class BatchIngest:
         d = np.ascontiguousarray(dst, dtype=np.uint32)
         if s.size != d.size:
             raise DataError("pairs: src/dst must have equal length")
-        if len(self._pending) == self._depth:
+        if self._sync and len(self._pending) == self._depth:
             self._run_oldest()
         slot = C.c_uint32()
         self._g._check(self._lib.dg_ingest_stage_coo(self._q, C.c_void_p(s.ctypes.data), C.c_void_p(d.ctypes.data),
                                                      s.size, C.byref(slot)))
-        self._pending.append((kind, int(slot.value), (s, d)))
-        if len(self._pending) == self._depth:   # keep depth - 1 copies in flight behind the running op
-            self._run_oldest()
+        if self._sync:
+            self._pending.append((kind, int(slot.value), (s, d)))
+            if len(self._pending) == self._depth:   # keep depth - 1 copies in flight behind the running op
+                self._run_oldest()
+            return
+        # (at most `depth` staged + 7 submitted ops are ever unfinished: older host arrays can go)
+        self._keep.append((s, d))
+        if len(self._keep) > self._depth + 8:
+            self._keep.pop(0)
+        fn = self._lib.dg_ingest_submit_insert if kind == "insert" else self._lib.dg_ingest_submit_delete
+        t = C.c_uint64()
+        rc = fn(self._q, int(slot.value), C.byref(t))
+        if rc != 0:
+            self._lib.dg_ingest_reset(self._q)
+            self._collect()
+            self._g._check(rc)
+
+    def _collect(self):
+        n = C.c_uint64()
+        rc = self._lib.dg_flush(self._g._h, C.byref(n))
+        self.applied += int(n.value)
+        self._keep.clear()
+        return rc
 
     def flush(self):
         while self._pending:
             self._run_oldest()
+        if not self._sync:
+            self._g._check(self._collect())

@@ -291,16 +291,17 @@ def test_device_resident_batches():
     assert g.active_edges() == o.active_edges()
 
 
-def test_pipelined_ingest_matches_sequential_ops():
-    """dg_ingest_*: host batches applied through the double-buffered ingest queue give the same
-    graph as insert_pairs / delete_pairs one after the other; a rejected batch raises from the
-    call that executes it and leaves the graph as the reference would (graph.hpp:168-171)."""
+@pytest.mark.parametrize("synchronous", [False, True])
+def test_pipelined_ingest_matches_sequential_ops(synchronous):
+    """dg_ingest_*: host batches applied through the ingest queue (ops submitted without a host wait, or one
+    wait per op) give the same graph as insert_pairs / delete_pairs one after the other; a rejected batch
+    raises and leaves the graph as the reference would — nothing behind it is applied (graph.hpp:168-171)."""
     from paper_2306_08252_b200 import DataError, DynamicGraph, GraphConfig
     rng = np.random.default_rng(21)
     V = 4000
     g = DynamicGraph(GraphConfig(pool_blocks=1 << 16), V, 32)
     o = CpuGraph(load_oracle(), "orc", V, 32, 1 << 28)
-    q = g.ingest(max_entries=30000, depth=3)
+    q = g.ingest(max_entries=30000, depth=3, synchronous=synchronous)
     ops = []
     for i in range(9):
         s = (rng.zipf(1.3, 30000) % V).astype(np.uint32)
@@ -328,6 +329,130 @@ def test_pipelined_ingest_matches_sequential_ops():
     a, b = g.export_csr(), o.export_csr()
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     q.close(); g.close()
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).cuda()
+
+
+def _same_graph(g, o):
+    assert g.active_edges() == o.active_edges()
+    a, b = g.export_csr(), o.export_csr()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(np.asarray(g.degrees()), np.asarray(o.degrees()))
+
+
+@pytest.mark.parametrize("block_size,group", [(32, "auto"), (32, "radix"), (7, "auto")])
+def test_submitted_ops_match_synchronous_ops(block_size, group):
+    """dg_submit_insert_coo / dg_submit_delete_coo / dg_flush: a stream of submitted batches (no host wait
+    between them; hubs, duplicates, deletes of absent edges) leaves the graph the reference's loop of
+    insert_batch / delete_batch leaves (graph.hpp:167-222); synchronous calls in between see every
+    submitted op applied."""
+    from paper_2306_08252_b200 import DynamicGraph, GraphConfig
+    rng = np.random.default_rng(5)
+    V = 6000
+    g = DynamicGraph(GraphConfig(pool_blocks=1 << 17, group=group), V, block_size)
+    o = CpuGraph(load_oracle(), "orc", V, block_size, 1 << 29)
+    keep, tickets = [], []
+    for i in range(14):
+        n = int(rng.integers(1, 40000))
+        s = (rng.zipf(1.25, n) % V).astype(np.uint32)
+        if i % 5 == 0:
+            s[: n // 2] = 3          # a hub: long chain, many targets
+        d = rng.integers(0, V // 4, n).astype(np.uint32)
+        ds, dd = _dev(s), _dev(d)
+        keep.append((ds, dd))
+        if i % 3 == 2:
+            tickets.append(g.submit_delete_pairs(ds, dd)); o.delete_pairs(s, d)
+        else:
+            tickets.append(g.submit_insert_pairs(ds, dd)); o.insert_pairs(s, d)
+        if i == 6:   # a synchronous call in the middle: waits for what was submitted
+            qs, qd = s[:500], d[:500]
+            assert np.array_equal(np.asarray(g.query_edges(qs, qd)), np.asarray(o.query(qs, qd)))
+            assert g.pending_ops() == 0
+    assert any(t != 0 for t in tickets)   # (ops really were submitted, not run synchronously)
+    assert g.flush() >= 1
+    assert g.pending_ops() == 0
+    assert g.last_op_report()["batch_entries"] == keep[-1][0].numel()   # the report of the last submitted op
+    _same_graph(g, o)
+    g.close()
+
+
+def test_submitted_failure_is_reported_before_anything_behind_it_mutates():
+    """graph.hpp:168-171 on the submitted path: a batch that fails validation leaves the graph untouched and
+    every op submitted behind it does not run; dg_flush returns the failure and how many ops were applied;
+    further submits are refused until the failure was returned; the stream can then be resumed."""
+    from paper_2306_08252_b200 import DataError, DynamicGraph, EngineError, GraphConfig
+    rng = np.random.default_rng(9)
+    V = 3000
+    g = DynamicGraph(GraphConfig(pool_blocks=1 << 16), V, 32)
+    o = CpuGraph(load_oracle(), "orc", V, 32, 1 << 28)
+    def batch(n):
+        return (rng.zipf(1.3, n) % V).astype(np.uint32), rng.integers(0, V, n).astype(np.uint32)
+    a, b, c = batch(20000), batch(20000), batch(20000)
+    bad_d = b[1].copy(); bad_d[11] = V + 5
+    dev = [(_dev(a[0]), _dev(a[1])), (_dev(b[0]), _dev(bad_d)), (_dev(c[0]), _dev(c[1])), (_dev(a[0]), _dev(a[1]))]
+    g.submit_insert_pairs(*dev[0]); o.insert_pairs(*a)
+    g.submit_insert_pairs(*dev[1])            # rejected: destination out of range (csr.hpp:67-72)
+    g.submit_insert_pairs(*dev[2])            # behind the failure: must not run
+    g.submit_delete_pairs(*dev[3])            # behind the failure: must not run
+    with pytest.raises(DataError, match="destination out of range"):
+        g.flush()
+    assert g._last_flush_applied == 1
+    _same_graph(g, o)
+    # resumed: the caller drops the bad batch and goes on
+    g.submit_insert_pairs(*dev[2]); o.insert_pairs(*c)
+    g.submit_delete_pairs(*dev[3]); o.delete_pairs(*a)
+    assert g.flush() == 2
+    _same_graph(g, o)
+    # an unreported failure is returned by the next synchronous call instead of running it
+    g.submit_insert_pairs(*dev[1])
+    g.submit_insert_pairs(*dev[0])
+    with pytest.raises(DataError):
+        g.insert_pairs(*a)
+    _same_graph(g, o)
+    g.insert_pairs(*a); o.insert_pairs(*a)
+    _same_graph(g, o)
+    # a fixed pool that cannot host the batch: rejected, graph unchanged (block_pool.hpp:177-189)
+    small = DynamicGraph(GraphConfig(pool_blocks=64), V, 32)
+    s = np.arange(2000, dtype=np.uint32); d = np.zeros(2000, dtype=np.uint32)
+    with pytest.raises(EngineError):
+        small.submit_insert_pairs(_dev(s), _dev(d))
+        small.flush()
+    assert small.active_edges() == 0
+    small.close(); g.close()
+
+
+def test_submitted_ops_on_a_growing_pool_grow_like_the_synchronous_path():
+    """GrowthPolicy (block_pool.hpp:162-189) under submitted inserts: wherever the pool may have to grow the
+    submit runs the op synchronously, so growth rounds and the final graph equal the synchronous run's."""
+    from paper_2306_08252_b200 import DynamicGraph, GraphConfig
+    rng = np.random.default_rng(3)
+    V, B = 5000, 8
+    batches = [((rng.zipf(1.4, 6000) % V).astype(np.uint32), rng.integers(0, V, 6000).astype(np.uint32)) for _ in range(10)]
+    out = []
+    for submitted in (False, True):
+        g = DynamicGraph(GraphConfig(pool_blocks=2000, pool_max_blocks=60000), V, B)
+        keep = []
+        for i, (s, d) in enumerate(batches):
+            if submitted:
+                ds, dd = _dev(s), _dev(d)
+                keep.append((ds, dd))
+                (g.submit_delete_pairs if i % 4 == 3 else g.submit_insert_pairs)(ds, dd)
+            else:
+                (g.delete_pairs if i % 4 == 3 else g.insert_pairs)(s, d)
+        if submitted:
+            g.flush()
+        st = g.stats()
+        out.append((st["growth_count"], st["pool_blocks_created"], g.active_edges(), g.digest()))
+        if submitted:
+            o = CpuGraph(load_oracle(), "orc", V, B, 1 << 28)
+            for i, (s, d) in enumerate(batches):
+                (o.delete_pairs if i % 4 == 3 else o.insert_pairs)(s, d)
+            _same_graph(g, o)
+        g.close()
+    assert out[0] == out[1] and out[0][0] >= 1
 
 
 def test_edge_queue_growth_policy():
