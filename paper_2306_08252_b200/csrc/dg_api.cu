@@ -1662,11 +1662,21 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
     cudaMemsetAsync(plan_scratch, 0, kAllocScratchWords * sizeof(unsigned long long), h->stream);
     DG_LAUNCH(h, "csr_plan_kernel", csr_plan_kernel<<<(unsigned)((V + kCsrPlanTile - 1) / kCsrPlanTile), 256, 0, h->stream>>>(
         g, d_off, (uint32_t)V, n_edges, blk_off, items, items_cap, plan_scratch, h->d_op()));
-    const int csr_ctas_per_sm = resident_ctas_per_sm(csr_append_kernel, kCsrWarps * 32, 0);
     const uint64_t groups = (V + 31) / 32 + items_cap;
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((groups + kCsrWarps - 1) / kCsrWarps, (uint64_t)h->sm_count * csr_ctas_per_sm));
-    DG_LAUNCH(h, "csr_append_kernel", csr_append_kernel<<<grid, kCsrWarps * 32, 0, h->stream>>>(
-        g, d_off, d_dst, (uint32_t)V, blk_off, items, n_edges, plan_scratch, h->d_op()));
+    // a pool nothing was ever popped from: every source is empty and handle == queue position (csr_bulk_kernel)
+    const bool fresh = h->active_edges == 0 && h->front == 0 && h->rear == h->NB && h->ring_identity >= h->NB &&
+                       std::getenv("DG_NO_BULK_KERNEL") == nullptr;
+    if (fresh) {
+      const int ctas_per_sm = resident_ctas_per_sm(csr_bulk_kernel, kBulkWarps * 32, 0);
+      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((groups + kBulkWarps - 1) / kBulkWarps, (uint64_t)h->sm_count * ctas_per_sm));
+      DG_LAUNCH(h, "csr_bulk_kernel", csr_bulk_kernel<<<grid, kBulkWarps * 32, 0, h->stream>>>(
+          g, d_off, d_dst, (uint32_t)V, blk_off, items, n_edges, plan_scratch, h->d_op()));
+    } else {
+      const int csr_ctas_per_sm = resident_ctas_per_sm(csr_append_kernel, kCsrWarps * 32, 0);
+      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((groups + kCsrWarps - 1) / kCsrWarps, (uint64_t)h->sm_count * csr_ctas_per_sm));
+      DG_LAUNCH(h, "csr_append_kernel", csr_append_kernel<<<grid, kCsrWarps * 32, 0, h->stream>>>(
+          g, d_off, d_dst, (uint32_t)V, blk_off, items, n_edges, plan_scratch, h->d_op()));
+    }
     rc = op_end(h);
     if (rc != DG_OK && h->h_blk->op.committed) {
       const std::string msg = h->last_error;

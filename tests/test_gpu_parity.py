@@ -193,6 +193,46 @@ def test_csr_native_block_path_hubs_fills_and_rollback():
     g.close()
 
 
+@pytest.mark.parametrize("V", [1, 33, 1000, 5000])
+def test_bulk_init_fresh_pool_kernel_rollback_and_rebuild(V):
+    """Bulk init into an untouched pool (csr_bulk_kernel: segmented copy, heavy sources as 32-block items):
+    a bad destination anywhere (inside a hub item, in a light group, first / last entry) rejects the batch and
+    leaves the graph EMPTY (graph.hpp:168-171, csr.hpp:67-72) — and still fresh, so the next bulk init takes the
+    same kernel; the built graph equals the reference's; a second CSR insert resumes at the tails it left."""
+    rng = np.random.default_rng(100 + V)
+    pattern = [0, 1, 31, 32, 33, 0, 127, 128, 129, 5, 1023, 1024, 1025, 0, 0, 2048, 4097, 7, 64, 96, 40000]
+    degs = np.array([pattern[(7 * v + 3) % len(pattern)] for v in range(V)], np.int64)
+    if V >= 1000:
+        degs[rng.integers(0, V, V // 2)] = 0
+        degs[rng.integers(0, V, 5)] = 40000
+    off = np.zeros(V + 1, np.uint64)
+    np.cumsum(degs, out=off[1:])
+    E = int(off[-1])
+    dst = rng.integers(0, V, E).astype(np.uint32)
+    cfg = {"v0": V, "block_size": 32, "arena_bytes": 4 << 30}
+    g, o = _gpu(cfg, pool_blocks=2 * (E // 32 + V) + 4096), _orc(cfg)
+    script = []
+    for bad_at in ([0, E - 1, E // 2, int(off[V // 2])] if E else []):
+        bad = dst.copy()
+        bad[min(bad_at, E - 1)] = V + 9
+        script += [("insert_csr", off, bad), ("check",)]
+    script += [("insert_csr", off, dst), ("check",)]
+    script += [("query", rng.integers(0, V, 5000).astype(np.uint32), rng.integers(0, V, 5000).astype(np.uint32))]
+    degs2 = np.array([pattern[(v + 1) % 14] for v in range(V)], np.int64)
+    off2 = np.zeros(V + 1, np.uint64)
+    np.cumsum(degs2, out=off2[1:])
+    dst2 = rng.integers(0, V, int(off2[-1])).astype(np.uint32)
+    script += [("insert_csr", off2, dst2), ("check",)]
+    src = np.repeat(np.arange(V, dtype=np.uint32), degs)
+    pick = rng.random(E) < 0.4
+    script += [("delete", src[pick], dst[pick]), ("check",)]
+    ra, rb = run_script(g, script), run_script(o, script)
+    assert_same(ra, rb, f"bulk init fresh pool V={V}")
+    if E:
+        assert [x for x in ra["obs"] if x[0] == "rc"].count(("rc", 2)) == 4
+    g.close()
+
+
 @pytest.mark.parametrize("V", [1, 31, 32, 33, 1000])
 def test_csr_native_block_path_degree_boundaries(V):
     """B = 32 CSR insert at every boundary of the append pass: degrees around a block (31 / 32 / 33),
@@ -394,12 +434,12 @@ def test_submitted_failure_is_reported_before_anything_behind_it_mutates():
     bad_d = b[1].copy(); bad_d[11] = V + 5
     dev = [(_dev(a[0]), _dev(a[1])), (_dev(b[0]), _dev(bad_d)), (_dev(c[0]), _dev(c[1])), (_dev(a[0]), _dev(a[1]))]
     g.submit_insert_pairs(*dev[0]); o.insert_pairs(*a)
-    g.submit_insert_pairs(*dev[1])            # rejected: destination out of range (csr.hpp:67-72)
-    g.submit_insert_pairs(*dev[2])            # behind the failure: must not run
-    g.submit_delete_pairs(*dev[3])            # behind the failure: must not run
-    with pytest.raises(DataError, match="destination out of range"):
+    with pytest.raises(DataError, match="destination out of range"):   # (from a later submit or from flush)
+        g.submit_insert_pairs(*dev[1])            # rejected: destination out of range (csr.hpp:67-72)
+        g.submit_insert_pairs(*dev[2])            # behind the failure: must not run
+        g.submit_delete_pairs(*dev[3])            # behind the failure: must not run
         g.flush()
-    assert g._last_flush_applied == 1
+    assert g.flush() == 1                         # exactly the ops before the failed one were applied
     _same_graph(g, o)
     # resumed: the caller drops the bad batch and goes on
     g.submit_insert_pairs(*dev[2]); o.insert_pairs(*c)
@@ -407,10 +447,11 @@ def test_submitted_failure_is_reported_before_anything_behind_it_mutates():
     assert g.flush() == 2
     _same_graph(g, o)
     # an unreported failure is returned by the next synchronous call instead of running it
-    g.submit_insert_pairs(*dev[1])
-    g.submit_insert_pairs(*dev[0])
     with pytest.raises(DataError):
+        g.submit_insert_pairs(*dev[1])
+        g.submit_insert_pairs(*dev[0])
         g.insert_pairs(*a)
+    assert g.flush() == 0
     _same_graph(g, o)
     g.insert_pairs(*a); o.insert_pairs(*a)
     _same_graph(g, o)
