@@ -1307,25 +1307,31 @@ csr_bulk_kernel(GraphView g, const unsigned long long* __restrict__ off, const u
     }
     return;
   }
-  __shared__ uint4 s_desc[kBulkWarps][32 * 4];   // {first batch entry, handle, entries, -} per block of the group
+  __shared__ uint4 s_desc[kBulkWarps][32 * 4 + 8];   // {first batch entry, handle, entries, entries padded to a sector} per block of the group
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
   uint4* desc = s_desc[warp];
   const uint32_t limit = g.dst_limit;
   const uint32_t h_base = (uint32_t)front_old;   // (handle of queue position p is p: the caller checked the pool is untouched)
-  unsigned long long bad = ~0ull;
+  uint32_t bad = 0xFFFFFFFFu;   // smallest batch index of an out-of-range destination seen by this lane (n_edges < 2^31)
+  const uint32_t* src_lane = dsts + lane;
+  uint32_t* out_lane = g.slab + lane;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t n_items = (uint32_t)(plan_tot >> 32);
   const uint32_t total = n_items + (V + 31u) / 32u;
   constexpr uint32_t kChunk = 4;   // units per ticket (one same-address atomic per chunk)
+  constexpr int kRows = 16;        // item rows in flight per warp (2 KB)
+  constexpr int kBlocks = 8;       // group blocks in flight per warp
   uint32_t w_cur = gw * kChunk, w_nxt = w_cur + 1;
   uint32_t ticket = 0;
   while (w_cur < total) {
     if ((w_cur % kChunk) == 0 && lane == 0) ticket = nwarps + atomicAdd(&op->med_cursor, 1u);
     if ((w_nxt % kChunk) == 0) w_nxt = __shfl_sync(kFull, ticket, 0) * kChunk;
     if (w_cur < n_items) {
-      // ---- heavy item: up to 32 consecutive blocks of one source, a straight copy
+      // ---- heavy item: up to 32 consecutive blocks of one source, a straight copy.  Slots past the source's
+      // entries are free (nothing reads past deg): they are filled with 0 up to the next 32-byte sector so no
+      // partial sector is written, and the range check needs no validity mask.
       const uint4* ip = reinterpret_cast<const uint4*>(items + w_cur);
       const uint4 ia = ip[0], ib = ip[1];
       const uint32_t chunk = ia.y, o0 = ib.x, c = ib.z, bo = ib.w;
@@ -1333,24 +1339,38 @@ csr_bulk_kernel(GraphView g, const unsigned long long* __restrict__ off, const u
       const uint32_t j0 = chunk * 32u;
       const uint32_t rows = min(32u, nb - j0);
       const uint32_t rem = c - j0 * 32u;            // entries from the item's first row on
-      const uint32_t* src = dsts + o0 + j0 * 32u;
+      const uint32_t first = o0 + j0 * 32u;
+      const uint32_t* src = src_lane + first;
       const uint32_t h0 = h_base + bo + j0;
-      uint32_t* out = g.slab + (unsigned long long)h0 * 32u;
+      uint32_t* out = out_lane + (unsigned long long)h0 * 32u;
       if ((uint32_t)lane < rows) g.next[h0 + lane] = (j0 + lane + 1u == nb) ? kNull : h0 + lane + 1u;
+      const uint32_t full = min(rows, rem >> 5) & ~(uint32_t)(kRows - 1);   // rows of complete 16-row batches
+      uint32_t r0 = 0;
 #pragma unroll 1
-      for (uint32_t r0 = 0; r0 < rows; r0 += 8) {
-        uint32_t x[8];
+      for (; r0 < full; r0 += kRows) {   // every slot of these rows holds an entry: no masks
+        uint32_t x[kRows];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < kRows; ++q) x[q] = src[(r0 + q) * 32u];
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) {
+          if (x[q] >= limit) bad = min(bad, first + (r0 + q) * 32u + lane);
+          out[(r0 + q) * 32u] = x[q];
+        }
+      }
+      const uint32_t pad_end = min(rows * 32u, (rem + 7u) & ~7u);
+#pragma unroll 1
+      for (; r0 < rows; r0 += 4) {
+        uint32_t x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
           const uint32_t idx = (r0 + q) * 32u + lane;
-          x[q] = idx < rem ? src[idx] : kTomb;
+          x[q] = idx < rem ? src[(r0 + q) * 32u] : 0u;
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
           const uint32_t idx = (r0 + q) * 32u + lane;
-          if (idx < rem && x[q] >= limit) bad = min(bad, (unsigned long long)o0 + j0 * 32u + idx);
-          // (padding up to the next 32-byte sector: no partial sector is written; slots past deg are free)
-          if (idx < ((rem + 7u) & ~7u) && r0 + q < rows) out[idx] = x[q];
+          if (x[q] >= limit) bad = min(bad, first + idx);
+          if (idx < pad_end) out[(r0 + q) * 32u] = x[q];
         }
       }
     } else {
@@ -1379,25 +1399,25 @@ csr_bulk_kernel(GraphView g, const unsigned long long* __restrict__ off, const u
       const uint32_t U = __shfl_sync(kFull, uincl, 31);
 #pragma unroll 1
       for (uint32_t j = 0; j < nbl; ++j) {
-        desc[uexcl + j] = make_uint4(o0 + j * 32u, h0 + j, c - j * 32u, 0u);
+        const uint32_t cnt = min(32u, c - j * 32u);
+        desc[uexcl + j] = make_uint4(o0 + j * 32u, h0 + j, cnt, (cnt + 7u) & ~7u);
         g.next[h0 + j] = (j + 1u == nbl) ? kNull : h0 + j + 1u;
       }
+      if (lane < kBlocks) desc[U + lane] = make_uint4(0u, 0u, 0u, 0u);   // the last batch reads past U: empty blocks
       __syncwarp();
 #pragma unroll 1
-      for (uint32_t u0 = 0; u0 < U; u0 += 4) {
-        uint4 dsc[4];
-        uint32_t x[4];
+      for (uint32_t u0 = 0; u0 < U; u0 += kBlocks) {
+        uint32_t x[kBlocks];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          dsc[q] = desc[min(u0 + q, U - 1u)];
-          if (u0 + q >= U) dsc[q].z = 0u;
-          x[q] = (uint32_t)lane < dsc[q].z ? dsts[dsc[q].x + lane] : kTomb;
+        for (int q = 0; q < kBlocks; ++q) {
+          const uint4 dq = desc[u0 + q];
+          x[q] = (uint32_t)lane < dq.z ? src_lane[dq.x] : 0u;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t cnt = dsc[q].z;
-          if ((uint32_t)lane < cnt && x[q] >= limit) bad = min(bad, (unsigned long long)dsc[q].x + lane);
-          if ((uint32_t)lane < min(32u, (cnt + 7u) & ~7u)) g.slab[(unsigned long long)dsc[q].y * 32u + lane] = x[q];
+        for (int q = 0; q < kBlocks; ++q) {
+          const uint4 dq = desc[u0 + q];
+          if (x[q] >= limit) bad = min(bad, dq.x + lane);
+          if ((uint32_t)lane < dq.w) out_lane[(unsigned long long)dq.y * 32u] = x[q];
         }
       }
       __syncwarp();   // the descriptors are rewritten by the next group
@@ -1405,7 +1425,7 @@ csr_bulk_kernel(GraphView g, const unsigned long long* __restrict__ off, const u
     w_cur = w_nxt;
     w_nxt = w_cur + 1;
   }
-  if (bad != ~0ull) atomicMin(&op->bad_index, bad);
+  if (bad != 0xFFFFFFFFu) atomicMin(&op->bad_index, (unsigned long long)bad);
   // the last CTA to finish publishes the queue front / live-edge count and the verdict
   __syncthreads();
   if (threadIdx.x == 0) {
