@@ -1104,9 +1104,16 @@ void enqueue_match_impl(dg_graph* h, const BatchView& b, const Worklist& w, uint
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   const size_t med_smem = kIsDelete ? kMedSmemDelete : kMedSmemQuery;
   const size_t long_smem = kIsDelete ? kLongSmemDelete : kLongSmemQuery;
-  // opt in to > 48 KB of dynamic shared memory (per device: cheap enough to repeat)
-  cudaFuncSetAttribute(match_med_kernel<kIsDelete, kNative>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)med_smem);
-  cudaFuncSetAttribute(match_long_kernel<kIsDelete, kNative>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_smem);
+  // opt in to > 48 KB of dynamic shared memory: once per device and instantiation (two host API calls per op otherwise)
+  {
+    static std::mutex mu;
+    static std::unordered_set<int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.insert(h->device).second) {
+      cudaFuncSetAttribute(match_med_kernel<kIsDelete, kNative>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)med_smem);
+      cudaFuncSetAttribute(match_long_kernel<kIsDelete, kNative>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_smem);
+    }
+  }
   // the tiers touch disjoint blocks: side by side, heaviest items first
   const int long_grid = (int)std::min<uint64_t>(long_items_bound(h, n_batch), (uint64_t)h->sm_count * 3);
   DG_LAUNCH(h, kIsDelete ? "match_long_kernel<delete>" : "match_long_kernel<query>",
