@@ -57,6 +57,12 @@ extern "C" {
  * RADIX = pack keys + LSD radix sort, O(n); COUNT = per-vertex counters + scan, O(V + n). */
 #define DG_FLAG_GROUP_RADIX 2u
 #define DG_FLAG_GROUP_COUNT 4u
+/* block_size = 0 asks for the reference's rule (compute_block_size, csr.hpp:77-88: round-half-up of edges per
+ * non-empty source of the first batch).  With this flag a result in [24, 48] becomes 32, the NATIVE block (one
+ * 128-byte line: the fused delete, the TMA-staged CSR append and the bulk-init copy are written for it; a 33-slot
+ * block is not even 16-byte aligned).  An explicit deviation from the reference's value — block counts, and with
+ * them the point where a fixed pool underflows, follow the block size actually used (dg_block_size reports it). */
+#define DG_FLAG_AUTO_BLOCK_NATIVE 8u
 
 /* reference: types.hpp:16-17 (kInvalidVertex / kNullBlock) */
 #define DG_INVALID_VERTEX 0xFFFFFFFFu

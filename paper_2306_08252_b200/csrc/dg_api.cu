@@ -1251,6 +1251,13 @@ Grouped group_radix(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, u
   return out;
 }
 
+// block size of a deferred pool from the first batch (compute_block_size, csr.hpp:77-88; DG_FLAG_AUTO_BLOCK_NATIVE)
+inline uint32_t auto_block_size(const dg_graph* h, uint64_t n_edges, uint64_t n_sources) {
+  const uint64_t rounded = std::max<uint64_t>(1, (n_edges + n_sources / 2) / n_sources);
+  if ((h->cfg.flags & DG_FLAG_AUTO_BLOCK_NATIVE) && rounded >= 24 && rounded <= 48) return 32u;
+  return (uint32_t)std::min<uint64_t>(rounded, 0x7FFFFFFFull);
+}
+
 int require_pool(dg_graph* h) {
   if (h->B == 0 || h->slab == nullptr)
     return fail(h, DG_ERR_ENGINE, "graph has no block pool yet (block_size 0 before the first insert)");
@@ -1611,8 +1618,7 @@ static int insert_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst
     // deferred pool: compute_block_size (csr.hpp:77-88) from this first batch
     if ((rc = op_end(h)) != DG_OK) return rc;
     const uint64_t T = h->h_blk->op.n_runs;
-    const uint64_t rounded = (n + T / 2) / T;
-    if ((rc = create_pool(h, (uint32_t)std::max<uint64_t>(1, rounded))) != DG_OK) return rc;
+    if ((rc = create_pool(h, auto_block_size(h, n, T))) != DG_OK) return rc;
     // the run arrays stay valid; re-arm the op words, keeping n_runs
     OpState& op = h->h_blk->op;
     op.err_index = ~0ull;
@@ -1707,8 +1713,7 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
     if ((rc = op_end(h)) != DG_OK) return rc;
     const uint64_t T = h->h_blk->op.aux0;
     if (T == 0) return fail(h, DG_ERR_DATA, "compute_block_size: first batch contains no edges");
-    const uint64_t rounded = (n_edges + T / 2) / T;
-    if ((rc = create_pool(h, (uint32_t)std::max<uint64_t>(1, rounded))) != DG_OK) return rc;
+    if ((rc = create_pool(h, auto_block_size(h, n_edges, T))) != DG_OK) return rc;
     OpState& op = h->h_blk->op;
     op.err_index = ~0ull;
     op.aux0 = 0;

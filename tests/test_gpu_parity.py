@@ -305,6 +305,24 @@ def test_auto_block_size_from_first_batch():
     assert g2.block_size() == want
     assert np.array_equal(g.export_csr()[1], g2.export_csr()[1])
     assert g.compute_block_size_pairs(s) == want
+    # DG_FLAG_AUTO_BLOCK_NATIVE: a computed size near 32 becomes the native block (an explicit, opt-in deviation);
+    # anything else keeps the reference's value.  Canonical state does not depend on the block size.
+    s3 = np.repeat(np.arange(300, dtype=np.uint32), 33)                      # 33 entries per source: the rule gives 33
+    d3 = rng.integers(0, 500, s3.size).astype(np.uint32)
+    assert compute_block_size(csr_from_pairs(BatchKind.Insert, 500, s3, d3)) == 33
+    for first, expect in (((s3, d3), 32), ((s, d), want)):
+        for as_csr in (False, True):
+            g3 = DynamicGraph(GraphConfig(pool_bytes=1 << 24, auto_block_native=True), 500, 0)
+            if as_csr:
+                g3.insert_batch(csr_from_pairs(BatchKind.Insert, 500, *first))
+            else:
+                g3.insert_pairs(*first)
+            assert g3.block_size() == expect
+            o3 = CpuGraph(load_oracle(), "orc", 500, 33 if expect == 32 else want, 1 << 26)
+            o3.insert_pairs(*first)
+            g3.delete_pairs(first[0][::3], first[1][::3]); o3.delete_pairs(first[0][::3], first[1][::3])
+            assert np.array_equal(g3.export_csr()[1], o3.export_csr()[1]) and g3.active_edges() == o3.active_edges()
+            g3.close()
 
 
 def test_device_resident_batches():
