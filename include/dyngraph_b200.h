@@ -393,6 +393,18 @@ int dg_exchange_end_round(dg_exchange* x);
  */
 int dg_digest_global(dg_graph* h, uint32_t rank, uint32_t world, uint32_t bits, uint64_t* out_digest, uint64_t* out_entries);
 
+/* plan_batch (graph.hpp:135-160) -> BatchPlan (graph.hpp:33-39): validates an INSERT batch exactly as
+ * dg_insert_batch_csr does (csr.hpp:49-73, dead-source rule graph.hpp:322-327; DG_ERR_DATA otherwise) and fills, per
+ * vertex, the fresh blocks the batch needs (blocks_required), their inclusive prefix sum in vertex order (prefix_sum:
+ * the reference's pop schedule) and the free slots of the vertex's last-insert block (space_remaining); *total_blocks
+ * (optional) = prefix_sum[V - 1].  Nothing is mutated.  `mem` says where the batch AND the three output arrays
+ * (V entries each) live.  space_remaining follows this library's compact chains: equal to the reference's after any
+ * insert-only history, smaller or equal after deletes (the reference keeps holes; physical layout is reported, not
+ * compared).  DG_ERR_ENGINE while the graph has no pool yet (block_size 0 before the first insert). */
+int dg_plan_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets, const uint32_t* destinations,
+                      uint64_t n_edges, int mem, uint64_t* blocks_required, uint64_t* prefix_sum,
+                      uint32_t* space_remaining, uint64_t* total_blocks);
+
 /* ---- host -> device batch ingest (nothing in the reference) ----------
  *
  * The reference harness hands insert_batch / delete_batch one host batch after the other

@@ -12,7 +12,7 @@
 // if the library is missing the program does not link.
 //
 // Not mirrored (physical layout, reported rather than compared — SURVEY.md §8a):
-// arena(), dictionary(), pool(), sentinel_of(), adjacency_blocks(), plan_batch().
+// arena(), dictionary(), pool(), sentinel_of(), adjacency_blocks().
 #pragma once
 
 #include <algorithm>
@@ -53,6 +53,14 @@ struct CsrBatch {
   std::uint64_t vertex_count() const { return offsets.empty() ? 0 : offsets.size() - 1; }
   std::uint64_t edge_count() const { return destinations.size(); }
   std::uint64_t degree(VertexId v) const { return offsets[v + 1] - offsets[v]; }
+};
+
+// graph.hpp:33-39
+struct BatchPlan {
+  std::vector<std::uint64_t> blocks_required;
+  std::vector<std::uint64_t> prefix_sum;
+  std::vector<std::uint32_t> space_remaining;
+  std::uint64_t total_blocks() const { return prefix_sum.empty() ? 0 : prefix_sum.back(); }
 };
 
 // csr.hpp:29-45 — stable counting sort of (source, destination) pairs
@@ -125,6 +133,19 @@ class DynamicGraph {
   std::uint64_t active_edges() const { return dg_active_edges(h_); }
   bool vertex_alive(VertexId v) const { return dg_vertex_alive(h_, v) != 0; }
 
+  // graph.hpp:135-160
+  BatchPlan plan_batch(const CsrBatch& batch) const {
+    if (batch.kind != BatchKind::Insert) throw DataError("plan_batch: expected an insert batch");
+    BatchPlan plan;
+    const std::uint64_t n = batch.vertex_count();
+    plan.blocks_required.resize(n);
+    plan.prefix_sum.resize(n);
+    plan.space_remaining.resize(n);
+    check(dg_plan_batch_csr(h_, batch.offsets.data(), batch.offsets.size(), batch.destinations.data(),
+                            batch.destinations.size(), DG_MEM_HOST, plan.blocks_required.data(),
+                            plan.prefix_sum.data(), plan.space_remaining.data(), nullptr));
+    return plan;
+  }
   // graph.hpp:167-188
   void insert_batch(const CsrBatch& batch) {
     if (batch.kind != BatchKind::Insert) throw DataError("plan_batch: expected an insert batch");

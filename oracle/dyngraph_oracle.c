@@ -279,6 +279,34 @@ static int validate_batch(Oracle* g, const uint64_t* off, uint64_t n_off, const 
   return ORC_OK;
 }
 
+/* plan_batch (graph.hpp:135-160): validate_insert, then per vertex space_remaining (:149-150), blocks_required
+ * (:152-153) and their inclusive prefix sum (:154-156).  Nothing is mutated. */
+int orc_plan_batch(void* p, const uint64_t* off, uint64_t n_off, const uint32_t* dsts, uint64_t n,
+                   uint64_t* blocks_required, uint64_t* prefix_sum, uint32_t* space_remaining) {
+  Oracle* g = (Oracle*)p;
+  int rc = validate_batch(g, off, n_off, dsts, n);
+  if (rc) return rc;
+  const uint64_t V = g->size;
+  for (uint64_t v = 0; v < V; ++v) /* validate_insert, graph.hpp:320-328 */
+    if (off[v + 1] > off[v] && !g->alive[v]) {
+      snprintf(g->err, sizeof g->err, "csr batch: insert lists edges for retired vertex %llu", (unsigned long long)v);
+      return ORC_ERR_DATA;
+    }
+  uint64_t running = 0;
+  for (uint64_t v = 0; v < V; ++v) {
+    const Sentinel* s = &g->sent[v];
+    const uint64_t space = s->block_count == 0 ? 0 : g->B - s->last_insert_offset;
+    const uint64_t deg = off[v + 1] - off[v];
+    const uint64_t overflow = deg > space ? deg - space : 0;
+    const uint64_t required = (overflow + g->B - 1) / g->B;
+    space_remaining[v] = (uint32_t)space;
+    blocks_required[v] = required;
+    running += required;
+    prefix_sum[v] = running;
+  }
+  return ORC_OK;
+}
+
 /* insert_batch (graph.hpp:167-188) = plan_batch (:135-160) + ensure_available
  * + per-vertex insert_adjacency (:333-372) + commit_front. */
 int orc_insert_csr(void* p, const uint64_t* off, uint64_t n_off, const uint32_t* dsts, uint64_t n) {

@@ -111,6 +111,17 @@ int ref_delete_csr(void* p, const std::uint64_t* off, std::uint64_t n_off, const
   auto* r = static_cast<Ref*>(p);
   return guarded(r, [&] { r->g->delete_batch(make_csr(dyngraph::BatchKind::Delete, off, n_off, dsts, n)); });
 }
+// DynamicGraph::plan_batch (graph.hpp:135-160), copied out of the BatchPlan vectors
+int ref_plan_batch(void* p, const std::uint64_t* off, std::uint64_t n_off, const std::uint32_t* dsts, std::uint64_t n,
+                   std::uint64_t* blocks_required, std::uint64_t* prefix_sum, std::uint32_t* space_remaining) {
+  auto* r = static_cast<Ref*>(p);
+  return guarded(r, [&] {
+    const auto plan = r->g->plan_batch(make_csr(dyngraph::BatchKind::Insert, off, n_off, dsts, n));
+    std::copy(plan.blocks_required.begin(), plan.blocks_required.end(), blocks_required);
+    std::copy(plan.prefix_sum.begin(), plan.prefix_sum.end(), prefix_sum);
+    std::copy(plan.space_remaining.begin(), plan.space_remaining.end(), space_remaining);
+  });
+}
 int ref_insert_coo(void* p, const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t n,
                    double* seconds) {
   auto* r = static_cast<Ref*>(p);

@@ -7,10 +7,10 @@ library; constructing a DynamicGraph does, and fails loudly if it is missing.
 """
 from .csr import BatchKind, CsrBatch, compute_block_size, csr_from_pairs
 from .errors import CudaError, DataError, EngineError, Error
-from .graph import BatchIngest, DynamicGraph, GraphConfig
+from .graph import BatchIngest, BatchPlan, DynamicGraph, GraphConfig
 
 __all__ = [
-    "BatchIngest",
+    "BatchIngest", "BatchPlan",
     "BatchKind", "CsrBatch", "compute_block_size", "csr_from_pairs",
     "CudaError", "DataError", "EngineError", "Error",
     "DynamicGraph", "GraphConfig",

@@ -125,6 +125,8 @@ SIGNATURES = {
     "dg_submit_delete_coo": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
     "dg_flush": (C.c_int, [_H, u64p]),
     "dg_pending_ops": (C.c_uint64, [_H]),
+    "dg_plan_batch_csr": (C.c_int, [_H, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_int,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, u64p]),
 }
 
 _lib = None

@@ -1734,6 +1734,57 @@ int dg_bulk_init_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets,
   return insert_with_growth(h, [&] { return insert_csr_impl(h, offsets, n_offsets, destinations, n_edges, mem, true); });
 }
 
+// plan_batch (graph.hpp:135-160): validation of an insert batch + the BatchPlan vectors, nothing mutated
+int dg_plan_batch_csr(dg_graph* h, const uint64_t* offsets, uint64_t n_offsets, const uint32_t* destinations,
+                      uint64_t n_edges, int mem, uint64_t* blocks_required, uint64_t* prefix_sum,
+                      uint32_t* space_remaining, uint64_t* total_blocks) {
+  if (!h || !blocks_required || !prefix_sum || !space_remaining) return DG_ERR_DATA;
+  h->last_error.clear();
+  if (const int erc = enter(h)) return erc;
+  if (n_offsets != h->size + 1)  // csr.hpp:50-53
+    return fail(h, DG_ERR_DATA, "csr batch: offsets length " + std::to_string(n_offsets) +
+                                    " does not match vertex count " + std::to_string(h->size) + " + 1");
+  if (n_edges >= (1ull << 31)) return fail(h, DG_ERR_ENGINE, "batch too large (n must be < 2^31)");
+  if (int rc = require_pool(h)) return rc;
+  const uint64_t V = h->size;
+  WsSizer sz;
+  sz.add<unsigned long long>(n_offsets); sz.add<uint32_t>(n_edges);
+  sz.add<uint32_t>(V + 2);
+  sz.add<unsigned long long>(V); sz.add<unsigned long long>(V); sz.add<uint32_t>(V);
+  sz.total += scan_ws_bytes(V);
+  int rc = ws_reserve(h, sz.total);
+  if (rc != DG_OK) return rc;
+  const unsigned long long* d_off;
+  const uint32_t* d_dst;
+  if ((rc = stage_in(h, reinterpret_cast<const unsigned long long*>(offsets), n_offsets, mem, &d_off)) != DG_OK) return rc;
+  if ((rc = stage_in(h, destinations, n_edges, mem, &d_dst)) != DG_OK) return rc;
+  if ((rc = op_begin(h, n_edges, V)) != DG_OK) return rc;
+  GraphView g = view(h);
+  uint32_t* run_start = ws_alloc<uint32_t>(h, V + 2);
+  const bool host_out = mem == DG_MEM_HOST;
+  unsigned long long* d_req = host_out ? ws_alloc<unsigned long long>(h, V) : reinterpret_cast<unsigned long long*>(blocks_required);
+  unsigned long long* d_pre = host_out ? ws_alloc<unsigned long long>(h, V) : reinterpret_cast<unsigned long long*>(prefix_sum);
+  uint32_t* d_space = host_out ? ws_alloc<uint32_t>(h, V) : space_remaining;
+  DG_LAUNCH(h, "csr_validate_offsets_kernel", csr_validate_offsets_kernel<<<grid_for(h, n_offsets, 256), 256, 0, h->stream>>>(
+      g, d_off, (uint32_t)n_offsets, n_edges, /*check_dead_source=*/1, run_start, h->d_op()));
+  if (n_edges > 0) {
+    DG_LAUNCH(h, "validate_dsts_kernel", validate_dsts_kernel<<<grid_for(h, n_edges, 256 * 4), 256, 0, h->stream>>>(g, d_dst, (uint32_t)n_edges, h->d_op()));
+  }
+  if (V > 0) {
+    launch_scan(h, "scan_kernel<batch_plan>", V, d_n_runs(h), BatchPlanIn{g, run_start}, BatchPlanOut{g, d_req, d_pre, d_space},
+                BatchPlanFin{h->d_op()});
+    if (host_out) {
+      DG_CUDA(h, cudaMemcpyAsync(blocks_required, d_req, V * 8, cudaMemcpyDeviceToHost, h->stream));
+      DG_CUDA(h, cudaMemcpyAsync(prefix_sum, d_pre, V * 8, cudaMemcpyDeviceToHost, h->stream));
+      DG_CUDA(h, cudaMemcpyAsync(space_remaining, d_space, V * 4, cudaMemcpyDeviceToHost, h->stream));
+    }
+  }
+  rc = op_end(h);
+  h->report.blocks_popped = 0;   // (a plan pops nothing)
+  if (rc == DG_OK && total_blocks) *total_blocks = h->h_blk->op.total_need;
+  return rc;
+}
+
 // ---- delete -------------------------------------------------------------------
 static int delete_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, int mem, bool check_only) {
   if (!h) return DG_ERR_DATA;

@@ -471,6 +471,34 @@ __device__ __forceinline__ unsigned long long plan_word(const GraphView& g, uint
   return ((unsigned long long)units << 32) | need;
 }
 
+// BatchPlan as the reference returns it (graph.hpp:33-39, :135-160): per vertex the free slots of its last-insert
+// block, the fresh blocks the batch needs, and their INCLUSIVE prefix sum in vertex order (the pop schedule) — an
+// ordered scan, unlike the range allocation the ops themselves use.
+struct BatchPlanIn {
+  GraphView g;
+  const uint32_t* run_start;   // 32-bit copy of the validated offsets
+  __device__ unsigned long long operator()(unsigned long long v) const {
+    const uint32_t c = run_start[v + 1] - run_start[v];
+    return plan_word(g, g.deg[v], c) & 0xFFFFFFFFull;
+  }
+};
+struct BatchPlanOut {
+  GraphView g;
+  unsigned long long* blocks_required;
+  unsigned long long* prefix_sum;
+  uint32_t* space_remaining;
+  __device__ void operator()(unsigned long long v, unsigned long long excl, unsigned long long need) const {
+    const uint32_t d = g.deg[v];
+    blocks_required[v] = need;
+    prefix_sum[v] = excl + need;
+    space_remaining[v] = blocks_for(g, d) * g.B - d;   // block_size - last_insert_offset; 0 without a block (graph.hpp:149-150)
+  }
+};
+struct BatchPlanFin {
+  OpState* op;
+  __device__ void operator()(unsigned long long total) const { op->total_need = total; }
+};
+
 struct PlanAux {
   uint32_t d, tail;  // degree / tail block of the source before the batch
 };

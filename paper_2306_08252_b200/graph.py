@@ -63,6 +63,17 @@ class _Arg:
             self.n = a.size
 
 
+@dataclass
+class BatchPlan:
+    """graph.hpp:33-39."""
+    blocks_required: np.ndarray
+    prefix_sum: np.ndarray
+    space_remaining: np.ndarray
+
+    def total_blocks(self) -> int:
+        return int(self.prefix_sum[-1]) if len(self.prefix_sum) else 0
+
+
 class DynamicGraph:
     def __init__(self, config: GraphConfig | None, initial_vertex_count: int, block_size: int):
         self._lib = _lib.load()
@@ -133,6 +144,19 @@ class DynamicGraph:
             raise DataError("delete_batch: expected a delete batch")  # graph.hpp:196-198
         off, dst = _Arg(batch.offsets, np.uint64), _Arg(batch.destinations, np.uint32)
         self._check(self._lib.dg_delete_batch_csr(self._h, off.ptr, off.n, dst.ptr, dst.n, dst.mem))
+
+    def plan_batch(self, batch: CsrBatch) -> "BatchPlan":
+        """graph.hpp:135-160: validation of an insert batch + its BatchPlan (nothing is mutated)."""
+        if batch.kind != BatchKind.Insert:
+            raise DataError("plan_batch: expected an insert batch")  # graph.hpp:136-138
+        off, dst = _Arg(np.asarray(batch.offsets), np.uint64), _Arg(np.asarray(batch.destinations), np.uint32)
+        n = max(off.n - 1, 0)
+        req, pre, space = np.zeros(n, np.uint64), np.zeros(n, np.uint64), np.zeros(n, np.uint32)
+        total = C.c_uint64()
+        self._check(self._lib.dg_plan_batch_csr(self._h, off.ptr, off.n, dst.ptr, dst.n, _lib.DG_MEM_HOST,
+                                                C.c_void_p(req.ctypes.data), C.c_void_p(pre.ctypes.data),
+                                                C.c_void_p(space.ctypes.data), C.byref(total)))
+        return BatchPlan(req, pre, space)
 
     def bulk_init(self, offsets, destinations):
         """ctor + first insert_batch of the whole graph (io/workload.hpp:113-139)."""

@@ -56,6 +56,7 @@ def _bind(lib, prefix: str):
         "degrees": (C.c_int, [_vp, _vp]),
         "export_csr": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int]),
         "digest": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "plan_batch": (C.c_int, [_vp, _vp, C.c_uint64, _vp, C.c_uint64, _vp, _vp, _vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, f"{prefix}_{name}")
@@ -131,6 +132,14 @@ class CpuGraph:
     def delete_csr(self, offsets, dsts):
         o, d = np.ascontiguousarray(offsets, np.uint64), _u32(dsts)
         return self._f("delete_csr")(self.h, _p(o), len(o), _p(d), len(d))
+
+    def plan_batch(self, offsets, dsts):
+        """(rc, blocks_required, prefix_sum, space_remaining) of plan_batch (graph.hpp:135-160)"""
+        o, d = np.ascontiguousarray(offsets, np.uint64), _u32(dsts)
+        n = max(len(o) - 1, 0)
+        req, pre, space = np.zeros(n, np.uint64), np.zeros(n, np.uint64), np.zeros(n, np.uint32)
+        rc = self._f("plan_batch")(self.h, _p(o), len(o), _p(d), len(d), _p(req), _p(pre), _p(space))
+        return rc, req, pre, space
 
     def query(self, src, dst):
         s, d = _u32(src), _u32(dst)

@@ -325,6 +325,54 @@ def test_auto_block_size_from_first_batch():
             g3.close()
 
 
+def test_plan_batch_over_the_abi():
+    """dg_plan_batch_csr = plan_batch (graph.hpp:135-160) -> BatchPlan (:33-39).  The reference's PlanBatch.* tests
+    (batch_engine_test.cpp:84-148) restated through the ABI, then random insert-only histories against the oracle
+    (after deletes space_remaining follows the compact chains here and the holes there: layout, not compared)."""
+    from paper_2306_08252_b200 import BatchKind, CsrBatch, DataError, DynamicGraph, EngineError, GraphConfig
+    def csr(off, dst, kind=BatchKind.Insert):
+        return CsrBatch(kind, np.array(off, np.uint64), np.array(dst, np.uint32))
+    g = DynamicGraph(GraphConfig(pool_blocks=1024), 3, 4)
+    plan = g.plan_batch(csr([0, 10, 10, 10], [1] * 10))
+    assert (plan.blocks_required[0], plan.space_remaining[0], plan.total_blocks()) == (3, 0, 3)     # CeilOfOverflowByBlockSize
+    g.insert_batch(csr([0, 6, 6, 6], [1] * 6))
+    plan = g.plan_batch(csr([0, 10, 10, 10], [2] * 10))
+    assert (plan.space_remaining[0], plan.blocks_required[0]) == (2, 2)                             # SpaceRemainingReducesRequirement
+    assert g.active_edges() == 6 and g.stats()["pool_blocks_in_use"] == 2                           # nothing was mutated
+    g = DynamicGraph(GraphConfig(pool_blocks=1024), 4, 4)
+    plan = g.plan_batch(csr([0, 0, 0, 1, 1], [0]))
+    assert list(plan.blocks_required) == [0, 0, 1, 0] and list(plan.prefix_sum) == [0, 0, 1, 1]     # ZeroDegreeNeedsNothing
+    for off, dst in (([0, 1, 1], [0]), ([0, 2, 1, 2, 2], [0, 1]), ([1, 1, 1, 1, 1], [0]), ([0, 1, 1, 1, 1], [4]),
+                     ([0, 1, 1, 1, 2], [0])):                                                       # MalformedCsrRejected
+        with pytest.raises(DataError):
+            g.plan_batch(csr(off, dst))
+    with pytest.raises(DataError):
+        g.plan_batch(csr([0, 0, 0, 0, 0], [], BatchKind.Delete))
+    g.delete_vertices(np.array([2], np.uint32))
+    with pytest.raises(DataError):                                                                  # graph.hpp:322-327
+        g.plan_batch(csr([0, 0, 0, 1, 1], [0]))
+    with pytest.raises(EngineError):                                                                # no pool yet
+        DynamicGraph(GraphConfig(pool_bytes=1 << 20), 4, 0).plan_batch(csr([0, 0, 0, 1, 1], [0]))
+    rng = np.random.default_rng(8)
+    orc = load_oracle()
+    for B in (1, 5, 32):
+        V = 3000
+        g = DynamicGraph(GraphConfig(pool_blocks=1 << 16), V, B)
+        o = CpuGraph(orc, "orc", V, B, 1 << 28)
+        for step in range(5):
+            n = int(rng.integers(1, 30000))
+            s = np.sort(rng.zipf(1.4, n) % V).astype(np.uint32)
+            d = rng.integers(0, V, n).astype(np.uint32)
+            off = np.zeros(V + 1, np.uint64)
+            np.cumsum(np.bincount(s, minlength=V), out=off[1:])
+            plan, (rc, req, pre, space) = g.plan_batch(csr(off, d)), o.plan_batch(off, d)
+            assert rc == 0 and np.array_equal(plan.blocks_required, req) and np.array_equal(plan.prefix_sum, pre)
+            assert np.array_equal(plan.space_remaining, space)
+            g.insert_batch(csr(off, d)); o.insert_csr(off, d)
+            assert g.last_op_report()["blocks_popped"] == plan.total_blocks()
+        g.close()
+
+
 def test_device_resident_batches():
     import torch
     from paper_2306_08252_b200 import DynamicGraph, GraphConfig
