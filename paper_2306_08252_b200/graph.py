@@ -193,12 +193,15 @@ class DynamicGraph:
         return int(t.value)
 
     def flush(self) -> int:
-        """Waits for every submitted op; raises the first failure; returns how many were applied."""
+        """Waits for every submitted op; raises the first failure; returns how many ops were applied since the last
+        flush() that returned (a flush that raises keeps its count for the next one: after a failure, call flush()
+        once more to learn how many ops went in before the failed one)."""
         n = C.c_uint64()
         rc = self._lib.dg_flush(self._h, C.byref(n))
-        self._last_flush_applied = int(n.value)
+        self._applied_pending = getattr(self, "_applied_pending", 0) + int(n.value)
         self._check(rc)
-        return int(n.value)
+        out, self._applied_pending = self._applied_pending, 0
+        return out
 
     def pending_ops(self) -> int:
         return int(self._lib.dg_pending_ops(self._h))
