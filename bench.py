@@ -67,6 +67,8 @@ def parse_args():
     ap.add_argument("--pool-initial-fraction", type=float, default=0.0,
                     help="start with this fraction of the pre-sized pool and let the growth policy (80 %% trigger / 25 %% "
                          "rounds / on-demand, block_pool.hpp:162-189) commit the rest in place; 0 = pre-sized, no growth")
+    ap.add_argument("--group", default="auto", choices=["auto", "count", "radix"],
+                    help="how COO batches are grouped by source (GraphConfig.group); auto = chosen per batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -375,7 +377,7 @@ def run_b200_arm(args):
                     g.close()
                 t0 = time.perf_counter()
                 g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream,
-                                             workspace_bytes=ws_hint, **grow), V, B)
+                                             workspace_bytes=ws_hint, group=args.group, **grow), V, B)
                 create_ms = (time.perf_counter() - t0) * 1e3
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 flush.zero_()
@@ -390,7 +392,7 @@ def run_b200_arm(args):
             if not args.no_profile:   # one more, untimed, build with per-kernel events
                 g.close()
                 g = DynamicGraph(GraphConfig(device=local, pool_blocks=pool_blocks, stream=stream.cuda_stream,
-                                             workspace_bytes=ws_hint, **grow), V, B)
+                                             workspace_bytes=ws_hint, group=args.group, **grow), V, B)
                 g.profile_enable(True)
                 g.bulk_init(off, csr_dst)
                 g.profile_enable(False)
@@ -530,6 +532,8 @@ def run_b200_arm(args):
             value_api = "ShardedDynamicGraph.insert_pairs / delete_pairs (synchronous per op)"
         reps = [step(i, reports=True) for i in range(W, W + K)]   # same batches again, untimed: op reports
         launches = sum(r[0]["kernel_launches"] + r[1]["kernel_launches"] for r in reps)
+        if sharded is None:
+            launches += 2 * K   # the timed pass submits its ops: one op_arm_kernel per op on top of the op's own kernels
         ins_ms, del_ms = split_pass()
         e2e = None
         if not args.no_e2e:
