@@ -191,9 +191,6 @@ struct dg_graph {
   std::string deferred_error;
 
   Workspace ws;
-  // compaction scratch (grown on demand, survives workspace resets)
-  unsigned long long* mv_hole = nullptr;
-  uint64_t mv_cap = 0;
 
   // independent kernels of one op (chain walks, the match tiers) run side by side on two
   // auxiliary streams between a fork and a join on the op's stream
@@ -700,12 +697,13 @@ void enter_quiet(const dg_graph* ch) {
 // ---- scan / sort launchers -------------------------------------------------
 template <class In, class Out, class Fin>
 void launch_scan(dg_graph* h, const char* name, uint64_t n_bound, const unsigned long long* n_ptr,
-                 In in, Out out, Fin fin) {
+                 In in, Out out, Fin fin, cudaStream_t stream = nullptr) {
+  if (stream == nullptr) stream = h->stream;
   const size_t words = scan_scratch_words(n_bound);
   unsigned long long* scratch = ws_alloc<unsigned long long>(h, words);
-  cudaMemsetAsync(scratch, 0, words * sizeof(unsigned long long), h->stream);
+  cudaMemsetAsync(scratch, 0, words * sizeof(unsigned long long), stream);
   const unsigned tiles = (unsigned)std::max<uint64_t>(1, (n_bound + kScanTile - 1) / kScanTile);
-  DG_LAUNCH(h, name, scan_kernel<<<tiles, kScanThreads, 0, h->stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
+  DG_LAUNCH(h, name, scan_kernel<<<tiles, kScanThreads, 0, stream>>>(n_ptr, scratch, h->d_op(), in, out, fin));
 }
 // unordered range allocation over [0, *n_ptr): see alloc_kernel
 template <class In, class Out, class Fin>
@@ -921,22 +919,6 @@ int insert_with_growth(dg_graph* h, F&& run) {
   }
   if (rc == DG_OK) after_pop(h, h->report.blocks_popped);
   return rc;
-}
-
-int ensure_mv_scratch(dg_graph* h, uint64_t entries) {
-  if (entries <= h->mv_cap) return DG_OK;
-  DG_CUDA(h, cudaStreamSynchronize(h->stream));
-  // (the old scratch is only given up once the new one exists: a failed allocation leaves the graph usable)
-  const uint64_t want = entries + entries / 4 + 1024;
-  unsigned long long* fresh = nullptr;
-  if (cudaMalloc(&fresh, want * sizeof(unsigned long long)) != cudaSuccess) {
-    cudaGetLastError();
-    return fail(h, DG_ERR_ENGINE, "compaction scratch: device allocation failed");
-  }
-  if (h->mv_hole) cudaFree(h->mv_hole);
-  h->mv_hole = fresh;
-  h->mv_cap = want;
-  return DG_OK;
 }
 
 // Stage a caller array on the device if it lives on the host.
@@ -1307,11 +1289,9 @@ int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs
   GraphView g = view(h);
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
   uint32_t* run_matched = w.zero3;   // (zeroed per run by the enumeration plan)
-  uint32_t* hole_cnt = w.zero3 + (runs_bound + 1);
-  uint32_t* surv_cnt = w.zero3 + 2 * (runs_bound + 1);
-  uint32_t* mv_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   uint32_t* free_off = ws_alloc<uint32_t>(h, runs_bound + 1);
   uint32_t* wl_mask = ws_alloc<uint32_t>(h, (wl_bound + 1) * g.mw);
+  uint32_t* hole_prefix = ws_alloc<uint32_t>(h, 2 * wl_bound + 2);   // holes / survivors before every work-list block
   unsigned long long* tally = tally_buf(h);   // persistent, zero between ops
   const bool par = !h->profiling;
   cudaStream_t s0 = side(h, 0), s1 = side(h, 1);
@@ -1352,41 +1332,40 @@ int delete_run(dg_graph* h, const BatchView& b, const Worklist& w, uint64_t runs
   else enqueue_match_impl<true, false>(h, b, w, n, run_matched, wl_mask, nullptr, s0, s1, s1);
   tl_mark(h, "match_long", s0);
   tl_mark(h, "match_med_tiny", s1);
-  if (par) {
+  if (par) {   // both tails need every tier's matches
     cudaEventRecord(h->ev_join[1], s1);
+    cudaEventRecord(h->ev_join[0], s0);
     cudaStreamWaitEvent(s0, h->ev_join[1], 0);
+    cudaStreamWaitEvent(s1, h->ev_join[0], 0);
   }
-  const size_t ws_mark = h->ws.off;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    h->ws.off = ws_mark;
-    cudaStream_t st = attempt == 0 ? s0 : h->stream;
-    if (attempt > 0) cudaMemsetAsync(hole_cnt, 0, 2 * (runs_bound + 1) * 4, st);
-    launch_alloc(h, "alloc_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{g, w.run_deg, run_matched},
-                 MovesOut{mv_off, free_off}, MovesFin{g, h->d_op(), h->mv_cap}, st);
-    DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_resident(h, wl_bound, 256, delete_holes_kernel), 256, 0, st>>>(
-        g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, free_off, wl_mask, hole_cnt,
-        h->mv_hole, h->d_op()));
-    DG_LAUNCH(h, "delete_moves_kernel", delete_moves_kernel<<<grid_resident(h, wl_bound, 256, delete_moves_kernel), 256, 0, st>>>(
-        g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, mv_off, hole_cnt, surv_cnt,
-        h->mv_hole, h->d_op()));
-    tl_mark(h, "hub_tail", st);
-    if (par && attempt == 0) {
-      cudaEventRecord(h->ev_join[0], s0);
-      cudaStreamWaitEvent(h->stream, h->ev_join[0], 0);
-    }
-    const int rc = op_end(h);
-    if (rc != DG_OK) return rc;
-    if (h->submitting) return DG_OK;   // (submit_coo sized the scratch for the worst case: no retry to decide on)
-    if (h->h_blk->op.aux1 == 0) return DG_OK;
-    // compaction scratch was too small: nothing past the tombstones was touched; grow and redo
-    const int rc2 = ensure_mv_scratch(h, h->h_blk->op.aux0);
-    if (rc2 != DG_OK) return rc2;
+  // compaction of the hub chains, two independent halves side by side:
+  //   s1: ring positions of the freed blocks -> repair (degree / tail / head) + reclaim;
+  //   s0: hole / survivor numbering (one ordered scan over the work list) -> moves.
+  // Scratch is bounded by the blocks in use: nothing to size after the match, no retry.
+  launch_alloc(h, "alloc_kernel<moves>", runs_bound, d_n_runs(h), MovesIn{g, w.run_deg, run_matched},
+               MovesOut{free_off}, MovesFin{g, h->d_op()}, s1);
+  DG_LAUNCH(h, "delete_holes_kernel", delete_holes_kernel<<<grid_resident(h, wl_bound, 256, delete_holes_kernel), 256, 0, s1>>>(
+      g, b, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, free_off, h->d_op()));
+  tl_mark(h, "t_repair", s1);
+  launch_scan(h, "scan_kernel<holes>", 2 * wl_bound, &h->d_op()->hole_items,
+              HoleScanIn{g, w.wl_off, w.wl_run, w.run_deg, run_matched, wl_mask, h->d_op()}, HoleScanOut{hole_prefix},
+              HoleScanFin{hole_prefix, h->d_op()}, s0);
+  tl_mark(h, "t_scan", s0);
+  DG_LAUNCH(h, "delete_moves_kernel", delete_moves_kernel<<<grid_resident(h, wl_bound, 256, delete_moves_kernel), 256, 0, s0>>>(
+      g, w.wl_off, w.wl_handle, w.wl_run, w.run_deg, run_matched, wl_mask, hole_prefix, h->d_op()));
+  tl_mark(h, "hub_tail", s0);
+  if (par) {
+    cudaEventRecord(h->ev_join[0], s0);
+    cudaEventRecord(h->ev_join[1], s1);
+    cudaStreamWaitEvent(h->stream, h->ev_join[0], 0);
+    cudaStreamWaitEvent(h->stream, h->ev_join[1], 0);
   }
-  return fail(h, DG_ERR_ENGINE, "delete: compaction scratch retry failed");
+  return op_end(h);
 }
 inline size_t delete_matched_ws(const dg_graph* h, uint64_t runs_bound) {
   const uint64_t wl_bound = std::max<uint64_t>(1, h->blocks_in_use());
-  return 5 * aligned((runs_bound + 1) * 4) + aligned((wl_bound + 1) * ((h->B + 31) / 32) * 4) + alloc_ws_bytes();
+  return 5 * aligned((runs_bound + 1) * 4) + aligned((wl_bound + 1) * ((h->B + 31) / 32) * 4) + alloc_ws_bytes() +
+         aligned((2 * wl_bound + 2) * 4) + scan_ws_bytes(2 * wl_bound);
 }
 
 // delete of a COO batch: group (either strategy) + enumeration plan with classification, then delete_run
@@ -1491,7 +1470,6 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
     const int rc = create_pool(h, block_size);
     if (rc != DG_OK) return bail(rc, h->last_error);
   }
-  if (ensure_mv_scratch(h, 1 << 16) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
   if (cudaMalloc(&h->zscratch, kZScratchWords * sizeof(unsigned long long)) != cudaSuccess) {
     cudaGetLastError();
     return bail(DG_ERR_ENGINE, "dg_create: device allocation failed");
@@ -1536,7 +1514,6 @@ void dg_destroy(dg_graph* h) {
   for (auto& pd : h->pending) cudaEventDestroy(pd.done);
   for (auto e : h->done_pool) cudaEventDestroy(e);
   cudaFree(h->ws.base);
-  cudaFree(h->mv_hole);
   cudaFree(h->cnt_buf);
   cudaFree(h->zscratch);
   for (int i = 0; i < 2; ++i) {
@@ -1825,7 +1802,8 @@ int dg_delete_batch_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, u
 //     in flight can pop at most must cover this insert (an insert pops at most one block per entry);
 //   - commit_front's growth rule (block_pool.hpp:162-172): cumulative consumption, counted with the same
 //     bounds, must stay below the trigger — the pool never has to grow behind a submitted op;
-//   - compaction scratch of the hub path of a delete: moves <= live edges / 2, allocated up front.
+//   - every scratch array of an op is bounded by the batch and by (an upper bound of) the blocks in use: nothing is
+//     sized from what an earlier op of the stream produced.
 static int submit_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uint64_t n, bool is_insert, uint64_t* ticket) {
   if (!h) return DG_ERR_DATA;
   if (ticket) *ticket = 0;
@@ -1851,12 +1829,6 @@ static int submit_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uin
     if (h->pool_vm && h->total_capacity > 0 &&
         (double)(h->consumed + h->pending_pop_bound + n) / (double)h->total_capacity >= h->trigger)
       async_ok = false;
-  }
-  if (async_ok && !is_insert) {
-    uint64_t live_bound = h->active_edges;
-    for (const auto& pd : h->pending)
-      if (pd.is_insert) live_bound += pd.n;
-    if (ensure_mv_scratch(h, live_bound / 2 + 1) != DG_OK) async_ok = false;
   }
   if (!async_ok) {
     int rc = drain(h);
@@ -2245,7 +2217,7 @@ int dg_memory_get(const dg_graph* h, dg_memory* out) {
   out->pool_bytes = h->NB ? h->blocks_in_use() * ((uint64_t)h->B * 4 + 4) : 0;
   out->queue_bytes = h->NB * 4;
   out->pool_reserved_bytes = h->pool_vm ? h->vm_slab.mapped + h->vm_next.mapped : h->NB * ((uint64_t)h->B * 4 + 4);   // committed device memory
-  out->workspace_bytes = h->ws.cap + h->mv_cap * 8;
+  out->workspace_bytes = h->ws.cap;
   return DG_OK;
 }
 

@@ -81,6 +81,7 @@ struct OpState {
   unsigned long long slots_fused;   // part of `slots` inspected by fused_delete_kernel
   unsigned int n_fmed;              // sources of the fused medium class listed by the enumeration plan
   unsigned int scatter_ctas;        // CTAs of group_scatter_kernel that have finished (fused_delete_kernel starts beside it)
+  unsigned long long hole_items;    // 2 x wl_blocks: items of the hole / survivor scan of the hub compaction (device-resident bound)
 };
 
 __device__ __forceinline__ void set_error(OpState* op, uint32_t code, uint32_t detail,
@@ -138,10 +139,13 @@ scan_kernel(const unsigned long long* __restrict__ n_ptr, unsigned long long* sc
   __shared__ unsigned long long s_tile_excl;
   __shared__ unsigned int s_tile;
   const unsigned long long n = *n_ptr;
+  const unsigned long long num_tiles = (n + kScanTile - 1) / kScanTile;
+  // (the grid is sized from a host-side bound: surplus CTAs leave before they take a ticket, so exactly num_tiles
+  // CTAs — the first to be scheduled — draw tiles 0 .. num_tiles - 1 in the order they start)
+  if (blockIdx.x >= num_tiles) return;
   if (threadIdx.x == 0) s_tile = atomicAdd(reinterpret_cast<unsigned int*>(scratch), 1u);
   __syncthreads();
   const unsigned int tile = s_tile;
-  const unsigned long long num_tiles = (n + kScanTile - 1) / kScanTile;
   if (tile >= num_tiles) return;
   unsigned long long* status = scratch + 2;
 

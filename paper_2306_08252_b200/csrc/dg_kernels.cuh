@@ -134,6 +134,7 @@ __device__ __forceinline__ void stage_rows32(const GraphView& g, uint32_t (*dst)
                 g.slab + (unsigned long long)hu * g.B + 32u * p + lane);
   }
 }
+__device__ __forceinline__ uint32_t low_bits32(uint32_t n) { return n >= 32u ? 0xFFFFFFFFu : ((1u << n) - 1u); }
 // second, independent hash for the membership filters
 __device__ __forceinline__ uint32_t filter_hash(uint32_t x, int bits) { return (x * 0x85EBCA6Bu) >> (32 - bits); }
 
@@ -1677,6 +1678,7 @@ struct EnumFin {
     op->n_fmed = total_c;   // sources of the fused medium class (their record slots came out of the scan)
     if (set_runs) op->n_runs = total_a >> 32;
     op->wl_blocks = total_b & 0xFFFFFFFFull;
+    op->hole_items = 2ull * (total_b & 0xFFFFFFFFull);
     op->n_big = total_b >> 32;
     if ((total_b & 0xFFFFFFFFull) > wl_cap) {  // cannot happen: wl_cap >= blocks in use (host mirror)
       op->err = 3;
@@ -2231,63 +2233,106 @@ match_long_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
 }
 
 // ---------------------------------------------------------------------------
-// delete: compaction plan — per source, moves <= min(matched, new degree)
+// delete, hub path: compaction of the chains the match tiers tombstoned.
+//
+// A source with m matches keeps nd = d - m entries: every hole (matched slot) BELOW nd takes a survivor (live slot)
+// from AT OR ABOVE nd; holes and survivors are equally many.  Which survivor fills which hole is free, so both are
+// simply numbered in chain order: ONE ordered scan over the work list gives every block the number of holes (and of
+// survivors) in the blocks before it, survivor j of a source moves into hole j of the source.  The hole list is never
+// materialised — a block's holes are the bits of its match mask — so the scratch is two prefix words per work-list
+// block, bounded by the blocks in use and known before the op is enqueued (round 1 kept a list of hole addresses
+// whose size, up to live edges / 2, was only known after the match: a host-side grow-and-retry in the middle of the op).
 // ---------------------------------------------------------------------------
 struct NoAux {};
+// blocks past each source's new tail go back to the ring: the plan hands every source its range of ring positions,
+// so the push needs neither atomics nor barriers (reclaim, block_pool.hpp:192-209)
 struct MovesIn {
   using Aux = NoAux;
   GraphView g;
   const uint32_t* run_deg;
   const uint32_t* run_matched;
-  // word a: blocks past the source's new tail (they go back to the ring: the plan hands every source
-  // its range of ring positions, so the push needs neither atomics nor barriers);  word b: moves
   __device__ Sum2 operator()(unsigned long long r, Aux&) const {
     const uint32_t m = run_matched[r];
     const uint32_t d = run_deg[r];
     const uint32_t nd = d - m;
     const uint32_t freed = (m != 0 && g.reclaim) ? blocks_for(g, d) - blocks_for(g, nd) : 0u;
-    return Sum2{freed, min(m, nd)};
+    return Sum2{freed, 0ull};
   }
 };
 struct MovesOut {
-  uint32_t* mv_off;
   uint32_t* free_off;
-  __device__ void operator()(unsigned long long r, unsigned long long excl_a, unsigned long long excl_b,
+  __device__ void operator()(unsigned long long r, unsigned long long excl_a, unsigned long long,
                              Sum2, const NoAux&) const {
-    mv_off[r] = (uint32_t)excl_b;
     free_off[r] = (uint32_t)excl_a;
   }
 };
 struct MovesFin {
   GraphView g;
   OpState* op;
-  unsigned long long mv_cap;
-  __device__ void operator()(unsigned long long total_a, unsigned long long total, unsigned int) const {
-    op->aux0 = total;                      // scratch entries needed
-    op->aux1 = total > mv_cap ? 1ull : 0ull;  // host grows the scratch and re-runs the tail
-    if (total <= mv_cap) {                 // reclaim (block_pool.hpp:192-209): one cursor bump for the whole batch
-      // (atomics: the warp-owned sources push to the same ring from fused_delete_kernel, side by side)
-      op->front_old = atomicAdd(&g.st->rear, total_a);   // first ring position of the pushed handles
-      atomicAdd(&op->pushed, total_a);
-    }
+  __device__ void operator()(unsigned long long total_a, unsigned long long, unsigned int) const {
+    // one cursor bump for the whole batch (atomics: the warp-owned sources push to the same ring from
+    // fused_delete_kernel, side by side)
+    op->front_old = atomicAdd(&g.st->rear, total_a);   // first ring position of the pushed handles
+    atomicAdd(&op->pushed, total_a);
   }
 };
 
-// delete, step A — a thread per block of the touched chains, reading only the
-// match masks: lists the holes below the new degree (tickets from per-source
-// counters), returns blocks past the new tail to the ring rear at the positions
-// the plan reserved for their source (block_pool.hpp:192-209) and, on a
-// source's first block, repairs degree / tail / head (detach_empty_tail,
-// graph.hpp:398-414).  No barriers, no shared cursor.
+// holes below / survivors at or above the new degree in work-list block w
+struct BlockHoles {
+  uint32_t holes, survivors;
+};
+__device__ __forceinline__ BlockHoles block_holes(const GraphView& g, const uint32_t* __restrict__ wl_off,
+                                                  const uint32_t* __restrict__ wl_run, const uint32_t* __restrict__ run_deg,
+                                                  const uint32_t* __restrict__ run_matched, const uint32_t* __restrict__ wl_mask,
+                                                  uint32_t w) {
+  const uint32_t r = wl_run[w] & kRunMask;
+  const uint32_t m = run_matched[r];
+  if (m == 0) return BlockHoles{0u, 0u};
+  const uint32_t d = run_deg[r];
+  const uint32_t nd = d - m;
+  const uint32_t base = (w - wl_off[r]) * g.B;
+  const uint32_t cnt = min(g.B, d - base);               // live + tombstoned slots of the block
+  const uint32_t lo = nd > base ? min(cnt, nd - base) : 0u;   // slots [0, lo) lie below the new degree
+  uint32_t below = 0, above = 0;
+  for (uint32_t i = 0; i < g.mw && 32u * i < cnt; ++i) {
+    const uint32_t bits = wl_mask[(unsigned long long)w * g.mw + i] & low_bits32(cnt - 32u * i);
+    const uint32_t lo_bits = lo > 32u * i ? low_bits32(lo - 32u * i) : 0u;
+    below += __popc(bits & lo_bits);
+    above += __popc(bits & ~lo_bits);
+  }
+  return BlockHoles{below, (cnt - lo) - above};
+}
+// ordered scan over 2 W items: [0, W) holes per block, [W, 2 W) survivors per block; prefix[i] = exclusive prefix
+struct HoleScanIn {
+  GraphView g;
+  const uint32_t *wl_off, *wl_run, *run_deg, *run_matched, *wl_mask;
+  const OpState* op;
+  __device__ unsigned long long operator()(unsigned long long i) const {
+    const unsigned long long W = op->wl_blocks;
+    const BlockHoles h = block_holes(g, wl_off, wl_run, run_deg, run_matched, wl_mask, (uint32_t)(i < W ? i : i - W));
+    return i < W ? h.holes : h.survivors;
+  }
+};
+// (prefixes are kept modulo 2^32: only differences inside one source are ever taken, and a source has < 2^32 slots)
+struct HoleScanOut {
+  uint32_t* prefix;
+  __device__ void operator()(unsigned long long i, unsigned long long excl, unsigned long long) const { prefix[i] = (uint32_t)excl; }
+};
+struct HoleScanFin {
+  uint32_t* prefix;
+  const OpState* op;
+  __device__ void operator()(unsigned long long total) const { prefix[2ull * op->wl_blocks] = (uint32_t)total; }
+};
+
+// delete, step A — a thread per block of the touched chains: returns blocks past the new tail to the ring rear at
+// the positions the plan reserved for their source (block_pool.hpp:192-209) and, on a source's first block,
+// repairs degree / tail / head (detach_empty_tail, graph.hpp:398-414).  No barriers, no shared cursor.
 __global__ void __launch_bounds__(256)
 delete_holes_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_off,
                     const uint32_t* __restrict__ wl_handle, const uint32_t* __restrict__ wl_run,
                     const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ run_matched,
-                    const uint32_t* __restrict__ mv_off, const uint32_t* __restrict__ free_off,
-                    const uint32_t* __restrict__ wl_mask,
-                    uint32_t* __restrict__ hole_cnt, unsigned long long* __restrict__ hole_addr,
-                    OpState* op) {
-  if (op->err || op->aux1) return;
+                    const uint32_t* __restrict__ free_off, OpState* op) {
+  if (op->err) return;
   __shared__ unsigned long long s_warp[8];
   const uint32_t W = (uint32_t)op->wl_blocks;
   const unsigned long long rear_old = op->front_old;
@@ -2301,28 +2346,6 @@ delete_holes_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_of
     const uint32_t d = run_deg[r];
     const uint32_t nd = d - m;
     const uint32_t new_nb = blocks_for(g, nd);
-    const uint32_t base = kb * g.B;
-    if (base < nd) {
-      const uint32_t lim = nd - base;  // slots [0, lim) of this block stay below the new degree
-      uint32_t nh = 0;
-      for (uint32_t i = 0; i < g.mw && 32 * i < lim; ++i) {
-        uint32_t bits = wl_mask[(unsigned long long)w * g.mw + i];
-        if (lim - 32 * i < 32) bits &= (1u << (lim - 32 * i)) - 1u;
-        nh += __popc(bits);
-      }
-      if (nh) {
-        uint32_t idx = mv_off[r] + atomicAdd(&hole_cnt[r], nh);
-        for (uint32_t i = 0; i < g.mw && 32 * i < lim; ++i) {
-          uint32_t bits = wl_mask[(unsigned long long)w * g.mw + i];
-          if (lim - 32 * i < 32) bits &= (1u << (lim - 32 * i)) - 1u;
-          while (bits) {
-            const uint32_t bit = __ffs(bits) - 1;
-            bits &= bits - 1;
-            hole_addr[idx++] = (unsigned long long)h * g.B + 32 * i + bit;
-          }
-        }
-      }
-    }
     if (kb >= new_nb && g.reclaim)   // past the new tail: back to the ring, at the source's reserved positions
       g.ring[(rear_old + free_off[r] + (kb - new_nb)) % g.ring_cap] = h;
     if (kb == 0) {
@@ -2348,42 +2371,96 @@ delete_holes_kernel(GraphView g, BatchView b, const uint32_t* __restrict__ wl_of
   }
 }
 
-// delete, step B — a thread per block again; only blocks reaching past the new
-// degree do anything: every live entry there takes the next hole of its source.
+// delete, step B — a WARP per block of the touched chains, lane = slot; only blocks reaching past the new degree do
+// anything: survivor j of the source (numbered in chain order by the scan) moves into hole j.  One binary search
+// over the source's hole prefixes (the same for every lane) finds the block of the block's first hole; each lane
+// then steps from there to the block of its own hole — consecutive survivors take consecutive holes.  Every lane's
+// chain of dependent loads is a handful long: under the fused kernel's memory load a dependent access costs ~2 us.
 __global__ void __launch_bounds__(256)
 delete_moves_kernel(GraphView g, const uint32_t* __restrict__ wl_off,
                     const uint32_t* __restrict__ wl_handle, const uint32_t* __restrict__ wl_run,
                     const uint32_t* __restrict__ run_deg, const uint32_t* __restrict__ run_matched,
-                    const uint32_t* __restrict__ mv_off, const uint32_t* __restrict__ hole_cnt,
-                    uint32_t* __restrict__ surv_cnt, const unsigned long long* __restrict__ hole_addr,
+                    const uint32_t* __restrict__ wl_mask, const uint32_t* __restrict__ prefix,
                     OpState* op) {
-  if (op->err || op->aux1) return;
-  __shared__ unsigned long long s_warp[8];
+  if (op->err) return;
   const uint32_t W = (uint32_t)op->wl_blocks;
-  unsigned long long moves = 0;
-  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
+  const uint32_t* H = prefix;        // holes in the work-list blocks before w (mod 2^32)
+  const uint32_t* S = prefix + W;    // survivors in the work-list blocks before w (+ all holes, mod 2^32)
+  const int lane = lane_id();
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t moves = 0;
+  const uint32_t warp_id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (uint32_t it = 0; warp_id + (unsigned long long)nwarps * 32u * it < W; ++it) {
+   // 32 work-list blocks per warp and step, one per lane, STRIDED by the warp count: their survivor counts are looked
+   // at in one round trip, and neighbouring blocks — the last blocks of a hub, where its survivors sit — belong to
+   // different warps, so they are moved in parallel
+   const unsigned long long wl = warp_id + (unsigned long long)nwarps * (32u * it + (uint32_t)lane);
+   unsigned todo = __ballot_sync(kFull, wl < W && S[wl + 1] != S[wl]);
+   while (todo) {
+    const uint32_t w = warp_id + nwarps * (32u * it + (uint32_t)(__ffs(todo) - 1));
+    todo &= todo - 1;
     const uint32_t r = wl_run[w] & kRunMask;
-    const uint32_t m = run_matched[r];
-    if (m == 0 || hole_cnt[r] == 0) continue;
-    const uint32_t kb = w - wl_off[r];
+    const uint32_t w0 = wl_off[r];
     const uint32_t d = run_deg[r];
-    const uint32_t nd = d - m;
-    const uint32_t base = kb * g.B;
+    const uint32_t nd = d - run_matched[r];
+    const uint32_t base = (w - w0) * g.B;
     const uint32_t cnt = min(g.B, d - base);
-    if (base + cnt <= nd) continue;
+    const uint32_t lo = nd > base ? min(cnt, nd - base) : 0u;
+    const uint32_t j0 = S[w] - S[w0];   // hole rank of this block's first survivor
+    const uint32_t Hw0 = H[w0];
+    // largest block of [w0, w0 + new_nb) with H - H[w0] <= j0 (an empty block shares its prefix with its successor):
+    // a 32-ary search, every lane probes one position per step — three dependent loads for 32 K blocks
+    uint32_t a = w0, z = w0 + blocks_for(g, nd);   // answer in [a, z)
+    while (z - a > 1) {
+      const uint32_t span = z - a;
+      const uint32_t stp = (span + 31u) / 32u;
+      const uint32_t probe = a + (uint32_t)lane * stp;
+      const bool le = probe < z && (uint32_t)(H[probe] - Hw0) <= j0;
+      const unsigned mle = __ballot_sync(kFull, le);   // a prefix of the lanes (H is monotone); lane 0 always holds
+      const uint32_t last = 31u - (uint32_t)__clz(mle);
+      a = a + last * stp;
+      z = min(z, a + stp);
+    }
     const uint32_t* blk = g.slab + (unsigned long long)wl_handle[w] * g.B;
-    const uint32_t mo = mv_off[r];
-    for (uint32_t s = (nd > base ? nd - base : 0u); s < cnt; ++s) {
-      const uint32_t e = blk[s];
-      if (e != kTomb) {
-        const uint32_t t = atomicAdd(&surv_cnt[r], 1u);
-        g.slab[hole_addr[mo + t]] = e;
+    uint32_t done = 0;   // survivors of the block's earlier 32-slot rows
+    for (uint32_t s0 = 0; s0 < cnt; s0 += 32) {
+      const uint32_t s = s0 + lane;
+      const uint32_t mword = wl_mask[(unsigned long long)w * g.mw + (s0 >> 5)];
+      const bool surv = s >= lo && s < cnt && !((mword >> lane) & 1u);
+      const unsigned sm = __ballot_sync(kFull, surv);
+      if (surv) {
+        const uint32_t e = blk[s];
+        const uint32_t j = j0 + done + __popc(sm & ((1u << lane) - 1u));   // this survivor's hole rank in the source
+        uint32_t hb = a;
+        uint32_t k = j - (uint32_t)(H[hb] - Hw0);
+        uint32_t nh = H[hb + 1] - H[hb];
+        while (k >= nh) {   // (survivors == holes: never past the last block with holes)
+          k -= nh;
+          ++hb;
+          nh = H[hb + 1] - H[hb];
+        }
+        // the k-th hole of block hb: set bits of its mask below the new degree
+        const uint32_t hlim = min(g.B, nd - (hb - w0) * g.B);
+        uint32_t slot = 0;
+        for (uint32_t i = 0; i < g.mw; ++i) {
+          const uint32_t bits = wl_mask[(unsigned long long)hb * g.mw + i] & (hlim > 32u * i ? low_bits32(hlim - 32u * i) : 0u);
+          const uint32_t c = __popc(bits);
+          if (k < c) {
+            slot = 32u * i + __fns(bits, 0, (int)k + 1);
+            break;
+          }
+          k -= c;
+        }
+        g.slab[(unsigned long long)wl_handle[hb] * g.B + slot] = e;
         ++moves;
       }
+      done += __popc(sm);
     }
+   }
   }
-  const unsigned long long tv = block_reduce_sum(moves, s_warp);
-  if (threadIdx.x == 0 && tv) atomicAdd(&op->moves, tv);
+#pragma unroll
+  for (int dl = 16; dl > 0; dl >>= 1) moves += __shfl_xor_sync(kFull, moves, dl);
+  if (lane == 0 && moves) atomicAdd(&op->moves, (unsigned long long)moves);
 }
 
 // query: scatter sorted hit flags back to the caller's order
