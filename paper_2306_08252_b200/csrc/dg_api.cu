@@ -996,7 +996,7 @@ struct Worklist {
   uint32_t* big_list;  // chains longer than kLaneWalk blocks
   uint32_t* run_head;  // fused delete only: head block of the warp-owned sources (else nullptr)
   uint4* fmed_rec;     // fused delete only: sources of the medium class (two words each)
-  uint32_t* zero3;     // delete only: run_matched / hole_cnt / surv_cnt, zeroed per run by the enumeration plan
+  uint32_t* zero3;     // delete only: run_matched (+ two spare words per run), zeroed per run by the enumeration plan
   uint32_t zstride;
   EnumLists lists(dg_graph* h) const {
     return EnumLists{run_deg, wl_off, med_items, long_items, big_list, (uint32_t)big_bound(h), h->d_op(), run_head, fmed_rec,

@@ -34,7 +34,7 @@ enum ErrDetail : uint32_t {
   kErrOffsetsMonotone = 5,// csr.hpp:57-61
   kErrOffsetsEnd = 6,     // csr.hpp:62-66
   kErrPoolUnderflow = 7,  // block_pool.hpp:177-189
-  kErrScratch = 8,        // internal: compaction scratch too small, host retries
+  kErrScratch = 8,        // internal: a work list did not fit its bound (cannot happen: bounds come from the blocks in use)
   kErrPeer = 9,           // sharded store: the batch was rejected on another rank (or a peer never arrived)
   kErrSkipped = 10,       // submitted behind an op that failed: not applied (the failed op reports first, graph.hpp:168-171)
 };

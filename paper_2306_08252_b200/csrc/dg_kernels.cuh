@@ -1540,7 +1540,7 @@ struct EnumLists {
   uint32_t* run_head;  // fused delete: head block of every warp-owned source (nullptr: no fusion)
   uint4* fmed_rec;     // fused delete: sources of the medium class (a warp per source), two 16-byte words each
                        // {run, vertex, first target, targets} {degree, head, -, -}, filled through op->n_fmed
-  uint32_t* zero3;     // delete: run_matched / hole_cnt / surv_cnt of the run start at zero (no memset)
+  uint32_t* zero3;     // delete: run_matched (+ two spare words) of the run start at zero (no memset)
   uint32_t zstride;
   __device__ void write(uint32_t r, uint32_t d, uint32_t nblk, uint32_t k, uint32_t head, uint32_t v, uint32_t es,
                         unsigned long long excl_b, uint32_t med_slot) const {

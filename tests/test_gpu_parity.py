@@ -110,8 +110,9 @@ def test_reclaimed_blocks_are_reused():
     g.close()
 
 
-def test_compaction_scratch_regrows():
-    """One delete entry removing 100k copies with 100k survivors behind them (moves >> batch)."""
+def test_compaction_moves_far_exceed_the_batch():
+    """One delete entry removing 100k copies with 100k survivors behind them (moves >> batch): the hub compaction
+    numbers holes and survivors by a scan over the chain instead of listing them, so nothing is sized by the moves."""
     n = 100000
     g = GpuGraph(8, 32, pool_blocks=1 << 14)
     o = CpuGraph(load_oracle(), "orc", 8, 32, 1 << 30)
