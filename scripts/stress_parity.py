@@ -24,12 +24,78 @@ def main():
     ap.add_argument("--hubs", action="store_true",
                     help="hub-heavy scripts instead of the verify mix: few vertices, zipf sources, 50K-400K-entry batches "
                          "(chains of thousands of blocks, table tiers with several 4096-target slices, heavy CSR items)")
+    ap.add_argument("--submit", action="store_true",
+                    help="streams of SUBMITTED COO updates (dg_submit_*_coo, no host wait between ops, one flush per stream; some "
+                         "streams carry a rejected batch in the middle): final canonical state against the oracle port")
     a = ap.parse_args()
     from paper_2306_08252_b200 import BatchKind, DynamicGraph, GraphConfig, csr_from_pairs
     from tests.drivers import CpuGraph, GpuGraph, assert_same, load_oracle, run_script
     from tests.workloads import make_workload
     orc = load_oracle()
     fails, t0 = 0, time.time()
+    if a.submit:
+        import torch
+        from paper_2306_08252_b200 import DataError, EngineError
+
+        def dev(x):
+            return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint32).view(np.int32)).cuda()
+        for seed in range(a.first, a.first + a.seeds):
+            rng = np.random.default_rng(seed)
+            V = int(rng.choice([60, 900, 6000, 50000]))
+            B = int(rng.choice([32, 32, 32, 5, 33]))
+            grow = bool(rng.integers(0, 3) == 0)
+            g = DynamicGraph(GraphConfig(pool_blocks=(512 if grow else 1 << 21), pool_max_blocks=(1 << 21 if grow else 0),
+                                         group=str(rng.choice(["auto", "radix", "count"]))), V, B)
+            o = CpuGraph(orc, "orc", V, B, 2 << 30, 0.5, True, 1)
+            keep, log, what = [], [], ""
+            try:
+                for stream in range(int(rng.integers(1, 4))):
+                    n_ops = int(rng.integers(2, 9))
+                    bad_at = int(rng.integers(0, n_ops)) if rng.integers(0, 4) == 0 else -1
+                    applied_expect, failed, reported = 0, False, False
+                    for it in range(n_ops):
+                        n = int(rng.choice([1, 300, 20000, 120000]))
+                        s = (rng.zipf(float(rng.choice([1.2, 1.6])), n) % V).astype(np.uint32)
+                        d = rng.integers(0, V, n).astype(np.uint32)
+                        kind = "insert" if not log or rng.random() < 0.55 else "delete"
+                        if kind == "delete":
+                            ps, pd = log[int(rng.integers(0, len(log)))]
+                            k = min(n, len(ps)) * 7 // 10
+                            s[:k], d[:k] = ps[:k], pd[:k]
+                        if it == bad_at:
+                            d = d.copy(); d[int(rng.integers(0, n))] = V + 3   # csr.hpp:67-72: the whole batch is rejected
+                        ds, dd = dev(s), dev(d)
+                        keep.append((ds, dd))
+                        try:
+                            (g.submit_insert_pairs if kind == "insert" else g.submit_delete_pairs)(ds, dd)
+                        except DataError:
+                            failed = reported = True
+                            break
+                        if it == bad_at:
+                            failed = True   # (reported by a later submit or by the flush; nothing behind it may run)
+                        elif not failed:
+                            (o.insert_pairs if kind == "insert" else o.delete_pairs)(s, d)
+                            applied_expect += 1
+                            if kind == "insert":
+                                log.append((s, d))
+                    try:
+                        n_applied = g.flush()
+                    except DataError:
+                        reported = True
+                        n_applied = g.flush()
+                    assert reported == failed, "a rejected batch was not reported (or a good stream was)"
+                    assert n_applied == applied_expect, f"applied {n_applied} != {applied_expect}"
+                    assert g.active_edges() == o.active_edges(), "active edges"
+                    assert np.array_equal(np.asarray(g.degrees()), np.asarray(o.degrees())), "degrees"
+                ga, oa = g.export_csr(), o.export_csr()
+                assert np.array_equal(ga[0], oa[0]) and np.array_equal(ga[1], oa[1]), "adjacency"
+            except (AssertionError, EngineError) as e:
+                fails += 1
+                print(f"FAIL submit seed={seed} V={V} B={B} grow={grow}: {str(e)[:200]}", flush=True)
+            finally:
+                g.close(); o.close()
+        print(f"stress_parity --submit: {a.seeds} seeds, {fails} failures, {time.time() - t0:.0f} s")
+        return 1 if fails else 0
     if a.hubs:
         for seed in range(a.first, a.first + a.seeds):
             rng = np.random.default_rng(seed)
