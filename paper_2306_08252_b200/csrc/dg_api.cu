@@ -638,7 +638,10 @@ int retire_oldest(dg_graph* h, bool wait) {
     DG_CUDA(h, cudaEventSynchronize(p.done));
   } else {
     const cudaError_t q = cudaEventQuery(p.done);
-    if (q == cudaErrorNotReady) return DG_OK;
+    if (q == cudaErrorNotReady) {
+      cudaGetLastError();   // (not an error: keep it out of the launch-error checks)
+      return DG_OK;
+    }
     DG_CUDA(h, q);
   }
   h->pending.pop_front();
