@@ -2410,7 +2410,8 @@ delete_moves_kernel(GraphView g, const uint32_t* __restrict__ wl_off,
     const uint32_t Hw0 = H[w0];
     // largest block of [w0, w0 + new_nb) with H - H[w0] <= j0 (an empty block shares its prefix with its successor):
     // a 32-ary search, every lane probes one position per step — three dependent loads for 32 K blocks
-    uint32_t a = w0, z = w0 + blocks_for(g, nd);   // answer in [a, z)
+    const uint32_t w_hend = w0 + blocks_for(g, nd);
+    uint32_t a = w0, z = w_hend;   // answer in [a, z)
     while (z - a > 1) {
       const uint32_t span = z - a;
       const uint32_t stp = (span + 31u) / 32u;
@@ -2431,14 +2432,15 @@ delete_moves_kernel(GraphView g, const uint32_t* __restrict__ wl_off,
       if (surv) {
         const uint32_t e = blk[s];
         const uint32_t j = j0 + done + __popc(sm & ((1u << lane) - 1u));   // this survivor's hole rank in the source
-        uint32_t hb = a;
-        uint32_t k = j - (uint32_t)(H[hb] - Hw0);
-        uint32_t nh = H[hb + 1] - H[hb];
-        while (k >= nh) {   // (survivors == holes: never past the last block with holes)
-          k -= nh;
-          ++hb;
-          nh = H[hb + 1] - H[hb];
+        // the block of THIS survivor's hole: at or after the block of the first one.  A lane-private binary search —
+        // holes may be sparse (a small batch in a long chain), so stepping block by block could take hundreds of
+        // dependent loads
+        uint32_t hb = a, hz = w_hend;
+        while (hz - hb > 1) {
+          const uint32_t mid = hb + ((hz - hb) >> 1);
+          if ((uint32_t)(H[mid] - Hw0) <= j) hb = mid; else hz = mid;
         }
+        uint32_t k = j - (uint32_t)(H[hb] - Hw0);
         // the k-th hole of block hb: set bits of its mask below the new degree
         const uint32_t hlim = min(g.B, nd - (hb - w0) * g.B);
         uint32_t slot = 0;
