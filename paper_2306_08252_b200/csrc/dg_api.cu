@@ -1653,12 +1653,18 @@ static int insert_csr_impl(dg_graph* h, const uint64_t* offsets, uint64_t n_offs
     CsrItem* items = ws_alloc<CsrItem>(h, items_cap);
     unsigned long long* plan_scratch = ws_alloc<unsigned long long>(h, kAllocScratchWords);
     cudaMemsetAsync(plan_scratch, 0, kAllocScratchWords * sizeof(unsigned long long), h->stream);
-    DG_LAUNCH(h, "csr_plan_kernel", csr_plan_kernel<<<(unsigned)((V + kCsrPlanTile - 1) / kCsrPlanTile), 256, 0, h->stream>>>(
-        g, d_off, (uint32_t)V, n_edges, blk_off, items, items_cap, plan_scratch, h->d_op()));
-    const uint64_t groups = (V + 31) / 32 + items_cap;
     // a pool nothing was ever popped from: every source is empty and handle == queue position (csr_bulk_kernel)
     const bool fresh = h->active_edges == 0 && h->front == 0 && h->rear == h->NB && h->ring_identity >= h->NB &&
                        std::getenv("DG_NO_BULK_KERNEL") == nullptr;
+    const unsigned plan_grid = (unsigned)((V + kCsrPlanTile - 1) / kCsrPlanTile);
+    if (fresh) {
+      DG_LAUNCH(h, "csr_plan_kernel", csr_plan_kernel<true><<<plan_grid, 256, 0, h->stream>>>(
+          g, d_off, (uint32_t)V, n_edges, blk_off, items, items_cap, plan_scratch, h->d_op()));
+    } else {
+      DG_LAUNCH(h, "csr_plan_kernel", csr_plan_kernel<false><<<plan_grid, 256, 0, h->stream>>>(
+          g, d_off, (uint32_t)V, n_edges, blk_off, items, items_cap, plan_scratch, h->d_op()));
+    }
+    const uint64_t groups = (V + 31) / 32 + items_cap;
     if (fresh) {
       const int ctas_per_sm = resident_ctas_per_sm(csr_bulk_kernel, kBulkWarps * 32, 0);
       const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((groups + kBulkWarps - 1) / kBulkWarps, (uint64_t)h->sm_count * ctas_per_sm));

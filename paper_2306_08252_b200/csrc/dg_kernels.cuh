@@ -845,6 +845,8 @@ struct __align__(16) CsrItem {   // 32 bytes: one 32-unit chunk of a heavy sourc
 // scratch: [0] packed cursor, [1] finished CTAs of the append pass; zeroed before the launch.
 constexpr int kCsrPlanItems = 4;
 constexpr int kCsrPlanTile = 256 * kCsrPlanItems;
+// kFresh: the pool is untouched (bulk init proper), so every source is empty — its degree and tail are not read.
+template <bool kFresh>
 __global__ void __launch_bounds__(256)
 csr_plan_kernel(GraphView g, const unsigned long long* __restrict__ off, uint32_t V, unsigned long long n_edges,
                 uint32_t* __restrict__ blk_off, CsrItem* __restrict__ items, unsigned long long items_cap,
@@ -861,7 +863,7 @@ csr_plan_kernel(GraphView g, const unsigned long long* __restrict__ off, uint32_
     const bool in = v < V;
     o0[j] = in ? off[v] : 0ull;
     o1[j] = in ? off[v + 1] : 0ull;
-    dg[j] = in ? g.deg[v] : 0u;
+    dg[j] = (in && !kFresh) ? g.deg[v] : 0u;
     aw[j] = in ? g.alive[v >> 5] : 0xFFFFFFFFu;
   }
   unsigned long long w[kCsrPlanItems], sum = 0;
@@ -910,7 +912,7 @@ csr_plan_kernel(GraphView g, const unsigned long long* __restrict__ off, uint32_
       const uint32_t n_it = (uint32_t)(w[j] >> 32);
       const unsigned long long ib = run >> 32;
       if (n_it != 0 && ib + n_it <= items_cap) {   // (overflow only with broken offsets: already an error)
-        const uint32_t tl = g.tail[v];
+        const uint32_t tl = kFresh ? kNull : g.tail[v];
         for (uint32_t k = 0; k < n_it; ++k) items[ib + k] = CsrItem{v, k, dg[j], tl, o0[j], cc[j], (uint32_t)run};
       }
     }
