@@ -186,6 +186,16 @@ struct dg_graph {
   uint64_t next_ticket = 1;
   uint64_t pending_pop_bound = 0; // sum over `pending`
   uint64_t submitted_applied = 0; // submitted ops retired successfully since the last dg_flush
+  // Early count: a submitted counting-path op that follows a submitted counting-path INSERT runs its group_count
+  // beside that insert's append pass (it needs the batch and clean counters only — the insert's plan hands the
+  // counters back zeroed): own rank buffers, own error words, merged by op_arm_kernel.
+  uint32_t* rank_alt[2] = {nullptr, nullptr};
+  uint64_t rank_alt_cap = 0, rank_alt_want = 0;
+  OpState* d_pre = nullptr;       // two sets of error words
+  cudaEvent_t ev_plan_done = nullptr, ev_early = nullptr;
+  bool early_possible = false;    // the last enqueued op is such an insert (ev_plan_done is recorded behind its plan)
+  uint32_t early_next = 0;
+  struct { bool active = false; uint32_t* rank = nullptr; OpState* pre = nullptr; } early;
   int deferred_rc = 0;            // first failure among retired submitted ops, not yet returned to the caller
   uint64_t deferred_ticket = 0;
   std::string deferred_error;
@@ -519,14 +529,20 @@ int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
   op.n_input = n_input;  // device-resident copy of the input length for scans
   op.n_aux = h->size + 1;
   tl_mark(h, "begin", h->stream);
+  h->early_possible = false;   // (set again by a submitted counting-path insert once its plan is enqueued)
   if (h->submitting) {
     // the op words are installed by a kernel that first looks at what the previous submitted op left behind
-    op_arm_kernel<<<1, 1, 0, h->stream>>>(op, h->d_state(), h->d_op(), h->pending.empty() ? 0 : 1);
+    const OpState* pre = nullptr;
+    if (h->early.active) {   // this op's group_count already ran on the side stream: its verdict first
+      DG_CUDA(h, cudaStreamWaitEvent(h->stream, h->ev_early, 0));
+      pre = h->early.pre;
+    }
+    op_arm_kernel<<<1, 1, 0, h->stream>>>(op, h->d_state(), h->d_op(), h->pending.empty() ? 0 : 1, pre);
     DG_CUDA(h, cudaPeekAtLastError());
   } else {
     DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
   }
-  h->launches = h->submitting ? 1 : 0;   // (op_arm_kernel)
+  h->launches = h->submitting ? (h->early.active ? 3 : 1) : 0;   // (op_arm_kernel; early: + op_pre_arm_kernel, group_count_kernel)
   h->zslot = 0;
   if (!h->zscratch_clean) {
     DG_CUDA(h, cudaMemsetAsync(h->zscratch, 0, kZScratchWords * sizeof(unsigned long long), h->stream));
@@ -594,6 +610,7 @@ int op_conclude(dg_graph* h, const DevBlock& blk, uint64_t n_input, uint64_t lau
 // (into its own pinned slot) and an event: its status is looked at when it is retired.
 int op_end(dg_graph* h) {
   tl_mark(h, "end", h->stream);
+  h->early.active = false;
   DG_CUDA(h, cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(DevBlock), cudaMemcpyDeviceToHost, h->stream));
   if (h->submitting && h->launch_error == cudaSuccess && !h->ws_overflow) {
     cudaEvent_t ev = nullptr;
@@ -1162,6 +1179,36 @@ inline size_t group_ws_bytes(const dg_graph* h, uint64_t n, bool with_index, uin
   return t;
 }
 
+// Early count (see dg_graph::rank_alt): call right before op_begin.  On success h->early.active is set and the op must
+// use h->early.rank instead of launching group_count_kernel itself.
+template <int kMode>
+void early_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n) {
+  h->early.active = false;
+  static const bool off = std::getenv("DG_NO_EARLY_COUNT") != nullptr;
+  if (off || !h->submitting || !h->early_possible || h->pending.empty() || !h->cnt_clean || h->aux[1] == nullptr) return;
+  if (n > h->rank_alt_cap) {   // (grown by submit_coo when nothing is in flight)
+    h->rank_alt_want = std::max(h->rank_alt_want, n);
+    return;
+  }
+  GraphView g = view(h);
+  const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
+  const GroupIndex gi{(uint32_t)(cap - 1), (uint32_t)h->size};
+  const uint32_t p = h->early_next++ & 1u;
+  cudaStream_t sx = h->aux[1];
+  cudaStreamWaitEvent(sx, h->ev_plan_done, 0);
+  op_pre_arm_kernel<<<1, 1, 0, sx>>>(h->d_pre + p);
+  group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, sx>>>(
+      g, gi, d_src, d_dst, (uint32_t)n, h->cnt_buf, h->rank_alt[p], h->d_pre + p);
+  if (cudaPeekAtLastError() != cudaSuccess || cudaEventRecord(h->ev_early, sx) != cudaSuccess) {
+    cudaGetLastError();
+    h->cnt_clean = false;   // (whatever ran may have counted: the next user clears the counters)
+    return;
+  }
+  h->early.active = true;
+  h->early.rank = h->rank_alt[p];
+  h->early.pre = h->d_pre + p;
+}
+
 // counting path, step 1: validate + count; allocates the run arrays the op's alloc pass fills
 template <int kMode>
 Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, bool with_index) {
@@ -1173,15 +1220,18 @@ Grouped group_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, u
   out.cnt_words = cap + 1;
   // fused delete (B = 32) resets every counter it touched; query / other block sizes leave them behind
   out.cnt = acquire_cnt(h, kMode == kPackDelete && h->B == 32);
-  out.rank = ws_alloc<uint32_t>(h, n);
+  const bool early = h->early.active;   // (the count already ran beside the previous op: see early_count)
+  out.rank = early ? h->early.rank : ws_alloc<uint32_t>(h, n);
   out.gdst = ws_alloc<uint32_t>(h, n);
   if (with_index) out.index = ws_alloc<uint32_t>(h, n);
   out.runs_bound = std::min<uint64_t>(n, nv);
   out.run_start = ws_alloc<uint32_t>(h, out.runs_bound + 1);
   out.run_end = ws_alloc<uint32_t>(h, out.runs_bound + 1);
   out.run_src = ws_alloc<uint32_t>(h, out.runs_bound + 1);
-  DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
-      g, out.gi, d_src, d_dst, (uint32_t)n, out.cnt, out.rank, h->d_op()));
+  if (!early) {
+    DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, h->stream>>>(
+        g, out.gi, d_src, d_dst, (uint32_t)n, out.cnt, out.rank, h->d_op()));
+  }
   tl_mark(h, "K1", h->stream);
   out.b = BatchView{nullptr, out.gdst, out.run_src, out.run_start, out.run_end};
   return out;
@@ -1486,7 +1536,10 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
       return bail(DG_ERR_CUDA, "dg_create: auxiliary stream");
   }
   if (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_main, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&h->ev_main, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_plan_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_early, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMalloc(&h->d_pre, 2 * sizeof(OpState)) != cudaSuccess)
     return bail(DG_ERR_CUDA, "dg_create: auxiliary stream");
   if (cfg.workspace_bytes && ws_reserve(h, cfg.workspace_bytes) != DG_OK) return bail(DG_ERR_ENGINE, h->last_error);
   e = cudaStreamSynchronize(h->stream);
@@ -1523,6 +1576,11 @@ void dg_destroy(dg_graph* h) {
     if (h->aux[i]) { cudaStreamSynchronize(h->aux[i]); cudaStreamDestroy(h->aux[i]); }
     if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
   }
+  if (h->ev_plan_done) cudaEventDestroy(h->ev_plan_done);
+  if (h->ev_early) cudaEventDestroy(h->ev_early);
+  cudaFree(h->d_pre);
+  cudaFree(h->rank_alt[0]);
+  cudaFree(h->rank_alt[1]);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_main) cudaEventDestroy(h->ev_main);
   for (auto& sp : h->prof_open) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
@@ -1562,23 +1620,33 @@ static int insert_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst
   const uint32_t *d_src, *d_dst;
   if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
   if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
-  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  if (counting && !check_only) early_count<kPackInsert>(h, d_src, d_dst, n);
+  if ((rc = op_begin(h, n, 0)) != DG_OK) {
+    if (h->early.active) h->cnt_clean = false;
+    h->early.active = false;
+    return rc;
+  }
   if (counting) {
     // count -> plan (one alloc pass over the entries) -> entry-parallel append: no grouped copy
     GraphView g = view(h);
     const uint64_t cap = std::bit_ceil(std::max<uint64_t>(h->size, 1));
     GroupIndex gi{(uint32_t)(cap - 1), (uint32_t)h->size};
     uint32_t* cnt = acquire_cnt(h, /*self_cleaning=*/true);   // the plan pass hands every touched counter back zeroed
-    uint32_t* rank = ws_alloc<uint32_t>(h, n);
+    const bool early = h->early.active;   // (the count already ran beside the previous insert's append: see early_count)
+    uint32_t* rank = early ? h->early.rank : ws_alloc<uint32_t>(h, n);
     uint4* info = ws_alloc<uint4>(h, cap + 2);
     const unsigned grid = (unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems));
-    DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kPackInsert><<<grid, 256, 0, h->stream>>>(
-        g, gi, d_src, d_dst, (uint32_t)n, cnt, rank, h->d_op()));
+    if (!early) {
+      DG_LAUNCH(h, "group_count_kernel", group_count_kernel<kPackInsert><<<grid, 256, 0, h->stream>>>(
+          g, gi, d_src, d_dst, (uint32_t)n, cnt, rank, h->d_op()));
+    }
     launch_alloc(h, "alloc_kernel<group+plan>", n, d_n_input(h), GroupPlanIn{g, gi, d_src, rank, cnt},
                  GroupPlanOut{gi, d_src, info, cnt},
                  PlanFin{g, h->d_op(), n, /*set_runs=*/1, /*commit_globals=*/(h->agree_x || check_only) ? 0 : 1});
     tl_mark(h, "plan", h->stream);
     if (check_only) return op_end(h);
+    if (h->submitting && h->ev_plan_done != nullptr && cudaEventRecord(h->ev_plan_done, h->stream) == cudaSuccess)
+      h->early_possible = true;   // the next submitted op may count beside this op's append pass
     enqueue_agree(h, /*commit_insert=*/true);
     DG_LAUNCH(h, "append_entries_kernel", append_entries_kernel<<<grid, 256, 0, h->stream>>>(
         g, gi, d_src, d_dst, rank, (uint32_t)n, info, h->d_op()));
@@ -1791,7 +1859,12 @@ static int delete_coo_impl(dg_graph* h, const uint32_t* src, const uint32_t* dst
   const uint32_t *d_src, *d_dst;
   if ((rc = stage_in(h, src, n, mem, &d_src)) != DG_OK) return rc;
   if ((rc = stage_in(h, dst, n, mem, &d_dst)) != DG_OK) return rc;
-  if ((rc = op_begin(h, n, 0)) != DG_OK) return rc;
+  if (!no_pool && use_counting(h, n)) early_count<kPackDelete>(h, d_src, d_dst, n);
+  if ((rc = op_begin(h, n, 0)) != DG_OK) {
+    if (h->early.active) h->cnt_clean = false;
+    h->early.active = false;
+    return rc;
+  }
   if (no_pool) {  // validation only (radix path packs + validates; B == 0 never takes the counting path)
     group_radix<kPackDelete>(h, d_src, d_dst, n, false, h->size - 1);
     return op_end(h);
@@ -1830,6 +1903,25 @@ static int submit_coo(dg_graph* h, const uint32_t* src, const uint32_t* dst, uin
   if (h->deferred_rc != DG_OK) {
     const int rc = drain(h);
     return rc != DG_OK ? rc : take_deferred(h);
+  }
+  // rank buffers of the early count: sized for the largest submitted batch seen, (re)allocated while nothing is in flight
+  h->rank_alt_want = std::max(h->rank_alt_want, n);
+  if (h->pending.empty() && h->rank_alt_want > h->rank_alt_cap) {
+    cudaStreamSynchronize(h->stream);
+    if (h->aux[1]) cudaStreamSynchronize(h->aux[1]);
+    uint32_t *a = nullptr, *b = nullptr;
+    const uint64_t want = h->rank_alt_want + h->rank_alt_want / 4;
+    if (cudaMalloc(&a, want * 4) == cudaSuccess && cudaMalloc(&b, want * 4) == cudaSuccess) {
+      cudaFree(h->rank_alt[0]);
+      cudaFree(h->rank_alt[1]);
+      h->rank_alt[0] = a;
+      h->rank_alt[1] = b;
+      h->rank_alt_cap = want;
+    } else {   // (no early count then: everything still works)
+      cudaGetLastError();
+      cudaFree(a);
+      cudaFree(b);
+    }
   }
   bool async_ok = h->B != 0 && h->slab != nullptr && !h->profiling && !h->timeline && h->agree_x == nullptr && n > 0;
   if (async_ok && is_insert) {

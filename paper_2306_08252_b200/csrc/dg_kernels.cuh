@@ -147,7 +147,14 @@ __device__ __forceinline__ uint32_t filter_hash(uint32_t x, int bits) { return (
 // first looks at the words the previous op left behind.  chain != 0: the previous op of the stream was
 // submitted too and has not been reported — if it failed (or an earlier one did: the poison word),
 // this op starts out rejected and every kernel of it returns at its first line.
-__global__ void op_arm_kernel(OpState fresh, DeviceState* st, OpState* op, int chain) {
+// pre: the words an EARLY group_count of this op reported into (it ran beside the previous op's last kernel, before
+// these op words existed): its verdict is merged here.
+__global__ void op_arm_kernel(OpState fresh, DeviceState* st, OpState* op, int chain, const OpState* pre) {
+  if (pre != nullptr && pre->err != 0) {
+    fresh.err = pre->err;
+    fresh.err_detail = pre->err_detail;
+    fresh.err_index = pre->err_index;
+  }
   if (chain && (st->poison != 0 || op->err != 0)) {
     st->poison = 1;
     fresh.err = 3u;   // DG_ERR_ENGINE
@@ -156,6 +163,12 @@ __global__ void op_arm_kernel(OpState fresh, DeviceState* st, OpState* op, int c
     st->poison = 0;
   }
   *op = fresh;
+}
+
+__global__ void op_pre_arm_kernel(OpState* pre) {
+  pre->err = 0u;
+  pre->err_detail = 0u;
+  pre->err_index = ~0ull;
 }
 
 // ---------------------------------------------------------------------------
