@@ -63,6 +63,13 @@ extern "C" {
  * block is not even 16-byte aligned).  An explicit deviation from the reference's value — block counts, and with
  * them the point where a fixed pool underflows, follow the block size actually used (dg_block_size reports it). */
 #define DG_FLAG_AUTO_BLOCK_NATIVE 8u
+/* Contract for dg_submit_*_coo: the device arrays handed to a submit call are COMPLETE when the call is made — nothing
+ * enqueued on the graph's stream (after the previous submit) produces them.  With this flag the library may start the
+ * op's first kernel (the per-source count, which reads only the batch) on a side stream beside the previous
+ * submitted op's last kernel, i.e. before the point in the graph's stream where the op itself is enqueued.  Without
+ * it every kernel of an op stays behind everything enqueued on the graph's stream before the call.  (The ingest queue
+ * needs no flag: it orders the early kernel behind the slot's own copy.) */
+#define DG_FLAG_SUBMIT_INPUTS_READY 16u
 
 /* reference: types.hpp:16-17 (kInvalidVertex / kNullBlock) */
 #define DG_INVALID_VERTEX 0xFFFFFFFFu

@@ -15,6 +15,7 @@ DG_FLAG_NO_RECLAIM = 1
 DG_FLAG_GROUP_RADIX = 2
 DG_FLAG_GROUP_COUNT = 4
 DG_FLAG_AUTO_BLOCK_NATIVE = 8
+DG_FLAG_SUBMIT_INPUTS_READY = 16
 DG_IPC_HANDLE_BYTES = 64
 
 u8p = C.POINTER(C.c_uint8)

@@ -194,6 +194,7 @@ struct dg_graph {
   OpState* d_pre = nullptr;       // two sets of error words
   cudaEvent_t ev_plan_done = nullptr, ev_early = nullptr;
   bool early_possible = false;    // the last enqueued op is such an insert (ev_plan_done is recorded behind its plan)
+  cudaEvent_t input_ready = nullptr;   // ingest queue: the copy-done event of the slot being submitted
   uint32_t early_next = 0;
   struct { bool active = false; uint32_t* rank = nullptr; OpState* pre = nullptr; } early;
   int deferred_rc = 0;            // first failure among retired submitted ops, not yet returned to the caller
@@ -1186,6 +1187,9 @@ void early_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint
   h->early.active = false;
   static const bool off = std::getenv("DG_NO_EARLY_COUNT") != nullptr;
   if (off || !h->submitting || !h->early_possible || h->pending.empty() || !h->cnt_clean || h->aux[1] == nullptr) return;
+  // the side stream is not behind what the caller enqueued on the graph's stream: the batch must be known complete —
+  // by contract (DG_FLAG_SUBMIT_INPUTS_READY) or through the ingest slot's copy-done event
+  if (h->input_ready == nullptr && !(h->cfg.flags & DG_FLAG_SUBMIT_INPUTS_READY)) return;
   if (n > h->rank_alt_cap) {   // (grown by submit_coo when nothing is in flight)
     h->rank_alt_want = std::max(h->rank_alt_want, n);
     return;
@@ -1196,6 +1200,7 @@ void early_count(dg_graph* h, const uint32_t* d_src, const uint32_t* d_dst, uint
   const uint32_t p = h->early_next++ & 1u;
   cudaStream_t sx = h->aux[1];
   cudaStreamWaitEvent(sx, h->ev_plan_done, 0);
+  if (h->input_ready != nullptr) cudaStreamWaitEvent(sx, h->input_ready, 0);
   op_pre_arm_kernel<<<1, 1, 0, sx>>>(h->d_pre + p);
   group_count_kernel<kMode><<<(unsigned)((n + 256 * kGroupItems - 1) / (256 * kGroupItems)), 256, 0, sx>>>(
       g, gi, d_src, d_dst, (uint32_t)n, h->cnt_buf, h->rank_alt[p], h->d_pre + p);
@@ -2855,7 +2860,9 @@ static int ingest_submit(dg_ingest* q, uint32_t slot, bool is_insert, uint64_t* 
   cudaSetDevice(h->device);
   if (q->state[slot] != 1) return fail(h, DG_ERR_DATA, "ingest: slot holds no staged batch");
   DG_CUDA(h, cudaStreamWaitEvent(h->stream, q->filled[slot], 0));
+  h->input_ready = q->filled[slot];   // (an early count on the side stream waits for the slot's copy too)
   const int rc = submit_coo(h, q->src[slot], q->dst[slot], q->n[slot], is_insert, ticket);
+  h->input_ready = nullptr;
   cudaEventRecord(q->freed[slot], h->stream);
   q->state[slot] = 0;
   return rc;

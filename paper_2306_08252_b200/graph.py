@@ -27,6 +27,9 @@ class GraphConfig:
     reclaim_on_delete: bool = True
     stream: int = 0              # cudaStream_t handle; 0 => library-owned stream
     group: str = "auto"          # how COO batches are grouped by source: "auto" | "radix" | "count"
+    # submit_*_pairs: the device arrays are complete when the call is made (nothing enqueued on the graph's stream
+    # produces them), so an op's first kernel may start beside the previous op's last (DG_FLAG_SUBMIT_INPUTS_READY)
+    submit_inputs_ready: bool = False
     auto_block_native: bool = False   # block_size 0: a computed size in [24, 48] becomes the native 32 (DG_FLAG_AUTO_BLOCK_NATIVE)
     workspace_bytes: int = 0     # per-op scratch reserved at construction (0 => grown on first use)
     # GrowthPolicy (block_pool.hpp:18-29): pool_max_blocks is the arena's role (0 => fixed pool)
@@ -84,6 +87,8 @@ class DynamicGraph:
         c.flags |= {"auto": 0, "radix": _lib.DG_FLAG_GROUP_RADIX, "count": _lib.DG_FLAG_GROUP_COUNT}[cfg.group]
         if cfg.auto_block_native:
             c.flags |= _lib.DG_FLAG_AUTO_BLOCK_NATIVE
+        if cfg.submit_inputs_ready:
+            c.flags |= _lib.DG_FLAG_SUBMIT_INPUTS_READY
         c.pool_bytes = cfg.pool_bytes
         c.pool_blocks = cfg.pool_blocks
         c.stream = cfg.stream or None

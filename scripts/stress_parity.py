@@ -45,7 +45,8 @@ def main():
             B = int(rng.choice([32, 32, 32, 5, 33]))
             grow = bool(rng.integers(0, 3) == 0)
             g = DynamicGraph(GraphConfig(pool_blocks=(512 if grow else 1 << 21), pool_max_blocks=(1 << 21 if grow else 0),
-                                         group=str(rng.choice(["auto", "radix", "count"]))), V, B)
+                                         group=str(rng.choice(["auto", "radix", "count"])),
+                                         submit_inputs_ready=bool(rng.integers(0, 4) != 0)), V, B)
             o = CpuGraph(orc, "orc", V, B, 2 << 30, 0.5, True, 1)
             keep, log, what = [], [], ""
             try:

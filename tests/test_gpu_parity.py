@@ -450,8 +450,9 @@ def _same_graph(g, o):
     assert np.array_equal(np.asarray(g.degrees()), np.asarray(o.degrees()))
 
 
+@pytest.mark.parametrize("inputs_ready", [False, True])
 @pytest.mark.parametrize("block_size,group", [(32, "auto"), (32, "radix"), (7, "auto")])
-def test_submitted_ops_match_synchronous_ops(block_size, group):
+def test_submitted_ops_match_synchronous_ops(block_size, group, inputs_ready):
     """dg_submit_insert_coo / dg_submit_delete_coo / dg_flush: a stream of submitted batches (no host wait
     between them; hubs, duplicates, deletes of absent edges) leaves the graph the reference's loop of
     insert_batch / delete_batch leaves (graph.hpp:167-222); synchronous calls in between see every
@@ -459,7 +460,9 @@ def test_submitted_ops_match_synchronous_ops(block_size, group):
     from paper_2306_08252_b200 import DynamicGraph, GraphConfig
     rng = np.random.default_rng(5)
     V = 6000
-    g = DynamicGraph(GraphConfig(pool_blocks=1 << 17, group=group), V, block_size)
+    # inputs_ready: DG_FLAG_SUBMIT_INPUTS_READY — an op's count may run beside the previous insert's append (the
+    # arrays here are complete when submitted: .cuda() of a host array is synchronous)
+    g = DynamicGraph(GraphConfig(pool_blocks=1 << 17, group=group, submit_inputs_ready=inputs_ready), V, block_size)
     o = CpuGraph(load_oracle(), "orc", V, block_size, 1 << 29)
     keep, tickets = [], []
     for i in range(14):
@@ -493,7 +496,7 @@ def test_submitted_failure_is_reported_before_anything_behind_it_mutates():
     from paper_2306_08252_b200 import DataError, DynamicGraph, EngineError, GraphConfig
     rng = np.random.default_rng(9)
     V = 3000
-    g = DynamicGraph(GraphConfig(pool_blocks=1 << 16), V, 32)
+    g = DynamicGraph(GraphConfig(pool_blocks=1 << 16, submit_inputs_ready=True), V, 32)
     o = CpuGraph(load_oracle(), "orc", V, 32, 1 << 28)
     def batch(n):
         return (rng.zipf(1.3, n) % V).astype(np.uint32), rng.integers(0, V, n).astype(np.uint32)
