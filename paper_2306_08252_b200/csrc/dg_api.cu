@@ -165,6 +165,7 @@ struct dg_graph {
   DevBlock* d_blk = nullptr;  // device
   DevBlock* h_blk = nullptr;  // pinned host mirror of the CURRENT op: one slot of h_ring
   DevBlock* h_ring = nullptr; // pinned status slots: every op reads back into its own, so submitted ops need no host wait
+  DevBlock* h_ring_dev = nullptr;   // the same slots as the device sees them (mapped host memory; nullptr: memcpy instead)
   uint32_t h_ring_next = 0;
   uint64_t front = 0, rear = 0, active_edges = 0;   // as of the last RETIRED op
 
@@ -612,7 +613,15 @@ int op_conclude(dg_graph* h, const DevBlock& blk, uint64_t n_input, uint64_t lau
 int op_end(dg_graph* h) {
   tl_mark(h, "end", h->stream);
   h->early.active = false;
-  DG_CUDA(h, cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(DevBlock), cudaMemcpyDeviceToHost, h->stream));
+  static_assert(sizeof(DevBlock) % 8 == 0, "status words");
+  if (h->h_ring_dev != nullptr) {   // stores into the mapped slot (see op_publish_kernel)
+    unsigned long long* slot_dev = reinterpret_cast<unsigned long long*>(h->h_ring_dev + (h->h_blk - h->h_ring));
+    op_publish_kernel<<<1, 32, 0, h->stream>>>(reinterpret_cast<const unsigned long long*>(h->d_blk), slot_dev,
+                                               (int)(sizeof(DevBlock) / 8));
+    DG_CUDA(h, cudaPeekAtLastError());
+  } else {
+    DG_CUDA(h, cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(DevBlock), cudaMemcpyDeviceToHost, h->stream));
+  }
   if (h->submitting && h->launch_error == cudaSuccess && !h->ws_overflow) {
     cudaEvent_t ev = nullptr;
     if (!h->done_pool.empty()) {
@@ -1508,12 +1517,17 @@ int dg_create(const dg_config* config, uint64_t initial_vertices, uint32_t block
       cudaMalloc(&h->deg, h->capacity * 4) != cudaSuccess ||
       cudaMalloc(&h->alive, words * 4) != cudaSuccess ||
       cudaMalloc(&h->d_blk, sizeof(DevBlock)) != cudaSuccess ||
-      cudaMallocHost(&h->h_ring, kStatusSlots * sizeof(DevBlock)) != cudaSuccess) {
+      cudaHostAlloc(&h->h_ring, kStatusSlots * sizeof(DevBlock), cudaHostAllocMapped) != cudaSuccess) {
     cudaGetLastError();
     return bail(DG_ERR_ENGINE, "vertex dictionary: device allocation failed");
   }
   std::memset(h->h_ring, 0, kStatusSlots * sizeof(DevBlock));
   h->h_blk = &h->h_ring[0];
+  if (std::getenv("DG_STATUS_MEMCPY") == nullptr) {
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, h->h_ring, 0) == cudaSuccess) h->h_ring_dev = static_cast<DevBlock*>(dp);
+    else cudaGetLastError();
+  }
   cudaMemsetAsync(h->d_blk, 0, sizeof(DevBlock), h->stream);
   cudaMemsetAsync(h->head, 0xFF, h->capacity * 4, h->stream);
   cudaMemsetAsync(h->tail, 0xFF, h->capacity * 4, h->stream);

@@ -165,6 +165,15 @@ __global__ void op_arm_kernel(OpState fresh, DeviceState* st, OpState* op, int c
   *op = fresh;
 }
 
+// The op's status {DeviceState, OpState} goes to its pinned host slot by STORES from this one-warp kernel (mapped
+// host memory), not by a device-to-host memcpy: a copy-engine transfer queues behind whatever the engine is busy
+// with — next to an ingest queue streaming 8 MB batches, a 256-byte status copy waited ~150 us per op and serialised
+// the ops with the batch copies.
+__global__ void op_publish_kernel(const unsigned long long* __restrict__ dev_words, unsigned long long* host_words, int n_words) {
+  for (int i = threadIdx.x; i < n_words; i += blockDim.x) host_words[i] = dev_words[i];
+  __threadfence_system();
+}
+
 __global__ void op_pre_arm_kernel(OpState* pre) {
   pre->err = 0u;
   pre->err_detail = 0u;
