@@ -542,7 +542,10 @@ int op_begin(dg_graph* h, uint64_t n_input, uint64_t n_runs) {
     op_arm_kernel<<<1, 1, 0, h->stream>>>(op, h->d_state(), h->d_op(), h->pending.empty() ? 0 : 1, pre);
     DG_CUDA(h, cudaPeekAtLastError());
   } else {
-    DG_CUDA(h, cudaMemcpyAsync(h->d_op(), &op, sizeof(OpState), cudaMemcpyHostToDevice, h->stream));
+    // (the same kernel for synchronous ops: the words travel as its argument — no host-to-device copy that would
+    // queue behind batch copies on the copy engine; nothing is in flight, so nothing to look at: chain = 0)
+    op_arm_kernel<<<1, 1, 0, h->stream>>>(op, h->d_state(), h->d_op(), 0, nullptr);
+    DG_CUDA(h, cudaPeekAtLastError());
   }
   h->launches = h->submitting ? (h->early.active ? 3 : 1) : 0;   // (op_arm_kernel; early: + op_pre_arm_kernel, group_count_kernel)
   h->zslot = 0;
